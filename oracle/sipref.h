@@ -1,0 +1,146 @@
+/*
+ * sipref.h -- CPU ORACLE for PARSDMM (Peters & Herrmann, arXiv 1902.09699).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ * The product path (paper_1902_09699_b200/, include/sip.h) never links,
+ * imports or calls anything in oracle/.  The two share no code, headers,
+ * tables or helpers.
+ *
+ * Plain C99, fp64, single-threaded, no FMA contraction (-ffp-contract=off),
+ * written to be checked against the paper by eye.  Citations "P:n" are
+ * /root/reference/PAPER.md line numbers; "L<n>" are the readings of the
+ * paper listed in DESIGN.md section 3 (SURVEY.md 8(c) ledger).
+ *
+ * Layout (reading L1): grids are (nz, ny, nx) row-major with x fastest,
+ * m[(iz*ny + iy)*nx + ix]; 2D grids have ny = 1.  Operator outputs use the
+ * COMPACT layouts of the paper: D_z x has (nz-1)*ny*nx entries, D_x x has
+ * nz*ny*(nx-1), TV = [D_z; D_y; D_x] (D_y only in 3D), F x = (G x)[mask].
+ */
+#ifndef SIPREF_H
+#define SIPREF_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { SIPREF_OP_I = 0, SIPREF_OP_DZ = 1, SIPREF_OP_DY = 2, SIPREF_OP_DX = 3,
+       SIPREF_OP_TV = 4, SIPREF_OP_BLUR_MASK = 5 };
+enum { SIPREF_BOUNDS = 0, SIPREF_L1 = 1, SIPREF_L2 = 2, SIPREF_ANNULUS = 3,
+       SIPREF_CARD = 4 };
+
+typedef struct {
+  int ndim;          /* 2 or 3 */
+  int64_t n[3];      /* nz, ny, nx  (ny = 1 when ndim = 2) */
+  double h[3];       /* hz, hy, hx */
+} sipref_grid;
+
+typedef struct {
+  int op, type;
+  double lo, hi;                 /* BOUNDS scalars                           */
+  const double *lo_vec, *hi_vec; /* optional per-entry bounds, length M      */
+  double sigma;                  /* L1 / L2 radius                           */
+  double sigma_lo, sigma_hi;     /* ANNULUS                                  */
+  int64_t k;                     /* CARD                                     */
+  int relative;                  /* 1: sigma* are fractions of the norm of
+                                    A m (l1 for L1, l2 for L2/ANNULUS) and
+                                    k = floor(k_frac * M)  (reading L4, L23) */
+  double k_frac;
+  const double *kernel; int kh, kw;  /* BLUR_MASK: kh x kw kernel, row major */
+  const unsigned char *mask;         /* BLUR_MASK: N bytes, 1 = observed     */
+} sipref_set;
+
+typedef struct {
+  int max_iter, n_cg;
+  double rho0, gamma0, eps_evol, eps_feas, eps_corr;
+  int adapt_every, check_every, hist_s;
+  double rho_ratio_cap, gamma_max;
+  int eq25;        /* 1: CG stops by Eq. 25; 0: exactly n_cg iterations    */
+  int fixed_work;  /* 1: stop test evaluated but never acted on            */
+  double cg_tol_floor; /* floor of the Eq. 25 target (10*eps of the dtype)  */
+} sipref_options;
+
+typedef struct {
+  int iterations, cg_total, converged, breakdown;
+  double r_evol;
+  /* optional per-iteration records (caller-allocated, may be NULL) */
+  int *cg_per_iter;     /* [max_iter]                                      */
+  int *branch;          /* [max_iter * (p+1)], Alg. 2 branch code or -1    */
+  double *rho_trace;    /* [max_iter * (p+1)] rho after the iteration      */
+  double *gamma_trace;  /* [max_iter * (p+1)]                              */
+  double *r_feas_trace; /* [max_iter * p], NaN when not a check iteration  */
+  double *r_evol_trace; /* [max_iter]                                      */
+  /* final values (caller-allocated, may be NULL) */
+  double *r_feas;       /* [p]   */
+  double *rho, *gamma;  /* [p+1] */
+} sipref_log;
+
+void sipref_default_options(sipref_options *o);
+
+/* number of grid points; M of an operator (compact) */
+int64_t sipref_npts(const sipref_grid *g);
+int64_t sipref_op_len(const sipref_grid *g, const sipref_set *s);
+
+/* y = A x  and  x = A^T y  (compact layouts) */
+void sipref_apply_A(const sipref_grid *g, const sipref_set *s, const double *x, double *y);
+void sipref_apply_AT(const sipref_grid *g, const sipref_set *s, const double *y, double *x);
+
+/* q = (sum_i rho_i A_i^T A_i + rho_{p+1} I) p,  Eq. 23 */
+void sipref_apply_C(const sipref_grid *g, int p, const sipref_set *sets,
+                    const double *rho, const double *pv, double *q);
+
+/* Euclidean projection of w (length M) onto the simple set C_i, Table 1.
+   The set's parameters must already be absolute (relative == 0). */
+void sipref_project(const sipref_set *s, int64_t M, const double *w, double *y);
+
+/* distance prox, Eq. 22 */
+void sipref_prox_dist(int64_t N, const double *m, double rho, const double *w, double *y);
+
+/* Warm-started CG on C x = b (Eq. 25 when eq25 != 0): returns iterations.
+   tol_out receives the relative-residual target used. */
+int sipref_cg(const sipref_grid *g, int p, const sipref_set *sets, const double *rho,
+              const double *b, double *x, int n_cg, int eq25, double *tol_out,
+              int *breakdown);
+
+/* Algorithm 2 on explicit vectors for one set: returns the branch code
+   (0 both, 1 alpha only, 2 beta only, 3 none) and writes rho/gamma. */
+int sipref_adapt_rho_gamma(int64_t M, const double *v_hat, const double *v_hat0,
+                           const double *v, const double *v0,
+                           const double *s, const double *s0,
+                           const double *y, const double *y0,
+                           double rho, double eps_corr, double *rho_new,
+                           double *gamma_new);
+
+/* Eq. 26 feasibility error of s = A x for one set (absolute parameters) */
+double sipref_feas(const sipref_set *s, int64_t M, const double *sv);
+
+/* Algorithm 1.  x (length N) receives the result.
+   init_x/init_y/init_v: optional warm start (NULL = reading L13 defaults:
+   x = m, y_i = A_i m, v_i = 0).  init_y/init_v are arrays of p+1 pointers.
+   init_rho/init_gamma: optional starting parameters (NULL = rho0/gamma0).
+   out_y/out_v (optional, p+1 pointers) receive the final y_i, v_i.
+   Returns 0 converged, 1 not converged, <0 error. */
+int sipref_parsdmm(const sipref_grid *g, int p, const sipref_set *sets,
+                   const sipref_options *o, const double *m, double *x,
+                   const double *init_x, double *const *init_y, double *const *init_v,
+                   const double *init_rho, const double *init_gamma,
+                   double *const *out_y, double *const *out_v,
+                   sipref_log *log);
+
+/* Algorithm 3 (multilevel).  Level l grid is the fine grid coarsened
+   (l-1) times by 2 (box mean + stride, reading L23); h doubles per level.
+   logs: array of n_levels logs (index 0 = finest), may be NULL. */
+int sipref_parsdmm_multilevel(const sipref_grid *g, int p, const sipref_set *sets,
+                              const sipref_options *o, int n_levels,
+                              const double *m, double *x, sipref_log *logs);
+
+/* multilevel transfers (exposed for pins) */
+void sipref_restrict(const sipref_grid *fine, const double *f, double *c);
+void sipref_interp(int64_t cz, int64_t cy, int64_t cx, const double *c,
+                   int64_t fz, int64_t fy, int64_t fx, double *f);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

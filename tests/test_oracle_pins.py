@@ -1,0 +1,528 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+CPU-only (runs under ``-m "not gpu"``).  Each test pins one oracle function
+to something other than the oracle itself: worked examples (tests/golden,
+each cited), closed forms, invariants, brute force on tiny inputs, textbook
+or library routines (numpy.linalg.solve, scipy isotonic regression, scipy
+SLSQP) and Dykstra's algorithm (paper Algorithm 4).
+"""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.optimize as so
+
+import oracle as O
+from sip_inputs import INF, SetDef, gaussian_kernel, tiny_model
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+rng0 = np.random.default_rng(12345)
+
+
+def dense_of(shape, sd, h=None):
+    """dense matrix of an oracle operator, column by column (A e_j)"""
+    N = int(np.prod(shape))
+    cols = [O.apply_A(shape, sd, np.eye(N)[j], h) for j in range(N)]
+    return np.stack(cols, axis=1)
+
+
+def dense_T(shape, sd, M, h=None):
+    rows = [O.apply_AT(shape, sd, np.eye(M)[j], h) for j in range(M)]
+    return np.stack(rows, axis=0)   # row j = A^T e_j  ->  equals A
+
+
+def d1(n, h=1.0):
+    """Eq. 8: (n-1) x n bidiagonal (-1, 1)/h"""
+    D = np.zeros((n - 1, n))
+    for i in range(n - 1):
+        D[i, i], D[i, i + 1] = -1.0, 1.0
+    return D / h
+
+
+# ------------------------------------------------------------ operators
+def test_dz_worked_example():
+    g = GOLD["dz_2x2"]
+    A = dense_of(tuple(g["shape"]), SetDef("DZ", "bounds"))
+    np.testing.assert_array_equal(A, np.array(g["matrix"], dtype=float))
+
+
+@pytest.mark.parametrize("shape,h", [((5, 4), (2.0, 3.0)), ((3, 4, 5), (2.0, 0.5, 3.0))])
+def test_operators_kronecker(shape, h):
+    """the 2D vertical derivative is D_z (x) I_x; lateral ones I (x) D."""
+    if len(shape) == 2:
+        nz, nx = shape
+        Dz = np.kron(d1(nz, h[0]), np.eye(nx))
+        Dx = np.kron(np.eye(nz), d1(nx, h[1]))
+        blocks = [Dz, Dx]
+        ops = [("DZ", Dz), ("DX", Dx)]
+    else:
+        nz, ny, nx = shape
+        Dz = np.kron(d1(nz, h[0]), np.eye(ny * nx))
+        Dy = np.kron(np.eye(nz), np.kron(d1(ny, h[1]), np.eye(nx)))
+        Dx = np.kron(np.eye(nz * ny), d1(nx, h[2]))
+        blocks = [Dz, Dy, Dx]
+        ops = [("DZ", Dz), ("DY", Dy), ("DX", Dx)]
+    for op, ref in ops:
+        np.testing.assert_allclose(dense_of(shape, SetDef(op, "bounds"), h), ref, atol=1e-15)
+    np.testing.assert_allclose(dense_of(shape, SetDef("TV", "l1"), h), np.vstack(blocks), atol=1e-15)
+    N = int(np.prod(shape))
+    np.testing.assert_array_equal(dense_of(shape, SetDef("I", "bounds"), h), np.eye(N))
+
+
+@pytest.mark.parametrize("shape", [(6, 7), (4, 5, 6)])
+def test_operators_constants_and_ramps(shape):
+    """derivatives annihilate constants; a unit-slope ramp maps to 1"""
+    h = (2.0, 0.5) if len(shape) == 2 else (2.0, 0.25, 0.5)
+    c = np.full(shape, 3.7)
+    for op in (["DZ", "DX"] if len(shape) == 2 else ["DZ", "DY", "DX"]):
+        assert np.abs(O.apply_A(shape, SetDef(op, "bounds"), c, h)).max() == 0.0
+    axes = {"DZ": 0, "DY": 1, "DX": len(shape) - 1}
+    for op, ax in axes.items():
+        if op == "DY" and len(shape) == 2:
+            continue
+        idx = np.indices(shape)[ax].astype(float) * h[ax]
+        np.testing.assert_allclose(O.apply_A(shape, SetDef(op, "bounds"), idx, h), 1.0, rtol=1e-14)
+
+
+def _blur_set(shape, seed=0, sym=False):
+    r = np.random.default_rng(seed)
+    K = gaussian_kernel(5, 1.5) if sym else r.uniform(0.1, 1.0, size=(3, 5))
+    mask = (r.uniform(size=shape) < 0.6).astype(np.uint8)
+    return SetDef("BLUR_MASK", "bounds", kernel=K, mask=mask)
+
+
+@pytest.mark.parametrize("shape", [(7, 9), (4, 5, 6), (9, 6)])
+def test_adjoint_identity(shape):
+    """<A a, b> = <a, A^T b> within 1e-12 for every operator"""
+    ops = ["I", "DZ", "DX", "TV"] + (["DY"] if len(shape) == 3 else ["BLUR"])
+    r = np.random.default_rng(7)
+    for op in ops:
+        sd = _blur_set(shape) if op == "BLUR" else SetDef(op, "bounds")
+        M = O.op_len(shape, sd)
+        for _ in range(5):
+            a = r.normal(size=int(np.prod(shape)))
+            b = r.normal(size=M)
+            lhs = O.apply_A(shape, sd, a) @ b
+            rhs = a @ O.apply_AT(shape, sd, b)
+            assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(a) * np.linalg.norm(b) * 10
+
+
+def test_blur_delta_response():
+    """G is a 'same' correlation (reading L21): a delta returns the mirrored
+    kernel; the restriction S keeps the masked pixels in index order"""
+    shape = (9, 11)
+    K = np.arange(15, dtype=float).reshape(3, 5) + 1.0
+    x = np.zeros(shape); x[4, 5] = 1.0
+    full = SetDef("BLUR_MASK", "bounds", kernel=K, mask=np.ones(shape, np.uint8))
+    y = O.apply_A(shape, full, x).reshape(shape)
+    np.testing.assert_array_equal(y[3:6, 3:8], K[::-1, ::-1])
+    assert y.sum() == K.sum()
+    mask = np.zeros(shape, np.uint8); mask[4, 5] = 1; mask[0, 0] = 1
+    sd = SetDef("BLUR_MASK", "bounds", kernel=K, mask=mask)
+    np.testing.assert_array_equal(O.apply_A(shape, sd, x), [0.0, K[1, 2]])
+
+
+# ------------------------------------------------------------ system matrix
+def test_gram_worked_examples():
+    g = GOLD["gram_dz_3x1"]
+    A = dense_of((3, 1), SetDef("DZ", "bounds"))
+    np.testing.assert_array_equal(A.T @ A, np.array(g["matrix"], float))
+    g2 = GOLD["system_I_plus_dz"]
+    # sets {I-box, D_z-box} with rho = {1 (I set), 1 (D_z set)} and rho_{p+1} -> 0
+    C = np.stack([O.apply_C((3, 1), [SetDef("I", "bounds"), SetDef("DZ", "bounds")],
+                            [1.0, 1.0, 0.0], np.eye(3)[j]) for j in range(3)], axis=1)
+    np.testing.assert_array_equal(C, np.array(g2["matrix"], float))
+    np.testing.assert_array_equal(C @ np.eye(3)[0], g2["times_e0"])
+
+
+@pytest.mark.parametrize("shape", [(5, 4), (3, 4, 3)])
+def test_apply_C_matches_dense_assembly(shape):
+    """Eq. 23 assembled densely from the operators' matrices"""
+    sets = [SetDef("I", "bounds"), SetDef("DZ", "bounds"), SetDef("DX", "card"), SetDef("TV", "l1")]
+    if len(shape) == 3:
+        sets.append(SetDef("DY", "bounds"))
+    else:
+        sets.append(_blur_set(shape, sym=True))
+    r = np.random.default_rng(3)
+    rho = r.uniform(0.1, 3.0, size=len(sets) + 1)
+    N = int(np.prod(shape))
+    C = rho[-1] * np.eye(N)
+    for i, sd in enumerate(sets):
+        A = dense_of(shape, sd)
+        C += rho[i] * A.T @ A
+    for _ in range(3):
+        p = r.normal(size=N)
+        np.testing.assert_allclose(O.apply_C(shape, sets, rho, p), C @ p, rtol=1e-12, atol=1e-12)
+    z = r.normal(size=(20, N))
+    assert np.all(np.einsum("ij,jk,ik->i", z, C, z) > 0)   # SPD
+    np.testing.assert_allclose(C, C.T, atol=1e-13)
+
+
+# ------------------------------------------------------------ CG
+def _system(shape, seed=5):
+    sets = [SetDef("TV", "l1"), SetDef("DZ", "bounds")]
+    r = np.random.default_rng(seed)
+    rho = r.uniform(0.2, 2.0, size=3)
+    N = int(np.prod(shape))
+    C = rho[-1] * np.eye(N)
+    for i, sd in enumerate(sets):
+        A = dense_of(shape, sd)
+        C += rho[i] * A.T @ A
+    return sets, rho, C
+
+
+def test_cg_exact_terminates_in_n():
+    """exact-arithmetic CG solves an SPD n x n system in <= n steps"""
+    shape = (4, 3)
+    sets, rho, C = _system(shape)
+    b = np.random.default_rng(1).normal(size=12)
+    x, it, tol, bd = O.cg(shape, sets, rho, b, np.zeros(12), n_cg=12, eq25=False)
+    np.testing.assert_allclose(x, np.linalg.solve(C, b), rtol=1e-9, atol=1e-9)
+    assert it <= 12 and bd == 0
+
+
+def test_cg_eq25_reduces_residual_tenfold():
+    """Eq. 25: stop once ||r||/||b|| < 0.1 x the warm-start value"""
+    shape = (6, 5)
+    sets, rho, C = _system(shape, 9)
+    r = np.random.default_rng(2)
+    b = r.normal(size=30)
+    x0 = r.normal(size=30)
+    x, it, tol, bd = O.cg(shape, sets, rho, b, x0, n_cg=100, eq25=True)
+    r0 = np.linalg.norm(b - C @ x0) / np.linalg.norm(b)
+    r1 = np.linalg.norm(b - C @ x) / np.linalg.norm(b)
+    assert tol == pytest.approx(0.1 * r0, rel=1e-12)
+    assert r1 < tol and it >= 1
+    # one iteration fewer does not reach it (the test is applied before each step)
+    x2, it2, _, _ = O.cg(shape, sets, rho, b, x0, n_cg=it - 1, eq25=True)
+    assert np.linalg.norm(b - C @ x2) / np.linalg.norm(b) >= tol * (1 - 1e-9)
+
+
+def test_cg_special_cases():
+    """C = rho I converges in one step; warm start at the solution
+    takes 0 steps; zero rhs gives x = 0"""
+    shape = (3, 3)
+    b = np.arange(9.0) + 1
+    x, it, _, _ = O.cg(shape, [], [2.0], b, np.zeros(9), n_cg=10, eq25=False)
+    np.testing.assert_allclose(x, b / 2.0, rtol=1e-15)
+    assert it == 1
+    sets, rho, C = _system(shape)
+    xs = np.linalg.solve(C, b)
+    _, it0, _, _ = O.cg(shape, sets, rho, C @ xs, xs, n_cg=10, eq25=True)
+    assert it0 <= 1
+    xz, itz, _, _ = O.cg(shape, sets, rho, np.zeros(9), np.ones(9), n_cg=10)
+    assert itz == 0 and np.all(xz == 0)
+
+
+# ------------------------------------------------------------ projectors
+def test_projector_worked_examples():
+    g = GOLD
+    np.testing.assert_array_equal(
+        O.project(SetDef("I", "bounds", lo=g["box"]["lo"], hi=g["box"]["hi"]), g["box"]["w"]), g["box"]["y"])
+    pd = g["prox_dist"]
+    assert O.prox_dist([pd["m"]], pd["rho"], [pd["w"]])[0] == pd["y"]
+    for key in ("l1_single", "l1_split"):
+        e = g[key]
+        np.testing.assert_allclose(O.project(SetDef("I", "l1", sigma=e["sigma"]), e["w"]), e["y"], atol=1e-15)
+    e = g["card"]
+    np.testing.assert_array_equal(O.project(SetDef("I", "card", k=e["k"]), e["w"]), e["y"])
+    e = g["l2_scale"]
+    np.testing.assert_allclose(O.project(SetDef("I", "l2", sigma=e["sigma_hi"]), e["w"]), e["y"], rtol=1e-15)
+    np.testing.assert_allclose(
+        O.project(SetDef("I", "annulus", sigma_lo=0.0, sigma_hi=e["sigma_hi"]), e["w"]), e["y"], rtol=1e-15)
+    e = g["annulus_up"]
+    np.testing.assert_allclose(
+        O.project(SetDef("I", "annulus", sigma_lo=e["sigma_lo"], sigma_hi=e["sigma_hi"]), e["w"]),
+        e["y"], rtol=1e-15)
+    # reading L7: annulus at 0 -> sigma_l e_1
+    np.testing.assert_array_equal(O.project(SetDef("I", "annulus", sigma_lo=2.0, sigma_hi=3.0),
+                                            [0.0, 0.0, 0.0]), [2.0, 0.0, 0.0])
+
+
+def _l1_bruteforce(w, sigma):
+    """Euclidean projection onto the l1 ball by KKT support enumeration:
+    for each support S, theta = (sum_S |w| - sigma)/|S|; keep supports with
+    theta >= 0, |w_j| > theta on S and |w_j| <= theta off S."""
+    a = np.abs(w)
+    if a.sum() <= sigma:
+        return w.copy()
+    n = len(w)
+    best = None
+    for r in range(1, n + 1):
+        for S in itertools.combinations(range(n), r):
+            S = list(S)
+            th = (a[S].sum() - sigma) / len(S)
+            off = [j for j in range(n) if j not in S]
+            if th >= 0 and np.all(a[S] > th) and np.all(a[off] <= th):
+                y = np.sign(w) * np.maximum(a - th, 0.0)
+                d = np.linalg.norm(y - w)
+                if best is None or d < best[0]:
+                    best = (d, y)
+    return best[1]
+
+
+def test_l1_ball_bruteforce():
+    r = np.random.default_rng(11)
+    for trial in range(150):
+        n = int(r.integers(1, 11))
+        w = r.normal(size=n) * r.choice([0.1, 1.0, 10.0])
+        if trial % 5 == 0:
+            w = np.round(w)          # ties
+        sigma = float(r.uniform(0, 1.2) * np.abs(w).sum())
+        y = O.project(SetDef("I", "l1", sigma=sigma), w)
+        np.testing.assert_allclose(y, _l1_bruteforce(w, sigma), rtol=1e-12, atol=1e-12)
+        assert np.abs(y).sum() <= sigma * (1 + 1e-12) + 1e-15
+
+
+def test_cardinality_bruteforce():
+    """minimal dropped energy over all C(n,k) supports; ties to lowest index"""
+    r = np.random.default_rng(12)
+    for trial in range(120):
+        n = int(r.integers(1, 11))
+        k = int(r.integers(0, n + 1))
+        w = r.normal(size=n)
+        if trial % 3 == 0:
+            w = np.round(w * 2) / 2
+        y = O.project(SetDef("I", "card", k=k), w)
+        best = min(((w[[j for j in range(n) if j not in S]] ** 2).sum(), S)
+                   for S in itertools.combinations(range(n), k))
+        assert ((w - y) ** 2).sum() == pytest.approx(best[0], abs=1e-14)
+        assert np.count_nonzero(y) <= k
+    # tie convention (reading L6)
+    np.testing.assert_array_equal(O.project(SetDef("I", "card", k=2), [2.0, -2.0, 1.0, 2.0]),
+                                  [2.0, -2.0, 0.0, 0.0])
+
+
+def test_projector_invariants():
+    """idempotence, feasibility, non-expansiveness (convex kinds)"""
+    r = np.random.default_rng(13)
+    sets = [SetDef("I", "bounds", lo=-0.5, hi=0.7), SetDef("I", "l1", sigma=2.0),
+            SetDef("I", "l2", sigma=1.5), SetDef("I", "annulus", sigma_lo=1.0, sigma_hi=2.0),
+            SetDef("I", "card", k=3)]
+    for sd in sets:
+        for _ in range(40):
+            a = r.normal(size=9) * 2
+            b = r.normal(size=9) * 2
+            pa = O.project(sd, a)
+            np.testing.assert_allclose(O.project(sd, pa), pa, rtol=1e-12, atol=1e-14)
+            if sd.kind == "bounds":
+                assert pa.min() >= -0.5 and pa.max() <= 0.7
+            if sd.kind == "l1":
+                assert np.abs(pa).sum() <= 2.0 * (1 + 1e-12)
+            if sd.kind in ("l2", "annulus"):
+                radius = sd.sigma if sd.kind == "l2" else sd.sigma_hi
+                assert np.linalg.norm(pa) <= radius * (1 + 1e-12)
+            if sd.kind == "annulus":
+                assert np.linalg.norm(pa) >= 1.0 * (1 - 1e-12)
+            if sd.kind == "card":
+                assert np.count_nonzero(pa) <= 3
+            if sd.kind in ("bounds", "l1", "l2"):
+                assert np.linalg.norm(pa - O.project(sd, b)) <= np.linalg.norm(a - b) * (1 + 1e-12)
+
+
+def test_feasibility_eq26():
+    e = GOLD["feas_bounds"]
+    assert O.feas(SetDef("I", "bounds", lo=e["lo"], hi=e["hi"]), e["s"]) == pytest.approx(e["r"])
+    # reading L19: ||s|| = 0
+    assert O.feas(SetDef("I", "bounds", lo=-1, hi=1), [0.0, 0.0]) == 0.0
+    assert O.feas(SetDef("I", "bounds", lo=1, hi=2), [0.0, 0.0]) == np.inf
+    assert O.feas(SetDef("I", "annulus", sigma_lo=1, sigma_hi=2), [0.0]) == np.inf
+
+
+# ------------------------------------------------------------ Algorithm 2
+def _alg2(dh, dvh, dg, dv, rho=0.7):
+    z = np.zeros_like(dh)
+    return O.adapt_rho_gamma(dvh, z, dv, z, dh, z, -dg, z, rho)   # y - y0 = -dg
+
+
+def test_alg2_four_branches():
+    """Algorithm 2 case table on constructed vectors whose
+    spectral estimates are known in closed form."""
+    c = GOLD["alg2_constants"]
+    u = np.array([1.0, 2.0, -1.0]); w = np.array([0.5, 0.0, 2.0])
+    perp = np.array([2.0, -1.0, 0.0])               # u . perp = 0 -> corr 0
+    # alpha: dh = 2u, dvh = 3u  -> corr 1, MG = SD = 1.5 -> ahat = 1.5
+    # beta : dg = 4w, dv = 1w   -> corr 1, MG = SD = 0.25 -> bhat = 0.25
+    r, g, br = _alg2(2 * u, 3 * u, 4 * w, 1 * w)
+    assert br == 0
+    assert r == pytest.approx(np.sqrt(1.5 * 0.25), rel=1e-14)
+    assert g == pytest.approx(1 + 2 * np.sqrt(1.5 * 0.25) / (1.5 + 0.25), rel=1e-14)
+    r, g, br = _alg2(2 * u, 3 * u, 4 * w, perp)       # beta corr = w.perp/...
+    assert (br, r, g) == (1, pytest.approx(1.5), c["gamma_alpha_only"])
+    r, g, br = _alg2(2 * u, perp, 4 * w, 1 * w)
+    assert (br, r, g) == (2, pytest.approx(0.25), c["gamma_beta_only"])
+    r, g, br = _alg2(2 * u, perp, 4 * w, np.zeros(3), rho=0.7)   # zero norm -> fails (L17)
+    assert (br, r, g) == (3, 0.7, c["gamma_none"])
+
+
+def test_alg2_sd_branch_and_gamma_two():
+    # dh = (1,0), dvh = (1,1): hv = 1, hh = 1, |dvh|^2 = 2 -> corr = 0.707,
+    # MG = 1, SD = 2, 2 MG > SD fails -> ahat = SD - MG/2 = 1.5
+    z2 = np.zeros(2)
+    r, g, br = _alg2(np.array([1.0, 0]), np.array([1.0, 1.0]), z2, z2)
+    assert br == 1 and r == pytest.approx(1.5)
+    # equal estimates give gamma = 1 + 2a/(2a) = 2 (clamped to 2 - 1e-3 by L15 in PARSDMM)
+    u = np.array([1.0, -2.0])
+    r, g, br = _alg2(u, 2 * u, u, 2 * u)
+    assert br == 0 and g == pytest.approx(2.0, abs=1e-15) and r == pytest.approx(2.0)
+    # correlation threshold eps_corr = 0.3: corr 0.25 fails, 0.35 passes
+    for corr, ok in ((0.25, False), (0.35, True)):
+        dh = np.array([1.0, 0.0]); dvh = np.array([corr, np.sqrt(1 - corr ** 2)])
+        _, _, br = _alg2(dh, dvh, z2, z2)
+        assert (br == 1) == ok
+
+
+# ------------------------------------------------------------ PARSDMM end to end
+def test_parsdmm_single_box_is_clamp():
+    """p = 1, bounds with A = I -> x = clamp(m) (within 1e-4)"""
+    m = tiny_model(3, (8, 8))
+    sd = SetDef("I", "bounds", lo=2000.0, hi=3500.0)
+    r = O.parsdmm((8, 8), [sd], m)
+    assert r.converged
+    assert O.relres(r.x, np.clip(m, 2000, 3500).ravel()) < 1e-4
+
+
+def _box_mono_exact(m, lo, hi):
+    """projection onto {lo <= x <= hi} with nondecreasing columns in z:
+    clip of the per-column isotonic regression (textbook; scipy routine)"""
+    out = np.empty_like(m)
+    for j in range(m.shape[1]):
+        out[:, j] = np.clip(so.isotonic_regression(m[:, j]).x, lo, hi)
+    return out
+
+
+@pytest.mark.parametrize("shape,seed", [((16, 16), 21), ((64, 64), 0)])
+def test_parsdmm_box_monotone_vs_isotonic(shape, seed):
+    m = tiny_model(seed, shape) if seed else __import__("sip_inputs").c1_model(0, shape)
+    sets = [SetDef("I", "bounds", lo=1500.0, hi=4500.0), SetDef("DZ", "bounds", lo=0.0, hi=INF)]
+    ref = _box_mono_exact(m, 1500.0, 4500.0)
+    r = O.parsdmm(shape, sets, m)
+    assert r.converged and r.r_feas.max() < 1e-3
+    # production stop (Eq. 28, eps_evol = 1e-2): accurate on the eps_evol scale
+    assert O.relres(r.x, ref) < 1e-2
+    t = O.parsdmm(shape, sets, m, eps_evol=1e-9, eps_feas=1e-9, n_cg=200, max_iter=20000)
+    assert O.relres(t.x, ref) < 1e-6
+
+
+def _dykstra(m, projs, iters=20000):
+    """Algorithm 4: parallel Dykstra with equal weights"""
+    p = len(projs)
+    x = m.copy()
+    v = [m.copy() for _ in range(p)]
+    for _ in range(iters):
+        y = [P(vi) for P, vi in zip(projs, v)]
+        x_new = sum(y) / p
+        v = [x_new + vi - yi for vi, yi in zip(v, y)]
+        if np.linalg.norm(x_new - x) <= 1e-14 * np.linalg.norm(x):
+            x = x_new
+            break
+        x = x_new
+    return x
+
+
+def test_parsdmm_vs_dykstra_box_mono_l2():
+    """box ∩ vertical monotonicity ∩ l2-ball around a center: every set has an
+    exact projector, so Algorithm 4 gives the reference projection"""
+    shape = (10, 6)
+    m = tiny_model(31, shape)
+    c0 = np.full(shape, 3000.0)
+    rad = 0.6 * np.linalg.norm(m - c0)
+    projs = [
+        lambda z: np.clip(z, 1500.0, 4500.0),
+        lambda z: np.column_stack([so.isotonic_regression(z[:, j]).x for j in range(shape[1])]),
+        lambda z: c0 + (z - c0) * min(1.0, rad / np.linalg.norm(z - c0)),
+    ]
+    ref = _dykstra(m, projs)
+    # PARSDMM projects m - c0 (translation invariance of the l2 ball)
+    sets = [SetDef("I", "bounds", lo=1500.0 - 3000.0, hi=4500.0 - 3000.0),
+            SetDef("DZ", "bounds", lo=0.0, hi=INF), SetDef("I", "l2", sigma=rad)]
+    t = O.parsdmm(shape, sets, m - c0, eps_evol=1e-10, eps_feas=1e-10, n_cg=200, max_iter=50000)
+    assert O.relres(t.x + c0.ravel(), ref) < 1e-6
+
+
+def _slsqp_tv(m, shape, sigma, lo, hi, mono=True):
+    """exact projection onto bounds ∩ {||TV x||_1 <= sigma} ∩ {D_z x >= 0}
+    by scipy SLSQP on the lifted QP (-t <= Dx <= t, sum t <= sigma)"""
+    D = dense_of(shape, SetDef("TV", "l1"))
+    Dz = dense_of(shape, SetDef("DZ", "bounds"))
+    N, M = D.shape[1], D.shape[0]
+    m = m.ravel()
+
+    def f(z):
+        return 0.5 * np.sum((z[:N] - m) ** 2)
+
+    def fg(z):
+        g = np.zeros_like(z); g[:N] = z[:N] - m
+        return g
+
+    A_ub = [np.hstack([D, -np.eye(M)]), np.hstack([-D, -np.eye(M)]),
+            np.hstack([np.zeros((1, N)), np.ones((1, M))])]
+    b_ub = [np.zeros(M), np.zeros(M), [sigma]]
+    if mono:
+        A_ub.append(np.hstack([-Dz, np.zeros((Dz.shape[0], M))])); b_ub.append(np.zeros(Dz.shape[0]))
+    A = np.vstack(A_ub); b = np.concatenate(b_ub)
+    cons = [{"type": "ineq", "fun": lambda z: b - A @ z, "jac": lambda z: -A}]
+    bounds = [(lo, hi)] * N + [(0, None)] * M
+    z0 = np.concatenate([np.clip(m, lo, hi), np.abs(D @ m)])
+    res = so.minimize(f, z0, jac=fg, constraints=cons, bounds=bounds, method="SLSQP",
+                      options=dict(maxiter=2000, ftol=1e-16))
+    return res.x[:N]
+
+
+@pytest.mark.parametrize("shape,seed", [((4, 4), 41), ((5, 4), 42), ((3, 3, 3), 43)])
+def test_parsdmm_tv_convex_vs_qp(shape, seed):
+    """bounds ∩ TV-l1 ∩ monotonicity (the C1/C4 set combination) on
+    tiny grids: the unique projection from a QP solver"""
+    m = tiny_model(seed, shape)
+    D = dense_of(shape, SetDef("TV", "l1"))
+    sigma = 0.5 * np.abs(D @ m.ravel()).sum()
+    ref = _slsqp_tv(m, shape, sigma, 1500.0, 4500.0)
+    sets = [SetDef("I", "bounds", lo=1500.0, hi=4500.0), SetDef("TV", "l1", sigma=sigma),
+            SetDef("DZ", "bounds", lo=0.0, hi=INF)]
+    t = O.parsdmm(shape, sets, m, eps_evol=1e-9, eps_feas=1e-9, n_cg=100, max_iter=100000)
+    assert O.relres(t.x, ref) < 1e-5
+    r = O.parsdmm(shape, sets, m)
+    assert O.relres(r.x, ref) < 2e-2
+
+
+# ------------------------------------------------------------ multilevel
+def test_multilevel_transfers_worked_examples():
+    e = GOLD["restrict_2x4"]
+    np.testing.assert_array_equal(O.restrict((2, 4), np.array(e["f"], float)), np.array(e["c"], float))
+    e = GOLD["interp_2x2_to_3x3"]
+    np.testing.assert_allclose(O.interp(np.array(e["c"], float), (3, 3)), np.array(e["f"], float))
+    c = np.full((3, 4, 5), 2.5)
+    np.testing.assert_allclose(O.interp(c, (5, 7, 9)), 2.5, rtol=1e-15)
+    np.testing.assert_allclose(O.restrict((4, 6, 8), np.full((4, 6, 8), 1.25)), 1.25)
+    # align-corners: corners map to corners
+    r = np.random.default_rng(2).normal(size=(3, 4))
+    f = O.interp(r, (5, 7))
+    np.testing.assert_allclose(f[::2, ::2], r)
+
+
+def test_multilevel_one_level_is_single_level():
+    p = __import__("sip_inputs").tiny(105, (8, 8), ("bounds", "l1", "slope"))
+    x1, st, logs = O.parsdmm_multilevel(p.shape, p.sets, p.m, 1, **p.options)
+    r = O.parsdmm(p.shape, p.sets, p.m, **p.options)
+    # level-1-only multilevel starts from y = v = 0 -- compare with that init
+    r0 = O.parsdmm(p.shape, p.sets, p.m, init=dict(y=[np.zeros(O.op_len(p.shape, s)) for s in p.sets]
+                                                    + [np.zeros(p.N)],
+                                                    v=None), **p.options)
+    np.testing.assert_array_equal(x1, r0.x)
+    assert logs[0].iterations == r0.iterations
+    assert r.iterations > 0
+
+
+def test_multilevel_converges_and_is_cheaper():
+    """P:533 "the multilevel strategy is much faster": fewer fine-grid CG
+    iterations than single level on a 64x64 convex instance"""
+    from sip_inputs import c1_model
+    m = c1_model(0, (64, 64))
+    sets = [SetDef("I", "bounds", lo=1500.0, hi=4500.0), SetDef("DZ", "bounds", lo=0.0, hi=INF)]
+    x, st, logs = O.parsdmm_multilevel((64, 64), sets, m, 3)
+    single = O.parsdmm((64, 64), sets, m)
+    assert logs[0].converged
+    assert O.relres(x, _box_mono_exact(m, 1500.0, 4500.0)) < 1e-2
+    assert logs[0].cg_total < single.cg_total
