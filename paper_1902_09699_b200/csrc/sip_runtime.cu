@@ -1,0 +1,1160 @@
+// sip_runtime.cu -- host runtime and C ABI (include/sip.h) of the B200 PARSDMM
+// hot path (arXiv 1902.09699).  One Engine<T> per grid level owns the device
+// state; the iteration (Algorithm 1) is enqueued as a fixed kernel sequence
+// whose decisions live in device memory (Ctrl), captured once into a CUDA
+// graph of `graph_iters` iterations and replayed; the host reads one flag per
+// graph launch (lagged by one launch) to learn that Eq. 28 stopped the run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sip.h"
+#include "sip_aux_kernels.cuh"
+
+using namespace sip;
+
+namespace {
+
+struct SipError {
+  sip_status code;
+  std::string msg;
+};
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw SipError{SIP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)};   \
+  } while (0)
+
+struct HostSet {
+  sip_op op;
+  sip_set_type type;
+  sip_set_params prm;
+  std::vector<double> lo_vec, hi_vec;   // compact layout
+  std::vector<double> kernel;
+  int kh = 0, kw = 0;
+  std::vector<uint8_t> mask;
+  int64_t M = 0;
+  int zero_in = 1;
+};
+
+struct Options {
+  double rho0 = 1e-2, gamma0 = 1.0, eps_corr = 0.3, rho_ratio_cap = 1e3, gamma_max = 2.0 - 1e-3;
+  int n_cg = 10, eq25 = 1, fixed_work = 0, adapt_every = 2, check_every = 5;
+  double eps_evol = -1.0;       // < 0: 10 * tol
+  double cg_tol_floor = -1.0;   // < 0: 10 * eps(dtype)
+  int warm_start = 0, graph_iters = 5;
+};
+
+inline int nblk_of(sip_op op, int ndim) {
+  return op == SIP_OP_TV ? (ndim == 3 ? 3 : 2) : 1;
+}
+inline void prims_of(sip_op op, int ndim, int* pr) {
+  switch (op) {
+    case SIP_OP_IDENTITY: pr[0] = PRIM_I; break;
+    case SIP_OP_DZ: pr[0] = PRIM_Z; break;
+    case SIP_OP_DY: pr[0] = PRIM_Y; break;
+    case SIP_OP_DX: pr[0] = PRIM_X; break;
+    case SIP_OP_TV:
+      pr[0] = PRIM_Z;
+      if (ndim == 3) { pr[1] = PRIM_Y; pr[2] = PRIM_X; } else { pr[1] = PRIM_X; }
+      break;
+    default: pr[0] = PRIM_F;
+  }
+}
+inline int kind_of(sip_set_type t) {
+  switch (t) {
+    case SIP_SET_BOUNDS: return K_BOUNDS;
+    case SIP_SET_L1_BALL: return K_L1;
+    case SIP_SET_L2_BALL: return K_L2;
+    case SIP_SET_ANNULUS: return K_ANN;
+    default: return K_CARD;
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------------------ engine
+struct EngineBase {
+  virtual ~EngineBase() {}
+};
+
+template <class T>
+struct Engine : EngineBase {
+  // configuration
+  int ndim;
+  int nz, ny, nx;
+  double h[3];
+  cudaStream_t stream;
+  int nsm = 148;
+  const std::vector<HostSet>* sets;
+  int p, P;
+  // device state
+  Prob<T> Pr;
+  std::vector<void*> allocs;
+  Ctrl* d_ctrl = nullptr;
+  Ctrl hc;
+  int* d_fmap = nullptr;      // blur mask compact index map
+  int* d_log_cg = nullptr; int* d_log_br = nullptr;
+  double* d_log_rho = nullptr; double* d_log_gam = nullptr; double* d_log_feas = nullptr;
+  double* d_log_evol = nullptr;
+  int log_cap = 0;
+  int* h_flag = nullptr;       // pinned: stopped flags of the last launches
+  cudaEvent_t ev_flag[2];
+  cudaEvent_t ev0, ev1;
+  // launch geometry
+  int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1;
+  size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0;
+  // graph
+  cudaGraphExec_t gexec = nullptr;
+  int g_iters = 0, g_ncg = -1;
+  long long launches = 0;       // kernels enqueued by the last project()
+  long long graph_kernels = 0;  // kernels in one captured graph
+  int last_k = 0;               // Ctrl.k after the last run
+  bool ran = false;
+  bool scratch_used = false;    // state buffers overwritten by a step-level call
+
+  ~Engine() override {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    for (void* a : allocs) cudaFree(a);
+    if (h_flag) cudaFreeHost(h_flag);
+    cudaEventDestroy(ev_flag[0]); cudaEventDestroy(ev_flag[1]);
+    cudaEventDestroy(ev0); cudaEventDestroy(ev1);
+  }
+
+  template <class Q>
+  Q* dalloc(size_t n) {
+    void* p_ = nullptr;
+    cudaError_t e = cudaMalloc(&p_, std::max<size_t>(n, 1) * sizeof(Q));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw SipError{SIP_ERR_OOM, "cudaMalloc of " + std::to_string(n * sizeof(Q)) + " bytes failed"};
+    }
+    allocs.push_back(p_);
+    return (Q*)p_;
+  }
+
+  // field of nblk blocks; returns pointer to block 0's first interior element
+  T* field(int nblk) {
+    T* base = dalloc<T>((size_t)nblk * Pr.g.ld);
+    CU(cudaMemsetAsync(base, 0, (size_t)nblk * Pr.g.ld * sizeof(T), stream));
+    return base + (size_t)GHOST * Pr.g.plane;
+  }
+
+  void setup(int ndim_, int nz_, int ny_, int nx_, const double* h_, cudaStream_t st,
+             const std::vector<HostSet>& s) {
+    ndim = ndim_; nz = nz_; ny = ny_; nx = nx_;
+    h[0] = h_[0]; h[1] = h_[1]; h[2] = h_[2];
+    stream = st;
+    sets = &s;
+    p = (int)s.size();
+    P = p + 1;
+    int dev;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    memset(&Pr, 0, sizeof(Pr));
+    Geo& g = Pr.g;
+    g.ndim = ndim; g.nz = nz; g.ny = ny; g.nx = nx; g.nz_g = nz; g.z0 = 0;
+    g.plane = ny * nx;
+    g.N = nz * g.plane;
+    g.ld = (int64_t)g.N + 2 * GHOST * (int64_t)g.plane;
+    g.ihz = 1.0 / h[0]; g.ihy = 1.0 / h[1]; g.ihx = 1.0 / h[2];
+    g.dplane.init((uint32_t)g.plane);
+    g.dnx.init((uint32_t)g.nx);
+    Pr.P = P; Pr.p = p;
+    Pr.rounds = KeyT<T>::ROUNDS;
+    Pr.ntiles_pb = (g.N + BLOCK - 1) / BLOCK;
+    int njobs = 0;
+    for (int i = 0; i < P; ++i) {
+      SetD<T>& S = Pr.set[i];
+      if (i == p) {
+        S.kind = K_DIST; S.nblk = 1; S.prim[0] = PRIM_I;
+      } else {
+        const HostSet& hs = s[i];
+        S.kind = kind_of(hs.type);
+        S.nblk = nblk_of(hs.op, ndim);
+        prims_of(hs.op, ndim, S.prim);
+        S.lo = hs.prm.lo; S.hi = hs.prm.hi;
+        if (hs.op == SIP_OP_BLUR_MASK) {
+          g.kh = hs.kh; g.kw = hs.kw;
+          for (int t = 0; t < hs.kh * hs.kw; ++t) Pr.taps[t] = hs.kernel[t];
+        }
+      }
+      S.global = (S.kind == K_L1 || S.kind == K_L2 || S.kind == K_ANN || S.kind == K_CARD);
+      S.job = S.sjob = -1;
+      if (S.kind == K_L1 || S.kind == K_CARD) { S.job = njobs++; S.sjob = njobs++; }
+      for (int b = 0; b < S.nblk; ++b) Pr.has[S.prim[b]] = 1;
+      if (S.global) Pr.nglob++;
+    }
+    // blur mask + compact map
+    for (int i = 0; i < p; ++i)
+      if (s[i].op == SIP_OP_BLUR_MASK) {
+        uint8_t* dm = dalloc<uint8_t>(g.N);
+        CU(cudaMemcpyAsync(dm, s[i].mask.data(), g.N, cudaMemcpyHostToDevice, stream));
+        g.mask = dm;
+        std::vector<int> fm(g.N);
+        int c = 0;
+        for (int q = 0; q < g.N; ++q) fm[q] = s[i].mask[q] ? c++ : -1;
+        d_fmap = dalloc<int>(g.N);
+        CU(cudaMemcpyAsync(d_fmap, fm.data(), g.N * sizeof(int), cudaMemcpyHostToDevice, stream));
+        CU(cudaStreamSynchronize(stream));
+        Pr.set[i].first_real = 0;
+        for (int q = 0; q < g.N; ++q) if (s[i].mask[q]) { Pr.set[i].first_real = q; break; }
+      }
+    // fields
+    for (int i = 0; i < P; ++i) {
+      SetD<T>& S = Pr.set[i];
+      S.y[0] = field(S.nblk); S.y[1] = field(S.nblk);
+      S.v[0] = field(S.nblk); S.v[1] = field(S.nblk);
+      S.vh0 = field(S.nblk);
+      S.w = S.global ? field(S.nblk) : nullptr;
+      S.s = (S.kind == K_L1 || S.kind == K_CARD) ? field(S.nblk) : nullptr;
+      if (i < p && (!s[i].lo_vec.empty() || !s[i].hi_vec.empty())) {
+        if (!s[i].lo_vec.empty()) S.lo_vec = upload_compact(i, s[i].lo_vec);
+        if (!s[i].hi_vec.empty()) S.hi_vec = upload_compact(i, s[i].hi_vec);
+      }
+    }
+    Pr.x = field(1);
+    Pr.m = field(1);
+    Pr.r = field(1);
+    Pr.pb[0] = field(1); Pr.pb[1] = field(1);
+    Pr.tb = Pr.has[PRIM_F] ? field(1) : nullptr;
+    for (int j = 0; j < HIST_S; ++j) Pr.hist[j] = field(1);
+    Pr.xs[0] = field(1); Pr.xs[1] = field(1);
+    // launch geometry
+    const int tiles = Pr.ntiles_pb;
+    g_pts = std::max(1, std::min(tiles, nsm * 8));
+    g_sel = std::max(1, std::min(tiles, nsm * 4));
+    g_p2 = std::max(1, std::min(tiles * 3, nsm * 8));
+    g_small = std::max(1, std::min(tiles, nsm * 4));
+    const int nv1 = P * NSLOT + NEVOL;
+    smem_p1 = (size_t)NWARP * nv1 * sizeof(double);
+    smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
+    smem_init = (size_t)NWARP * P * 2 * sizeof(double);
+    const int gmax = std::max(std::max(g_pts, g_sel), g_p2);
+    Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
+    Pr.counter = dalloc<unsigned>(1);
+    CU(cudaMemsetAsync(Pr.counter, 0, sizeof(unsigned), stream));
+    Pr.gh_cnt = dalloc<unsigned>((size_t)MAXJOBS * NBUCK);
+    Pr.gh_s0 = dalloc<unsigned long long>((size_t)MAXJOBS * NBUCK);
+    Pr.gh_s1 = dalloc<unsigned long long>((size_t)MAXJOBS * NBUCK);
+    CU(cudaMemsetAsync(Pr.gh_cnt, 0, sizeof(unsigned) * MAXJOBS * NBUCK, stream));
+    CU(cudaMemsetAsync(Pr.gh_s0, 0, sizeof(unsigned long long) * MAXJOBS * NBUCK, stream));
+    CU(cudaMemsetAsync(Pr.gh_s1, 0, sizeof(unsigned long long) * MAXJOBS * NBUCK, stream));
+    Pr.ntiles_max = 3 * tiles;
+    Pr.tiecnt = dalloc<int>((size_t)std::max(njobs, 1) * Pr.ntiles_max);
+    d_ctrl = dalloc<Ctrl>(1);
+    Pr.ctrl = d_ctrl;
+    CU(cudaMallocHost(&h_flag, 2 * sizeof(int)));
+    CU(cudaEventCreateWithFlags(&ev_flag[0], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ev_flag[1], cudaEventDisableTiming));
+    CU(cudaEventCreate(&ev0));
+    CU(cudaEventCreate(&ev1));
+    CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    memset(&hc, 0, sizeof(hc));
+    hc.njobs = njobs;
+    for (int i = 0; i < P; ++i) {
+      const SetD<T>& S = Pr.set[i];
+      if (S.job >= 0) {
+        hc.job[S.job].kind = S.kind; hc.job[S.job].set = i; hc.job[S.job].on_s = 0;
+        hc.job[S.sjob].kind = S.kind; hc.job[S.sjob].set = i; hc.job[S.sjob].on_s = 1;
+      }
+    }
+    CU(cudaStreamSynchronize(stream));
+  }
+
+  // per-entry bounds: compact (host, fp64) -> padded device field
+  const T* upload_compact(int i, const std::vector<double>& v) {
+    const SetD<T>& S = Pr.set[i];
+    T* f = field(S.nblk);
+    double* tmp = nullptr;
+    CU(cudaMalloc(&tmp, v.size() * sizeof(double)));
+    CU(cudaMemcpyAsync(tmp, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+    long long boff = 0;
+    for (int b = 0; b < S.nblk; ++b) {
+      k_pack<T, double><<<g_small_(), BLOCK, 0, stream>>>(Pr.g, S.prim[b], d_fmap, boff,
+                                                         f + (int64_t)b * Pr.g.ld, tmp, 1);
+      boff += block_len(S.prim[b]);
+    }
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(stream));
+    cudaFree(tmp);
+    return f;
+  }
+  int g_small_() const { return std::max(1, std::min((Pr.g.N + BLOCK - 1) / BLOCK, nsm * 4)); }
+
+  long long block_len(int prim) const {
+    const Geo& g = Pr.g;
+    switch (prim) {
+      case PRIM_I: return g.N;
+      case PRIM_Z: return (long long)(g.nz - 1) * g.plane;
+      case PRIM_Y: return (long long)g.nz * (g.ny - 1) * g.nx;
+      case PRIM_X: return (long long)g.nz * g.ny * (g.nx - 1);
+      default: {
+        long long c = 0;
+        for (int i = 0; i < p; ++i)
+          if ((*sets)[i].op == SIP_OP_BLUR_MASK) { c = (*sets)[i].M; break; }
+        return c;
+      }
+    }
+  }
+  long long set_len(int i) const {
+    long long c = 0;
+    for (int b = 0; b < Pr.set[i].nblk; ++b) c += block_len(Pr.set[i].prim[b]);
+    return c;
+  }
+
+  // ---- iteration enqueue ------------------------------------------------
+  void enqueue_iteration(int n_cg) {
+    const Geo& g = Pr.g;
+    (void)g;
+    if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 0, 0); ++launches; }
+    k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr); ++launches;
+    for (int j = 0; j < n_cg; ++j) {
+      if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 1, j); ++launches; }
+      k_cg1<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches;
+      k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches;
+    }
+    k_pass1<T><<<g_pts, BLOCK, smem_p1, stream>>>(Pr); ++launches;
+    if (hc.njobs > 0) {
+      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
+        k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r); ++launches;
+      }
+      bool card = false;
+      for (int i = 0; i < p; ++i) if (Pr.set[i].kind == K_CARD) card = true;
+      if (card) { k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr); ++launches; }
+    }
+    if (Pr.nglob > 0) { k_pass2<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); ++launches; }
+    k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches;
+  }
+
+  void ensure_graph(int iters, int n_cg) {
+    if (gexec && g_iters == iters && g_ncg == n_cg) return;
+    if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+    cudaGraph_t graph;
+    long long before = launches;
+    CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) enqueue_iteration(n_cg);
+    cudaError_t e = cudaStreamEndCapture(stream, &graph);
+    if (e != cudaSuccess) throw SipError{SIP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e)};
+    graph_kernels = launches - before;
+    launches = before;
+    CU(cudaGraphInstantiate(&gexec, graph, 0));
+    cudaGraphDestroy(graph);
+    g_iters = iters;
+    g_ncg = n_cg;
+  }
+
+  void ensure_log(int max_iter) {
+    if (log_cap >= max_iter) return;
+    log_cap = max_iter;
+    d_log_cg = dalloc<int>(max_iter);
+    d_log_br = dalloc<int>((size_t)max_iter * P);
+    d_log_rho = dalloc<double>((size_t)max_iter * P);
+    d_log_gam = dalloc<double>((size_t)max_iter * P);
+    d_log_feas = dalloc<double>((size_t)max_iter * std::max(p, 1));
+    d_log_evol = dalloc<double>(max_iter);
+  }
+
+  // ---- control block -----------------------------------------------------
+  void fill_ctrl(const Options& o, int max_iter, double eps_feas, double eps_evol, double floor_,
+                 const double* rho_in, const double* gamma_in) {
+    Ctrl c = hc;   // keeps job kinds/sets
+    c.k = 1; c.stopped = 0; c.converged = 0; c.first_adapt_done = 0; c.adapt_calls = 0;
+    c.hist_head = 0; c.hist_count = 1; c.breakdown = 0; c.numeric_err = 0; c.zero_x = 0;
+    c.cg_j = 0; c.cg_active = 0; c.cg_count = 0; c.cg_total = 0;
+    c.P = P; c.p = p;
+    c.opt.n_cg = o.n_cg; c.opt.eq25 = o.eq25; c.opt.fixed_work = o.fixed_work;
+    c.opt.adapt_every = o.adapt_every; c.opt.check_every = o.check_every; c.opt.max_iter = max_iter;
+    c.opt.eps_evol = eps_evol; c.opt.eps_feas = eps_feas; c.opt.eps_corr = o.eps_corr;
+    c.opt.rho_ratio_cap = o.rho_ratio_cap; c.opt.gamma_max = o.gamma_max; c.opt.cg_tol_floor = floor_;
+    for (int i = 0; i < P; ++i) {
+      c.rho[i] = rho_in ? rho_in[i] : o.rho0;
+      c.gamma[i] = gamma_in ? gamma_in[i] : o.gamma0;
+    }
+    for (int i = 0; i < p; ++i) {
+      const HostSet& hs = (*sets)[i];
+      c.u_sigma[i] = hs.prm.sigma;
+      c.u_sig_lo[i] = hs.prm.sigma_lo;
+      c.u_sig_hi[i] = hs.prm.sigma_hi;
+      c.u_kfrac[i] = hs.prm.k_frac;
+      c.u_k[i] = hs.prm.k;
+      c.rel[i] = hs.prm.relative;
+      c.zin[i] = hs.zero_in;
+      c.mreal[i] = hs.M;
+    }
+    c.mreal[p] = Pr.g.N;
+    make_coeffs(Pr, c.rho, &c.cI, &c.cz, &c.cy, &c.cx, &c.cF);
+    c.log_cg = d_log_cg; c.log_branch = d_log_br; c.log_rho = d_log_rho; c.log_gamma = d_log_gam;
+    c.log_feas = d_log_feas; c.log_evol = d_log_evol; c.log_len = log_cap;
+    hc = c;
+    CU(cudaMemcpyAsync(d_ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, stream));
+  }
+
+  void fill_logs_nan(int max_iter) {
+    k_fill<int><<<g_small_(), BLOCK, 0, stream>>>(d_log_br, (long long)max_iter * P, -1);
+    k_fill<double><<<g_small_(), BLOCK, 0, stream>>>(d_log_feas, (long long)max_iter * std::max(p, 1), NAN);
+    k_fill<double><<<g_small_(), BLOCK, 0, stream>>>(d_log_evol, (long long)max_iter, NAN);
+    k_fill<int><<<g_small_(), BLOCK, 0, stream>>>(d_log_cg, (long long)max_iter, 0);
+  }
+
+  // init_yv: 1 = y_i = A_i m, v_i = 0; 0 = keep Y[1]/V[1] (prolonged / warm)
+  void run_init(int init_x, int init_yv) {
+    k_init<T><<<g_pts, BLOCK, smem_init, stream>>>(Pr, init_x, init_yv);
+    ++launches;
+  }
+
+  // replay graphs until the device says stopped (lagged poll)
+  void run_iterations(int max_iter, int gi, int n_cg) {
+    if (gi <= 0) {
+      // no graph: launch iteration by iteration, poll every check_every
+      for (int it = 0; it < max_iter; ++it) {
+        enqueue_iteration(n_cg);
+        if ((it + 1) % std::max(1, hc.opt.check_every) == 0 || it + 1 == max_iter) {
+          CU(cudaMemcpyAsync(h_flag, &d_ctrl->stopped, sizeof(int), cudaMemcpyDeviceToHost, stream));
+          CU(cudaStreamSynchronize(stream));
+          if (h_flag[0]) break;
+        }
+      }
+      return;
+    }
+    ensure_graph(gi, n_cg);
+    const int nlaunch = (max_iter + gi - 1) / gi;
+    const bool poll = !hc.opt.fixed_work;
+    for (int l = 0; l < nlaunch; ++l) {
+      CU(cudaGraphLaunch(gexec, stream));
+      launches += graph_kernels;
+      if (!poll) continue;
+      CU(cudaMemcpyAsync(&h_flag[l & 1], &d_ctrl->stopped, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      CU(cudaEventRecord(ev_flag[l & 1], stream));
+      if (l >= 1) {
+        CU(cudaEventSynchronize(ev_flag[(l - 1) & 1]));
+        if (h_flag[(l - 1) & 1]) break;
+      }
+    }
+  }
+
+  void read_ctrl() {
+    CU(cudaMemcpyAsync(&hc, d_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream));
+    CU(cudaStreamSynchronize(stream));
+  }
+
+  // full single-level solve on the engine's m; x result stays in Pr.x
+  void solve(const Options& o, int max_iter, double eps_feas, double eps_evol, int init_x, int init_yv,
+             const double* rho_in, const double* gamma_in) {
+    ensure_log(max_iter);
+    const double floor_ = o.cg_tol_floor > 0 ? o.cg_tol_floor
+                                             : 10.0 * (sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON);
+    fill_ctrl(o, max_iter, eps_feas, eps_evol, floor_, rho_in, gamma_in);
+    fill_logs_nan(max_iter);
+    run_init(init_x, init_yv);
+    run_iterations(max_iter, o.graph_iters, o.n_cg);
+    read_ctrl();
+    ran = true;
+    scratch_used = false;
+  }
+
+  void fill_result(sip_result* r, float ms) {
+    if (!r) return;
+    memset(r, 0, sizeof(*r));
+    r->iterations = std::min(hc.k, hc.opt.max_iter);
+    r->cg_iterations = hc.cg_total;
+    r->converged = hc.converged;
+    r->breakdown = hc.breakdown;
+    r->r_evol = hc.r_evol;
+    r->ms = ms;
+    for (int i = 0; i < p; ++i) r->r_feas[i] = hc.r_feas[i];
+    for (int i = 0; i < P; ++i) { r->rho[i] = hc.rho[i]; r->gamma[i] = hc.gamma[i]; }
+  }
+
+  // device field block (of the final parity) of set i
+  T* final_field(int i, int which) {
+    // the last iteration k wrote parity (k+1)&1; if stopped by max_iter the
+    // control kernel advanced k past max_iter (k = max_iter + 1)
+    const int kk = std::min(hc.k, hc.opt.max_iter);
+    const int par = (kk + 1) & 1;
+    return which == 0 ? Pr.set[i].y[par] : Pr.set[i].v[par];
+  }
+
+  // make the final y/v the k = 1 read buffers (warm start / multilevel source)
+  void rotate_final_to_read() {
+    const int kk = std::min(hc.k, hc.opt.max_iter);
+    const int par = (kk + 1) & 1;
+    if (par == 1) return;
+    for (int i = 0; i < P; ++i) {
+      SetD<T>& S = Pr.set[i];
+      std::swap(S.y[0], S.y[1]);
+      std::swap(S.v[0], S.v[1]);
+    }
+    if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }   // params changed
+  }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ grid
+struct sip_grid_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  sip_dtype dtype = SIP_F32;
+  int ndim = 2;
+  int64_t n[3] = {1, 1, 1};   // nz, ny, nx
+  double h[3] = {1, 1, 1};
+  int nranks = 1, rank = 0;
+  std::vector<HostSet> sets;
+  Options opt;
+  std::string err;
+  std::unique_ptr<EngineBase> eng;                 // finest level
+  std::vector<std::unique_ptr<EngineBase>> levels; // multilevel (index 0 = finest)
+  bool have_m = false;
+  long long last_launches = 0;
+};
+
+namespace {
+
+template <class T>
+Engine<T>* engine_of(sip_grid g) {
+  if (!g->eng) {
+    auto e = std::make_unique<Engine<T>>();
+    e->setup(g->ndim, (int)g->n[0], (int)g->n[1], (int)g->n[2], g->h, g->stream, g->sets);
+    g->eng = std::move(e);
+  }
+  return static_cast<Engine<T>*>(g->eng.get());
+}
+
+template <class T>
+void copy_in(Engine<T>* e, const void* src, T* dst, size_t n) {
+  CU(cudaMemcpyAsync(dst, src, n * sizeof(T), is_device_ptr(src) ? cudaMemcpyDeviceToDevice
+                                                                  : cudaMemcpyHostToDevice, e->stream));
+}
+template <class T>
+void copy_out(Engine<T>* e, const T* src, void* dst, size_t n) {
+  CU(cudaMemcpyAsync(dst, src, n * sizeof(T), is_device_ptr(dst) ? cudaMemcpyDeviceToDevice
+                                                                  : cudaMemcpyDeviceToHost, e->stream));
+}
+
+double eps_evol_of(const sip_grid g, double tol) {
+  if (g->opt.eps_evol > 0) return g->opt.eps_evol;
+  return tol > 0 ? 10.0 * tol : 1e-2;
+}
+
+template <class T>
+sip_status project_T(sip_grid g, const void* m, void* x, int max_iter, double tol, sip_result* res) {
+  Engine<T>* e = engine_of<T>(g);
+  const size_t N = (size_t)e->Pr.g.N;
+  const double eps_feas = tol > 0 ? tol : 1e-3;
+  e->launches = 0;
+  CU(cudaEventRecord(e->ev0, e->stream));
+  copy_in(e, m, const_cast<T*>(e->Pr.m), N);
+  const bool warm = g->opt.warm_start && e->ran && !e->scratch_used;
+  if (warm) {
+    e->rotate_final_to_read();
+    std::vector<double> rho(e->hc.rho, e->hc.rho + e->P), gam(e->hc.gamma, e->hc.gamma + e->P);
+    e->solve(g->opt, max_iter, eps_feas, eps_evol_of(g, tol), 0, 0, rho.data(), gam.data());
+  } else {
+    e->solve(g->opt, max_iter, eps_feas, eps_evol_of(g, tol), 1, 1, nullptr, nullptr);
+  }
+  copy_out(e, e->Pr.x, x, N);
+  CU(cudaEventRecord(e->ev1, e->stream));
+  CU(cudaEventSynchronize(e->ev1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  e->fill_result(res, ms);
+  g->have_m = true;
+  g->last_launches = e->launches;
+  if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, "NaN/Inf in the PARSDMM state"};
+  return e->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
+}
+
+template <class T>
+sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int max_iter, double tol,
+                        sip_result* per_level) {
+  // level grids: each axis halves (y stays 1 in 2D), h doubles (reading L2)
+  if ((int)g->levels.size() != n_levels) {
+    g->levels.clear();
+    for (int l = 0; l < n_levels; ++l) {
+      auto e = std::make_unique<Engine<T>>();
+      const int f = 1 << l;
+      double hl[3] = {g->h[0] * f, g->ndim == 3 ? g->h[1] * f : 1.0, g->h[2] * f};
+      e->setup(g->ndim, (int)(g->n[0] / f), g->ndim == 3 ? (int)(g->n[1] / f) : 1, (int)(g->n[2] / f),
+               hl, g->stream, g->sets);
+      g->levels.push_back(std::move(e));
+    }
+  }
+  auto L = [&](int l) { return static_cast<Engine<T>*>(g->levels[l].get()); };
+  Engine<T>* fine = L(0);
+  const size_t N = (size_t)fine->Pr.g.N;
+  const double eps_feas = tol > 0 ? tol : 1e-3;
+  CU(cudaEventRecord(fine->ev0, g->stream));
+  copy_in(fine, m, const_cast<T*>(fine->Pr.m), N);
+  for (int l = 1; l < n_levels; ++l) {
+    k_restrict<T><<<L(l)->g_small_(), BLOCK, 0, g->stream>>>(L(l - 1)->Pr.g, L(l)->Pr.g, L(l - 1)->Pr.m,
+                                                          const_cast<T*>(L(l)->Pr.m));
+  }
+  CU(cudaGetLastError());
+  long long launches = n_levels - 1;
+  std::vector<double> rho, gam;
+  for (int l = n_levels - 1; l >= 0; --l) {
+    Engine<T>* e = L(l);
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a)); CU(cudaEventCreate(&b));
+    CU(cudaEventRecord(a, g->stream));
+    e->launches = 0;
+    if (l == n_levels - 1) {
+      // coarsest: x = m_L, y_i = v_i = 0 (reading L13)
+      for (int i = 0; i < e->P; ++i) {
+        SetD<T>& S = e->Pr.set[i];
+        CU(cudaMemsetAsync(S.y[1] - (size_t)GHOST * e->Pr.g.plane, 0, (size_t)S.nblk * e->Pr.g.ld * sizeof(T), g->stream));
+        CU(cudaMemsetAsync(S.v[1] - (size_t)GHOST * e->Pr.g.plane, 0, (size_t)S.nblk * e->Pr.g.ld * sizeof(T), g->stream));
+      }
+      e->solve(g->opt, max_iter, eps_feas, eps_evol_of(g, tol), 1, 0, nullptr, nullptr);
+    } else {
+      Engine<T>* c = L(l + 1);
+      // prolong x, y_i, v_i of the coarse level's final state (Algorithm 3)
+      const int gs = e->g_small_();
+      k_prolong<T><<<gs, BLOCK, 0, g->stream>>>(e->Pr.g, c->Pr.g, PRIM_I, c->Pr.x, e->Pr.x);
+      e->launches++;
+      for (int i = 0; i < e->P; ++i) {
+        const SetD<T>& Sc = c->Pr.set[i];
+        SetD<T>& Sf = e->Pr.set[i];
+        const T* yc = c->final_field(i, 0);
+        const T* vc = c->final_field(i, 1);
+        for (int bl = 0; bl < Sf.nblk; ++bl) {
+          k_prolong<T><<<gs, BLOCK, 0, g->stream>>>(e->Pr.g, c->Pr.g, Sf.prim[bl], yc + (int64_t)bl * c->Pr.g.ld,
+                                                    Sf.y[1] + (int64_t)bl * e->Pr.g.ld);
+          k_prolong<T><<<gs, BLOCK, 0, g->stream>>>(e->Pr.g, c->Pr.g, Sf.prim[bl], vc + (int64_t)bl * c->Pr.g.ld,
+                                                    Sf.v[1] + (int64_t)bl * e->Pr.g.ld);
+          e->launches += 2;
+        }
+        (void)Sc;
+      }
+      CU(cudaGetLastError());
+      e->solve(g->opt, max_iter, eps_feas, eps_evol_of(g, tol), 0, 0, rho.data(), gam.data());
+    }
+    rho.assign(e->hc.rho, e->hc.rho + e->P);   // rho, gamma carry over (L23)
+    gam.assign(e->hc.gamma, e->hc.gamma + e->P);
+    CU(cudaEventRecord(b, g->stream));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    if (per_level) e->fill_result(&per_level[l], ms);
+    launches += e->launches;
+    if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, "NaN/Inf in the PARSDMM state"};
+  }
+  copy_out(fine, fine->Pr.x, x, N);
+  CU(cudaStreamSynchronize(g->stream));
+  g->last_launches = launches;
+  return fine->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
+}
+
+template <class T>
+sip_status apply_op_T(sip_grid g, int set_id, const void* x, void* y) {
+  Engine<T>* e = engine_of<T>(g);
+  const Geo& G = e->Pr.g;
+  const SetD<T>& S = e->Pr.set[set_id];
+  T* xin = e->Pr.pb[0];
+  copy_in(e, x, xin, G.N);
+  T* out = e->Pr.hist[0];   // scratch: nblk blocks needed -> use hist slots
+  T* tmp[3] = {e->Pr.hist[0], e->Pr.hist[1], e->Pr.hist[2]};
+  (void)out;
+  // k_apply_op writes block b at out + b*ld: use contiguous scratch of nblk*ld
+  T* scratch = e->template dalloc<T>((size_t)S.nblk * G.ld);
+  k_apply_op<T><<<e->g_small_(), BLOCK, 0, e->stream>>>(e->Pr, set_id, xin, scratch);
+  const long long M = e->set_len(set_id);
+  T* comp = e->template dalloc<T>(M);
+  long long boff = 0;
+  for (int b = 0; b < S.nblk; ++b) {
+    k_pack<T, T><<<e->g_small_(), BLOCK, 0, e->stream>>>(G, S.prim[b], e->d_fmap, boff, scratch + (int64_t)b * G.ld, comp, 0);
+    boff += e->block_len(S.prim[b]);
+  }
+  CU(cudaGetLastError());
+  copy_out(e, comp, y, M);
+  CU(cudaStreamSynchronize(e->stream));
+  (void)tmp;
+  // release the scratch (last two allocations)
+  cudaFree(comp); e->allocs.pop_back();
+  cudaFree(scratch); e->allocs.pop_back();
+  return SIP_OK;
+}
+
+template <class T>
+void set_rho_coeffs(Engine<T>* e, const double* rho) {
+  Ctrl c = e->hc;
+  for (int i = 0; i < e->P; ++i) c.rho[i] = rho[i];
+  make_coeffs(e->Pr, c.rho, &c.cI, &c.cz, &c.cy, &c.cx, &c.cF);
+  e->hc = c;
+  CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+}
+
+template <class T>
+sip_status apply_system_T(sip_grid g, const double* rho, const void* pin, void* qout) {
+  Engine<T>* e = engine_of<T>(g);
+  const Geo& G = e->Pr.g;
+  set_rho_coeffs(e, rho);
+  T* pv = e->Pr.pb[0];
+  T* q = e->Pr.pb[1];
+  copy_in(e, pin, pv, G.N);
+  if (e->Pr.has[PRIM_F]) {
+    // tb = S G p: reuse k_blur_t mode 0 on x := p
+    Prob<T> P2 = e->Pr;
+    P2.x = pv;
+    Ctrl c = e->hc; c.stopped = 0;
+    e->hc = c;
+    CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2, 0, 0);
+  }
+  k_apply_sys<T><<<e->g_small_(), BLOCK, 0, e->stream>>>(e->Pr, e->d_ctrl, pv, nullptr, q, 0);
+  CU(cudaGetLastError());
+  copy_out(e, q, qout, G.N);
+  CU(cudaStreamSynchronize(e->stream));
+  return SIP_OK;
+}
+
+template <class T>
+sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg, int eq25, int* iters) {
+  Engine<T>* e = engine_of<T>(g);
+  const Geo& G = e->Pr.g;
+  // control block for a bare CG solve: Eq. 25 from r0 = b - C x
+  e->ensure_log(1);
+  const double floor_ = g->opt.cg_tol_floor > 0 ? g->opt.cg_tol_floor
+                                                : 10.0 * (sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON);
+  Options o = g->opt;
+  o.n_cg = n_cg; o.eq25 = eq25;
+  e->fill_ctrl(o, 1, 1e-3, 1e-2, floor_, rho, nullptr);
+  T* bb = e->Pr.hist[1];
+  copy_in(e, b, bb, G.N);
+  copy_in(e, x, e->Pr.x, G.N);
+  // r = b - C x and the CG flags: run k_rhs on a problem whose right-hand
+  // side is b, i.e. rho_i y_i + v_i replaced: use a 1-set identity view
+  Prob<T> P2 = e->Pr;
+  P2.P = 1;   // only the distance block contributes to b: rho*y + v with y = b/rho, v = 0
+  P2.set[0] = e->Pr.set[e->P - 1];
+  P2.set[0].y[0] = P2.set[0].y[1] = bb;
+  T* zero = e->Pr.hist[2];
+  CU(cudaMemsetAsync(zero, 0, G.N * sizeof(T), e->stream));
+  P2.set[0].v[0] = P2.set[0].v[1] = zero;
+  // scale: k_rhs computes rho_{P2.set0} * y + v with rho = C.rho[0]; set rho[0] = 1 in a copy
+  Ctrl c = e->hc;
+  c.rho[0] = 1.0;   // coefficient of b (the C coefficients keep the caller's rho)
+  e->hc = c;
+  CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+  if (e->Pr.has[PRIM_F]) { k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2, 0, 0); }
+  k_rhs<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2);
+  for (int j = 0; j < n_cg; ++j) {
+    if (e->Pr.has[PRIM_F]) k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, 1, j);
+    k_cg1<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
+    k_cg2<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
+  }
+  CU(cudaGetLastError());
+  e->read_ctrl();
+  copy_out(e, e->Pr.x, x, G.N);
+  CU(cudaStreamSynchronize(e->stream));
+  if (iters) *iters = e->hc.cg_count;
+  return SIP_OK;
+}
+
+template <class T>
+sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
+  Engine<T>* e = engine_of<T>(g);
+  if (!e->ran) throw SipError{SIP_ERR_STATE, "sip_project_set needs a previous sip_project"};
+  const Geo& G = e->Pr.g;
+  SetD<T>& S = e->Pr.set[set_id];
+  const long long M = e->set_len(set_id);
+  T* comp = e->template dalloc<T>(M);
+  copy_in(e, w, comp, M);
+  // Run the hot-path kernels on a control block for iteration k = 2 (no
+  // adapt, no check): pass1 reads y[0]/v[0] and writes y[1]/v[1]; pass2
+  // writes y[1].  Only this set's select job is active.  The grid's state
+  // buffers are used as scratch (a later warm start is refused).
+  Ctrl c = e->hc;
+  c.k = 2; c.stopped = 0; c.first_adapt_done = 0; c.adapt_calls = 0;
+  c.opt.check_every = 1 << 30;
+  c.opt.adapt_every = 2;
+  for (int i = 0; i < e->P; ++i) { c.rho[i] = 1.0; c.gamma[i] = 1.0; }
+  for (int jb = 0; jb < c.njobs; ++jb) {
+    Job& J = c.job[jb];
+    const int i = J.set;
+    J.round = 0; J.prefix = 0; J.cnt_above = 0; J.sum_above = 0; J.theta = 0; J.tau = 0;
+    J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0;
+    J.sigma = c.sigma[i]; J.k = c.kcard[i];
+    J.mode = (J.on_s || i != set_id) ? JM_OFF : JM_SEARCH;
+    if (J.mode == JM_SEARCH && J.kind == K_CARD) {
+      if (J.k <= 0) J.mode = JM_ZERO;
+      else if (J.k >= c.mreal[i]) J.mode = JM_ALL;
+    }
+  }
+  if (S.global) {
+    long long boff = 0;
+    for (int b = 0; b < S.nblk; ++b) {
+      k_pack<T, T><<<e->g_small_(), BLOCK, 0, e->stream>>>(G, S.prim[b], e->d_fmap, boff,
+                                                           S.w + (int64_t)b * G.ld, comp, 1);
+      boff += e->block_len(S.prim[b]);
+    }
+    if (S.kind == K_L2 || S.kind == K_ANN) {
+      // the radial factor comes from pass1's ||w||^2 in the hot path; here w
+      // is given, so its norm is formed on the host (step-level entry only)
+      std::vector<T> hw(M);
+      copy_out(e, comp, hw.data(), M);
+      CU(cudaStreamSynchronize(e->stream));
+      double w2 = 0.0;
+      for (long long q = 0; q < M; ++q) w2 += (double)hw[q] * (double)hw[q];
+      const double n = std::sqrt(w2);
+      double f = 1.0; int z = 0;
+      if (n == 0.0) z = c.sig_lo[set_id] > 0.0;
+      else if (n > c.sig_hi[set_id]) f = c.sig_hi[set_id] / n;
+      else if (n < c.sig_lo[set_id]) f = c.sig_lo[set_id] / n;
+      c.ann_scale[set_id] = f; c.ann_zero[set_id] = z;
+    }
+    e->hc = c;
+    CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    if (S.job >= 0) {
+      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) k_select<T><<<e->g_sel, BLOCK, 0, e->stream>>>(e->Pr, r);
+      if (S.kind == K_CARD) k_tiecount<T><<<e->g_p2, BLOCK, 0, e->stream>>>(e->Pr);
+    }
+    k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
+  } else {
+    // pointwise: gamma = 0 and v = 0 make x-bar = y_old and w = y_old, so
+    // pass1 evaluates y = P(w) on the given w placed in y[0]
+    c.gamma[set_id] = 0.0;
+    e->hc = c;
+    CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    long long boff = 0;
+    for (int b = 0; b < S.nblk; ++b) {
+      k_pack<T, T><<<e->g_small_(), BLOCK, 0, e->stream>>>(G, S.prim[b], e->d_fmap, boff,
+                                                           S.y[0] + (int64_t)b * G.ld, comp, 1);
+      CU(cudaMemsetAsync(S.v[0] + (int64_t)b * G.ld, 0, G.N * sizeof(T), e->stream));
+      boff += e->block_len(S.prim[b]);
+    }
+    k_pass1<T><<<e->g_pts, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
+  }
+  CU(cudaGetLastError());
+  long long boff = 0;
+  for (int b = 0; b < S.nblk; ++b) {
+    k_pack<T, T><<<e->g_small_(), BLOCK, 0, e->stream>>>(G, S.prim[b], e->d_fmap, boff,
+                                                         S.y[1] + (int64_t)b * G.ld, comp, 0);
+    boff += e->block_len(S.prim[b]);
+  }
+  copy_out(e, comp, y, M);
+  CU(cudaStreamSynchronize(e->stream));
+  cudaFree(comp); e->allocs.pop_back();
+  e->ran = false;
+  e->read_ctrl();
+  e->ran = true;      // parameters (sigma, k) stay resolved; state is scratch
+  e->scratch_used = true;
+  return SIP_OK;
+}
+
+template <class T>
+sip_status get_state_T(sip_grid g, int set_id, int which, void* out) {
+  Engine<T>* e = engine_of<T>(g);
+  if (!e->ran) throw SipError{SIP_ERR_STATE, "no projection state"};
+  const Geo& G = e->Pr.g;
+  const SetD<T>& S = e->Pr.set[set_id];
+  const long long M = (set_id == e->p) ? G.N : e->set_len(set_id);
+  T* src = e->final_field(set_id, which);
+  T* comp = e->template dalloc<T>(M);
+  long long boff = 0;
+  for (int b = 0; b < S.nblk; ++b) {
+    k_pack<T, T><<<e->g_small_(), BLOCK, 0, e->stream>>>(G, S.prim[b], e->d_fmap, boff, src + (int64_t)b * G.ld, comp, 0);
+    boff += e->block_len(S.prim[b]);
+  }
+  CU(cudaGetLastError());
+  copy_out(e, comp, out, M);
+  CU(cudaStreamSynchronize(e->stream));
+  cudaFree(comp); e->allocs.pop_back();
+  return SIP_OK;
+}
+
+template <class T>
+sip_status get_log_T(sip_grid g, int max_iter, int* cg, int* branch, double* rho_t, double* gam_t,
+                     double* feas, double* evol) {
+  Engine<T>* e = engine_of<T>(g);
+  if (!e->ran) throw SipError{SIP_ERR_STATE, "no projection log"};
+  const int n = std::min(max_iter, e->log_cap);
+  const int P = e->P, p = e->p;
+  if (cg) CU(cudaMemcpy(cg, e->d_log_cg, n * sizeof(int), cudaMemcpyDeviceToHost));
+  if (branch) CU(cudaMemcpy(branch, e->d_log_br, (size_t)n * P * sizeof(int), cudaMemcpyDeviceToHost));
+  if (rho_t) CU(cudaMemcpy(rho_t, e->d_log_rho, (size_t)n * P * sizeof(double), cudaMemcpyDeviceToHost));
+  if (gam_t) CU(cudaMemcpy(gam_t, e->d_log_gam, (size_t)n * P * sizeof(double), cudaMemcpyDeviceToHost));
+  if (feas && p) CU(cudaMemcpy(feas, e->d_log_feas, (size_t)n * p * sizeof(double), cudaMemcpyDeviceToHost));
+  if (evol) CU(cudaMemcpy(evol, e->d_log_evol, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return SIP_OK;
+}
+
+template <class F>
+sip_status guarded(sip_grid g, F&& f) {
+  try {
+    int cur;
+    if (g && cudaGetDevice(&cur) == cudaSuccess && cur != g->device) cudaSetDevice(g->device);
+    return f();
+  } catch (const SipError& e) {
+    if (g) g->err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (g) g->err = "host allocation failed";
+    return SIP_ERR_OOM;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* sip_status_string(sip_status s) {
+  switch (s) {
+    case SIP_OK: return "ok";
+    case SIP_NOT_CONVERGED: return "not converged (max_iter reached)";
+    case SIP_ERR_ARG: return "invalid argument";
+    case SIP_ERR_CONFIG: return "unsupported configuration";
+    case SIP_ERR_PARAM: return "invalid set parameter";
+    case SIP_ERR_SHAPE: return "shape mismatch";
+    case SIP_ERR_CUDA: return "CUDA error";
+    case SIP_ERR_NCCL: return "NCCL error";
+    case SIP_ERR_OOM: return "out of memory";
+    case SIP_ERR_NUMERIC: return "numerical failure (NaN/Inf)";
+    case SIP_ERR_STATE: return "call out of order";
+  }
+  return "unknown status";
+}
+
+const char* sip_last_error(sip_grid g) { return g ? g->err.c_str() : "null grid"; }
+
+sip_status sip_comm_unique_id(uint8_t out[128]) {
+  if (!out) return SIP_ERR_ARG;
+  memset(out, 0, 128);
+  return SIP_ERR_CONFIG;   // multi-rank z-slab path: not in this build
+}
+
+sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtype dtype,
+                           const sip_comm_desc* comm, void* cuda_stream, sip_grid* out) {
+  if (!out || !n || (ndim != 2 && ndim != 3) || (dtype != SIP_F32 && dtype != SIP_F64)) return SIP_ERR_ARG;
+  *out = nullptr;
+  for (int a = 0; a < ndim; ++a) if (n[a] < 2) return SIP_ERR_SHAPE;
+  if (h) for (int a = 0; a < ndim; ++a) if (!(h[a] > 0)) return SIP_ERR_PARAM;
+  if (comm && comm->nranks > 1) return SIP_ERR_CONFIG;
+  int64_t N = 1;
+  for (int a = 0; a < ndim; ++a) N *= n[a];
+  if (N >= (1ll << 31) - 8) return SIP_ERR_SHAPE;
+  auto g = new (std::nothrow) sip_grid_s();
+  if (!g) return SIP_ERR_OOM;
+  if (cudaGetDevice(&g->device) != cudaSuccess) { cudaGetLastError(); delete g; return SIP_ERR_CUDA; }
+  g->stream = (cudaStream_t)cuda_stream;
+  g->dtype = dtype;
+  g->ndim = ndim;
+  if (ndim == 2) {
+    g->n[0] = n[0]; g->n[1] = 1; g->n[2] = n[1];
+    g->h[0] = h ? h[0] : 1.0; g->h[1] = 1.0; g->h[2] = h ? h[1] : 1.0;
+  } else {
+    for (int a = 0; a < 3; ++a) { g->n[a] = n[a]; g->h[a] = h ? h[a] : 1.0; }
+  }
+  *out = g;
+  return SIP_OK;
+}
+
+sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type type,
+                       const sip_set_params* prm, int* set_id) {
+  if (!g || !prm) return SIP_ERR_ARG;
+  if (op < SIP_OP_IDENTITY || op > SIP_OP_BLUR_MASK || type < SIP_SET_BOUNDS || type > SIP_SET_CARDINALITY)
+    return SIP_ERR_ARG;
+  if ((int)g->sets.size() >= SIP_MAX_SETS) { g->err = "more than 16 sets"; return SIP_ERR_CONFIG; }
+  if (op == SIP_OP_DY && g->ndim != 3) { g->err = "D_y needs a 3D grid"; return SIP_ERR_CONFIG; }
+  return guarded(g, [&]() -> sip_status {
+    HostSet hs;
+    hs.op = op; hs.type = type; hs.prm = *prm;
+    hs.prm.lo_vec = hs.prm.hi_vec = nullptr;
+    const int64_t N = g->n[0] * g->n[1] * g->n[2];
+    const int64_t nz = g->n[0], ny = g->n[1], nx = g->n[2];
+    if (op == SIP_OP_BLUR_MASK) {
+      const sip_blur_mask_desc* d = (const sip_blur_mask_desc*)op_desc;
+      if (!d || !d->kernel || !d->mask) return SIP_ERR_ARG;
+      if (g->ndim != 2) { g->err = "blur/mask operator is 2D only"; return SIP_ERR_CONFIG; }
+      if (d->kh < 1 || d->kw < 1 || d->kh % 2 == 0 || d->kw % 2 == 0 || d->kh > 9 || d->kw > 9 ||
+          d->kh / 2 > GHOST * 2 || d->kw / 2 > 4) return SIP_ERR_PARAM;
+      for (auto& s2 : g->sets) if (s2.op == SIP_OP_BLUR_MASK) { g->err = "one blur/mask operator per grid"; return SIP_ERR_CONFIG; }
+      hs.kernel.assign(d->kernel, d->kernel + d->kh * d->kw);
+      hs.kh = d->kh; hs.kw = d->kw;
+      hs.mask.resize(N);
+      if (is_device_ptr(d->mask)) CU(cudaMemcpy(hs.mask.data(), d->mask, N, cudaMemcpyDeviceToHost));
+      else memcpy(hs.mask.data(), d->mask, N);
+      int64_t c = 0;
+      for (int64_t q = 0; q < N; ++q) c += hs.mask[q] ? 1 : 0;
+      hs.M = c;
+    } else {
+      switch (op) {
+        case SIP_OP_IDENTITY: hs.M = N; break;
+        case SIP_OP_DZ: hs.M = (nz - 1) * ny * nx; break;
+        case SIP_OP_DY: hs.M = nz * (ny - 1) * nx; break;
+        case SIP_OP_DX: hs.M = nz * ny * (nx - 1); break;
+        default: hs.M = (nz - 1) * ny * nx + (g->ndim == 3 ? nz * (ny - 1) * nx : 0) + nz * ny * (nx - 1);
+      }
+    }
+    // parameter checks
+    if (type == SIP_SET_BOUNDS) {
+      if (!prm->lo_vec && !prm->hi_vec && !(prm->lo <= prm->hi)) return SIP_ERR_PARAM;
+      auto grab = [&](const double* src, std::vector<double>& dst) {
+        dst.resize(hs.M);
+        if (is_device_ptr(src)) CU(cudaMemcpy(dst.data(), src, hs.M * sizeof(double), cudaMemcpyDeviceToHost));
+        else memcpy(dst.data(), src, hs.M * sizeof(double));
+      };
+      if (prm->lo_vec) grab(prm->lo_vec, hs.lo_vec);
+      if (prm->hi_vec) grab(prm->hi_vec, hs.hi_vec);
+      for (int64_t q = 0; q < hs.M; ++q) {
+        const double lo = hs.lo_vec.empty() ? prm->lo : hs.lo_vec[q];
+        const double hi = hs.hi_vec.empty() ? prm->hi : hs.hi_vec[q];
+        if (!(lo <= hi)) return SIP_ERR_PARAM;
+        if (lo > 0.0 || hi < 0.0) hs.zero_in = 0;
+      }
+      if (hs.M == 0 && (prm->lo > 0.0 || prm->hi < 0.0)) hs.zero_in = 0;
+    } else if (type == SIP_SET_L1_BALL || type == SIP_SET_L2_BALL) {
+      if (!(prm->sigma >= 0)) return SIP_ERR_PARAM;
+    } else if (type == SIP_SET_ANNULUS) {
+      if (!(prm->sigma_lo >= 0) || !(prm->sigma_lo <= prm->sigma_hi)) return SIP_ERR_PARAM;
+      hs.zero_in = prm->sigma_lo <= 0.0;
+    } else if (type == SIP_SET_CARDINALITY) {
+      if (prm->relative) { if (!(prm->k_frac >= 0 && prm->k_frac <= 1)) return SIP_ERR_PARAM; }
+      else if (prm->k < 0 || prm->k > hs.M) return SIP_ERR_PARAM;
+    }
+    g->sets.push_back(std::move(hs));
+    g->eng.reset();
+    g->levels.clear();
+    if (set_id) *set_id = (int)g->sets.size() - 1;
+    return SIP_OK;
+  });
+}
+
+sip_status sip_set_option(sip_grid g, const char* key, double value) {
+  if (!g || !key) return SIP_ERR_ARG;
+  std::string k(key);
+  Options& o = g->opt;
+  if (k == "rho0") { if (!(value > 0)) return SIP_ERR_PARAM; o.rho0 = value; }
+  else if (k == "gamma0") { if (!(value >= 1 && value < 2)) return SIP_ERR_PARAM; o.gamma0 = value; }
+  else if (k == "n_cg") { if (value < 0) return SIP_ERR_PARAM; o.n_cg = (int)value; }
+  else if (k == "eq25") o.eq25 = value != 0;
+  else if (k == "fixed_work") o.fixed_work = value != 0;
+  else if (k == "eps_evol") o.eps_evol = value;
+  else if (k == "eps_corr") o.eps_corr = value;
+  else if (k == "adapt_every") { if (value != 2) { g->err = "adapt_every must be 2 (ping-pong snapshots)"; return SIP_ERR_PARAM; } o.adapt_every = 2; }
+  else if (k == "check_every") { if (value < 1) return SIP_ERR_PARAM; o.check_every = (int)value; }
+  else if (k == "rho_ratio_cap") { if (!(value >= 1)) return SIP_ERR_PARAM; o.rho_ratio_cap = value; }
+  else if (k == "gamma_max") { if (!(value >= 1 && value < 2)) return SIP_ERR_PARAM; o.gamma_max = value; }
+  else if (k == "cg_tol_floor") o.cg_tol_floor = value;
+  else if (k == "warm_start") o.warm_start = value != 0;
+  else if (k == "graph_iters") { if (value < 0) return SIP_ERR_PARAM; o.graph_iters = (int)value; }
+  else { g->err = "unknown option " + k; return SIP_ERR_ARG; }
+  return SIP_OK;
+}
+
+sip_status sip_project(sip_grid g, const void* m, void* x, int max_iter, double tol, sip_result* res) {
+  if (!g || !m || !x || max_iter < 1 || m == x) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? project_T<float>(g, m, x, max_iter, tol, res)
+                               : project_T<double>(g, m, x, max_iter, tol, res);
+  });
+}
+
+sip_status sip_project_multilevel(sip_grid g, const void* m, void* x, int n_levels, int coarsen,
+                                  int max_iter, double tol, sip_result* per_level) {
+  if (!g || !m || !x || n_levels < 1 || coarsen != 2 || max_iter < 1 || m == x) return SIP_ERR_ARG;
+  for (auto& s : g->sets)
+    if (s.op == SIP_OP_BLUR_MASK || !s.lo_vec.empty() || !s.hi_vec.empty()) {
+      g->err = "multilevel: blur/mask operators and per-entry bounds are not supported";
+      return SIP_ERR_CONFIG;
+    }
+  const int f = 1 << (n_levels - 1);
+  for (int a = 0; a < 3; ++a) {
+    if (a == 1 && g->ndim == 2) continue;
+    if (g->n[a] % f != 0 || g->n[a] / f < 2) { g->err = "grid not divisible for the levels"; return SIP_ERR_CONFIG; }
+  }
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? multilevel_T<float>(g, m, x, n_levels, max_iter, tol, per_level)
+                               : multilevel_T<double>(g, m, x, n_levels, max_iter, tol, per_level);
+  });
+}
+
+void sip_destroy(sip_grid g) {
+  if (!g) return;
+  int cur;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur != g->device) cudaSetDevice(g->device);
+  if (g->stream) cudaStreamSynchronize(g->stream);
+  g->levels.clear();
+  g->eng.reset();
+  delete g;
+}
+
+sip_status sip_apply_op(sip_grid g, int set_id, const void* x, void* y) {
+  if (!g || !x || !y || set_id < 0 || set_id >= (int)g->sets.size()) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? apply_op_T<float>(g, set_id, x, y) : apply_op_T<double>(g, set_id, x, y);
+  });
+}
+
+sip_status sip_apply_system(sip_grid g, const double* rho, const void* p, void* q) {
+  if (!g || !rho || !p || !q) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? apply_system_T<float>(g, rho, p, q) : apply_system_T<double>(g, rho, p, q);
+  });
+}
+
+sip_status sip_cg(sip_grid g, const double* rho, const void* b, void* x, int n_cg, int eq25, int* iterations) {
+  if (!g || !rho || !b || !x || n_cg < 0) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? cg_T<float>(g, rho, b, x, n_cg, eq25, iterations)
+                               : cg_T<double>(g, rho, b, x, n_cg, eq25, iterations);
+  });
+}
+
+sip_status sip_project_set(sip_grid g, int set_id, const void* w, void* y) {
+  if (!g || !w || !y || set_id < 0 || set_id >= (int)g->sets.size()) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? project_set_T<float>(g, set_id, w, y) : project_set_T<double>(g, set_id, w, y);
+  });
+}
+
+sip_status sip_get_state(sip_grid g, int set_id, int which, void* out) {
+  if (!g || !out || set_id < 0 || set_id > (int)g->sets.size() || (which != 0 && which != 1)) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? get_state_T<float>(g, set_id, which, out) : get_state_T<double>(g, set_id, which, out);
+  });
+}
+
+sip_status sip_get_log(sip_grid g, int max_iter, int* cg, int* branch, double* rho_trace,
+                       double* gamma_trace, double* r_feas, double* r_evol) {
+  if (!g || max_iter < 0) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? get_log_T<float>(g, max_iter, cg, branch, rho_trace, gamma_trace, r_feas, r_evol)
+                               : get_log_T<double>(g, max_iter, cg, branch, rho_trace, gamma_trace, r_feas, r_evol);
+  });
+}
+
+sip_status sip_get_sizes(sip_grid g, int* p, int64_t* n_local, int set_id, int64_t* m_compact) {
+  if (!g) return SIP_ERR_ARG;
+  if (p) *p = (int)g->sets.size();
+  if (n_local) *n_local = g->n[0] * g->n[1] * g->n[2];
+  if (m_compact) {
+    if (set_id < 0 || set_id > (int)g->sets.size()) return SIP_ERR_ARG;
+    *m_compact = set_id == (int)g->sets.size() ? g->n[0] * g->n[1] * g->n[2] : g->sets[set_id].M;
+  }
+  return SIP_OK;
+}
+
+sip_status sip_get_launch_count(sip_grid g, int64_t* launches) {
+  if (!g || !launches) return SIP_ERR_ARG;
+  *launches = g->last_launches;
+  return SIP_OK;
+}
+
+}  // extern "C"
