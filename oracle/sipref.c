@@ -589,8 +589,12 @@ static int parsdmm_run(const sipref_grid *g, int p, const sipref_set *in_sets,
       else sipref_prox_dist(N, m, rho[i], w, yn);               /* Eq. 22 */
       if (adapt) /* Alg. 2 line 1 with the OLD y and v (reading L10) */
         for (int64_t j = 0; j < M[i]; ++j) vh[i][j] = v[i][j] + rho[i] * (y[i][j] - s[i][j]);
+      /* dual update, Eq. 21 line 4: v + rho (y - x-bar) = rho (y - w) since
+         w = x-bar - v/rho.  The second form is exact (v = 0) when the
+         constraint is inactive (y = w); the first leaves rounding noise that
+         Algorithm 2 would correlate (reading L26). */
       for (int64_t j = 0; j < M[i]; ++j) {
-        v[i][j] = v[i][j] + rho[i] * (yn[j] - xbar[j]);         /* dual update */
+        v[i][j] = rho[i] * (yn[j] - w[j]);
         y[i][j] = yn[j];
       }
     }
