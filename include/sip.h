@@ -133,8 +133,11 @@ sip_status sip_comm_unique_id(uint8_t out[128]);
    (NULL = all 1, reading L2).  comm: NULL for one GPU, else the z-slab
    decomposition: the rank owns planes [z0, z0+nz_local) with the first
    nz mod nranks ranks holding one extra plane; m/x passed to this rank are
-   its local slab.  cuda_stream: cudaStream_t (NULL = legacy default stream).
-   The current CUDA device at the call is the grid's device. */
+   its local slab.  cuda_stream: the caller's cudaStream_t (NULL = legacy
+   default stream); every call orders its work after the work already queued
+   on it, runs on a library-owned non-blocking stream (capturable into CUDA
+   graphs) and returns after completion.  The current CUDA device at the
+   call is the grid's device. */
 sip_status sip_create_grid(int ndim, const int64_t *n, const double *h, sip_dtype dtype,
                            const sip_comm_desc *comm, void *cuda_stream, sip_grid *out);
 

@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(BLOCK) k_pass1(const __grid_constant__ Prob<T>
         const double sv = s[prim];
         const double yo = (double)yr[off], vo = (double)vr[off];
         const double xbar = gam * sv + (1.0 - gam) * yo;       // relaxation
-        const double w = xbar - vo / rho;
+        const double w = (double)(T)(xbar - vo / rho);          // as stored for global sets
         if (pointwise) {
           double yn;
           if (S.kind == K_DIST) {
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(BLOCK) k_pass1(const __grid_constant__ Prob<T>
             }
           }
           const T ynt = (T)yn;
-          const T vnt = (T)(vo + rho * ((double)ynt - xbar));   // Eq. 21 dual update
+          const T vnt = (T)(rho * ((double)ynt - w));   // Eq. 21 dual update as rho (y - w), L26
           if (dots) {
             const double dg = -((double)ynt - (double)yw[off]);
             const double dv = (double)vnt - (double)vw[off];

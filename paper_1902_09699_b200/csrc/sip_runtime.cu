@@ -507,7 +507,9 @@ struct Engine : EngineBase {
 // ------------------------------------------------------------------ grid
 struct sip_grid_s {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;        // library-owned work stream (capturable)
+  cudaStream_t user_stream = nullptr;   // caller's stream: work is ordered after it
+  cudaEvent_t fence = nullptr;
   sip_dtype dtype = SIP_F32;
   int ndim = 2;
   int64_t n[3] = {1, 1, 1};   // nz, ny, nx
@@ -899,6 +901,10 @@ sip_status guarded(sip_grid g, F&& f) {
   try {
     int cur;
     if (g && cudaGetDevice(&cur) == cudaSuccess && cur != g->device) cudaSetDevice(g->device);
+    if (g && g->fence) {   // order the library stream after the caller's stream
+      CU(cudaEventRecord(g->fence, g->user_stream));
+      CU(cudaStreamWaitEvent(g->stream, g->fence, 0));
+    }
     return f();
   } catch (const SipError& e) {
     if (g) g->err = e.msg;
@@ -952,7 +958,13 @@ sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtyp
   auto g = new (std::nothrow) sip_grid_s();
   if (!g) return SIP_ERR_OOM;
   if (cudaGetDevice(&g->device) != cudaSuccess) { cudaGetLastError(); delete g; return SIP_ERR_CUDA; }
-  g->stream = (cudaStream_t)cuda_stream;
+  g->user_stream = (cudaStream_t)cuda_stream;
+  if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&g->fence, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    delete g;
+    return SIP_ERR_CUDA;
+  }
   g->dtype = dtype;
   g->ndim = ndim;
   if (ndim == 2) {
@@ -1092,6 +1104,8 @@ void sip_destroy(sip_grid g) {
   if (g->stream) cudaStreamSynchronize(g->stream);
   g->levels.clear();
   g->eng.reset();
+  if (g->fence) cudaEventDestroy(g->fence);
+  if (g->stream) cudaStreamDestroy(g->stream);
   delete g;
 }
 
