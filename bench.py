@@ -1,0 +1,337 @@
+"""Benchmark of the B200 PARSDMM hot path (arXiv 1902.09699).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4]
+                    [--iters-per-step 10] [--impl cuda|reference]
+
+A step is one call of the public API, sip_project, in fixed-work mode
+(Eq. 25 off -> exactly n_cg = 10 CG steps per iteration; the
+Eq. 26-28 stop test computed but not acted on; Algorithm 2 on) running
+`iters_per_step` outer PARSDMM iterations on the config's seeded synthetic
+model.  Ten iterations cover every row of SURVEY 8(a): rhs, CG, transform +
+relaxation, pointwise / l1 / cardinality / annulus projections, duals,
+5 adapt calls and 2 stop checks.  The metric is BASELINE.json's:
+PARSDMM iterations/s (also grid-points x sets / s and the HBM roofline).
+
+value   = iterations of all ranks / max over ranks of the summed device time
+          of the K timed steps (library CUDA events around each call; L2 is
+          flushed by a 256 MiB write between steps, outside the timing).
+e2e     = the same metric through the same call with host (pinned) m and x:
+          the H2D copy of m and the D2H copy of x are inside the timed call.
+roofline: the dominant kernel (k_cg2: x += a p, r -= a C p) -- its device
+          time comes from CUDA event nodes captured in the iteration graph
+          (option "profile") in a separate profiled step of the same workload.
+--impl reference: the CPU oracle (oracle/, plain C fp64, 1 thread) timed on
+          a bounded sample of the same workload (the reference arm of this
+          tier: there is no reference implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import sip_inputs as G  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return PEAKS_FALLBACK
+
+
+def op_len(shape, op):
+    """compact length M of an operator (for the algorithmic byte model)"""
+    if len(shape) == 2:
+        nz, nx = shape
+        ny = 1
+    else:
+        nz, ny, nx = shape
+    N = nz * ny * nx
+    dz, dy, dx = (nz - 1) * ny * nx, (nz * (ny - 1) * nx if len(shape) == 3 else 0), nz * ny * (nx - 1)
+    return {"I": N, "DZ": dz, "DY": dy, "DX": dx, "TV": dz + dy + dx}.get(op, N // 2)
+
+
+def byte_model(prob, n_cg=10, word=4):
+    """algorithmic bytes: per CG kernel launch and per iteration"""
+    N = prob.N
+    Ms = [op_len(prob.shape, sd.op) for sd in prob.sets] + [N]
+    SM = sum(Ms)
+    T = sum(op_len(prob.shape, sd.op) for sd in prob.sets if sd.kind in ("l1", "card", "annulus", "l2"))
+    cg1 = 3 * N * word          # read r, p_{j-1}; write p_j
+    cg2 = 5 * N * word          # read x, r, p; write x, r
+    a, c = 0.5, 0.2
+    it = word * (8 * N * n_cg + (2 * SM + 2 * N) + (4 * SM + 2 * N) + T + N
+                 + a * (4 * SM + 2 * N) + c * (5 * N + T))
+    return dict(cg1=cg1, cg2=cg2, iteration=it)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region"""
+
+    def __init__(self, gpu=0):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(v, world, device=None):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(v, world, device=None):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ oracle arm
+def oracle_sample(prob, iters, reps=1):
+    """the CPU oracle (fixed-work PARSDMM) on the same workload; seconds/iteration"""
+    import oracle as O
+    opts = dict(prob.options)
+    opts.update(max_iter=iters, eq25=0, fixed_work=1)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.parsdmm(prob.shape, prob.sets, prob.m, **opts)
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def run_reference(args, prob):
+    world, rank, _ = dist_init()
+    if rank != 0:
+        return 0
+    ips = args.ref_iters
+    for _ in range(args.warmup):
+        oracle_sample(prob, 1)
+    ts = []
+    for _ in range(args.steps):
+        ts += oracle_sample(prob, ips)
+    total = sum(ts)
+    val = args.steps * ips / total
+    line = {
+        "impl": "reference", "metric": "PARSDMM iterations/s", "value": val, "unit": "it/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": prob.name, "grid": list(prob.shape), "sets": len(prob.sets),
+                   "iters_per_step": ips, "mode": "fixed_work"},
+        "pts_sets_per_s": val * prob.N * len(prob.sets),
+        "cpu_baseline": {"value": val, "unit": "it/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{args.steps} steps x {ips} fixed-work iterations of {prob.name} "
+                                   f"(single-threaded fp64 C oracle)"},
+        "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ CUDA arm
+def run_cuda(args, prob):
+    import torch
+    world, rank, local = dist_init()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1902_09699_b200 import grid_for
+
+    dt = torch.float32 if prob.dtype == "f32" else torch.float64
+    ips = args.iters_per_step
+    g = grid_for(prob)
+    g.set_option("fixed_work", 1)
+    g.set_option("eq25", 0)
+    g.set_option("n_cg", args.n_cg)
+    m = torch.tensor(prob.m, dtype=dt, device="cuda").contiguous()
+    x = torch.empty_like(m)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2
+
+    def step():
+        res, st = g.project(m, x, max_iter=ips, tol=1e-3)
+        return res
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    times, launches = [], 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            res = step()
+            times.append(res["ms"])
+            launches += g.launch_count()
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t_total = max_over_ranks(sum(times), world, "cuda")          # ms
+    iters_all = sum_over_ranks(args.steps * ips, world, "cuda")
+    value = iters_all / (t_total / 1e3) / world                   # replicas: each rank iterates its own problem
+    value_job = iters_all / (t_total / 1e3)
+
+    # e2e: host pinned m / x, copies inside the timed call
+    mh = torch.tensor(prob.m, dtype=dt).pin_memory()
+    xh = torch.empty_like(mh).pin_memory()
+    for _ in range(1):
+        g.project(mh, xh, max_iter=ips, tol=1e-3)
+    etimes = []
+    for _ in range(max(1, args.steps // 2)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = g.project(mh, xh, max_iter=ips, tol=1e-3)[0]
+        etimes.append(time.perf_counter() - t0)
+    e2e_t = max_over_ranks(sum(etimes), world, "cuda")
+    e2e_val = sum_over_ranks(len(etimes) * ips, world, "cuda") / e2e_t
+    nbytes = prob.N * (4 if prob.dtype == "f32" else 8)
+
+    # profiled step: per-kernel device time from event nodes in the graph
+    g.set_option("profile", 1)
+    flush.zero_()
+    torch.cuda.synchronize()
+    g.project(m, x, max_iter=ips, tol=1e-3)
+    prof = g.profile()
+    g.set_option("profile", 0)
+    model = byte_model(prob, args.n_cg, 4 if prob.dtype == "f32" else 8)
+    peaks = load_peaks()
+    cg2_ms, cg2_n = prof["cg2"]
+    cg2_avg_s = cg2_ms / max(cg2_n, 1) / 1e3
+    achieved = model["cg2"] / cg2_avg_s / 1e9 if cg2_avg_s > 0 else None
+    step_prof_ms = sum(v[0] for v in prof.values())
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        tr = json.load(open(tpath)).get(prob.name, {}).get("k_cg2")
+        traffic = tr
+    it_model_gbs = model["iteration"] * (args.steps * ips) / (sum(times) / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        ts = oracle_sample(prob, args.cpu_iters)
+        cpu = {"value": args.cpu_iters / sum(ts), "unit": "it/s", "cores": 1, "kind": "oracle",
+               "sample": f"{args.cpu_iters} fixed-work iterations of {prob.name} "
+                         f"(single-threaded fp64 C oracle, {sum(ts):.1f} s)"}
+    if rank == 0:
+        line = {
+            "metric": "PARSDMM iterations/s", "value": value_job, "unit": "it/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prob.dtype == "f32" else "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{prob.name} {'x'.join(map(str, prob.shape))} "
+                                   f"{', '.join(sd.op + ':' + sd.kind for sd in prob.sets)}",
+                       "grid": list(prob.shape), "sets": len(prob.sets), "iters_per_step": ips,
+                       "n_cg": args.n_cg, "mode": "fixed_work (Eq.25 off, stop test not acted on)",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+            "pts_sets_per_s": value_job * prob.N * len(prob.sets),
+            "iteration_model_gbs": it_model_gbs,
+            "per_rank_it_s": value,
+            "roofline": {"kernel": "k_cg2", "bound": "hbm", "achieved": achieved,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
+                         "traffic": traffic, "peak_source": peaks["source"],
+                         "bytes_per_launch": model["cg2"], "avg_launch_us": cg2_avg_s * 1e6,
+                         "share_of_step": cg2_ms / step_prof_ms if step_prof_ms else None},
+            "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": nbytes,
+                    "d2h_bytes_per_step": nbytes},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--iters-per-step", type=int, default=10)
+    ap.add_argument("--n-cg", type=int, default=10)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--ref-iters", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    prob = G.CONFIGS[args.config]()
+    if args.impl == "reference":
+        return run_reference(args, prob)
+    return run_cuda(args, prob)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -157,7 +157,9 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void *op_desc, sip_set_type 
    (L16), "gamma_max" 2-1e-3 (L15), "cg_tol_floor" 10*eps(dtype) (L18),
    "warm_start" 0 (1 = start from the grid's x, y_i, v_i, rho_i, gamma_i of
    the previous call instead of reading L13), "graph_iters" 5 (iterations
-   per captured CUDA graph; 0 = no graph).  Unknown key: SIP_ERR_ARG. */
+   per captured CUDA graph; 0 = no graph), "profile" 0 (1 = per-kernel event
+   timing, see sip_get_profile; adds one host sync per graph launch).
+   Unknown key: SIP_ERR_ARG. */
 sip_status sip_set_option(sip_grid g, const char *key, double value);
 
 /* Project m onto the intersection (Algorithm 1).  m (read only) and x are
@@ -221,6 +223,13 @@ sip_status sip_get_log(sip_grid g, int max_iter, int *cg, int *branch, double *r
 
 /* Number of sets p, grid points N (this rank) and compact length of set i. */
 sip_status sip_get_sizes(sip_grid g, int *p, int64_t *n_local, int set_id, int64_t *m_compact);
+
+/* Device time per kernel kind of the last sip_project run with option
+   "profile" = 1 (CUDA event nodes between consecutive kernels, captured in
+   the graph).  Kinds, in order: 0 blur (S G p), 1 rhs, 2 cg1, 3 cg2,
+   4 pass1, 5 select, 6 tiecount, 7 pass2, 8 control.  ms[q] is the summed
+   milliseconds, count[q] the number of launches (arrays of n <= 9). */
+sip_status sip_get_profile(sip_grid g, int n, double *ms, int64_t *count);
 
 /* Number of kernel launches enqueued by the last sip_project (bench evidence). */
 sip_status sip_get_launch_count(sip_grid g, int64_t *launches);

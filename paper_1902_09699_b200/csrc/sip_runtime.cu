@@ -17,6 +17,7 @@
 
 #include "../../include/sip.h"
 #include "sip_aux_kernels.cuh"
+#include "sip_vec.cuh"
 
 using namespace sip;
 
@@ -51,7 +52,7 @@ struct Options {
   int n_cg = 10, eq25 = 1, fixed_work = 0, adapt_every = 2, check_every = 5;
   double eps_evol = -1.0;       // < 0: 10 * tol
   double cg_tol_floor = -1.0;   // < 0: 10 * eps(dtype)
-  int warm_start = 0, graph_iters = 5;
+  int warm_start = 0, graph_iters = 5, profile = 0;
 };
 
 inline int nblk_of(sip_op op, int ndim) {
@@ -115,11 +116,13 @@ struct Engine : EngineBase {
   cudaEvent_t ev_flag[2];
   cudaEvent_t ev0, ev1;
   // launch geometry
-  int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1;
+  int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1;
+  bool vec = false;
   size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0;
   // graph
   cudaGraphExec_t gexec = nullptr;
   int g_iters = 0, g_ncg = -1;
+  bool g_prof = false;
   long long launches = 0;       // kernels enqueued by the last project()
   long long graph_kernels = 0;  // kernels in one captured graph
   int last_k = 0;               // Ctrl.k after the last run
@@ -239,11 +242,15 @@ struct Engine : EngineBase {
     g_sel = std::max(1, std::min(tiles, nsm * 4));
     g_p2 = std::max(1, std::min(tiles * 3, nsm * 8));
     g_small = std::max(1, std::min(tiles, nsm * 4));
+    // vectorised CG kernels: W = 16/sizeof(T) points per thread along x
+    constexpr int W = VT<T>::W;
+    vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
+    g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
-    const int gmax = std::max(std::max(g_pts, g_sel), g_p2);
+    const int gmax = std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec);
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     Pr.counter = dalloc<unsigned>(1);
     CU(cudaMemsetAsync(Pr.counter, 0, sizeof(unsigned), stream));
@@ -263,6 +270,7 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1v<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
     memset(&hc, 0, sizeof(hc));
     hc.njobs = njobs;
     for (int i = 0; i < P; ++i) {
@@ -317,34 +325,79 @@ struct Engine : EngineBase {
   }
 
   // ---- iteration enqueue ------------------------------------------------
-  void enqueue_iteration(int n_cg) {
-    const Geo& g = Pr.g;
-    (void)g;
-    if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 0, 0); ++launches; }
-    k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr); ++launches;
-    for (int j = 0; j < n_cg; ++j) {
-      if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 1, j); ++launches; }
-      k_cg1<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches;
-      k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches;
+  // profiling: an event is recorded before the first kernel and after every
+  // kernel; consecutive pairs give each kernel's device time (kind list)
+  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, NKIND };
+  bool prof = false;
+  std::vector<cudaEvent_t> pev;      // events of one graph (capture order)
+  std::vector<int> pkind;            // kind of the kernel ending at pev[i+1]
+  size_t pev_used = 0;
+  double prof_ms[NKIND] = {0};
+  long long prof_cnt[NKIND] = {0};
+
+  void mark(int kind) {
+    if (!prof) return;
+    if (pev_used == pev.size()) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      pev.push_back(e);
     }
-    k_pass1<T><<<g_pts, BLOCK, smem_p1, stream>>>(Pr); ++launches;
+    // inside stream capture the record must be an external event node
+    cudaStreamCaptureStatus cs;
+    CU(cudaStreamIsCapturing(stream, &cs));
+    if (cs == cudaStreamCaptureStatusActive) CU(cudaEventRecordWithFlags(pev[pev_used], stream, cudaEventRecordExternal));
+    else CU(cudaEventRecord(pev[pev_used], stream));
+    if (pev_used > 0) pkind.push_back(kind);
+    ++pev_used;
+  }
+
+  void enqueue_iteration(int n_cg) {
+    if (prof && pev_used == 0) mark(-1);
+    if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 0, 0); ++launches; mark(KB_BLUR); }
+    k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr); ++launches; mark(KB_RHS);
+    for (int j = 0; j < n_cg; ++j) {
+      if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 1, j); ++launches; mark(KB_BLUR); }
+      if (vec) {
+        k_cg1v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG1);
+        k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
+      } else {
+        k_cg1<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG1);
+        k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
+      }
+    }
+    if (vec) k_pass1v<T><<<g_vec, BLOCK, smem_p1, stream>>>(Pr);
+    else k_pass1<T><<<g_pts, BLOCK, smem_p1, stream>>>(Pr);
+    ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
-        k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r); ++launches;
+        k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r); ++launches; mark(KB_SELECT);
       }
       bool card = false;
       for (int i = 0; i < p; ++i) if (Pr.set[i].kind == K_CARD) card = true;
-      if (card) { k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr); ++launches; }
+      if (card) { k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr); ++launches; mark(KB_TIE); }
     }
-    if (Pr.nglob > 0) { k_pass2<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); ++launches; }
-    k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches;
+    if (Pr.nglob > 0) { k_pass2<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); ++launches; mark(KB_PASS2); }
+    k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches; mark(KB_CTRL);
+  }
+
+  void harvest_profile() {
+    if (!prof || pev_used < 2) return;
+    CU(cudaEventSynchronize(pev[pev_used - 1]));
+    for (size_t i = 0; i + 1 < pev_used; ++i) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, pev[i], pev[i + 1]));
+      prof_ms[pkind[i]] += ms;
+      prof_cnt[pkind[i]] += 1;
+    }
   }
 
   void ensure_graph(int iters, int n_cg) {
-    if (gexec && g_iters == iters && g_ncg == n_cg) return;
+    if (gexec && g_iters == iters && g_ncg == n_cg && g_prof == prof) return;
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
     cudaGraph_t graph;
     long long before = launches;
+    pev_used = 0;
+    pkind.clear();
     CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < iters; ++i) enqueue_iteration(n_cg);
     cudaError_t e = cudaStreamEndCapture(stream, &graph);
@@ -355,6 +408,7 @@ struct Engine : EngineBase {
     cudaGraphDestroy(graph);
     g_iters = iters;
     g_ncg = n_cg;
+    g_prof = prof;
   }
 
   void ensure_log(int max_iter) {
@@ -421,7 +475,9 @@ struct Engine : EngineBase {
     if (gi <= 0) {
       // no graph: launch iteration by iteration, poll every check_every
       for (int it = 0; it < max_iter; ++it) {
+        if (prof) { pev_used = 0; pkind.clear(); }
         enqueue_iteration(n_cg);
+        harvest_profile();
         if ((it + 1) % std::max(1, hc.opt.check_every) == 0 || it + 1 == max_iter) {
           CU(cudaMemcpyAsync(h_flag, &d_ctrl->stopped, sizeof(int), cudaMemcpyDeviceToHost, stream));
           CU(cudaStreamSynchronize(stream));
@@ -436,6 +492,7 @@ struct Engine : EngineBase {
     for (int l = 0; l < nlaunch; ++l) {
       CU(cudaGraphLaunch(gexec, stream));
       launches += graph_kernels;
+      harvest_profile();
       if (!poll) continue;
       CU(cudaMemcpyAsync(&h_flag[l & 1], &d_ctrl->stopped, sizeof(int), cudaMemcpyDeviceToHost, stream));
       CU(cudaEventRecord(ev_flag[l & 1], stream));
@@ -558,6 +615,8 @@ sip_status project_T(sip_grid g, const void* m, void* x, int max_iter, double to
   const size_t N = (size_t)e->Pr.g.N;
   const double eps_feas = tol > 0 ? tol : 1e-3;
   e->launches = 0;
+  e->prof = g->opt.profile != 0;
+  for (int q = 0; q < Engine<T>::NKIND; ++q) { e->prof_ms[q] = 0; e->prof_cnt[q] = 0; }
   CU(cudaEventRecord(e->ev0, e->stream));
   copy_in(e, m, const_cast<T*>(e->Pr.m), N);
   const bool warm = g->opt.warm_start && e->ran && !e->scratch_used;
@@ -757,8 +816,13 @@ sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg,
   k_rhs<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2);
   for (int j = 0; j < n_cg; ++j) {
     if (e->Pr.has[PRIM_F]) k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, 1, j);
-    k_cg1<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
-    k_cg2<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
+    if (e->vec) {   // the same kernels as the hot path
+      k_cg1v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
+      k_cg2v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
+    } else {
+      k_cg1<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
+      k_cg2<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
+    }
   }
   CU(cudaGetLastError());
   e->read_ctrl();
@@ -840,7 +904,8 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
       CU(cudaMemsetAsync(S.v[0] + (int64_t)b * G.ld, 0, G.N * sizeof(T), e->stream));
       boff += e->block_len(S.prim[b]);
     }
-    k_pass1<T><<<e->g_pts, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
+    if (e->vec) k_pass1v<T><<<e->g_vec, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
+    else k_pass1<T><<<e->g_pts, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
   }
   CU(cudaGetLastError());
   long long boff = 0;
@@ -1066,6 +1131,7 @@ sip_status sip_set_option(sip_grid g, const char* key, double value) {
   else if (k == "cg_tol_floor") o.cg_tol_floor = value;
   else if (k == "warm_start") o.warm_start = value != 0;
   else if (k == "graph_iters") { if (value < 0) return SIP_ERR_PARAM; o.graph_iters = (int)value; }
+  else if (k == "profile") o.profile = value != 0;
   else { g->err = "unknown option " + k; return SIP_ERR_ARG; }
   return SIP_OK;
 }
@@ -1163,6 +1229,22 @@ sip_status sip_get_sizes(sip_grid g, int* p, int64_t* n_local, int set_id, int64
     *m_compact = set_id == (int)g->sets.size() ? g->n[0] * g->n[1] * g->n[2] : g->sets[set_id].M;
   }
   return SIP_OK;
+}
+
+sip_status sip_get_profile(sip_grid g, int n, double* ms, int64_t* count) {
+  if (!g || n < 0) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    if (!g->eng) throw SipError{SIP_ERR_STATE, "no projection"};
+    auto fill = [&](auto* e) {
+      for (int q = 0; q < n && q < 9; ++q) {
+        if (ms) ms[q] = e->prof_ms[q];
+        if (count) count[q] = e->prof_cnt[q];
+      }
+    };
+    if (g->dtype == SIP_F32) fill(static_cast<Engine<float>*>(g->eng.get()));
+    else fill(static_cast<Engine<double>*>(g->eng.get()));
+    return SIP_OK;
+  });
 }
 
 sip_status sip_get_launch_count(sip_grid g, int64_t* launches) {

@@ -61,8 +61,9 @@ EXPORTS = [
     "sip_comm_unique_id", "sip_create_grid", "sip_add_set", "sip_set_option", "sip_project",
     "sip_project_multilevel", "sip_destroy", "sip_status_string", "sip_last_error",
     "sip_apply_op", "sip_apply_system", "sip_cg", "sip_project_set", "sip_get_state",
-    "sip_get_log", "sip_get_sizes", "sip_get_launch_count",
+    "sip_get_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile",
 ]
+KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control"]
 
 _lib = None
 
@@ -101,6 +102,7 @@ def lib():
         L.sip_get_sizes.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.c_int,
                                     C.POINTER(C.c_int64)]
         L.sip_get_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+        L.sip_get_profile.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -264,6 +266,14 @@ class Grid:
         return dict(cg=cg, branch=br.reshape(max_iter, P), rho=rt.reshape(max_iter, P),
                     gamma=gt.reshape(max_iter, P), r_feas=ft[: max_iter * p].reshape(max_iter, p),
                     r_evol=et)
+
+    def profile(self):
+        """per-kernel-kind device ms and launch counts of the last project()"""
+        n = len(KERNEL_KINDS)
+        ms = np.zeros(n)
+        cnt = np.zeros(n, dtype=np.int64)
+        self._check(lib().sip_get_profile(self.h, n, _ptr(ms), _ptr(cnt)))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_KINDS)}
 
     def launch_count(self):
         n = C.c_int64(0)

@@ -55,7 +55,8 @@ def blur_set(shape, seed=3, lo=-INF, hi=INF):
     return SetDef("BLUR_MASK", "bounds", lo=lo, hi=hi, kernel=K, mask=mask)
 
 
-SHAPES = [(37, 53), (300, 301), (9, 13, 17), (40, 24, 70)]
+# odd nx -> scalar kernels; nx % 4 == 0 -> vectorised kernels (16-byte lanes)
+SHAPES = [(37, 53), (300, 301), (9, 13, 17), (40, 24, 70), (64, 96), (130, 1028), (12, 20, 36)]
 
 
 # ------------------------------------------------------------ operators
@@ -98,9 +99,9 @@ def test_apply_system(dtype, shape):
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("eq25", [True, False])
-def test_cg(dtype, eq25):
-    shape = (60, 90)
-    sets = [SetDef("TV", "l1"), SetDef("DZ", "bounds"), blur_set(shape)]
+@pytest.mark.parametrize("shape,blur", [((60, 90), True), ((60, 96), False), ((10, 12, 20), False)])
+def test_cg(dtype, eq25, shape, blur):
+    sets = [SetDef("TV", "l1"), SetDef("DZ", "bounds")] + ([blur_set(shape)] if blur else [])
     g = mk_grid(shape, sets, dtype)
     r = np.random.default_rng(4)
     rho = r.uniform(0.1, 3.0, size=len(sets) + 1)
@@ -157,8 +158,10 @@ def _proj_case(kind, shape, dtype, seed):
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("kind", ["l1", "card", "card_ties", "annulus", "l2", "bounds", "bounds_vec",
                                   "blur_box"])
-@pytest.mark.parametrize("shape", [(53, 71), (300, 301)])
+@pytest.mark.parametrize("shape", [(53, 71), (300, 301), (64, 128), (12, 16, 20)])
 def test_project_set(dtype, kind, shape):
+    if kind == "blur_box" and len(shape) == 3:
+        pytest.skip("blur/mask operator is 2D")
     sd, w = _proj_case(kind, shape, dtype, 10 + len(kind))
     g = mk_grid(shape, [sd], dtype)
     m = dev(np.zeros(shape), dtype)
@@ -211,8 +214,11 @@ TINY = [
 ]
 
 
+@pytest.mark.parametrize("path", ["vec", "scalar"])
 @pytest.mark.parametrize("seed,shape,kinds", TINY)
-def test_tiny_bitexact_control_flow(seed, shape, kinds):
+def test_tiny_bitexact_control_flow(seed, shape, kinds, path, monkeypatch):
+    if path == "scalar":
+        monkeypatch.setenv("SIP_NO_VEC", "1")
     prob = G.tiny(seed, shape, kinds)
     x, res, log, g = run_gpu(prob, want_log=True)
     ref = O.parsdmm(prob.shape, prob.sets, prob.m, **prob.options)
