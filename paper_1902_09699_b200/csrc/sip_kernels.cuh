@@ -44,6 +44,11 @@ struct Prob {
   unsigned long long* gh_s1;
   int* tiecnt;                    // [MAXJOBS][ntiles]
   int ntiles_max;
+  // flattened segments (sip_flat.cuh): pass1 = x work + every (set, block);
+  // pass2 = every (global set, block)
+  int nseg1, nseg2;
+  short seg_set[64], seg_blk[64];
+  short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)
 };
 

@@ -17,7 +17,7 @@
 
 #include "../../include/sip.h"
 #include "sip_aux_kernels.cuh"
-#include "sip_vec.cuh"
+#include "sip_flat.cuh"
 
 using namespace sip;
 
@@ -179,6 +179,7 @@ struct Engine : EngineBase {
     Pr.P = P; Pr.p = p;
     Pr.rounds = KeyT<T>::ROUNDS;
     Pr.ntiles_pb = (g.N + BLOCK - 1) / BLOCK;
+    Pr.nseg1 = 0;   // counts (set, block) segments below; +1 for the x segment after
     int njobs = 0;
     for (int i = 0; i < P; ++i) {
       SetD<T>& S = Pr.set[i];
@@ -200,7 +201,12 @@ struct Engine : EngineBase {
       if (S.kind == K_L1 || S.kind == K_CARD) { S.job = njobs++; S.sjob = njobs++; }
       for (int b = 0; b < S.nblk; ++b) Pr.has[S.prim[b]] = 1;
       if (S.global) Pr.nglob++;
+      for (int b = 0; b < S.nblk; ++b) {
+        Pr.seg_set[1 + Pr.nseg1] = (short)i; Pr.seg_blk[1 + Pr.nseg1] = (short)b; Pr.nseg1++;
+        if (S.global) { Pr.seg2_set[Pr.nseg2] = (short)i; Pr.seg2_blk[Pr.nseg2] = (short)b; Pr.nseg2++; }
+      }
     }
+    Pr.nseg1 += 1;   // segment 0: the per-point x work
     // blur mask + compact map
     for (int i = 0; i < p; ++i)
       if (s[i].op == SIP_OP_BLUR_MASK) {
@@ -271,6 +277,7 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
     CU(cudaFuncSetAttribute(k_pass1v<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1f<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
     memset(&hc, 0, sizeof(hc));
     hc.njobs = njobs;
     for (int i = 0; i < P; ++i) {
@@ -365,18 +372,28 @@ struct Engine : EngineBase {
         k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
       }
     }
-    if (vec) k_pass1v<T><<<g_vec, BLOCK, smem_p1, stream>>>(Pr);
+    if (vec) k_pass1f<T><<<g_vec, BLOCK, smem_p1, stream>>>(Pr);
     else k_pass1<T><<<g_pts, BLOCK, smem_p1, stream>>>(Pr);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
-        k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r); ++launches; mark(KB_SELECT);
+        if (vec) k_selectf<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
+        else k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
+        ++launches; mark(KB_SELECT);
       }
       bool card = false;
       for (int i = 0; i < p; ++i) if (Pr.set[i].kind == K_CARD) card = true;
-      if (card) { k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr); ++launches; mark(KB_TIE); }
+      if (card) {
+        if (vec) k_tiecountf<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
+        else k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
+        ++launches; mark(KB_TIE);
+      }
     }
-    if (Pr.nglob > 0) { k_pass2<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); ++launches; mark(KB_PASS2); }
+    if (Pr.nglob > 0) {
+      if (vec) k_pass2f<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr);
+      else k_pass2<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr);
+      ++launches; mark(KB_PASS2);
+    }
     k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches; mark(KB_CTRL);
   }
 
@@ -887,10 +904,17 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     e->hc = c;
     CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     if (S.job >= 0) {
-      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) k_select<T><<<e->g_sel, BLOCK, 0, e->stream>>>(e->Pr, r);
-      if (S.kind == K_CARD) k_tiecount<T><<<e->g_p2, BLOCK, 0, e->stream>>>(e->Pr);
+      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
+        if (e->vec) k_selectf<T><<<e->g_sel, BLOCK, 0, e->stream>>>(e->Pr, r);
+        else k_select<T><<<e->g_sel, BLOCK, 0, e->stream>>>(e->Pr, r);
+      }
+      if (S.kind == K_CARD) {
+        if (e->vec) k_tiecountf<T><<<e->g_p2, BLOCK, 0, e->stream>>>(e->Pr);
+        else k_tiecount<T><<<e->g_p2, BLOCK, 0, e->stream>>>(e->Pr);
+      }
     }
-    k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
+    if (e->vec) k_pass2f<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
+    else k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
   } else {
     // pointwise: gamma = 0 and v = 0 make x-bar = y_old and w = y_old, so
     // pass1 evaluates y = P(w) on the given w placed in y[0]
@@ -904,7 +928,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
       CU(cudaMemsetAsync(S.v[0] + (int64_t)b * G.ld, 0, G.N * sizeof(T), e->stream));
       boff += e->block_len(S.prim[b]);
     }
-    if (e->vec) k_pass1v<T><<<e->g_vec, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
+    if (e->vec) k_pass1f<T><<<e->g_vec, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
     else k_pass1<T><<<e->g_pts, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
   }
   CU(cudaGetLastError());
