@@ -259,22 +259,36 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     const U prefix = (U)J.prefix;
     const bool sums = (J.kind == K_L1);
     const int tot = S.nblk * nch;
-    for (int q = blockIdx.x * BLOCK + threadIdx.x; q < tot; q += gridDim.x * BLOCK) {
-      const int bl = q / nch;
-      const int c = q - bl * nch;
+    // warp-uniform trip count: lanes of a warp aggregate equal buckets
+    // (__match_any_sync) so each distinct bucket costs one shared atomic;
+    // fp32 significands (24 bits) of <= 32 lanes sum exactly in 32 bits
+    for (int q0 = blockIdx.x * BLOCK + (threadIdx.x & ~31); q0 < tot; q0 += gridDim.x * BLOCK) {
+      const int q = q0 + (threadIdx.x & 31);
+      const bool ok = q < tot;
+      const int qq = ok ? q : tot - 1;
+      const int bl = qq / nch;
+      const int c = qq - bl * nch;
       T v[W];
       VT<T>::ldT(buf + (int64_t)bl * g.ld + (int64_t)c * W, v);
 #pragma unroll
       for (int e = 0; e < W; ++e) {
         const U key = K::key(v[e]);
-        if (round > 1 && (U)(key >> plo) != prefix) continue;
-        const int d = (int)((key >> lo) & dmask);
-        atomicAdd(&h_cnt[d], 1u);
+        const bool in = ok && (round == 1 || (U)(key >> plo) == prefix);
+        const int d = in ? (int)((key >> lo) & dmask) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, d);
+        if (d < 0) continue;
+        const bool leader = (threadIdx.x & 31) == (__ffs(grp) - 1);
+        if (leader) atomicAdd(&h_cnt[d], (unsigned)__popc(grp));
         if (sums) {
           unsigned long long sh_, sl_;
           SigT<T>::split(key, &sh_, &sl_);
-          atomicAdd(&h_s0[d], sl_);
-          if (sh_) atomicAdd(&h_s1[d], sh_);
+          if (sizeof(T) == 4) {
+            const unsigned s = __reduce_add_sync(grp, (unsigned)sl_);
+            if (leader) atomicAdd(&h_s0[d], (unsigned long long)s);
+          } else {
+            atomicAdd(&h_s0[d], sl_);
+            if (sh_) atomicAdd(&h_s1[d], sh_);
+          }
         }
       }
     }

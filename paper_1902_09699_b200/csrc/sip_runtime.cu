@@ -276,7 +276,6 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    CU(cudaFuncSetAttribute(k_pass1v<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
     CU(cudaFuncSetAttribute(k_pass1f<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
     memset(&hc, 0, sizeof(hc));
     hc.njobs = njobs;
@@ -361,7 +360,9 @@ struct Engine : EngineBase {
   void enqueue_iteration(int n_cg) {
     if (prof && pev_used == 0) mark(-1);
     if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 0, 0); ++launches; mark(KB_BLUR); }
-    k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr); ++launches; mark(KB_RHS);
+    if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
+    else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
+    ++launches; mark(KB_RHS);
     for (int j = 0; j < n_cg; ++j) {
       if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 1, j); ++launches; mark(KB_BLUR); }
       if (vec) {
