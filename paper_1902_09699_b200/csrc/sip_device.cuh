@@ -187,7 +187,7 @@ __host__ __device__ inline void digit_bits(int total_bits, int r, int* lo, int* 
   *nb = hi - l;
 }
 
-// exact significand split for the bucket sums: value = (s1 * 2^26 + s0) * 2^(e - bias)
+// exact significand split for the bucket sums: value = (s1 * 2^32 + s0) * 2^(e - bias)
 template <class T> struct SigT;
 template <> struct SigT<float> {
   __device__ static void split(uint32_t key, unsigned long long* s_hi, unsigned long long* s_lo) {
@@ -205,8 +205,8 @@ template <> struct SigT<double> {
                                unsigned long long* s_lo) {
     unsigned long long e = key >> 52, m = key & 0xfffffffffffffull;
     unsigned long long sig = (e ? (1ull << 52) : 0ull) | m;
-    *s_hi = sig >> 26;
-    *s_lo = sig & ((1ull << 26) - 1);
+    *s_hi = sig >> 32;
+    *s_lo = sig & 0xffffffffull;
   }
   __device__ static double scale(unsigned long long key) {  // 2^(max(e,1) - 1075)
     int e = (int)(key >> 52);

@@ -129,49 +129,52 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1f(const __grid_constant__ Pro
       VT<T>::ld(xs_rd + pt0, xo);
       prim_chunk<T>(g, prim, xs_rd, pt0, lane, L, xo, s0);
     }
-    const double rho = C.rho[i], gam = C.gamma[i];
-    double a_w2 = 0, a_hv = 0, a_hh = 0, a_vh = 0, a_gv = 0, a_gg = 0, a_vv = 0, a_fn = 0, a_s2 = 0;
+    // per-point arithmetic in the storage precision T (reading L20); the
+    // reductions are summed per chunk in T and accumulated in fp64
+    const T rho = (T)C.rho[i], gam = (T)C.gamma[i], one = (T)1;
+    const T irho = (T)(1.0 / C.rho[i]), i1rho = (T)(1.0 / (1.0 + C.rho[i]));
+    const T tlo = (T)S.lo, thi = (T)S.hi;
+    T a_w2 = 0, a_hv = 0, a_hh = 0, a_vh = 0, a_gv = 0, a_gg = 0, a_vv = 0, a_fn = 0, a_s2 = 0;
     T yn[W], vn[W], wv[W], vh[W], st_s[W];
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       const bool pad = !valid || pad_vec(g, prim, L, e);
-      const double sv = pad ? 0.0 : s[e];
-      st_s[e] = (T)sv;
-      const double yoe = (double)yo[e], voe = (double)vo[e];
-      const double xbar = gam * sv + (1.0 - gam) * yoe;          // relaxation
-      const double w = (double)(T)(xbar - voe / rho);
-      wv[e] = pad ? (T)0 : (T)w;
+      const T sv = pad ? (T)0 : (T)s[e];
+      st_s[e] = sv;
+      const T xbar = gam * sv + (one - gam) * yo[e];                // relaxation
+      // fp64 keeps the exact divisions of the oracle; fp32 uses reciprocals
+      const T w = xbar - (sizeof(T) == 8 ? vo[e] / rho : vo[e] * irho);
+      wv[e] = pad ? (T)0 : w;
       if (pointwise) {
-        double y;
+        T y;
         if (S.kind == K_DIST) {
-          y = ((double)mm[e] + rho * w) / (1.0 + rho);            // Eq. 22
+          y = sizeof(T) == 8 ? (mm[e] + rho * w) / (one + rho) : (mm[e] + rho * w) * i1rho;   // Eq. 22
         } else {
-          const double l = S.lo_vec ? (double)lo[e] : S.lo;
-          const double h = S.hi_vec ? (double)hi[e] : S.hi;
-          y = w < l ? l : (w > h ? h : w);                        // box clamp
+          const T l = S.lo_vec ? lo[e] : tlo;
+          const T h = S.hi_vec ? hi[e] : thi;
+          y = w < l ? l : (w > h ? h : w);                          // box clamp
           if (check && !pad) {
-            const double cl = sv < l ? l : (sv > h ? h : sv);
+            const T cl = sv < l ? l : (sv > h ? h : sv);
             a_fn += (sv - cl) * (sv - cl);
           }
         }
-        const double yt = (double)(T)y;
-        const double vt = (double)(T)(rho * (yt - w));             // Eq. 21 as rho (y - w), L26
-        yn[e] = pad ? (T)0 : (T)yt;
-        vn[e] = pad ? (T)0 : (T)vt;
+        const T vt = rho * (y - w);                                 // Eq. 21 as rho (y - w), L26
+        yn[e] = pad ? (T)0 : y;
+        vn[e] = pad ? (T)0 : vt;
         if (dots && !pad) {
-          const double dg = -(yt - (double)y0[e]);
-          const double dv = vt - (double)v0[e];
+          const T dg = y0[e] - y;
+          const T dv = vt - v0[e];
           a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
         }
       } else if (!pad) {
         a_w2 += w * w;
       }
       if (adapt) {                                                  // Alg. 2 line 1
-        const double vht = (double)(T)(voe + rho * (yoe - sv));
-        vh[e] = pad ? (T)0 : (T)vht;
+        const T vht = vo[e] + rho * (yo[e] - sv);
+        vh[e] = pad ? (T)0 : vht;
         if (dots && !pad) {
-          const double dvh = vht - (double)vh0[e];
-          const double dh = sv - s0[e];
+          const T dvh = vht - vh0[e];
+          const T dh = sv - (T)s0[e];
           a_hv += dh * dvh; a_hh += dh * dh; a_vh += dvh * dvh;
         }
       }
@@ -230,78 +233,148 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1f(const __grid_constant__ Pro
 }
 
 // ------------------------------------------------------------ select (vectorised)
+// Histograms use native 32-bit shared atomics only (64-bit shared atomic add
+// compiles to a CAS spin loop): the significand is split into 16-bit limbs
+// whose per-CTA sums are flushed to 64-bit global atomics every SEL_FLUSH
+// elements (so no 32-bit limb sum can overflow).  Counts and sums stay exact
+// integers, so the result is independent of the accumulation order.
+constexpr int SEL_U = 4;                           // chunks in flight per thread
+constexpr int SEL_FLUSH_IT = 65536 / (BLOCK * 4 * SEL_U);   // iterations between flushes
+
+template <class T> struct Limbs;
+template <> struct Limbs<float> {
+  static constexpr int N = 2;                      // 24-bit significand: 16 + 8 bits
+  __device__ static void split(uint32_t key, unsigned* l) {
+    const uint32_t e = key >> 23, m = key & 0x7fffffu;
+    const uint32_t sig = (e ? (1u << 23) : 0u) | m;
+    l[0] = sig & 0xffffu; l[1] = sig >> 16;
+  }
+};
+template <> struct Limbs<double> {
+  static constexpr int N = 4;                      // 53-bit significand: 4 x 16 bits
+  __device__ static void split(unsigned long long key, unsigned* l) {
+    const unsigned long long e = key >> 52, m = key & 0xfffffffffffffull;
+    const unsigned long long sig = (e ? (1ull << 52) : 0ull) | m;
+    l[0] = (unsigned)(sig & 0xffffu); l[1] = (unsigned)((sig >> 16) & 0xffffu);
+    l[2] = (unsigned)((sig >> 32) & 0xffffu); l[3] = (unsigned)(sig >> 48);
+  }
+};
+
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<T> P, int round) {
   using K = KeyT<T>;
   using U = typename K::U;
+  using LB = Limbs<T>;
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
   __shared__ unsigned h_cnt[NBUCK];
-  __shared__ unsigned long long h_s0[NBUCK];
-  __shared__ unsigned long long h_s1[NBUCK];
+  __shared__ unsigned h_l[LB::N][NBUCK];
   const Geo& g = P.g;
   const bool check = (C.k % C.opt.check_every) == 0;
   int lo, nb, plo = 0, pnb = 0;
   digit_bits(K::BITS, round, &lo, &nb);
   if (round > 1) digit_bits(K::BITS, round - 1, &plo, &pnb);
   const U dmask = (U)((1u << nb) - 1u);
+  const int nbk = 1 << nb;
   const int nch = g.N / W;
   bool any = false;
   for (int jb = 0; jb < C.njobs; ++jb) {
     const Job& J = C.job[jb];
     if (J.mode != JM_SEARCH || J.round != round - 1 || (J.on_s && !check)) continue;
     any = true;
-    for (int d = threadIdx.x; d < NBUCK; d += BLOCK) { h_cnt[d] = 0u; h_s0[d] = 0ull; h_s1[d] = 0ull; }
-    __syncthreads();
+    unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
+    unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
+    unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
     const SetD<T>& S = P.set[J.set];
     const T* buf = J.on_s ? S.s : S.w;
     const U prefix = (U)J.prefix;
     const bool sums = (J.kind == K_L1);
     const int tot = S.nblk * nch;
-    // warp-uniform trip count: lanes of a warp aggregate equal buckets
-    // (__match_any_sync) so each distinct bucket costs one shared atomic;
-    // fp32 significands (24 bits) of <= 32 lanes sum exactly in 32 bits
-    for (int q0 = blockIdx.x * BLOCK + (threadIdx.x & ~31); q0 < tot; q0 += gridDim.x * BLOCK) {
-      const int q = q0 + (threadIdx.x & 31);
-      const bool ok = q < tot;
-      const int qq = ok ? q : tot - 1;
-      const int bl = qq / nch;
-      const int c = qq - bl * nch;
-      T v[W];
-      VT<T>::ldT(buf + (int64_t)bl * g.ld + (int64_t)c * W, v);
+    auto clear = [&]() {
+      for (int d = threadIdx.x; d < nbk; d += BLOCK) {
+        h_cnt[d] = 0u;
 #pragma unroll
-      for (int e = 0; e < W; ++e) {
-        const U key = K::key(v[e]);
-        const bool in = ok && (round == 1 || (U)(key >> plo) == prefix);
-        const int d = in ? (int)((key >> lo) & dmask) : -1;
-        const unsigned grp = __match_any_sync(0xffffffffu, d);
-        if (d < 0) continue;
-        const bool leader = (threadIdx.x & 31) == (__ffs(grp) - 1);
-        if (leader) atomicAdd(&h_cnt[d], (unsigned)__popc(grp));
+        for (int q = 0; q < LB::N; ++q) h_l[q][d] = 0u;
+      }
+    };
+    auto flush = [&]() {
+      __syncthreads();
+      for (int d = threadIdx.x; d < nbk; d += BLOCK) {
+        if (h_cnt[d] == 0u) continue;
+        atomicAdd(gc + d, h_cnt[d]);
         if (sums) {
-          unsigned long long sh_, sl_;
-          SigT<T>::split(key, &sh_, &sl_);
-          if (sizeof(T) == 4) {
-            const unsigned s = __reduce_add_sync(grp, (unsigned)sl_);
-            if (leader) atomicAdd(&h_s0[d], (unsigned long long)s);
-          } else {
-            atomicAdd(&h_s0[d], sl_);
-            if (sh_) atomicAdd(&h_s1[d], sh_);
+          unsigned long long s0 = (unsigned long long)h_l[0][d] + ((unsigned long long)h_l[1][d] << 16);
+          atomicAdd(g0 + d, s0);
+          if (LB::N > 2) {
+            unsigned long long s1 = (unsigned long long)h_l[LB::N > 2 ? 2 : 0][d] +
+                                    ((unsigned long long)h_l[LB::N > 3 ? 3 : 0][d] << 16);
+            if (s1) atomicAdd(g1 + d, s1);
           }
         }
       }
-    }
+      __syncthreads();
+      clear();
+      __syncthreads();
+    };
+    clear();
     __syncthreads();
-    unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
-    unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
-    unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
-    for (int d = threadIdx.x; d < (1 << nb); d += BLOCK) {
-      if (h_cnt[d]) atomicAdd(gc + d, h_cnt[d]);
-      if (h_s0[d]) atomicAdd(g0 + d, h_s0[d]);
-      if (h_s1[d]) atomicAdd(g1 + d, h_s1[d]);
+    const int stride = gridDim.x * BLOCK * SEL_U;
+    int it = 0;
+    // block-uniform trip count (the periodic flush synchronises the CTA)
+    for (int b0 = blockIdx.x * BLOCK * SEL_U; b0 < tot; b0 += stride) {
+      const int q0 = b0 + threadIdx.x;
+      T v[SEL_U][W];
+      bool ok[SEL_U];
+#pragma unroll
+      for (int u = 0; u < SEL_U; ++u) {   // all loads of the iteration first
+        const int q = q0 + u * BLOCK;
+        ok[u] = q < tot;
+        const int qq = ok[u] ? q : tot - 1;
+        const int bl = qq / nch;
+        VT<T>::ldT(buf + (int64_t)bl * g.ld + (int64_t)(qq - bl * nch) * W, v[u]);
+      }
+      // merge runs of equal buckets inside the thread before the atomics
+      int pd = -1;
+      unsigned pc = 0, pl[LB::N];
+#pragma unroll
+      for (int q = 0; q < LB::N; ++q) pl[q] = 0u;
+#pragma unroll
+      for (int u = 0; u < SEL_U; ++u) {
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+          const U key = K::key(v[u][e]);
+          if (!ok[u] || (round > 1 && (U)(key >> plo) != prefix)) continue;
+          const int d = (int)((key >> lo) & dmask);
+          if (d != pd) {
+            if (pd >= 0) {
+              atomicAdd(&h_cnt[pd], pc);
+              if (sums)
+#pragma unroll
+                for (int q = 0; q < LB::N; ++q) if (pl[q]) atomicAdd(&h_l[q][pd], pl[q]);
+            }
+            pd = d; pc = 0;
+#pragma unroll
+            for (int q = 0; q < LB::N; ++q) pl[q] = 0u;
+          }
+          pc += 1;
+          if (sums) {
+            unsigned l[LB::N];
+            LB::split(key, l);
+#pragma unroll
+            for (int q = 0; q < LB::N; ++q) pl[q] += l[q];
+          }
+        }
+      }
+      if (pd >= 0) {
+        atomicAdd(&h_cnt[pd], pc);
+        if (sums)
+#pragma unroll
+          for (int q = 0; q < LB::N; ++q) if (pl[q]) atomicAdd(&h_l[q][pd], pl[q]);
+      }
+      if (++it == SEL_FLUSH_IT) { it = 0; flush(); }
     }
-    __syncthreads();
+    flush();
   }
   if (!any) return;
   if (last_block(P.counter)) {

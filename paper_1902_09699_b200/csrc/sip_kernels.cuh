@@ -538,7 +538,7 @@ __device__ void resolve_round(const Prob<T>& P, Job& J, int round, const unsigne
   for (int d = d0; d < d0 + per && d < nbk; ++d) {
     c_loc += __ldcg(hc + d);
     U kb = (U)(((U)J.prefix << nb) | (U)d) << lo;
-    s_loc += ((double)__ldcg(h1 + d) * 67108864.0 + (double)__ldcg(h0 + d)) * SigT<T>::scale(kb);
+    s_loc += ((double)__ldcg(h1 + d) * 4294967296.0 + (double)__ldcg(h0 + d)) * SigT<T>::scale(kb);
   }
   s_cnt[threadIdx.x] = c_loc;
   s_sum[threadIdx.x] = s_loc;
@@ -559,7 +559,7 @@ __device__ void resolve_round(const Prob<T>& P, Job& J, int round, const unsigne
   for (int d = min(d0 + per, nbk) - 1; d >= d0; --d) {
     U kb = (U)(((U)J.prefix << nb) | (U)d) << lo;
     c_ge += __ldcg(hc + d);
-    s_ge += ((double)__ldcg(h1 + d) * 67108864.0 + (double)__ldcg(h0 + d)) * SigT<T>::scale(kb);
+    s_ge += ((double)__ldcg(h1 + d) * 4294967296.0 + (double)__ldcg(h0 + d)) * SigT<T>::scale(kb);
     bool ok;
     if (J.kind == K_L1) ok = (s_ge - (double)K::val(kb) * (double)c_ge) > J.sigma;  // f(e_d) > sigma
     else ok = c_ge >= J.k;                                                        // C(>=d) >= k
@@ -588,7 +588,7 @@ __device__ void resolve_round(const Prob<T>& P, Job& J, int round, const unsigne
     for (int d = min(d0 + per, nbk) - 1; d > dstar; --d) {
       U kb = (U)(((U)J.prefix << nb) | (U)d) << lo;
       c += __ldcg(hc + d);
-      sm += ((double)__ldcg(h1 + d) * 67108864.0 + (double)__ldcg(h0 + d)) * SigT<T>::scale(kb);
+      sm += ((double)__ldcg(h1 + d) * 4294967296.0 + (double)__ldcg(h0 + d)) * SigT<T>::scale(kb);
     }
     s_cab = c;
     s_sab = sm;
