@@ -964,6 +964,7 @@ template <class T>
 __global__ void k_control(const __grid_constant__ Prob<T> P) {
   Ctrl& C = *P.ctrl;
   if (threadIdx.x != 0 || C.stopped) return;
+  if (C.numeric_err) { C.stopped = 1; return; }   // set by a kernel (variant mismatch)
   const int k = C.k;
   const int Pn = P.P, p = P.p;
   const bool adapt = is_adapt_it(k, C.opt.adapt_every);

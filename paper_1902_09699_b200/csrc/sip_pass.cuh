@@ -1,0 +1,437 @@
+// sip_pass.cuh -- specialised set passes of Algorithm 1 (sm_100a).
+//
+// k_pass1t / k_pass2t are k_pass1f / k_pass2f with the iteration type fixed
+// at graph-capture time: the pattern of adapt iterations (mod(k, 2) = 1,
+// P:291) and stop checks (every 5th) repeats every 10 iterations, so
+// a captured graph of 10 iterations knows, for each launch, whether Alg. 2's
+// inner products and the Eq. 26/27 statistics are needed (template values
+// AD, CK in {0, 1}; 2 = decide at run time from the control block).  Inside,
+// each (set, block) segment dispatches on the set kind to a body compiled
+// for that kind only, so no thread executes predicated code of other kinds.
+// Per-point arithmetic is in the storage type T; every reduction is
+// accumulated in fp64 (reading L20).
+#pragma once
+#include "sip_flat.cuh"
+
+namespace sip {
+
+struct IterFlags { bool adapt, dots, check; };
+
+template <int AD, int CK>
+__device__ __forceinline__ IterFlags iter_flags(Ctrl& C) {
+  const int k = C.k;
+  const bool ad = is_adapt_it(k, C.opt.adapt_every);
+  const bool ck = (k % C.opt.check_every) == 0;
+  if (AD != 2 || CK != 2) {   // the captured variant must match the device iteration
+    if (threadIdx.x == 0 && blockIdx.x == 0 &&
+        ((AD != 2 && ad != (AD == 1)) || (CK != 2 && ck != (CK == 1))))
+      C.numeric_err = 3;
+  }
+  IterFlags f;
+  f.adapt = AD == 2 ? ad : (AD == 1);
+  f.check = CK == 2 ? ck : (CK == 1);
+  f.dots = f.adapt && C.first_adapt_done;
+  return f;
+}
+
+// A_prim x on a chunk in the storage precision (Eq. 8; pads -> 0)
+template <class T>
+__device__ __forceinline__ void prim_chunkT(const Geo& g, int prim, const T* x, int pt0, int lane,
+                                            const Loc& L, const T* xc, T* s) {
+  constexpr int W = VT<T>::W;
+  if (prim == PRIM_I) {
+#pragma unroll
+    for (int e = 0; e < W; ++e) s[e] = xc[e];
+  } else if (prim == PRIM_X) {
+    T xr = __shfl_down_sync(0xffffffffu, xc[0], 1);
+    if (lane == 31) xr = x[pt0 + W];
+    const T ih = (T)g.ihx;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      const T nx_ = e < W - 1 ? xc[e + 1] : xr;
+      s[e] = (L.ix + e < g.nx - 1) ? (nx_ - xc[e]) * ih : (T)0;
+    }
+  } else {
+    const bool z = prim == PRIM_Z;
+    T t[W];
+    VT<T>::ldT(x + pt0 + (z ? g.plane : g.nx), t);
+    const bool hi = z ? (L.gz < g.nz_g - 1) : (L.iy < g.ny - 1);
+    const T ih = (T)(z ? g.ihz : g.ihy);
+#pragma unroll
+    for (int e = 0; e < W; ++e) s[e] = hi ? (t[e] - xc[e]) * ih : (T)0;
+  }
+}
+
+// one (set, block) chunk of pass 1; KIND: 0 box, 1 distance block, 2 global set
+template <class T, int KIND>
+__device__ __forceinline__ void p1_block(const Prob<T>& P, const Ctrl& C, int i, int bl, const IterFlags& f,
+                                         int par, int pt0, bool valid, const Loc& L, int lane,
+                                         const T* xs_rd, const T* xc, double* acc, int nv) {
+  constexpr int W = VT<T>::W;
+  const Geo& g = P.g;
+  const SetD<T>& S = P.set[i];
+  const int prim = S.prim[bl];
+  const int64_t off = (int64_t)bl * g.ld + pt0;
+  const bool pointwise = KIND != 2;
+  T yo[W], vo[W], lo[W], hi[W], mm[W], y0[W], v0[W], vh0[W], xo[W];
+  VT<T>::ldT(S.y[par] + off, yo);
+  VT<T>::ldT(S.v[par] + off, vo);
+  if (KIND == 0 && S.lo_vec) VT<T>::ldT(S.lo_vec + off, lo);
+  if (KIND == 0 && S.hi_vec) VT<T>::ldT(S.hi_vec + off, hi);
+  if (KIND == 1) VT<T>::ldT(P.m + pt0, mm);
+  if (f.dots) {
+    VT<T>::ldT(S.vh0 + off, vh0);
+    VT<T>::ldT(xs_rd + pt0, xo);
+    if (pointwise) {
+      VT<T>::ldT(S.y[par ^ 1] + off, y0);
+      VT<T>::ldT(S.v[par ^ 1] + off, v0);
+    }
+  }
+  T s[W], s0[W];
+  prim_chunkT<T>(g, prim, P.x, pt0, lane, L, xc, s);
+  if (f.dots) prim_chunkT<T>(g, prim, xs_rd, pt0, lane, L, xo, s0);
+  const T rho = (T)C.rho[i], gam = (T)C.gamma[i], one = (T)1;
+  const T irho = (T)(1.0 / C.rho[i]), i1rho = (T)(1.0 / (1.0 + C.rho[i]));
+  const T tlo = (T)S.lo, thi = (T)S.hi;
+  T a_w2 = 0, a_hv = 0, a_hh = 0, a_vh = 0, a_gv = 0, a_gg = 0, a_vv = 0, a_fn = 0, a_s2 = 0;
+  T yn[W], vn[W], wv[W], vh[W], st_s[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const bool pad = !valid || pad_vec(g, prim, L, e);
+    const T sv = pad ? (T)0 : s[e];
+    st_s[e] = sv;
+    const T xbar = gam * sv + (one - gam) * yo[e];                   // relaxation
+    // fp64 keeps the oracle's exact divisions; fp32 multiplies by reciprocals
+    const T w = xbar - (sizeof(T) == 8 ? vo[e] / rho : vo[e] * irho);
+    wv[e] = pad ? (T)0 : w;
+    if (pointwise) {
+      T y;
+      if (KIND == 1) {
+        y = sizeof(T) == 8 ? (mm[e] + rho * w) / (one + rho) : (mm[e] + rho * w) * i1rho;  // Eq. 22
+      } else {
+        const T l = S.lo_vec ? lo[e] : tlo;
+        const T h = S.hi_vec ? hi[e] : thi;
+        y = w < l ? l : (w > h ? h : w);                             // box clamp
+        if (f.check && !pad) {
+          const T cl = sv < l ? l : (sv > h ? h : sv);
+          a_fn += (sv - cl) * (sv - cl);
+        }
+      }
+      const T vt = rho * (y - w);                                    // Eq. 21 as rho (y - w), L26
+      yn[e] = pad ? (T)0 : y;
+      vn[e] = pad ? (T)0 : vt;
+      if (f.dots && !pad) {
+        const T dg = y0[e] - y;
+        const T dv = vt - v0[e];
+        a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+      }
+    } else if (!pad) {
+      a_w2 += w * w;
+    }
+    if (f.adapt) {                                                   // Alg. 2 line 1
+      const T vht = vo[e] + rho * (yo[e] - sv);
+      vh[e] = pad ? (T)0 : vht;
+      if (f.dots && !pad) {
+        const T dvh = vht - vh0[e];
+        const T dh = sv - s0[e];
+        a_hv += dh * dvh; a_hh += dh * dh; a_vh += dvh * dvh;
+      }
+    }
+    if (f.check && !pad) a_s2 += sv * sv;
+  }
+  if (valid) {
+    if (pointwise) {
+      VT<T>::stT(S.y[par ^ 1] + off, yn);
+      VT<T>::stT(S.v[par ^ 1] + off, vn);
+    } else {
+      VT<T>::stT(S.w + off, wv);
+      if (f.check && S.s) VT<T>::stT(S.s + off, st_s);
+    }
+    if (f.adapt) VT<T>::stT(S.vh0 + off, vh);
+  }
+  const int base = i * NSLOT;
+  if (KIND == 2 && (S.kind == K_L2 || S.kind == K_ANN)) warp_acc(acc, nv, base + SLOT_W2, (double)a_w2);
+  if (f.dots) {
+    warp_acc(acc, nv, base + SLOT_HV, (double)a_hv);
+    warp_acc(acc, nv, base + SLOT_HH, (double)a_hh);
+    warp_acc(acc, nv, base + SLOT_VHVH, (double)a_vh);
+    if (pointwise) {
+      warp_acc(acc, nv, base + SLOT_GV, (double)a_gv);
+      warp_acc(acc, nv, base + SLOT_GG, (double)a_gg);
+      warp_acc(acc, nv, base + SLOT_VV, (double)a_vv);
+    }
+  }
+  if (f.check) {
+    if (KIND == 0) warp_acc(acc, nv, base + SLOT_FN, (double)a_fn);
+    warp_acc(acc, nv, base + SLOT_S2, (double)a_s2);
+  }
+}
+
+template <class T, int AD, int CK>
+__global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Prob<T> P) {
+  constexpr int W = VT<T>::W;
+  Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  extern __shared__ double acc[];
+  __shared__ double sh[NWARP + 1];
+  const Geo& g = P.g;
+  const IterFlags f = iter_flags<AD, CK>(C);
+  const int nv = P.P * NSLOT + NEVOL;
+  const int par = C.k & 1;
+  const int a = C.adapt_calls;
+  const T* xs_rd = P.xs[(a + 1) & 1];
+  T* xs_wr = P.xs[a & 1];
+  const int hcount = C.hist_count, hhead = C.hist_head;
+  const int hslot = (hhead + 1) % HIST_S;
+  for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
+  __syncthreads();
+  const int nch = g.N / W;
+  const int gps = (nch + 31) >> 5;                     // warp groups per segment
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * NWARP;
+  const int g0 = blockIdx.x * NWARP + (threadIdx.x >> 5);
+  int seg = g0 / gps, cg = g0 - seg * gps;
+  while (seg < P.nseg1) {
+    const int c = cg * 32 + lane;
+    const bool valid = c < nch;
+    const int pt0 = (valid ? c : nch - 1) * W;
+    const Loc L = locate(g, pt0);
+    T xc[W];
+    VT<T>::ldT(P.x + pt0, xc);
+    if (seg == 0) {   // x history (Eq. 27) and Alg. 2's x snapshot
+      if (f.check) {
+        T h[HIST_S][W];
+#pragma unroll
+        for (int js = 0; js < HIST_S; ++js)
+          if ((hhead - js + HIST_S) % HIST_S < hcount) VT<T>::ldT(P.hist[js] + pt0, h[js]);
+        T x2 = 0;
+#pragma unroll
+        for (int e = 0; e < W; ++e) x2 += valid ? xc[e] * xc[e] : (T)0;
+        warp_acc(acc, nv, P.P * NSLOT, (double)x2);
+#pragma unroll
+        for (int js = 0; js < HIST_S; ++js) {
+          if ((hhead - js + HIST_S) % HIST_S >= hcount) continue;
+          T d2 = 0;
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            const T d = xc[e] - h[js][e];
+            d2 += valid ? d * d : (T)0;
+          }
+          warp_acc(acc, nv, P.P * NSLOT + 1 + js, (double)d2);
+        }
+      }
+      if (valid) {
+        VT<T>::stT(P.hist[hslot] + pt0, xc);
+        if (f.adapt) VT<T>::stT(xs_wr + pt0, xc);
+      }
+    } else {
+      const int i = P.seg_set[seg], bl = P.seg_blk[seg];
+      switch (P.set[i].kind) {
+        case K_BOUNDS: p1_block<T, 0>(P, C, i, bl, f, par, pt0, valid, L, lane, xs_rd, xc, acc, nv); break;
+        case K_DIST: p1_block<T, 1>(P, C, i, bl, f, par, pt0, valid, L, lane, xs_rd, xc, acc, nv); break;
+        default: p1_block<T, 2>(P, C, i, bl, f, par, pt0, valid, L, lane, xs_rd, xc, acc, nv); break;
+      }
+    }
+    cg += nw;
+    while (cg >= gps) { cg -= gps; ++seg; }
+  }
+  double* stage = P.partials + (size_t)gridDim.x * nv;
+  if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
+    for (int v = threadIdx.x; v < nv; v += BLOCK) {
+      const double val = __ldcg(stage + v);
+      if (v < P.P * NSLOT) C.sums[v / NSLOT][v % NSLOT] = val;
+      else C.evol[v - P.P * NSLOT] = val;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < P.P; ++i) {   // l2 / annulus radial factors (Table 1, L7)
+        const int kd = P.set[i].kind;
+        if (kd != K_L2 && kd != K_ANN) continue;
+        const double n = sqrt(__ldcg(stage + i * NSLOT + SLOT_W2));
+        double fct = 1.0;
+        int z = 0;
+        if (n == 0.0) z = (C.sig_lo[i] > 0.0);
+        else if (n > C.sig_hi[i]) fct = C.sig_hi[i] / n;
+        else if (n < C.sig_lo[i]) fct = C.sig_lo[i] / n;
+        C.ann_scale[i] = fct;
+        C.ann_zero[i] = z;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ pass 2
+// KIND: 0 l1 ball (soft threshold at theta), 1 cardinality (keep > tau and the
+// first keep_eq == tau in index order), 2 l2 ball / annulus (radial factor)
+template <class T, int KIND>
+__device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, int bl, int lt, int tpb,
+                                        const IterFlags& f, int par, double* acc, int nv, int* s_w) {
+  using K = KeyT<T>;
+  using U = typename K::U;
+  constexpr int W = VT<T>::W;
+  const Geo& g = P.g;
+  const SetD<T>& S = P.set[i];
+  const int prim = S.prim[bl];
+  const int nch = g.N / W;
+  const int c = lt * BLOCK + threadIdx.x;
+  const bool valid = c < nch;
+  const int pt0 = (valid ? c : nch - 1) * W;
+  const Loc L = locate(g, pt0);
+  const int64_t off = (int64_t)bl * g.ld + pt0;
+  T wv[W], y0[W], v0[W];
+  VT<T>::ldT(S.w + off, wv);
+  if (f.dots) {
+    VT<T>::ldT(S.y[par ^ 1] + off, y0);
+    VT<T>::ldT(S.v[par ^ 1] + off, v0);
+  }
+  bool pad[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) pad[e] = !valid || pad_vec(g, prim, L, e);
+  T y[W];
+  if (KIND == 0) {
+    const Job& J = C.job[S.job];
+    const T th = (T)J.theta;
+    const bool done = J.mode == JM_DONE, keep = (J.mode == JM_INSIDE || J.mode == JM_ALL);
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      const T w = wv[e];
+      if (done) {
+        const T a = (sizeof(T) == 8) ? (T)(fabs((double)w) - J.theta) : fabsf((float)w) - th;
+        y[e] = a > (T)0 ? (w > (T)0 ? a : -a) : (T)0;   // soft threshold
+      } else {
+        y[e] = keep ? w : (T)0;
+      }
+    }
+  } else if (KIND == 1) {
+    const Job& J = C.job[S.job];
+    const U tau = (U)J.tau;
+    bool keep[W];
+    int cnt = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      const U key = K::key(wv[e]);
+      keep[e] = (J.mode == JM_ALL) || (J.mode == JM_DONE && key > tau);
+      cnt += (J.mode == JM_DONE && !pad[e] && key == tau) ? 1 : 0;
+    }
+    if (J.mode == JM_DONE) {
+      if (J.ties) {   // the first keep_eq entries == tau in index order (L6)
+        const int* toff = P.tiecnt + (size_t)S.job * P.ntiles_max;
+        long long r = (long long)toff[bl * tpb + lt] + block_excl_count(cnt, s_w);
+#pragma unroll
+        for (int e = 0; e < W; ++e)
+          if (!pad[e] && K::key(wv[e]) == tau) { if (r < J.keep_eq) keep[e] = true; ++r; }
+      } else {
+#pragma unroll
+        for (int e = 0; e < W; ++e) if (K::key(wv[e]) == tau) keep[e] = true;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < W; ++e) y[e] = keep[e] ? wv[e] : (T)0;
+  } else {
+    const T sc = (T)C.ann_scale[i];
+    const int az = C.ann_zero[i];
+#pragma unroll
+    for (int e = 0; e < W; ++e)
+      y[e] = az ? ((bl == 0 && pt0 + e == S.first_real) ? (T)C.sig_lo[i] : (T)0) : wv[e] * sc;
+  }
+  const T rho = (T)C.rho[i];
+  T yn[W], vn[W];
+  T a_gv = 0, a_gg = 0, a_vv = 0;
+#pragma unroll
+  for (int e = 0; e < W; ++e) {
+    const T yt = pad[e] ? (T)0 : y[e];
+    const T vt = pad[e] ? (T)0 : rho * (yt - wv[e]);    // Eq. 21 as rho (y - w), L26
+    yn[e] = yt;
+    vn[e] = vt;
+    if (f.dots && !pad[e]) {
+      const T dg = y0[e] - yt;
+      const T dv = vt - v0[e];
+      a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+    }
+  }
+  if (valid) {
+    VT<T>::stT(S.y[par ^ 1] + off, yn);
+    VT<T>::stT(S.v[par ^ 1] + off, vn);
+  }
+  if (f.dots) {
+    warp_acc(acc, nv, i * 4 + 0, (double)a_gv);
+    warp_acc(acc, nv, i * 4 + 1, (double)a_gg);
+    warp_acc(acc, nv, i * 4 + 2, (double)a_vv);
+  }
+}
+
+template <class T, int AD, int CK>
+__global__ void __launch_bounds__(BLOCK) k_pass2t(const __grid_constant__ Prob<T> P) {
+  using K = KeyT<T>;
+  using U = typename K::U;
+  constexpr int W = VT<T>::W;
+  Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  extern __shared__ double acc[];
+  __shared__ double sh[NWARP + 1];
+  __shared__ int s_w[NWARP];
+  const Geo& g = P.g;
+  const IterFlags f = iter_flags<AD, CK>(C);
+  const int nv = P.P * 4;
+  const int par = C.k & 1;
+  for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
+  __syncthreads();
+  const int nch = g.N / W;
+  const int tpb = (nch + BLOCK - 1) / BLOCK;
+  int sg = blockIdx.x / tpb, lt = blockIdx.x - sg * tpb;
+  while (sg < P.nseg2) {
+    const int i = P.seg2_set[sg], bl = P.seg2_blk[sg];
+    switch (P.set[i].kind) {
+      case K_L1: p2_tile<T, 0>(P, C, i, bl, lt, tpb, f, par, acc, nv, s_w); break;
+      case K_CARD: p2_tile<T, 1>(P, C, i, bl, lt, tpb, f, par, acc, nv, s_w); break;
+      default: p2_tile<T, 2>(P, C, i, bl, lt, tpb, f, par, acc, nv, s_w); break;
+    }
+    lt += gridDim.x;
+    while (lt >= tpb) { lt -= tpb; ++sg; }
+  }
+  // Eq. 26 numerators of l1 / cardinality sets from s (check iterations)
+  if (f.check) {
+    for (int i = 0; i < P.P; ++i) {
+      const SetD<T>& S = P.set[i];
+      if (!S.global || S.sjob < 0) continue;
+      const Job& Js = C.job[S.sjob];
+      double fn = 0.0;
+      if (Js.mode == JM_DONE) {
+        const int tot = S.nblk * nch;
+        for (int q = blockIdx.x * BLOCK + threadIdx.x; q < tot; q += gridDim.x * BLOCK) {
+          const int bl = q / nch, c = q - bl * nch;
+          T sv[W];
+          VT<T>::ldT(S.s + (int64_t)bl * g.ld + (int64_t)c * W, sv);
+          T a2 = 0;
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            if (S.kind == K_L1) {
+              const T th = (T)Js.theta;
+              const T a = sv[e] < (T)0 ? -sv[e] : sv[e];
+              const T m = a < th ? a : th;
+              a2 += m * m;
+            } else if (K::key(sv[e]) < (U)Js.tau) {
+              a2 += sv[e] * sv[e];
+            }
+          }
+          fn += (double)a2;
+        }
+      }
+      warp_acc(acc, nv, i * 4 + 3, fn);
+    }
+  }
+  double* stage = P.partials + (size_t)gridDim.x * nv;
+  if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
+    for (int v = threadIdx.x; v < nv; v += BLOCK) {
+      const int i = v / 4, q = v % 4;
+      if (!P.set[i].global) continue;
+      const double val = __ldcg(stage + v);
+      if (q == 0) C.sums[i][SLOT_GV] = val;
+      if (q == 1) C.sums[i][SLOT_GG] = val;
+      if (q == 2) C.sums[i][SLOT_VV] = val;
+      if (q == 3 && P.set[i].sjob >= 0) C.sums[i][SLOT_FN] = val;
+    }
+  }
+}
+
+}  // namespace sip

@@ -17,7 +17,7 @@
 
 #include "../../include/sip.h"
 #include "sip_aux_kernels.cuh"
-#include "sip_flat.cuh"
+#include "sip_pass.cuh"
 
 using namespace sip;
 
@@ -52,7 +52,7 @@ struct Options {
   int n_cg = 10, eq25 = 1, fixed_work = 0, adapt_every = 2, check_every = 5;
   double eps_evol = -1.0;       // < 0: 10 * tol
   double cg_tol_floor = -1.0;   // < 0: 10 * eps(dtype)
-  int warm_start = 0, graph_iters = 5, profile = 0;
+  int warm_start = 0, graph_iters = 10, profile = 0;
 };
 
 inline int nblk_of(sip_op op, int ndim) {
@@ -123,6 +123,7 @@ struct Engine : EngineBase {
   cudaGraphExec_t gexec = nullptr;
   int g_iters = 0, g_ncg = -1;
   bool g_prof = false;
+  int g_ce = 0;
   long long launches = 0;       // kernels enqueued by the last project()
   long long graph_kernels = 0;  // kernels in one captured graph
   int last_k = 0;               // Ctrl.k after the last run
@@ -276,7 +277,6 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    CU(cudaFuncSetAttribute(k_pass1f<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
     memset(&hc, 0, sizeof(hc));
     hc.njobs = njobs;
     for (int i = 0; i < P; ++i) {
@@ -357,7 +357,34 @@ struct Engine : EngineBase {
     ++pev_used;
   }
 
-  void enqueue_iteration(int n_cg) {
+  // kernel variants by iteration type: kpos = k (1-based) when the launch
+  // position fixes it, 0 = decide on the device (see sip_pass.cuh)
+  void launch_pass1(int kpos) {
+    if (!vec) { k_pass1<T><<<g_pts, BLOCK, smem_p1, stream>>>(Pr); return; }
+    const int ad = kpos > 0 ? (kpos % 2 == 1) : 2;
+    const int ck = kpos > 0 ? (kpos % hc.opt.check_every == 0) : 2;
+    switch (ad * 3 + ck) {
+      case 0: k_pass1t<T, 0, 0><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
+      case 1: k_pass1t<T, 0, 1><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
+      case 3: k_pass1t<T, 1, 0><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
+      case 4: k_pass1t<T, 1, 1><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
+      default: k_pass1t<T, 2, 2><<<g_vec, BLOCK, smem_p1, stream>>>(Pr);
+    }
+  }
+  void launch_pass2(int kpos) {
+    if (!vec) { k_pass2<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); return; }
+    const int ad = kpos > 0 ? (kpos % 2 == 1) : 2;
+    const int ck = kpos > 0 ? (kpos % hc.opt.check_every == 0) : 2;
+    switch (ad * 3 + ck) {
+      case 0: k_pass2t<T, 0, 0><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
+      case 1: k_pass2t<T, 0, 1><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
+      case 3: k_pass2t<T, 1, 0><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
+      case 4: k_pass2t<T, 1, 1><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
+      default: k_pass2t<T, 2, 2><<<g_p2, BLOCK, smem_p2, stream>>>(Pr);
+    }
+  }
+
+  void enqueue_iteration(int n_cg, int kpos = 0) {
     if (prof && pev_used == 0) mark(-1);
     if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 0, 0); ++launches; mark(KB_BLUR); }
     if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
@@ -373,8 +400,7 @@ struct Engine : EngineBase {
         k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
       }
     }
-    if (vec) k_pass1f<T><<<g_vec, BLOCK, smem_p1, stream>>>(Pr);
-    else k_pass1<T><<<g_pts, BLOCK, smem_p1, stream>>>(Pr);
+    launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
@@ -391,8 +417,7 @@ struct Engine : EngineBase {
       }
     }
     if (Pr.nglob > 0) {
-      if (vec) k_pass2f<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr);
-      else k_pass2<T><<<g_p2, BLOCK, smem_p2, stream>>>(Pr);
+      launch_pass2(kpos);
       ++launches; mark(KB_PASS2);
     }
     k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches; mark(KB_CTRL);
@@ -410,14 +435,18 @@ struct Engine : EngineBase {
   }
 
   void ensure_graph(int iters, int n_cg) {
-    if (gexec && g_iters == iters && g_ncg == n_cg && g_prof == prof) return;
+    if (gexec && g_iters == iters && g_ncg == n_cg && g_prof == prof && g_ce == hc.opt.check_every) return;
     if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
     cudaGraph_t graph;
     long long before = launches;
     pev_used = 0;
     pkind.clear();
     CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < iters; ++i) enqueue_iteration(n_cg);
+    // the adapt / check pattern repeats every lcm(2, check_every) iterations
+    const int ce = std::max(1, hc.opt.check_every);
+    const int period = (ce % 2 == 0) ? ce : 2 * ce;
+    const bool fixed = (iters % period == 0);
+    for (int i = 0; i < iters; ++i) enqueue_iteration(n_cg, fixed ? i + 1 : 0);
     cudaError_t e = cudaStreamEndCapture(stream, &graph);
     if (e != cudaSuccess) throw SipError{SIP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e)};
     graph_kernels = launches - before;
@@ -427,6 +456,7 @@ struct Engine : EngineBase {
     g_iters = iters;
     g_ncg = n_cg;
     g_prof = prof;
+    g_ce = hc.opt.check_every;
   }
 
   void ensure_log(int max_iter) {
@@ -494,7 +524,7 @@ struct Engine : EngineBase {
       // no graph: launch iteration by iteration, poll every check_every
       for (int it = 0; it < max_iter; ++it) {
         if (prof) { pev_used = 0; pkind.clear(); }
-        enqueue_iteration(n_cg);
+        enqueue_iteration(n_cg, it + 1);
         harvest_profile();
         if ((it + 1) % std::max(1, hc.opt.check_every) == 0 || it + 1 == max_iter) {
           CU(cudaMemcpyAsync(h_flag, &d_ctrl->stopped, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -653,7 +683,7 @@ sip_status project_T(sip_grid g, const void* m, void* x, int max_iter, double to
   e->fill_result(res, ms);
   g->have_m = true;
   g->last_launches = e->launches;
-  if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, "NaN/Inf in the PARSDMM state"};
+  if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, e->hc.numeric_err == 3 ? "internal: kernel variant does not match the iteration" : "NaN/Inf in the PARSDMM state"};
   return e->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
 }
 
@@ -731,7 +761,7 @@ sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int ma
     cudaEventDestroy(a); cudaEventDestroy(b);
     if (per_level) e->fill_result(&per_level[l], ms);
     launches += e->launches;
-    if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, "NaN/Inf in the PARSDMM state"};
+    if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, e->hc.numeric_err == 3 ? "internal: kernel variant does not match the iteration" : "NaN/Inf in the PARSDMM state"};
   }
   copy_out(fine, fine->Pr.x, x, N);
   CU(cudaStreamSynchronize(g->stream));
@@ -914,7 +944,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
         else k_tiecount<T><<<e->g_p2, BLOCK, 0, e->stream>>>(e->Pr);
       }
     }
-    if (e->vec) k_pass2f<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
+    if (e->vec) k_pass2t<T, 2, 2><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
     else k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
   } else {
     // pointwise: gamma = 0 and v = 0 make x-bar = y_old and w = y_old, so
@@ -929,7 +959,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
       CU(cudaMemsetAsync(S.v[0] + (int64_t)b * G.ld, 0, G.N * sizeof(T), e->stream));
       boff += e->block_len(S.prim[b]);
     }
-    if (e->vec) k_pass1f<T><<<e->g_vec, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
+    if (e->vec) k_pass1t<T, 2, 2><<<e->g_vec, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
     else k_pass1<T><<<e->g_pts, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
   }
   CU(cudaGetLastError());

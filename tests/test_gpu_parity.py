@@ -284,3 +284,47 @@ def _abs(sd, prob):
     if sd.kind == "card":
         s.k = int(np.floor(sd.k_frac * a.size))
     return s
+
+
+# ------------------------------------------------------------ multilevel (Algorithm 3)
+ML_CASES = [
+    ((16, 16), 2, ("bounds", "l1", "slope")),
+    ((8, 8, 8), 2, ("bounds", "l1", "slope", "cardz", "annulus")),
+    ((16, 8, 16), 3, ("bounds", "l1", "slope")),
+]
+
+
+@pytest.mark.parametrize("shape,levels,kinds", ML_CASES)
+def test_multilevel_matches_oracle(shape, levels, kinds):
+    prob = G.tiny(120 + len(shape) + levels, shape, kinds)
+    g = grid_for(prob)
+    m = dev(prob.m, "f64")
+    x = torch.empty_like(m)
+    per, st = g.project_multilevel(m, x, levels, max_iter=200, tol=1e-3)
+    xo, sto, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, levels, **prob.options)
+    for l in range(levels):
+        assert per[l]["iterations"] == logs[l].iterations, (l, per[l]["iterations"], logs[l].iterations)
+        assert per[l]["cg_iterations"] == logs[l].cg_total
+    assert rel(host(x), xo) < 1e-6
+
+
+def test_multilevel_one_level_equals_zero_init_single_level():
+    prob = G.tiny(131, (8, 8), ("bounds", "l1", "slope"))
+    g = grid_for(prob)
+    m = dev(prob.m, "f64")
+    x1 = torch.empty_like(m)
+    g.project_multilevel(m, x1, 1, max_iter=200)
+    xo, _, _ = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 1, **prob.options)
+    assert rel(host(x1), xo) < 1e-9
+
+
+def test_multilevel_fp32_small_c5_like():
+    prob = G.c5(seed=4, shape=(32, 32, 16))
+    x_ref, _, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3,
+                                          **oracle_opts(prob))
+    g = grid_for(prob)
+    m = dev(prob.m, "f32")
+    x = torch.empty_like(m)
+    per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
+    assert rel(host(x), x_ref) < 1e-3
+    assert [p["iterations"] for p in per] == [lg.iterations for lg in logs]
