@@ -495,7 +495,7 @@ struct Engine : EngineBase {
       c.u_k[i] = hs.prm.k;
       c.rel[i] = hs.prm.relative;
       c.zin[i] = hs.zero_in;
-      c.mreal[i] = hs.M;
+      c.mreal[i] = set_len(i);   // compact M on this level's grid (k = floor(k_frac M_l), L23)
     }
     c.mreal[p] = Pr.g.N;
     make_coeffs(Pr, c.rho, &c.cI, &c.cz, &c.cy, &c.cx, &c.cF);
@@ -623,7 +623,8 @@ struct sip_grid_s {
   std::vector<HostSet> sets;
   Options opt;
   std::string err;
-  std::unique_ptr<EngineBase> eng;                 // finest level
+  std::unique_ptr<EngineBase> eng;                 // single-level engine
+  EngineBase* last = nullptr;                      // engine of the last projection (finest level)
   std::vector<std::unique_ptr<EngineBase>> levels; // multilevel (index 0 = finest)
   bool have_m = false;
   long long last_launches = 0;
@@ -683,6 +684,7 @@ sip_status project_T(sip_grid g, const void* m, void* x, int max_iter, double to
   e->fill_result(res, ms);
   g->have_m = true;
   g->last_launches = e->launches;
+  g->last = e;
   if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, e->hc.numeric_err == 3 ? "internal: kernel variant does not match the iteration" : "NaN/Inf in the PARSDMM state"};
   return e->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
 }
@@ -693,6 +695,7 @@ sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int ma
   // level grids: each axis halves (y stays 1 in 2D), h doubles (reading L2)
   if ((int)g->levels.size() != n_levels) {
     g->levels.clear();
+    g->last = nullptr;
     for (int l = 0; l < n_levels; ++l) {
       auto e = std::make_unique<Engine<T>>();
       const int f = 1 << l;
@@ -766,6 +769,7 @@ sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int ma
   copy_out(fine, fine->Pr.x, x, N);
   CU(cudaStreamSynchronize(g->stream));
   g->last_launches = launches;
+  g->last = fine;
   return fine->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
 }
 
@@ -980,8 +984,13 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
 }
 
 template <class T>
+Engine<T>* last_engine(sip_grid g) {
+  return g->last ? static_cast<Engine<T>*>(g->last) : engine_of<T>(g);
+}
+
+template <class T>
 sip_status get_state_T(sip_grid g, int set_id, int which, void* out) {
-  Engine<T>* e = engine_of<T>(g);
+  Engine<T>* e = last_engine<T>(g);
   if (!e->ran) throw SipError{SIP_ERR_STATE, "no projection state"};
   const Geo& G = e->Pr.g;
   const SetD<T>& S = e->Pr.set[set_id];
@@ -1003,7 +1012,7 @@ sip_status get_state_T(sip_grid g, int set_id, int which, void* out) {
 template <class T>
 sip_status get_log_T(sip_grid g, int max_iter, int* cg, int* branch, double* rho_t, double* gam_t,
                      double* feas, double* evol) {
-  Engine<T>* e = engine_of<T>(g);
+  Engine<T>* e = last_engine<T>(g);
   if (!e->ran) throw SipError{SIP_ERR_STATE, "no projection log"};
   const int n = std::min(max_iter, e->log_cap);
   const int P = e->P, p = e->p;
@@ -1163,6 +1172,7 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type 
     g->sets.push_back(std::move(hs));
     g->eng.reset();
     g->levels.clear();
+    g->last = nullptr;
     if (set_id) *set_id = (int)g->sets.size() - 1;
     return SIP_OK;
   });
@@ -1289,15 +1299,15 @@ sip_status sip_get_sizes(sip_grid g, int* p, int64_t* n_local, int set_id, int64
 sip_status sip_get_profile(sip_grid g, int n, double* ms, int64_t* count) {
   if (!g || n < 0) return SIP_ERR_ARG;
   return guarded(g, [&]() -> sip_status {
-    if (!g->eng) throw SipError{SIP_ERR_STATE, "no projection"};
+    if (!g->last) throw SipError{SIP_ERR_STATE, "no projection"};
     auto fill = [&](auto* e) {
       for (int q = 0; q < n && q < 9; ++q) {
         if (ms) ms[q] = e->prof_ms[q];
         if (count) count[q] = e->prof_cnt[q];
       }
     };
-    if (g->dtype == SIP_F32) fill(static_cast<Engine<float>*>(g->eng.get()));
-    else fill(static_cast<Engine<double>*>(g->eng.get()));
+    if (g->dtype == SIP_F32) fill(static_cast<Engine<float>*>(g->last));
+    else fill(static_cast<Engine<double>*>(g->last));
     return SIP_OK;
   });
 }
