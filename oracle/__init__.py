@@ -53,7 +53,7 @@ class Set(C.Structure):
         ("sigma", C.c_double), ("sigma_lo", C.c_double), ("sigma_hi", C.c_double),
         ("k", C.c_int64), ("relative", C.c_int), ("k_frac", C.c_double),
         ("kernel", C.POINTER(C.c_double)), ("kh", C.c_int), ("kw", C.c_int),
-        ("mask", C.POINTER(C.c_ubyte)),
+        ("mask", C.POINTER(C.c_ubyte)), ("key_f32", C.c_int),
     ]
 
 
@@ -65,6 +65,7 @@ class Options(C.Structure):
         ("adapt_every", C.c_int), ("check_every", C.c_int), ("hist_s", C.c_int),
         ("rho_ratio_cap", C.c_double), ("gamma_max", C.c_double),
         ("eq25", C.c_int), ("fixed_work", C.c_int), ("cg_tol_floor", C.c_double),
+        ("decide_f32", C.c_int),
     ]
 
 

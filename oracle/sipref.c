@@ -55,6 +55,7 @@ void sipref_default_options(sipref_options *o) {
   o->eq25 = 1;
   o->fixed_work = 0;
   o->cg_tol_floor = 10.0 * DBL_EPSILON; /* reading L18 (fp32 runs: 10*FLT_EPSILON) */
+  o->decide_f32 = 0;
 }
 
 /* ------------------------------------------------------------------ */
@@ -296,10 +297,15 @@ static int cmp_keyidx(const void *pa, const void *pb) {
   if (a->a < b->a) return 1;
   return (a->i > b->i) - (a->i < b->i);
 }
-static void proj_card(int64_t M, const double *w, int64_t k, double *y) {
+/* key_f32 (reading L27): the ranking is taken on |w| rounded to fp32, the
+   precision in which an fp32 run takes the same integer decision */
+static void proj_card(int64_t M, const double *w, int64_t k, int key_f32, double *y) {
   if (k >= M) { memcpy(y, w, (size_t)M * sizeof(double)); return; }
   keyidx *t = (keyidx *)malloc((size_t)(M > 0 ? M : 1) * sizeof(keyidx));
-  for (int64_t i = 0; i < M; ++i) { t[i].a = fabs(w[i]); t[i].i = i; }
+  for (int64_t i = 0; i < M; ++i) {
+    t[i].a = key_f32 ? (double)(float)fabs(w[i]) : fabs(w[i]);
+    t[i].i = i;
+  }
   qsort(t, (size_t)M, sizeof(keyidx), cmp_keyidx);
   memset(y, 0, (size_t)M * sizeof(double));
   for (int64_t j = 0; j < k; ++j) y[t[j].i] = w[t[j].i];
@@ -336,7 +342,7 @@ void sipref_project(const sipref_set *s, int64_t M, const double *w, double *y) 
       for (int64_t i = 0; i < M; ++i) y[i] = w[i] * f;
       break;
     }
-    case SIPREF_CARD: proj_card(M, w, s->k, y); break;
+    case SIPREF_CARD: proj_card(M, w, s->k, s->key_f32, y); break;
   }
 }
 
@@ -515,6 +521,7 @@ static int parsdmm_run(const sipref_grid *g, int p, const sipref_set *in_sets,
   int64_t *M = (int64_t *)calloc((size_t)P, sizeof(int64_t));
   for (int i = 0; i < p; ++i) {
     resolve_set(g, &in_sets[i], m, &sets[i]);
+    sets[i].key_f32 = o->decide_f32;
     M[i] = sipref_op_len(g, &sets[i]);
   }
   sets[p].op = SIPREF_OP_I;

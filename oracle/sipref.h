@@ -49,6 +49,8 @@ typedef struct {
   double k_frac;
   const double *kernel; int kh, kw;  /* BLUR_MASK: kh x kw kernel, row major */
   const unsigned char *mask;         /* BLUR_MASK: N bytes, 1 = observed     */
+  int key_f32;                       /* CARD: rank |w| rounded to fp32 (set by
+                                        the solver from options.decide_f32)  */
 } sipref_set;
 
 typedef struct {
@@ -59,6 +61,8 @@ typedef struct {
   int eq25;        /* 1: CG stops by Eq. 25; 0: exactly n_cg iterations    */
   int fixed_work;  /* 1: stop test evaluated but never acted on            */
   double cg_tol_floor; /* floor of the Eq. 25 target (10*eps of the dtype)  */
+  int decide_f32;      /* 1: integer decisions (cardinality support) taken on
+                          fp32-rounded keys, as an fp32 run takes them (L27) */
 } sipref_options;
 
 typedef struct {
