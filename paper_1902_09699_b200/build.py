@@ -10,7 +10,6 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsip.so")
 SOURCES = ["sip_runtime.cu"]
-DEPS = ["sip_runtime.cu", "sip_kernels.cuh", "sip_device.cuh", "sip_aux_kernels.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -23,7 +22,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, d) for d in DEPS] + [os.path.join(ROOT, "include", "sip.h")]
+    deps = [os.path.join(CSRC, d) for d in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "sip.h"),
+                                                                os.path.abspath(__file__)]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 

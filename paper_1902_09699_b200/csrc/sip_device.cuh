@@ -123,6 +123,7 @@ struct Job {
   long long cnt_eq;              // entries == tau
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
+  unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
 };
 
 struct Ctrl {

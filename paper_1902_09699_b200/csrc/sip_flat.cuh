@@ -41,6 +41,24 @@ __device__ __forceinline__ void prim_chunk(const Geo& g, int prim, const T* x, i
   }
 }
 
+// exclusive rank of this thread's flags within the CTA tile (fixed order:
+// warps in order, lanes in order, elements in order)
+__device__ __forceinline__ int block_excl_count(int cnt, int* s_w) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) s_w[wp] = inc;
+  __syncthreads();
+  int before = 0;
+  for (int q = 0; q < wp; ++q) before += s_w[q];
+  __syncthreads();
+  return before + inc - cnt;
+}
+
 template <class T>
 __global__ void __launch_bounds__(BLOCK, 2) k_pass1f(const __grid_constant__ Prob<T> P) {
   constexpr int W = VT<T>::W;
@@ -270,6 +288,8 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
   if (C.stopped) return;
   __shared__ unsigned h_cnt[NBUCK];
   __shared__ unsigned h_l[LB::N][NBUCK];
+  __shared__ int s_wc[NWARP];
+  __shared__ unsigned s_base;
   const Geo& g = P.g;
   const bool check = (C.k % C.opt.check_every) == 0;
   int lo, nb, plo = 0, pnb = 0;
@@ -321,57 +341,90 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     __syncthreads();
     const int stride = gridDim.x * BLOCK * SEL_U;
     int it = 0;
-    // block-uniform trip count (the periodic flush synchronises the CTA)
-    for (int b0 = blockIdx.x * BLOCK * SEL_U; b0 < tot; b0 += stride) {
-      const int q0 = b0 + threadIdx.x;
-      T v[SEL_U][W];
-      bool ok[SEL_U];
-#pragma unroll
-      for (int u = 0; u < SEL_U; ++u) {   // all loads of the iteration first
-        const int q = q0 + u * BLOCK;
-        ok[u] = q < tot;
-        const int qq = ok[u] ? q : tot - 1;
-        const int bl = qq / nch;
-        VT<T>::ldT(buf + (int64_t)bl * g.ld + (int64_t)(qq - bl * nch) * W, v[u]);
-      }
-      // merge runs of equal buckets inside the thread before the atomics
-      int pd = -1;
-      unsigned pc = 0, pl[LB::N];
-#pragma unroll
-      for (int q = 0; q < LB::N; ++q) pl[q] = 0u;
-#pragma unroll
-      for (int u = 0; u < SEL_U; ++u) {
-#pragma unroll
-        for (int e = 0; e < W; ++e) {
-          const U key = K::key(v[u][e]);
-          if (!ok[u] || (round > 1 && (U)(key >> plo) != prefix)) continue;
-          const int d = (int)((key >> lo) & dmask);
-          if (d != pd) {
-            if (pd >= 0) {
-              atomicAdd(&h_cnt[pd], pc);
-              if (sums)
-#pragma unroll
-                for (int q = 0; q < LB::N; ++q) if (pl[q]) atomicAdd(&h_l[q][pd], pl[q]);
-            }
-            pd = d; pc = 0;
-#pragma unroll
-            for (int q = 0; q < LB::N; ++q) pl[q] = 0u;
-          }
-          pc += 1;
-          if (sums) {
-            unsigned l[LB::N];
-            LB::split(key, l);
-#pragma unroll
-            for (int q = 0; q < LB::N; ++q) pl[q] += l[q];
-          }
-        }
-      }
+    // fp32 candidate compaction: round 2 appends the keys of the round-1
+    // bucket (its survivors), rounds >= 3 read only those
+    unsigned* cand = (sizeof(T) == 4) ? P.cand[jb] : nullptr;
+    const bool make_cand = cand && round == 2;
+    const bool use_cand = cand && round >= 3;
+    const int ntot = use_cand ? (int)J.cand_n : tot;
+    int pd = -1;
+    unsigned pc = 0, pl[LB::N];
+    auto hflush = [&]() {
       if (pd >= 0) {
         atomicAdd(&h_cnt[pd], pc);
         if (sums)
 #pragma unroll
           for (int q = 0; q < LB::N; ++q) if (pl[q]) atomicAdd(&h_l[q][pd], pl[q]);
       }
+    };
+    auto hkey = [&](U key) {   // merge runs of equal buckets inside the thread
+      const int d = (int)((key >> lo) & dmask);
+      if (d != pd) {
+        hflush();
+        pd = d; pc = 0;
+#pragma unroll
+        for (int q = 0; q < LB::N; ++q) pl[q] = 0u;
+      }
+      pc += 1;
+      if (sums) {
+        unsigned l[LB::N];
+        LB::split(key, l);
+#pragma unroll
+        for (int q = 0; q < LB::N; ++q) pl[q] += l[q];
+      }
+    };
+    // block-uniform trip count (the periodic flush synchronises the CTA)
+    for (int b0 = blockIdx.x * BLOCK * SEL_U; b0 < ntot; b0 += stride) {
+      const int q0 = b0 + threadIdx.x;
+      pd = -1; pc = 0;
+      if (use_cand) {
+        U kk[SEL_U];
+        bool ok[SEL_U];
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u) {
+          const int q = q0 + u * BLOCK;
+          ok[u] = q < ntot;
+          kk[u] = ok[u] ? (U)__ldcg(cand + q) : (U)0;
+        }
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u)
+          if (ok[u] && (U)(kk[u] >> plo) == prefix) hkey(kk[u]);
+      } else {
+        T v[SEL_U][W];
+        bool ok[SEL_U];
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u) {   // all loads of the iteration first
+          const int q = q0 + u * BLOCK;
+          ok[u] = q < tot;
+          const int qq = ok[u] ? q : tot - 1;
+          const int bl = qq / nch;
+          VT<T>::ldT(buf + (int64_t)bl * g.ld + (int64_t)(qq - bl * nch) * W, v[u]);
+        }
+        unsigned mine = 0;   // survivors of this thread (bit u*W+e)
+#pragma unroll
+        for (int u = 0; u < SEL_U; ++u) {
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            const U key = K::key(v[u][e]);
+            const bool in = ok[u] && (round == 1 || (U)(key >> plo) == prefix);
+            if (in) { hkey(key); mine |= 1u << (u * W + e); }
+          }
+        }
+        if (make_cand) {   // CTA-aggregated append: one global atomic per CTA iteration
+          const int cnt = __popc(mine);
+          const int before = block_excl_count(cnt, s_wc);
+          if (threadIdx.x == BLOCK - 1) s_base = atomicAdd(&C.job[jb].cand_n, (unsigned)(before + cnt));
+          __syncthreads();
+          unsigned pos = s_base + before;
+#pragma unroll
+          for (int u = 0; u < SEL_U; ++u)
+#pragma unroll
+            for (int e = 0; e < W; ++e)
+              if (mine & (1u << (u * W + e))) cand[pos++] = (unsigned)K::key(v[u][e]);
+          __syncthreads();
+        }
+      }
+      hflush();
       if (++it == SEL_FLUSH_IT) { it = 0; flush(); }
     }
     flush();
@@ -393,24 +446,6 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
 }
 
 // ------------------------------------------------------------ ties / pass2 (CTA tiles)
-// exclusive rank of this thread's flags within the CTA tile (fixed order:
-// warps in order, lanes in order, elements in order)
-__device__ __forceinline__ int block_excl_count(int cnt, int* s_w) {
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  int inc = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int t = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += t;
-  }
-  if (lane == 31) s_w[wp] = inc;
-  __syncthreads();
-  int before = 0;
-  for (int q = 0; q < wp; ++q) before += s_w[q];
-  __syncthreads();
-  return before + inc - cnt;
-}
-
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_tiecountf(const __grid_constant__ Prob<T> P) {
   using K = KeyT<T>;

@@ -47,6 +47,10 @@ struct Prob {
   // flattened segments (sip_flat.cuh): pass1 = x work + every (set, block);
   // pass2 = every (global set, block)
   int nseg1, nseg2;
+  // fused round 1 of the radix search in pass 1 (fp32): smem histogram per
+  // w-job at dynamic smem offset h1_off (bytes); cand[job] = round-2 survivors
+  int fuse_r1, h1_off;
+  unsigned* cand[MAXJOBS];
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)
@@ -948,7 +952,7 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
   for (int jb = 0; jb < C.njobs; ++jb) {
     Job& J = C.job[jb];
     const int i = J.set;
-    J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0;
+    J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u;
     J.theta = 0.0; J.tau = 0ull; J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0.0;
     J.sigma = C.sigma[i];
     J.k = C.kcard[i];

@@ -62,108 +62,161 @@ __device__ __forceinline__ void prim_chunkT(const Geo& g, int prim, const T* x, 
   }
 }
 
-// one (set, block) chunk of pass 1; KIND: 0 box, 1 distance block, 2 global set
+// chunks per thread per warp group of pass 1 (amortises the per-group setup)
+constexpr int P1_U = 4;
+
+// PU chunks (stride 32) of one (set, block) segment; KIND: 0 box, 1 distance
+// block, 2 global set.  Reductions are summed in T per chunk, in fp64 across
+// chunks, and reduced across the warp once per group.
 template <class T, int KIND>
-__device__ __forceinline__ void p1_block(const Prob<T>& P, const Ctrl& C, int i, int bl, const IterFlags& f,
-                                         int par, int pt0, bool valid, const Loc& L, int lane,
-                                         const T* xs_rd, const T* xc, double* acc, int nv) {
+__device__ __forceinline__ void p1_seg(const Prob<T>& P, const Ctrl& C, int i, int bl, const IterFlags& f,
+                                       int par, int cbase, int nch, int lane, const T* xs_rd, double* acc,
+                                       int nv, unsigned* h1) {
   constexpr int W = VT<T>::W;
   const Geo& g = P.g;
   const SetD<T>& S = P.set[i];
   const int prim = S.prim[bl];
-  const int64_t off = (int64_t)bl * g.ld + pt0;
   const bool pointwise = KIND != 2;
-  T yo[W], vo[W], lo[W], hi[W], mm[W], y0[W], v0[W], vh0[W], xo[W];
-  VT<T>::ldT(S.y[par] + off, yo);
-  VT<T>::ldT(S.v[par] + off, vo);
-  if (KIND == 0 && S.lo_vec) VT<T>::ldT(S.lo_vec + off, lo);
-  if (KIND == 0 && S.hi_vec) VT<T>::ldT(S.hi_vec + off, hi);
-  if (KIND == 1) VT<T>::ldT(P.m + pt0, mm);
-  if (f.dots) {
-    VT<T>::ldT(S.vh0 + off, vh0);
-    VT<T>::ldT(xs_rd + pt0, xo);
-    if (pointwise) {
-      VT<T>::ldT(S.y[par ^ 1] + off, y0);
-      VT<T>::ldT(S.v[par ^ 1] + off, v0);
-    }
-  }
-  T s[W], s0[W];
-  prim_chunkT<T>(g, prim, P.x, pt0, lane, L, xc, s);
-  if (f.dots) prim_chunkT<T>(g, prim, xs_rd, pt0, lane, L, xo, s0);
+  const T* yr = S.y[par] + (int64_t)bl * g.ld;
+  const T* vr = S.v[par] + (int64_t)bl * g.ld;
+  T* yw = S.y[par ^ 1] + (int64_t)bl * g.ld;
+  T* vw = S.v[par ^ 1] + (int64_t)bl * g.ld;
+  T* vhp = S.vh0 + (int64_t)bl * g.ld;
+  T* wp = S.w ? S.w + (int64_t)bl * g.ld : nullptr;
+  T* sp = S.s ? S.s + (int64_t)bl * g.ld : nullptr;
+  const T* lop = S.lo_vec ? S.lo_vec + (int64_t)bl * g.ld : nullptr;
+  const T* hip = S.hi_vec ? S.hi_vec + (int64_t)bl * g.ld : nullptr;
   const T rho = (T)C.rho[i], gam = (T)C.gamma[i], one = (T)1;
   const T irho = (T)(1.0 / C.rho[i]), i1rho = (T)(1.0 / (1.0 + C.rho[i]));
   const T tlo = (T)S.lo, thi = (T)S.hi;
-  T a_w2 = 0, a_hv = 0, a_hh = 0, a_vh = 0, a_gv = 0, a_gg = 0, a_vv = 0, a_fn = 0, a_s2 = 0;
-  T yn[W], vn[W], wv[W], vh[W], st_s[W];
+  // fused round 1 of the radix search on w (fp32; see k_selectf): smem
+  // histogram of the top 11 key bits, count + significand offset in 10-bit limbs
+  unsigned* hc = (KIND == 2 && h1 && S.job >= 0) ? h1 + (S.job >> 1) * 3 * NBUCK : nullptr;
+  const bool hsum = S.kind == K_L1;
+  double d_w2 = 0, d_hv = 0, d_hh = 0, d_vh = 0, d_gv = 0, d_gg = 0, d_vv = 0, d_fn = 0, d_s2 = 0;
+#pragma unroll 1
+  for (int u = 0; u < P1_U; ++u) {
+    const int c = cbase + u * 32 + lane;
+    const bool valid = c < nch;
+    const int pt0 = (valid ? c : nch - 1) * W;
+    const Loc L = locate(g, pt0);
+    T xc[W], yo[W], vo[W], lo[W], hi[W], mm[W], y0[W], v0[W], vh0[W], xo[W];
+    VT<T>::ldT(P.x + pt0, xc);
+    VT<T>::ldT(yr + pt0, yo);
+    VT<T>::ldT(vr + pt0, vo);
+    if (KIND == 0 && lop) VT<T>::ldT(lop + pt0, lo);
+    if (KIND == 0 && hip) VT<T>::ldT(hip + pt0, hi);
+    if (KIND == 1) VT<T>::ldT(P.m + pt0, mm);
+    if (f.dots) {
+      VT<T>::ldT(vhp + pt0, vh0);
+      VT<T>::ldT(xs_rd + pt0, xo);
+      if (pointwise) {
+        VT<T>::ldT(yw + pt0, y0);
+        VT<T>::ldT(vw + pt0, v0);
+      }
+    }
+    T s[W], s0[W];
+    prim_chunkT<T>(g, prim, P.x, pt0, lane, L, xc, s);
+    if (f.dots) prim_chunkT<T>(g, prim, xs_rd, pt0, lane, L, xo, s0);
+    T a_w2 = 0, a_hv = 0, a_hh = 0, a_vh = 0, a_gv = 0, a_gg = 0, a_vv = 0, a_fn = 0, a_s2 = 0;
+    T yn[W], vn[W], wv[W], vh[W], st_s[W];
 #pragma unroll
-  for (int e = 0; e < W; ++e) {
-    const bool pad = !valid || pad_vec(g, prim, L, e);
-    const T sv = pad ? (T)0 : s[e];
-    st_s[e] = sv;
-    const T xbar = gam * sv + (one - gam) * yo[e];                   // relaxation
-    // fp64 keeps the oracle's exact divisions; fp32 multiplies by reciprocals
-    const T w = xbar - (sizeof(T) == 8 ? vo[e] / rho : vo[e] * irho);
-    wv[e] = pad ? (T)0 : w;
-    if (pointwise) {
-      T y;
-      if (KIND == 1) {
-        y = sizeof(T) == 8 ? (mm[e] + rho * w) / (one + rho) : (mm[e] + rho * w) * i1rho;  // Eq. 22
-      } else {
-        const T l = S.lo_vec ? lo[e] : tlo;
-        const T h = S.hi_vec ? hi[e] : thi;
-        y = w < l ? l : (w > h ? h : w);                             // box clamp
-        if (f.check && !pad) {
-          const T cl = sv < l ? l : (sv > h ? h : sv);
-          a_fn += (sv - cl) * (sv - cl);
+    for (int e = 0; e < W; ++e) {
+      const bool pad = !valid || pad_vec(g, prim, L, e);
+      const T sv = pad ? (T)0 : s[e];
+      st_s[e] = sv;
+      const T xbar = gam * sv + (one - gam) * yo[e];                   // relaxation
+      // fp64 keeps the oracle's exact divisions; fp32 multiplies by reciprocals
+      const T w = xbar - (sizeof(T) == 8 ? vo[e] / rho : vo[e] * irho);
+      wv[e] = pad ? (T)0 : w;
+      if (pointwise) {
+        T y;
+        if (KIND == 1) {
+          y = sizeof(T) == 8 ? (mm[e] + rho * w) / (one + rho) : (mm[e] + rho * w) * i1rho;  // Eq. 22
+        } else {
+          const T l = lop ? lo[e] : tlo;
+          const T h = hip ? hi[e] : thi;
+          y = w < l ? l : (w > h ? h : w);                             // box clamp
+          if (f.check && !pad) {
+            const T cl = sv < l ? l : (sv > h ? h : sv);
+            a_fn += (sv - cl) * (sv - cl);
+          }
+        }
+        const T vt = rho * (y - w);                                    // Eq. 21 as rho (y - w), L26
+        yn[e] = pad ? (T)0 : y;
+        vn[e] = pad ? (T)0 : vt;
+        if (f.dots && !pad) {
+          const T dg = y0[e] - y;
+          const T dv = vt - v0[e];
+          a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+        }
+      } else if (!pad) {
+        a_w2 += w * w;
+      }
+      if (f.adapt) {                                                   // Alg. 2 line 1
+        const T vht = vo[e] + rho * (yo[e] - sv);
+        vh[e] = pad ? (T)0 : vht;
+        if (f.dots && !pad) {
+          const T dvh = vht - vh0[e];
+          const T dh = sv - s0[e];
+          a_hv += dh * dvh; a_hh += dh * dh; a_vh += dvh * dvh;
         }
       }
-      const T vt = rho * (y - w);                                    // Eq. 21 as rho (y - w), L26
-      yn[e] = pad ? (T)0 : y;
-      vn[e] = pad ? (T)0 : vt;
-      if (f.dots && !pad) {
-        const T dg = y0[e] - y;
-        const T dv = vt - v0[e];
-        a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+      if (f.check && !pad) a_s2 += sv * sv;
+    }
+    if (valid) {
+      if (pointwise) {
+        VT<T>::stT(yw + pt0, yn);
+        VT<T>::stT(vw + pt0, vn);
+      } else {
+        VT<T>::stT(wp + pt0, wv);
+        if (f.check && sp) VT<T>::stT(sp + pt0, st_s);
       }
-    } else if (!pad) {
-      a_w2 += w * w;
+      if (f.adapt) VT<T>::stT(vhp + pt0, vh);
     }
-    if (f.adapt) {                                                   // Alg. 2 line 1
-      const T vht = vo[e] + rho * (yo[e] - sv);
-      vh[e] = pad ? (T)0 : vht;
-      if (f.dots && !pad) {
-        const T dvh = vht - vh0[e];
-        const T dh = sv - s0[e];
-        a_hv += dh * dvh; a_hh += dh * dh; a_vh += dvh * dvh;
+    if (sizeof(T) == 4 && KIND == 2 && hc && valid) {
+      int pd = -1;
+      unsigned pc = 0, pa = 0, pb = 0;
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        if (pad_vec(g, prim, L, e)) continue;
+        const unsigned key = __float_as_uint((float)wv[e]) & 0x7fffffffu;
+        const int d = (int)(key >> 20);
+        if (d != pd) {
+          if (pd >= 0) {
+            atomicAdd(&hc[pd], pc);
+            if (hsum) { atomicAdd(&hc[NBUCK + pd], pa); atomicAdd(&hc[2 * NBUCK + pd], pb); }
+          }
+          pd = d; pc = 0; pa = 0; pb = 0;
+        }
+        pc += 1;
+        pa += key & 1023u;
+        pb += (key >> 10) & 1023u;
+      }
+      if (pd >= 0) {
+        atomicAdd(&hc[pd], pc);
+        if (hsum) { atomicAdd(&hc[NBUCK + pd], pa); atomicAdd(&hc[2 * NBUCK + pd], pb); }
       }
     }
-    if (f.check && !pad) a_s2 += sv * sv;
-  }
-  if (valid) {
-    if (pointwise) {
-      VT<T>::stT(S.y[par ^ 1] + off, yn);
-      VT<T>::stT(S.v[par ^ 1] + off, vn);
-    } else {
-      VT<T>::stT(S.w + off, wv);
-      if (f.check && S.s) VT<T>::stT(S.s + off, st_s);
-    }
-    if (f.adapt) VT<T>::stT(S.vh0 + off, vh);
+    d_w2 += (double)a_w2; d_hv += (double)a_hv; d_hh += (double)a_hh; d_vh += (double)a_vh;
+    d_gv += (double)a_gv; d_gg += (double)a_gg; d_vv += (double)a_vv; d_fn += (double)a_fn;
+    d_s2 += (double)a_s2;
   }
   const int base = i * NSLOT;
-  if (KIND == 2 && (S.kind == K_L2 || S.kind == K_ANN)) warp_acc(acc, nv, base + SLOT_W2, (double)a_w2);
+  if (KIND == 2 && (S.kind == K_L2 || S.kind == K_ANN)) warp_acc(acc, nv, base + SLOT_W2, d_w2);
   if (f.dots) {
-    warp_acc(acc, nv, base + SLOT_HV, (double)a_hv);
-    warp_acc(acc, nv, base + SLOT_HH, (double)a_hh);
-    warp_acc(acc, nv, base + SLOT_VHVH, (double)a_vh);
+    warp_acc(acc, nv, base + SLOT_HV, d_hv);
+    warp_acc(acc, nv, base + SLOT_HH, d_hh);
+    warp_acc(acc, nv, base + SLOT_VHVH, d_vh);
     if (pointwise) {
-      warp_acc(acc, nv, base + SLOT_GV, (double)a_gv);
-      warp_acc(acc, nv, base + SLOT_GG, (double)a_gg);
-      warp_acc(acc, nv, base + SLOT_VV, (double)a_vv);
+      warp_acc(acc, nv, base + SLOT_GV, d_gv);
+      warp_acc(acc, nv, base + SLOT_GG, d_gg);
+      warp_acc(acc, nv, base + SLOT_VV, d_vv);
     }
   }
   if (f.check) {
-    if (KIND == 0) warp_acc(acc, nv, base + SLOT_FN, (double)a_fn);
-    warp_acc(acc, nv, base + SLOT_S2, (double)a_s2);
+    if (KIND == 0) warp_acc(acc, nv, base + SLOT_FN, d_fn);
+    warp_acc(acc, nv, base + SLOT_S2, d_s2);
   }
 }
 
@@ -184,56 +237,88 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Pro
   const int hcount = C.hist_count, hhead = C.hist_head;
   const int hslot = (hhead + 1) % HIST_S;
   for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
+  unsigned* h1 = P.fuse_r1 ? reinterpret_cast<unsigned*>(reinterpret_cast<char*>(acc) + P.h1_off) : nullptr;
+  if (h1)
+    for (int v = threadIdx.x; v < P.fuse_r1 * 3 * NBUCK; v += BLOCK) h1[v] = 0u;
   __syncthreads();
   const int nch = g.N / W;
-  const int gps = (nch + 31) >> 5;                     // warp groups per segment
+  const int gch = 32 * P1_U;                           // chunks per warp group
+  const int gps = (nch + gch - 1) / gch;               // warp groups per segment
   const int lane = threadIdx.x & 31;
   const int nw = gridDim.x * NWARP;
   const int g0 = blockIdx.x * NWARP + (threadIdx.x >> 5);
-  int seg = g0 / gps, cg = g0 - seg * gps;
-  while (seg < P.nseg1) {
-    const int c = cg * 32 + lane;
-    const bool valid = c < nch;
-    const int pt0 = (valid ? c : nch - 1) * W;
-    const Loc L = locate(g, pt0);
-    T xc[W];
-    VT<T>::ldT(P.x + pt0, xc);
+  // chunk-major order: the segments of one chunk range are processed by
+  // consecutive warps, so x (and x^{k0}) come from DRAM once
+  const int nseg = P.nseg1;
+  const int total = gps * nseg;
+  for (int grp = g0; grp < total; grp += nw) {
+    const int cg = grp / nseg;
+    const int seg = grp - cg * nseg;
+    const int cbase = cg * gch;
     if (seg == 0) {   // x history (Eq. 27) and Alg. 2's x snapshot
-      if (f.check) {
-        T h[HIST_S][W];
+      double x2 = 0.0, d2[HIST_S] = {0, 0, 0, 0, 0};
+      for (int u = 0; u < P1_U; ++u) {
+        const int c = cbase + u * 32 + lane;
+        const bool valid = c < nch;
+        const int pt0 = (valid ? c : nch - 1) * W;
+        T xc[W];
+        VT<T>::ldT(P.x + pt0, xc);
+        if (f.check) {
+          T h[HIST_S][W];
 #pragma unroll
-        for (int js = 0; js < HIST_S; ++js)
-          if ((hhead - js + HIST_S) % HIST_S < hcount) VT<T>::ldT(P.hist[js] + pt0, h[js]);
-        T x2 = 0;
+          for (int js = 0; js < HIST_S; ++js)
+            if ((hhead - js + HIST_S) % HIST_S < hcount) VT<T>::ldT(P.hist[js] + pt0, h[js]);
+          T t2 = 0;
 #pragma unroll
-        for (int e = 0; e < W; ++e) x2 += valid ? xc[e] * xc[e] : (T)0;
-        warp_acc(acc, nv, P.P * NSLOT, (double)x2);
+          for (int e = 0; e < W; ++e) t2 += valid ? xc[e] * xc[e] : (T)0;
+          x2 += (double)t2;
 #pragma unroll
-        for (int js = 0; js < HIST_S; ++js) {
-          if ((hhead - js + HIST_S) % HIST_S >= hcount) continue;
-          T d2 = 0;
+          for (int js = 0; js < HIST_S; ++js) {
+            if ((hhead - js + HIST_S) % HIST_S >= hcount) continue;
+            T t = 0;
 #pragma unroll
-          for (int e = 0; e < W; ++e) {
-            const T d = xc[e] - h[js][e];
-            d2 += valid ? d * d : (T)0;
+            for (int e = 0; e < W; ++e) {
+              const T d = xc[e] - h[js][e];
+              t += valid ? d * d : (T)0;
+            }
+            d2[js] += (double)t;
           }
-          warp_acc(acc, nv, P.P * NSLOT + 1 + js, (double)d2);
+        }
+        if (valid) {
+          VT<T>::stT(P.hist[hslot] + pt0, xc);
+          if (f.adapt) VT<T>::stT(xs_wr + pt0, xc);
         }
       }
-      if (valid) {
-        VT<T>::stT(P.hist[hslot] + pt0, xc);
-        if (f.adapt) VT<T>::stT(xs_wr + pt0, xc);
+      if (f.check) {
+        warp_acc(acc, nv, P.P * NSLOT, x2);
+#pragma unroll
+        for (int js = 0; js < HIST_S; ++js)
+          if ((hhead - js + HIST_S) % HIST_S < hcount) warp_acc(acc, nv, P.P * NSLOT + 1 + js, d2[js]);
       }
     } else {
       const int i = P.seg_set[seg], bl = P.seg_blk[seg];
       switch (P.set[i].kind) {
-        case K_BOUNDS: p1_block<T, 0>(P, C, i, bl, f, par, pt0, valid, L, lane, xs_rd, xc, acc, nv); break;
-        case K_DIST: p1_block<T, 1>(P, C, i, bl, f, par, pt0, valid, L, lane, xs_rd, xc, acc, nv); break;
-        default: p1_block<T, 2>(P, C, i, bl, f, par, pt0, valid, L, lane, xs_rd, xc, acc, nv); break;
+        case K_BOUNDS: p1_seg<T, 0>(P, C, i, bl, f, par, cbase, nch, lane, xs_rd, acc, nv, h1); break;
+        case K_DIST: p1_seg<T, 1>(P, C, i, bl, f, par, cbase, nch, lane, xs_rd, acc, nv, h1); break;
+        default: p1_seg<T, 2>(P, C, i, bl, f, par, cbase, nch, lane, xs_rd, acc, nv, h1); break;
       }
     }
-    cg += nw;
-    while (cg >= gps) { cg -= gps; ++seg; }
+  }
+  if (h1) {   // flush the round-1 histograms (exact integer sums) to global
+    __syncthreads();
+    for (int jj = 0; jj < P.fuse_r1; ++jj) {
+      const int jb = 2 * jj;
+      const unsigned* hc = h1 + jj * 3 * NBUCK;
+      for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+        const unsigned cnt = hc[d];
+        if (!cnt) continue;
+        atomicAdd(P.gh_cnt + (size_t)jb * NBUCK + d, cnt);
+        const unsigned long long base = ((d >> 3) ? (1ull << 23) : 0ull) + ((unsigned long long)(d & 7) << 20);
+        const unsigned long long sum = (unsigned long long)cnt * base + hc[NBUCK + d] +
+                                       ((unsigned long long)hc[2 * NBUCK + d] << 10);
+        atomicAdd(P.gh_s0 + (size_t)jb * NBUCK + d, sum);
+      }
+    }
   }
   double* stage = P.partials + (size_t)gridDim.x * nv;
   if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
@@ -255,6 +340,23 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Pro
         else if (n < C.sig_lo[i]) fct = C.sig_lo[i] / n;
         C.ann_scale[i] = fct;
         C.ann_zero[i] = z;
+      }
+    }
+    if (h1) {   // resolve round 1 of the w jobs (k_selectf continues at round 2)
+      __syncthreads();
+      for (int jj = 0; jj < P.fuse_r1; ++jj) {
+        const int jb = 2 * jj;
+        Job& J = C.job[jb];
+        if (J.mode == JM_SEARCH && J.round == 0) {
+          resolve_round<T>(P, J, 1, P.gh_cnt + (size_t)jb * NBUCK, P.gh_s0 + (size_t)jb * NBUCK,
+                           P.gh_s1 + (size_t)jb * NBUCK);
+        }
+        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+          P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;
+          P.gh_s0[(size_t)jb * NBUCK + d] = 0ull;
+          P.gh_s1[(size_t)jb * NBUCK + d] = 0ull;
+        }
+        __syncthreads();
       }
     }
   }

@@ -18,6 +18,7 @@
 #include "../../include/sip.h"
 #include "sip_aux_kernels.cuh"
 #include "sip_pass.cuh"
+#include "sip_zmarch.cuh"
 
 using namespace sip;
 
@@ -118,6 +119,8 @@ struct Engine : EngineBase {
   // launch geometry
   int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1;
   bool vec = false;
+  ZGeo zg{};                     // z-marching CG geometry (sip_zmarch.cuh)
+  size_t smem_z = 0;
   size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0;
   // graph
   cudaGraphExec_t gexec = nullptr;
@@ -253,11 +256,46 @@ struct Engine : EngineBase {
     constexpr int W = VT<T>::W;
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
+    // z-marching CG: 3D grids whose rows split into whole warps of W-chunks
+    zg.on = 0;
+    if (vec && ndim == 3 && g.nx % (32 * W) == 0 && !getenv("SIP_NO_ZMARCH")) {
+      const int nxw = g.nx / (32 * W);
+      if (nxw >= 8 && nxw % 8 == 0) { zg.txw = 8; zg.tyw = 1; }
+      else if (nxw < 8 && 8 % nxw == 0) { zg.txw = nxw; zg.tyw = 8 / nxw; }
+      else zg.txw = 0;
+      if (zg.txw && g.ny % zg.tyw == 0) {
+        zg.row_pts = zg.txw * 32 * W;
+        zg.tiles_x = g.nx / zg.row_pts;
+        zg.tiles_y = g.ny / zg.tyw;
+        const int tiles = zg.tiles_x * zg.tiles_y;
+        int nzc = std::max(1, std::min(g.nz, (nsm * 4 + tiles - 1) / tiles));
+        zg.zc = (g.nz + nzc - 1) / nzc;
+        zg.nzc = (g.nz + zg.zc - 1) / zg.zc;
+        zg.on = 1;
+        smem_z = (size_t)2 * (zg.tyw + 2) * zg.row_pts * sizeof(T);
+      }
+    }
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);
+    // fp32 vectorised path: round 1 of the radix search is fused into pass 1
+    // (one smem histogram per w-job) and round 2 compacts its survivors
+    Pr.fuse_r1 = 0;
+    if (vec && sizeof(T) == 4 && njobs > 0 && getenv("SIP_FUSE_R1")) {   // measured slower on C4: opt-in
+      Pr.fuse_r1 = njobs / 2;
+      Pr.h1_off = (int)((smem_p1 + 15) / 16 * 16);
+      smem_p1 = (size_t)Pr.h1_off + (size_t)Pr.fuse_r1 * 3 * NBUCK * sizeof(unsigned);
+    }
+    if (vec && sizeof(T) == 4)
+      for (int i = 0; i < P; ++i) {
+        const SetD<T>& S = Pr.set[i];
+        if (S.job < 0) continue;
+        Pr.cand[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
+        Pr.cand[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
+      }
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
-    const int gmax = std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec);
+    const int gz_ = zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1;
+    const int gmax = std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_);
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     Pr.counter = dalloc<unsigned>(1);
     CU(cudaMemsetAsync(Pr.counter, 0, sizeof(unsigned), stream));
@@ -277,6 +315,11 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
     memset(&hc, 0, sizeof(hc));
     hc.njobs = njobs;
     for (int i = 0; i < P; ++i) {
@@ -392,7 +435,13 @@ struct Engine : EngineBase {
     ++launches; mark(KB_RHS);
     for (int j = 0; j < n_cg; ++j) {
       if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 1, j); ++launches; mark(KB_BLUR); }
-      if (vec) {
+      if (zg.on) {
+        const int gz = zg.tiles_x * zg.tiles_y * zg.nzc;
+        // measured on C4: z-marching wins for k_cg1 (operand recomputed from
+        // two arrays at 5 positions), the flat sweep for k_cg2 (profiles/)
+        k_cg1z<T, true><<<gz, BLOCK, smem_z, stream>>>(Pr, zg, j); ++launches; mark(KB_CG1);
+        k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
+      } else if (vec) {
         k_cg1v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG1);
         k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
       } else {
@@ -868,7 +917,11 @@ sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg,
   k_rhs<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2);
   for (int j = 0; j < n_cg; ++j) {
     if (e->Pr.has[PRIM_F]) k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, 1, j);
-    if (e->vec) {   // the same kernels as the hot path
+    if (e->zg.on) {   // the same kernels as the hot path
+      const int gz = e->zg.tiles_x * e->zg.tiles_y * e->zg.nzc;
+      k_cg1z<T, true><<<gz, BLOCK, e->smem_z, e->stream>>>(e->Pr, e->zg, j);
+      k_cg2v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
+    } else if (e->vec) {
       k_cg1v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
       k_cg2v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
     } else {
@@ -906,7 +959,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     Job& J = c.job[jb];
     const int i = J.set;
     J.round = 0; J.prefix = 0; J.cnt_above = 0; J.sum_above = 0; J.theta = 0; J.tau = 0;
-    J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0;
+    J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0; J.cand_n = 0;
     J.sigma = c.sigma[i]; J.k = c.kcard[i];
     J.mode = (J.on_s || i != set_id) ? JM_OFF : JM_SEARCH;
     if (J.mode == JM_SEARCH && J.kind == K_CARD) {
