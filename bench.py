@@ -178,7 +178,7 @@ def run_reference(args, prob):
     line = {
         "impl": "reference", "metric": "PARSDMM iterations/s", "value": val, "unit": "it/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": prob.name, "grid": list(prob.shape), "sets": len(prob.sets),
                    "iters_per_step": ips, "mode": "fixed_work"},
@@ -197,18 +197,27 @@ def run_cuda(args, prob):
     import torch
     world, rank, local = dist_init()
     torch.cuda.set_device(local)
+    from paper_1902_09699_b200 import grid_for
+    from paper_1902_09699_b200.dist import comm_desc, local_slab_of
+
+    comm = None
+    m_np = prob.m
     if world > 1:
+        # z slabs over NCCL: strong scaling of one problem;
+        # torch.distributed only bootstraps the library's NCCL communicator
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1902_09699_b200 import grid_for
-
+        comm = comm_desc()
+        m_np = local_slab_of(prob.m, world, rank)
     dt = torch.float32 if prob.dtype == "f32" else torch.float64
     ips = args.iters_per_step
-    g = grid_for(prob)
+    g = grid_for(prob, comm=comm)
     g.set_option("fixed_work", 1)
     g.set_option("eq25", 0)
     g.set_option("n_cg", args.n_cg)
-    m = torch.tensor(prob.m, dtype=dt, device="cuda").contiguous()
+    if args.virtual_ranks > 1:
+        g.set_option("virtual_ranks", args.virtual_ranks)
+    m = torch.tensor(m_np, dtype=dt, device="cuda").contiguous()
     x = torch.empty_like(m)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2
 
@@ -232,13 +241,12 @@ def run_cuda(args, prob):
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    t_total = max_over_ranks(sum(times), world, "cuda")          # ms
-    iters_all = sum_over_ranks(args.steps * ips, world, "cuda")
-    value = iters_all / (t_total / 1e3) / world                   # replicas: each rank iterates its own problem
-    value_job = iters_all / (t_total / 1e3)
+    t_total = max_over_ranks(sum(times), world, "cuda")          # ms, slowest rank
+    value_job = args.steps * ips / (t_total / 1e3)                # iterations of the one (sharded) problem
+    value = value_job
 
     # e2e: host pinned m / x, copies inside the timed call
-    mh = torch.tensor(prob.m, dtype=dt).pin_memory()
+    mh = torch.tensor(m_np, dtype=dt).pin_memory()
     xh = torch.empty_like(mh).pin_memory()
     for _ in range(1):
         g.project(mh, xh, max_iter=ips, tol=1e-3)
@@ -250,8 +258,8 @@ def run_cuda(args, prob):
         res = g.project(mh, xh, max_iter=ips, tol=1e-3)[0]
         etimes.append(time.perf_counter() - t0)
     e2e_t = max_over_ranks(sum(etimes), world, "cuda")
-    e2e_val = sum_over_ranks(len(etimes) * ips, world, "cuda") / e2e_t
-    nbytes = prob.N * (4 if prob.dtype == "f32" else 8)
+    e2e_val = len(etimes) * ips / e2e_t
+    nbytes = m_np.size * (4 if prob.dtype == "f32" else 8)        # this rank's slab (one GPU: the grid)
 
     # profiled step: per-kernel device time from event nodes in the graph
     g.set_option("profile", 1)
@@ -261,6 +269,8 @@ def run_cuda(args, prob):
     prof = g.profile()
     g.set_option("profile", 0)
     model = byte_model(prob, args.n_cg, 4 if prob.dtype == "f32" else 8)
+    if world > 1:   # this rank's k_cg2 launches move its slab
+        model["cg2"] = model["cg2"] * m_np.size // prob.N
     peaks = load_peaks()
     cg2_ms, cg2_n = prof["cg2"]
     cg2_avg_s = cg2_ms / max(cg2_n, 1) / 1e3
@@ -274,7 +284,7 @@ def run_cuda(args, prob):
     it_model_gbs = model["iteration"] * (args.steps * ips) / (sum(times) / 1e3) / 1e9
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ts = oracle_sample(prob, args.cpu_iters)
         cpu = {"value": args.cpu_iters / sum(ts), "unit": "it/s", "cores": 1, "kind": "oracle",
                "sample": f"{args.cpu_iters} fixed-work iterations of {prob.name} "
@@ -284,17 +294,20 @@ def run_cuda(args, prob):
             "metric": "PARSDMM iterations/s", "value": value_job, "unit": "it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prob.dtype == "f32" else "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prob.dtype == "f32" else "f64",
             "data": "synthetic",
             "config": {"workload": f"{prob.name} {'x'.join(map(str, prob.shape))} "
                                    f"{', '.join(sd.op + ':' + sd.kind for sd in prob.sets)}",
                        "grid": list(prob.shape), "sets": len(prob.sets), "iters_per_step": ips,
                        "n_cg": args.n_cg, "mode": "fixed_work (Eq.25 off, stop test not acted on)",
                        "l2": "flushed (256 MiB write) between timed steps",
-                       "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+                       "parallelism": ("1 GPU" if world == 1 else
+                                       f"z-slab x{world} (NCCL halos + gathered reductions)")
+                                      + (f", {args.virtual_ranks} virtual z-slabs on the GPU"
+                                         if args.virtual_ranks > 1 else "")},
             "pts_sets_per_s": value_job * prob.N * len(prob.sets),
             "iteration_model_gbs": it_model_gbs,
-            "per_rank_it_s": value,
+            "comm_ms_per_step": prof.get("comm", (0.0, 0))[0],
             "roofline": {"kernel": "k_cg2", "bound": "hbm", "achieved": achieved,
                          "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
@@ -326,6 +339,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--virtual-ranks", type=int, default=1,
+                    help="run the z-slab path with G slabs on the one GPU (diagnostic)")
     args = ap.parse_args()
     prob = G.CONFIGS[args.config]()
     if args.impl == "reference":

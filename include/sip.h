@@ -125,15 +125,27 @@ typedef struct {
 /* ---- lifecycle ------------------------------------------------------- */
 
 /* 128-byte NCCL unique id for a multi-rank grid (rank 0 calls it, the caller
-   broadcasts it, e.g. with torch.distributed). */
+   broadcasts it, e.g. with torch.distributed).  NCCL (libnccl.so.2) is
+   loaded at the first call; SIP_ERR_NCCL if it is missing. */
 sip_status sip_comm_unique_id(uint8_t out[128]);
+
+/* The z-slab rule: of nz planes split over nranks, rank
+   owns [z0, z0 + nz_local); nz_local = nz / nranks, plus one for the first
+   nz mod nranks ranks.  Host only, no device work.  SIP_ERR_ARG on nz < 1,
+   nranks < 1, rank outside [0, nranks) or NULL outputs. */
+sip_status sip_slab(int64_t nz, int nranks, int rank, int64_t *z0, int64_t *nz_local);
 
 /* Create a grid (compgrid).
    ndim: 2 or 3.  n: ndim counts, z first (each >= 2).  h: ndim spacings > 0
    (NULL = all 1, reading L2).  comm: NULL for one GPU, else the z-slab
    decomposition: the rank owns planes [z0, z0+nz_local) with the first
    nz mod nranks ranks holding one extra plane; m/x passed to this rank are
-   its local slab.  cuda_stream: the caller's cudaStream_t (NULL = legacy
+   its local slab (n stays the GLOBAL counts).  Every rank must call with
+   the same n, h, dtype, sets and options; creation runs ncclCommInitRank
+   (collective).  A multi-rank grid needs nx % (16 / sizeof(dtype)) == 0, no
+   blur/mask operator and a single level; each step's reductions and 1-plane
+   halos are exchanged with grouped NCCL send/recv (SIP_ERR_NCCL on
+   failure).  cuda_stream: the caller's cudaStream_t (NULL = legacy
    default stream); every call orders its work after the work already queued
    on it, runs on a library-owned non-blocking stream (capturable into CUDA
    graphs) and returns after completion.  The current CUDA device at the
@@ -156,9 +168,14 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void *op_desc, sip_set_type 
    "adapt_every" 2, "check_every" 5, "rho_ratio_cap" 1e3
    (L16), "gamma_max" 2-1e-3 (L15), "cg_tol_floor" 10*eps(dtype) (L18),
    "warm_start" 0 (1 = start from the grid's x, y_i, v_i, rho_i, gamma_i of
-   the previous call instead of reading L13), "graph_iters" 5 (iterations
+   the previous call instead of reading L13), "graph_iters" 10 (iterations
    per captured CUDA graph; 0 = no graph), "profile" 0 (1 = per-kernel event
-   timing, see sip_get_profile; adds one host sync per graph launch).
+   timing, see sip_get_profile; adds one host sync per graph launch),
+   "virtual_ranks" 1 (G > 1: run the z-slab decomposition of G ranks on this
+   one device -- the same per-slab kernels, finalisers and exchange schedule
+   as the NCCL path, with device copies for the transfers; m and x stay
+   whole-grid arrays; single-level sip_project only; SIP_ERR_PARAM unless
+   1 <= G <= nz and integral).
    Unknown key: SIP_ERR_ARG. */
 sip_status sip_set_option(sip_grid g, const char *key, double value);
 

@@ -278,6 +278,21 @@ template <> struct Limbs<double> {
   }
 };
 
+// multi-rank: a job's histogram in the gather slot, HJOB doubles per job:
+// sums s0, s1 (u64 x NBUCK each), then the counts (u32 x NBUCK)
+constexpr int HJOB = NBUCK * 2 + NBUCK / 2;
+template <class T>
+__device__ inline void publish_hist(const Prob<T>& P, int jb, const unsigned* gc, const unsigned long long* g0,
+                                    const unsigned long long* g1) {
+  double* base = P.xg + (size_t)P.rank * P.xslot + (size_t)jb * HJOB;
+  unsigned long long* s0 = reinterpret_cast<unsigned long long*>(base);
+  unsigned long long* s1 = s0 + NBUCK;
+  unsigned* cn = reinterpret_cast<unsigned*>(s1 + NBUCK);
+  for (int d = threadIdx.x; d < NBUCK; d += blockDim.x) {
+    s0[d] = __ldcg(g0 + d); s1[d] = __ldcg(g1 + d); cn[d] = __ldcg(gc + d);
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<T> P, int round) {
   using K = KeyT<T>;
@@ -437,7 +452,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
       unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
       unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
       unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
-      resolve_round<T>(P, J, round, gc, g0, g1);
+      if (P.nranks > 1) publish_hist(P, jb, gc, g0, g1);
+      else resolve_round<T>(P, J, round, gc, g0, g1);
+      __syncthreads();
       for (int d = threadIdx.x; d < NBUCK; d += BLOCK) { gc[d] = 0u; g0[d] = 0ull; g1[d] = 0ull; }
       __syncthreads();
     }
@@ -455,6 +472,7 @@ __global__ void __launch_bounds__(BLOCK) k_tiecountf(const __grid_constant__ Pro
   if (C.stopped) return;
   __shared__ int s_w[NWARP];
   __shared__ long long s_c[BLOCK];
+  __shared__ double s_sh[NWARP + 1];
   const Geo& g = P.g;
   const int nch = g.N / W;
   const int tpb = (nch + BLOCK - 1) / BLOCK;
@@ -489,6 +507,13 @@ __global__ void __launch_bounds__(BLOCK) k_tiecountf(const __grid_constant__ Pro
       if (J.mode != JM_DONE || !J.ties) continue;
       int* tc = P.tiecnt + (size_t)S.job * P.ntiles_max;
       const int nt = S.nblk * tpb;
+      if (P.nranks > 1)   // this rank's ties per block, for the cross-rank offsets (k_fin)
+        for (int bl = 0; bl < S.nblk; ++bl) {
+          double c = 0.0;
+          for (int t = bl * tpb + threadIdx.x; t < (bl + 1) * tpb; t += BLOCK) c += (double)__ldcg(tc + t);
+          c = block_sum(c, s_sh);
+          if (threadIdx.x == 0) P.xg[(size_t)P.rank * P.xslot + i * 3 + bl] = c;
+        }
       const int per = (nt + BLOCK - 1) / BLOCK;
       const int t0 = threadIdx.x * per;
       long long loc = 0;

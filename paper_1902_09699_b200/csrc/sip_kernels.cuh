@@ -54,10 +54,69 @@ struct Prob {
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)
+  // z-slab decomposition: with nranks > 1 the last CTA of a
+  // reducing kernel publishes its rank-local values to slot `rank` of the
+  // gather buffer xg (nranks slots of xslot doubles) instead of deciding;
+  // the runtime exchanges the slots and k_fin (sip_team.cuh) sums them in
+  // rank order and runs the same finaliser on every rank.
+  int nranks, rank;
+  double* xg;
+  int xslot;
 };
 
 __device__ __forceinline__ bool is_adapt_it(int k, int every) {
   return every <= 1 || (k % every) == 1;   // mod(k, update-frequency) = 1
+}
+
+// ------------------------------------------------------------ finalisers
+// The decision taken once the global value of a reduction is known.  One
+// thread (fin_rhs / fin_cg1 / fin_cg2) or one CTA (the template ones below).
+
+// after the rhs: ||b||^2, ||r0||^2 -> Eq. 25 target and the CG flags (L18)
+__device__ inline void fin_rhs(Ctrl& C, const double* v) {
+  const double bbv = v[0], rrv = v[1];
+  C.bb = bbv; C.rr = rrv; C.rr_prev = rrv; C.beta = 0.0;
+  C.cg_j = 0; C.cg_count = 0;
+  C.zero_x = (bbv == 0.0);
+  double tol = 0.0;
+  if (bbv > 0.0) {
+    tol = 0.1 * sqrt(rrv) / sqrt(bbv);          // Eq. 25
+    if (tol < C.opt.cg_tol_floor) tol = C.opt.cg_tol_floor;
+  }
+  C.tol = tol;
+  int active = (bbv > 0.0) && (rrv > 0.0) && (C.opt.n_cg > 0);
+  if (active && C.opt.eq25 && sqrt(rrv) / sqrt(bbv) < tol) active = 0;
+  C.cg_active = active;
+}
+
+// after <p_j, C p_j>: alpha, or breakdown (p.q <= 0, reading L18)
+__device__ inline void fin_cg1(Ctrl& C, const double* v) {
+  if (v[0] > 0.0) {
+    C.alpha = C.rr / v[0];
+  } else {
+    C.cg_active = 0;
+    C.breakdown = 1;
+  }
+}
+
+// after <r, r>: beta, Eq. 25 test, CG counters
+__device__ inline void fin_cg2(Ctrl& C, const double* v, int j) {
+  const double rn = v[0];
+  C.beta = rn / C.rr;
+  C.rr_prev = C.rr;
+  C.rr = rn;
+  C.cg_count += 1;
+  C.cg_j = j + 1;
+  int active = (C.cg_j < C.opt.n_cg) && (rn > 0.0);
+  if (active && C.opt.eq25 && sqrt(rn) / sqrt(C.bb) < C.tol) active = 0;
+  C.cg_active = active;
+}
+
+// rank-local values -> this rank's gather slot (threads of one CTA, strided)
+template <class T>
+__device__ __forceinline__ void publish(const Prob<T>& P, const double* v, int n, int tid, int nt) {
+  double* dst = P.xg + (size_t)P.rank * P.xslot;
+  for (int i = tid; i < n; i += nt) dst[i] = v[i];   // v: shared, or global written by this CTA
 }
 
 // ------------------------------------------------------------ value fetchers
@@ -1068,6 +1127,25 @@ __global__ void k_control(const __grid_constant__ Prob<T> P) {
   if (C.k > C.opt.max_iter) C.stopped = 1;
 }
 
+// init finaliser (one thread): relative parameters from the norms of A_i m
+// (readings L4, L23), cardinality k, select jobs
+template <class T>
+__device__ inline void fin_init(const Prob<T>& P, Ctrl& C, const double* stage) {
+  for (int i = 0; i < P.p; ++i) {
+    const double n1 = stage[2 * i], n2 = sqrt(stage[2 * i + 1]);
+    const int kd = P.set[i].kind, rel = C.rel[i];
+    double sg = C.u_sigma[i], lo = C.u_sig_lo[i], hi = C.u_sig_hi[i];
+    if (rel && kd == K_L1) sg *= n1;
+    if (rel && kd == K_L2) sg *= n2;
+    if (rel && kd == K_ANN) { lo *= n2; hi *= n2; }
+    if (kd == K_L2) { lo = 0.0; hi = sg; }
+    C.sigma[i] = sg; C.sig_lo[i] = lo; C.sig_hi[i] = hi;
+    C.kcard[i] = (rel && kd == K_CARD) ? (long long)floor(C.u_kfrac[i] * (double)C.mreal[i]) : C.u_k[i];
+  }
+  for (int i = 0; i < MAXP; ++i) { C.ann_scale[i] = 1.0; C.ann_zero[i] = 0; }
+  reset_jobs(P, C);
+}
+
 // ------------------------------------------------------------ init
 // x = m (unless warm), y_i = A_i m, v_i = 0 (reading L13), zero work fields,
 // norms of A_i m for relative parameters (readings L4, L23)
@@ -1112,22 +1190,8 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Prob<T> 
   }
   double* stage = P.partials + (size_t)gridDim.x * nv;
   if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < P.p; ++i) {
-        const double n1 = __ldcg(stage + 2 * i), n2 = sqrt(__ldcg(stage + 2 * i + 1));
-        const int kd = P.set[i].kind, rel = C.rel[i];
-        double sg = C.u_sigma[i], lo = C.u_sig_lo[i], hi = C.u_sig_hi[i];
-        if (rel && kd == K_L1) sg *= n1;
-        if (rel && kd == K_L2) sg *= n2;
-        if (rel && kd == K_ANN) { lo *= n2; hi *= n2; }
-        if (kd == K_L2) { lo = 0.0; hi = sg; }
-        C.sigma[i] = sg; C.sig_lo[i] = lo; C.sig_hi[i] = hi;
-        C.kcard[i] = (rel && kd == K_CARD) ? (long long)floor(C.u_kfrac[i] * (double)C.mreal[i])
-                                           : C.u_k[i];
-      }
-      for (int i = 0; i < MAXP; ++i) { C.ann_scale[i] = 1.0; C.ann_zero[i] = 0; }
-      reset_jobs(P, C);
-    }
+    if (P.nranks > 1) publish(P, stage, nv, threadIdx.x, BLOCK);
+    else if (threadIdx.x == 0) fin_init<T>(P, C, stage);
   }
 }
 

@@ -220,6 +220,33 @@ __device__ __forceinline__ void p1_seg(const Prob<T>& P, const Ctrl& C, int i, i
   }
 }
 
+// pass-1 finaliser (one CTA): Alg. 2 / Eq. 26-27 sums into the control
+// block, l2 / annulus radial factors (Table 1, L7)
+template <class T>
+__device__ inline void fin_pass1(const Prob<T>& P, Ctrl& C, const double* stage) {
+  const int nv = P.P * NSLOT + NEVOL;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    const double val = stage[v];
+    if (v < P.P * NSLOT) C.sums[v / NSLOT][v % NSLOT] = val;
+    else C.evol[v - P.P * NSLOT] = val;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < P.P; ++i) {
+      const int kd = P.set[i].kind;
+      if (kd != K_L2 && kd != K_ANN) continue;
+      const double n = sqrt(stage[i * NSLOT + SLOT_W2]);
+      double fct = 1.0;
+      int z = 0;
+      if (n == 0.0) z = (C.sig_lo[i] > 0.0);
+      else if (n > C.sig_hi[i]) fct = C.sig_hi[i] / n;
+      else if (n < C.sig_lo[i]) fct = C.sig_lo[i] / n;
+      C.ann_scale[i] = fct;
+      C.ann_zero[i] = z;
+    }
+  }
+}
+
 template <class T, int AD, int CK>
 __global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Prob<T> P) {
   constexpr int W = VT<T>::W;
@@ -286,7 +313,14 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Pro
         }
         if (valid) {
           VT<T>::stT(P.hist[hslot] + pt0, xc);
-          if (f.adapt) VT<T>::stT(xs_wr + pt0, xc);
+          if (f.adapt) {
+            VT<T>::stT(xs_wr + pt0, xc);
+            if (pt0 >= g.N - g.plane) {   // the upper ghost plane too (x^{k0} at z+1 on a z slab)
+              T xg_[W];
+              VT<T>::ldT(P.x + pt0 + g.plane, xg_);
+              VT<T>::stT(xs_wr + pt0 + g.plane, xg_);
+            }
+          }
         }
       }
       if (f.check) {
@@ -322,26 +356,11 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Pro
   }
   double* stage = P.partials + (size_t)gridDim.x * nv;
   if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
-    for (int v = threadIdx.x; v < nv; v += BLOCK) {
-      const double val = __ldcg(stage + v);
-      if (v < P.P * NSLOT) C.sums[v / NSLOT][v % NSLOT] = val;
-      else C.evol[v - P.P * NSLOT] = val;
+    if (P.nranks > 1) {
+      publish(P, stage, nv, threadIdx.x, BLOCK);
+      return;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < P.P; ++i) {   // l2 / annulus radial factors (Table 1, L7)
-        const int kd = P.set[i].kind;
-        if (kd != K_L2 && kd != K_ANN) continue;
-        const double n = sqrt(__ldcg(stage + i * NSLOT + SLOT_W2));
-        double fct = 1.0;
-        int z = 0;
-        if (n == 0.0) z = (C.sig_lo[i] > 0.0);
-        else if (n > C.sig_hi[i]) fct = C.sig_hi[i] / n;
-        else if (n < C.sig_lo[i]) fct = C.sig_lo[i] / n;
-        C.ann_scale[i] = fct;
-        C.ann_zero[i] = z;
-      }
-    }
+    fin_pass1<T>(P, C, stage);
     if (h1) {   // resolve round 1 of the w jobs (k_selectf continues at round 2)
       __syncthreads();
       for (int jj = 0; jj < P.fuse_r1; ++jj) {
@@ -462,6 +481,22 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
   }
 }
 
+// pass-2 finaliser (one CTA): Alg. 2 beta-side sums and the Eq. 26
+// numerators of the global sets
+template <class T>
+__device__ inline void fin_pass2(const Prob<T>& P, Ctrl& C, const double* stage) {
+  const int nv = P.P * 4;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    const int i = v / 4, q = v % 4;
+    if (!P.set[i].global) continue;
+    const double val = stage[v];
+    if (q == 0) C.sums[i][SLOT_GV] = val;
+    if (q == 1) C.sums[i][SLOT_GG] = val;
+    if (q == 2) C.sums[i][SLOT_VV] = val;
+    if (q == 3 && P.set[i].sjob >= 0) C.sums[i][SLOT_FN] = val;
+  }
+}
+
 template <class T, int AD, int CK>
 __global__ void __launch_bounds__(BLOCK) k_pass2t(const __grid_constant__ Prob<T> P) {
   using K = KeyT<T>;
@@ -524,15 +559,8 @@ __global__ void __launch_bounds__(BLOCK) k_pass2t(const __grid_constant__ Prob<T
   }
   double* stage = P.partials + (size_t)gridDim.x * nv;
   if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
-    for (int v = threadIdx.x; v < nv; v += BLOCK) {
-      const int i = v / 4, q = v % 4;
-      if (!P.set[i].global) continue;
-      const double val = __ldcg(stage + v);
-      if (q == 0) C.sums[i][SLOT_GV] = val;
-      if (q == 1) C.sums[i][SLOT_GG] = val;
-      if (q == 2) C.sums[i][SLOT_VV] = val;
-      if (q == 3 && P.set[i].sjob >= 0) C.sums[i][SLOT_FN] = val;
-    }
+    if (P.nranks > 1) publish(P, stage, nv, threadIdx.x, BLOCK);
+    else fin_pass2<T>(P, C, stage);
   }
 }
 

@@ -5,6 +5,7 @@
 // graph of `graph_iters` iterations and replayed; the host reads one flag per
 // graph launch (lagged by one launch) to learn that Eq. 28 stopped the run.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -17,8 +18,7 @@
 
 #include "../../include/sip.h"
 #include "sip_aux_kernels.cuh"
-#include "sip_pass.cuh"
-#include "sip_zmarch.cuh"
+#include "sip_team.cuh"
 
 using namespace sip;
 
@@ -160,9 +160,13 @@ struct Engine : EngineBase {
     return base + (size_t)GHOST * Pr.g.plane;
   }
 
+  // slab: this engine owns global planes [z0_, z0_ + nz_) of nz_g_ (rank of nranks_)
+  int z0 = 0, nz_g = 0, nranks = 1, rank = 0;
+
   void setup(int ndim_, int nz_, int ny_, int nx_, const double* h_, cudaStream_t st,
-             const std::vector<HostSet>& s) {
+             const std::vector<HostSet>& s, int z0_ = 0, int nz_g_ = -1, int nranks_ = 1, int rank_ = 0) {
     ndim = ndim_; nz = nz_; ny = ny_; nx = nx_;
+    z0 = z0_; nz_g = nz_g_ < 0 ? nz_ : nz_g_; nranks = nranks_; rank = rank_;
     h[0] = h_[0]; h[1] = h_[1]; h[2] = h_[2];
     stream = st;
     sets = &s;
@@ -173,7 +177,7 @@ struct Engine : EngineBase {
     CU(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     memset(&Pr, 0, sizeof(Pr));
     Geo& g = Pr.g;
-    g.ndim = ndim; g.nz = nz; g.ny = ny; g.nx = nx; g.nz_g = nz; g.z0 = 0;
+    g.ndim = ndim; g.nz = nz; g.ny = ny; g.nx = nx; g.nz_g = nz_g; g.z0 = z0;
     g.plane = ny * nx;
     g.N = nz * g.plane;
     g.ld = (int64_t)g.N + 2 * GHOST * (int64_t)g.plane;
@@ -181,6 +185,7 @@ struct Engine : EngineBase {
     g.dplane.init((uint32_t)g.plane);
     g.dnx.init((uint32_t)g.nx);
     Pr.P = P; Pr.p = p;
+    Pr.nranks = nranks; Pr.rank = rank;
     Pr.rounds = KeyT<T>::ROUNDS;
     Pr.ntiles_pb = (g.N + BLOCK - 1) / BLOCK;
     Pr.nseg1 = 0;   // counts (set, block) segments below; +1 for the x segment after
@@ -211,6 +216,8 @@ struct Engine : EngineBase {
       }
     }
     Pr.nseg1 += 1;   // segment 0: the per-point x work
+    if (z0 > 0)
+      for (int i = 0; i < P; ++i) Pr.set[i].first_real = -1;   // global index 0 is on rank 0 (L7)
     // blur mask + compact map
     for (int i = 0; i < p; ++i)
       if (s[i].op == SIP_OP_BLUR_MASK) {
@@ -280,7 +287,7 @@ struct Engine : EngineBase {
     // fp32 vectorised path: round 1 of the radix search is fused into pass 1
     // (one smem histogram per w-job) and round 2 compacts its survivors
     Pr.fuse_r1 = 0;
-    if (vec && sizeof(T) == 4 && njobs > 0 && getenv("SIP_FUSE_R1")) {   // measured slower on C4: opt-in
+    if (vec && sizeof(T) == 4 && njobs > 0 && nranks == 1 && getenv("SIP_FUSE_R1")) {   // measured slower on C4: opt-in
       Pr.fuse_r1 = njobs / 2;
       Pr.h1_off = (int)((smem_p1 + 15) / 16 * 16);
       smem_p1 = (size_t)Pr.h1_off + (size_t)Pr.fuse_r1 * 3 * NBUCK * sizeof(unsigned);
@@ -297,6 +304,13 @@ struct Engine : EngineBase {
     const int gz_ = zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1;
     const int gmax = std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_);
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
+    if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
+      int xs_ = 0;
+      for (int st = ST_INIT; st <= ST_PASS2; ++st) xs_ = std::max(xs_, site_payload(st, P, njobs));
+      Pr.xslot = (xs_ + 31) / 32 * 32;
+      Pr.xg = dalloc<double>((size_t)nranks * Pr.xslot);
+      CU(cudaMemsetAsync(Pr.xg, 0, (size_t)nranks * Pr.xslot * sizeof(double), stream));
+    }
     Pr.counter = dalloc<unsigned>(1);
     CU(cudaMemsetAsync(Pr.counter, 0, sizeof(unsigned), stream));
     Pr.gh_cnt = dalloc<unsigned>((size_t)MAXJOBS * NBUCK);
@@ -356,7 +370,7 @@ struct Engine : EngineBase {
     const Geo& g = Pr.g;
     switch (prim) {
       case PRIM_I: return g.N;
-      case PRIM_Z: return (long long)(g.nz - 1) * g.plane;
+      case PRIM_Z: return (long long)(z0 + g.nz < nz_g ? g.nz : g.nz - 1) * g.plane;   // pad plane: last global
       case PRIM_Y: return (long long)g.nz * (g.ny - 1) * g.nx;
       case PRIM_X: return (long long)g.nz * g.ny * (g.nx - 1);
       default: {
@@ -367,6 +381,22 @@ struct Engine : EngineBase {
       }
     }
   }
+  // compact length of a block over the whole (all-slab) grid
+  long long block_len_global(int prim) const {
+    const Geo& g = Pr.g;
+    switch (prim) {
+      case PRIM_I: return (long long)nz_g * g.plane;
+      case PRIM_Z: return (long long)(nz_g - 1) * g.plane;
+      case PRIM_Y: return (long long)nz_g * (g.ny - 1) * g.nx;
+      case PRIM_X: return (long long)nz_g * g.ny * (g.nx - 1);
+      default: return block_len(prim);   // blur/mask: single rank only
+    }
+  }
+  long long set_len_global(int i) const {
+    long long c = 0;
+    for (int b = 0; b < Pr.set[i].nblk; ++b) c += block_len_global(Pr.set[i].prim[b]);
+    return c;
+  }
   long long set_len(int i) const {
     long long c = 0;
     for (int b = 0; b < Pr.set[i].nblk; ++b) c += block_len(Pr.set[i].prim[b]);
@@ -376,7 +406,8 @@ struct Engine : EngineBase {
   // ---- iteration enqueue ------------------------------------------------
   // profiling: an event is recorded before the first kernel and after every
   // kernel; consecutive pairs give each kernel's device time (kind list)
-  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, NKIND };
+  // KB_COMM: a z-slab site's exchange + finalisers (multi-rank only)
+  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, NKIND };
   bool prof = false;
   std::vector<cudaEvent_t> pev;      // events of one graph (capture order)
   std::vector<int> pkind;            // kind of the kernel ending at pev[i+1]
@@ -427,49 +458,70 @@ struct Engine : EngineBase {
     }
   }
 
-  void enqueue_iteration(int n_cg, int kpos = 0) {
-    if (prof && pev_used == 0) mark(-1);
-    if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 0, 0); ++launches; mark(KB_BLUR); }
+  // ---- phase launchers (one rank's part of each step) -------------------
+  void launch_blur(int mode, int j) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, mode, j); ++launches; }
+  void launch_rhs() {
     if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
     else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
-    ++launches; mark(KB_RHS);
+    ++launches;
+  }
+  void launch_cg1(int j) {
+    if (zg.on) {
+      // measured on C4: z-marching wins for k_cg1 (operand recomputed from
+      // two arrays at 5 positions), the flat sweep for k_cg2 (profiles/)
+      k_cg1z<T, true><<<zg.tiles_x * zg.tiles_y * zg.nzc, BLOCK, smem_z, stream>>>(Pr, zg, j);
+    } else if (vec) {
+      k_cg1v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
+    } else {
+      k_cg1<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
+    }
+    ++launches;
+  }
+  void launch_cg2(int j) {
+    if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
+    else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
+    ++launches;
+  }
+  void launch_select(int r) {
+    if (vec) k_selectf<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
+    else k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
+    ++launches;
+  }
+  bool has_card() const {
+    for (int i = 0; i < p; ++i) if (Pr.set[i].kind == K_CARD) return true;
+    return false;
+  }
+  void launch_tie() {
+    if (vec) k_tiecountf<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
+    else k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
+    ++launches;
+  }
+  void launch_control() { k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches; }
+  void launch_fin(int site, int j, int round) {
+    k_fin<T><<<1, BLOCK, 0, stream>>>(Pr, site, j, round);
+    ++launches;
+  }
+
+  void enqueue_iteration(int n_cg, int kpos = 0) {
+    if (prof && pev_used == 0) mark(-1);
+    if (Pr.has[PRIM_F]) { launch_blur(0, 0); mark(KB_BLUR); }
+    launch_rhs(); mark(KB_RHS);
     for (int j = 0; j < n_cg; ++j) {
-      if (Pr.has[PRIM_F]) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, 1, j); ++launches; mark(KB_BLUR); }
-      if (zg.on) {
-        const int gz = zg.tiles_x * zg.tiles_y * zg.nzc;
-        // measured on C4: z-marching wins for k_cg1 (operand recomputed from
-        // two arrays at 5 positions), the flat sweep for k_cg2 (profiles/)
-        k_cg1z<T, true><<<gz, BLOCK, smem_z, stream>>>(Pr, zg, j); ++launches; mark(KB_CG1);
-        k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
-      } else if (vec) {
-        k_cg1v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG1);
-        k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
-      } else {
-        k_cg1<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG1);
-        k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j); ++launches; mark(KB_CG2);
-      }
+      if (Pr.has[PRIM_F]) { launch_blur(1, j); mark(KB_BLUR); }
+      launch_cg1(j); mark(KB_CG1);
+      launch_cg2(j); mark(KB_CG2);
     }
     launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
-      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
-        if (vec) k_selectf<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
-        else k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
-        ++launches; mark(KB_SELECT);
-      }
-      bool card = false;
-      for (int i = 0; i < p; ++i) if (Pr.set[i].kind == K_CARD) card = true;
-      if (card) {
-        if (vec) k_tiecountf<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
-        else k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
-        ++launches; mark(KB_TIE);
-      }
+      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
+      if (has_card()) { launch_tie(); mark(KB_TIE); }
     }
     if (Pr.nglob > 0) {
       launch_pass2(kpos);
       ++launches; mark(KB_PASS2);
     }
-    k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches; mark(KB_CTRL);
+    launch_control(); mark(KB_CTRL);
   }
 
   void harvest_profile() {
@@ -544,9 +596,9 @@ struct Engine : EngineBase {
       c.u_k[i] = hs.prm.k;
       c.rel[i] = hs.prm.relative;
       c.zin[i] = hs.zero_in;
-      c.mreal[i] = set_len(i);   // compact M on this level's grid (k = floor(k_frac M_l), L23)
+      c.mreal[i] = set_len_global(i);   // compact M on this level's grid (k = floor(k_frac M_l), L23)
     }
-    c.mreal[p] = Pr.g.N;
+    c.mreal[p] = (long long)nz_g * Pr.g.plane;
     make_coeffs(Pr, c.rho, &c.cI, &c.cz, &c.cy, &c.cx, &c.cF);
     c.log_cg = d_log_cg; c.log_branch = d_log_br; c.log_rho = d_log_rho; c.log_gamma = d_log_gam;
     c.log_feas = d_log_feas; c.log_evol = d_log_evol; c.log_len = log_cap;
@@ -656,6 +708,355 @@ struct Engine : EngineBase {
   }
 };
 
+// ------------------------------------------------------------------ z slabs
+// Slab rule: nz planes split as evenly as possible, the first
+// nz mod G ranks holding one extra plane.
+inline void slab_of(int nz, int G, int r, int* z0, int* n) {
+  const int q = nz / G, m = nz % G;
+  *n = q + (r < m ? 1 : 0);
+  *z0 = r * q + std::min(r, m);
+}
+
+// NCCL, resolved at run time (the library loads without it; a multi-rank grid
+// needs it).  Only the stable C API is used: unique id, init, send/recv in
+// groups, destroy.  With torch imported first, its libnccl.so.2 is reused.
+typedef struct { char internal[128]; } nccl_uid;
+typedef void* nccl_comm_t;
+enum { NCCL_CHAR = 0 };
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  int (*GetUniqueId)(nccl_uid*) = nullptr;
+  int (*CommInitRank)(nccl_comm_t*, int, nccl_uid, int) = nullptr;
+  int (*CommDestroy)(nccl_comm_t) = nullptr;
+  int (*Send)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  int (*Recv)(void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+NcclApi& nccl() {
+  static NcclApi a = [] {
+    NcclApi n;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) { n.err = std::string("libnccl.so.2 not found: ") + dlerror(); return n; }
+    auto sym = [&](const char* s) { return dlsym(h, s); };
+    n.GetUniqueId = (int (*)(nccl_uid*))sym("ncclGetUniqueId");
+    n.CommInitRank = (int (*)(nccl_comm_t*, int, nccl_uid, int))sym("ncclCommInitRank");
+    n.CommDestroy = (int (*)(nccl_comm_t))sym("ncclCommDestroy");
+    n.Send = (int (*)(const void*, size_t, int, int, nccl_comm_t, cudaStream_t))sym("ncclSend");
+    n.Recv = (int (*)(void*, size_t, int, int, nccl_comm_t, cudaStream_t))sym("ncclRecv");
+    n.GroupStart = (int (*)())sym("ncclGroupStart");
+    n.GroupEnd = (int (*)())sym("ncclGroupEnd");
+    n.GetErrorString = (const char* (*)(int))sym("ncclGetErrorString");
+    n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.Send && n.Recv && n.GroupStart &&
+           n.GroupEnd && n.GetErrorString;
+    if (!n.ok) n.err = "libnccl.so.2 lacks the send/recv API";
+    return n;
+  }();
+  return a;
+}
+#define NC(call)                                                                              \
+  do {                                                                                        \
+    int r_ = (call);                                                                          \
+    if (r_ != 0) throw SipError{SIP_ERR_NCCL, std::string(#call) + ": " + nccl().GetErrorString(r_)}; \
+  } while (0)
+
+// one plane transfer of a field block (element pointers as bytes)
+enum { H_LO = 1,    // fill my lower ghost plane (z0 - 1) from the rank below
+       H_HI = 2,    // fill my upper ghost plane (z0 + nz) from the rank above
+       H_BOTH = 3 };
+struct PlaneX {
+  char *lo_ghost, *first, *last, *hi_ghost;
+  size_t bytes;
+  int dir;
+};
+
+// The exchange step of a site: halos of the listed planes plus the gather of
+// every rank's slot (n doubles at slot r of rank r's buffer) to all ranks.
+// xf[l] / xg[l]: the planes and gather buffer of the l-th LOCAL rank.
+struct Comm {
+  int G = 1;
+  virtual ~Comm() {}
+  virtual void exchange(const std::vector<std::vector<PlaneX>>& xf, const std::vector<double*>& xg,
+                        size_t slot, size_t n, cudaStream_t st) = 0;
+};
+
+// All G slabs on this device (option "virtual_ranks"): the same decomposition,
+// finalisers and exchange schedule as the NCCL path, the transfers as device
+// copies on the grid's stream (captured into the iteration graph).
+struct LocalComm : Comm {
+  void exchange(const std::vector<std::vector<PlaneX>>& xf, const std::vector<double*>& xg, size_t slot,
+                size_t n, cudaStream_t st) override {
+    for (int r = 0; r < G; ++r)
+      for (size_t k = 0; k < xf[r].size(); ++k) {
+        const PlaneX& X = xf[r][k];
+        if ((X.dir & H_LO) && r > 0)
+          CU(cudaMemcpyAsync(X.lo_ghost, xf[r - 1][k].last, X.bytes, cudaMemcpyDeviceToDevice, st));
+        if ((X.dir & H_HI) && r < G - 1)
+          CU(cudaMemcpyAsync(X.hi_ghost, xf[r + 1][k].first, X.bytes, cudaMemcpyDeviceToDevice, st));
+      }
+    if (n)
+      for (int r = 0; r < G; ++r)
+        for (int q = 0; q < G; ++q)
+          if (q != r)
+            CU(cudaMemcpyAsync(xg[q] + r * slot, xg[r] + r * slot, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  }
+};
+
+// One rank per GPU: one NCCL group per site (grouped send/recv: the halo
+// planes with the z neighbours, the slot with every peer).  Sends and
+// receives between a pair are issued in the same order on both sides.
+struct NcclComm : Comm {
+  int rank = 0;
+  nccl_comm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+  void exchange(const std::vector<std::vector<PlaneX>>& xf, const std::vector<double*>& xg, size_t slot,
+                size_t n, cudaStream_t st) override {
+    if (xf[0].empty() && !n) return;
+    NcclApi& A = nccl();
+    NC(A.GroupStart());
+    for (const PlaneX& X : xf[0]) {
+      if (X.dir & H_LO) {
+        if (rank > 0) NC(A.Recv(X.lo_ghost, X.bytes, NCCL_CHAR, rank - 1, comm, st));
+        if (rank < G - 1) NC(A.Send(X.last, X.bytes, NCCL_CHAR, rank + 1, comm, st));
+      }
+      if (X.dir & H_HI) {
+        if (rank < G - 1) NC(A.Recv(X.hi_ghost, X.bytes, NCCL_CHAR, rank + 1, comm, st));
+        if (rank > 0) NC(A.Send(X.first, X.bytes, NCCL_CHAR, rank - 1, comm, st));
+      }
+    }
+    if (n)
+      for (int q = 0; q < G; ++q) {
+        if (q == rank) continue;
+        NC(A.Send(xg[0] + rank * slot, n * sizeof(double), NCCL_CHAR, q, comm, st));
+        NC(A.Recv(xg[0] + q * slot, n * sizeof(double), NCCL_CHAR, q, comm, st));
+      }
+    NC(A.GroupEnd());
+  }
+};
+
+// fields whose planes a site exchanges
+enum FieldSel { FS_X, FS_R, FS_P0, FS_P1, FS_M, FS_Y0, FS_Y1, FS_V0, FS_V1 };
+enum SetSel { SS_ALL = 0, SS_POINTWISE = 1, SS_GLOBAL = 2 };
+struct HaloReq { int sel, sets, dir; };
+
+// The engines of this process's ranks (1 with NCCL, G with virtual ranks) run
+// each step in lock-step: every engine launches its part, then the site's
+// exchange, then every engine's k_fin.  The whole iteration is one CUDA graph.
+template <class T>
+struct Team : EngineBase {
+  std::vector<std::unique_ptr<Engine<T>>> eng;
+  Comm* comm = nullptr;
+  int G = 1;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int g_iters = 0, g_ncg = -1, g_ce = 0;
+  bool g_prof = false;
+  long long launches = 0, graph_kernels = 0;
+  int* h_flag = nullptr;
+  cudaEvent_t ev_flag[2];
+  bool ran = false;
+
+  ~Team() override {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (h_flag) cudaFreeHost(h_flag);
+    cudaEventDestroy(ev_flag[0]); cudaEventDestroy(ev_flag[1]);
+  }
+
+  // ranks [r0, r0 + nlocal) of G live in this process
+  void setup(int ndim, int nz_g, int ny, int nx, const double* h, cudaStream_t st, const std::vector<HostSet>& s,
+             int G_, int r0, int nlocal, Comm* c) {
+    G = G_; comm = c; stream = st;
+    for (const HostSet& hs : s)
+      if (!hs.lo_vec.empty() || !hs.hi_vec.empty())
+        throw SipError{SIP_ERR_CONFIG, "per-entry bounds on z slabs: not in this build"};
+    for (int l = 0; l < nlocal; ++l) {
+      int z0, nzl;
+      slab_of(nz_g, G, r0 + l, &z0, &nzl);
+      if (nzl < 1) throw SipError{SIP_ERR_CONFIG, "fewer z planes than ranks"};
+      auto e = std::make_unique<Engine<T>>();
+      e->setup(ndim, nzl, ny, nx, h, st, s, z0, nz_g, G, r0 + l);
+      if (!e->vec)
+        throw SipError{SIP_ERR_CONFIG, "multi-rank grids need nx % (16 / sizeof(dtype)) == 0 and no blur/mask operator"};
+      eng.push_back(std::move(e));
+    }
+    CU(cudaMallocHost(&h_flag, 2 * sizeof(int)));
+    CU(cudaEventCreateWithFlags(&ev_flag[0], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ev_flag[1], cudaEventDisableTiming));
+  }
+
+  void add_planes(Engine<T>& e, const HaloReq& q, std::vector<PlaneX>& out) {
+    const Geo& g = e.Pr.g;
+    const size_t pl = (size_t)g.plane;
+    auto push = [&](T* b) {
+      PlaneX X;
+      X.lo_ghost = (char*)(b - pl);
+      X.first = (char*)b;
+      X.last = (char*)(b + (size_t)(g.nz - 1) * pl);
+      X.hi_ghost = (char*)(b + (size_t)g.nz * pl);
+      X.bytes = pl * sizeof(T);
+      X.dir = q.dir;
+      out.push_back(X);
+    };
+    switch (q.sel) {
+      case FS_X: push(e.Pr.x); return;
+      case FS_R: push(e.Pr.r); return;
+      case FS_P0: push(e.Pr.pb[0]); return;
+      case FS_P1: push(e.Pr.pb[1]); return;
+      case FS_M: push(const_cast<T*>(e.Pr.m)); return;
+      default: break;
+    }
+    const bool isy = q.sel == FS_Y0 || q.sel == FS_Y1;
+    const int par = (q.sel == FS_Y1 || q.sel == FS_V1) ? 1 : 0;
+    for (int i = 0; i < e.P; ++i) {
+      SetD<T>& S = e.Pr.set[i];
+      if (q.sets == SS_POINTWISE && S.global) continue;
+      if (q.sets == SS_GLOBAL && !S.global) continue;
+      for (int b = 0; b < S.nblk; ++b)   // only D_z blocks reach across planes (D_z^T in the rhs)
+        if (S.prim[b] == PRIM_Z) push((isy ? S.y[par] : S.v[par]) + (int64_t)b * g.ld);
+    }
+  }
+
+  // exchange (halos + gather of `site`'s payload) and the finalisers
+  void site(int st_, int j, int round, std::initializer_list<HaloReq> reqs, bool fin = true) {
+    std::vector<std::vector<PlaneX>> xf(eng.size());
+    std::vector<double*> xg(eng.size());
+    for (size_t l = 0; l < eng.size(); ++l) {
+      for (const HaloReq& q : reqs) add_planes(*eng[l], q, xf[l]);
+      xg[l] = eng[l]->Pr.xg;
+    }
+    const size_t n = fin ? (size_t)site_payload(st_, eng[0]->P, eng[0]->hc.njobs) : 0;
+    comm->exchange(xf, xg, (size_t)eng[0]->Pr.xslot, n, stream);
+    if (fin)
+      for (auto& e : eng) { e->launch_fin(st_, j, round); ++launches; }
+    eng[0]->mark(Engine<T>::KB_COMM);
+  }
+
+  template <class F>
+  void each(F&& f, int kind = -1) {
+    for (auto& e : eng) { long long b = e->launches; f(*e); launches += e->launches - b; }
+    if (kind >= 0) eng[0]->mark(kind);
+  }
+
+  // one outer iteration; kpos (1-based position in the 10-iteration pattern)
+  // fixes the y / v parity and the iteration type at capture
+  void enqueue_iteration(int n_cg, int kpos) {
+    const int wr = (kpos & 1) ^ 1;   // parity written by this iteration
+    Engine<T>& e0 = *eng[0];
+    if (e0.prof && e0.pev_used == 0) e0.mark(-1);
+    using E = Engine<T>;
+    each([&](Engine<T>& e) { e.launch_rhs(); }, E::KB_RHS);
+    site(ST_RHS, 0, 0, {{FS_R, 0, H_BOTH}});
+    for (int j = 0; j < n_cg; ++j) {
+      each([&](Engine<T>& e) { e.launch_cg1(j); }, E::KB_CG1);
+      site(ST_CG1, j, 0, {{(j & 1) ? FS_P1 : FS_P0, 0, H_BOTH}});
+      each([&](Engine<T>& e) { e.launch_cg2(j); }, E::KB_CG2);
+      if (j == n_cg - 1) site(ST_CG2, j, 0, {{FS_X, 0, H_BOTH}});   // x^{k+1} for pass 1 and the next rhs
+      else site(ST_CG2, j, 0, {{FS_R, 0, H_BOTH}});
+    }
+    each([&](Engine<T>& e) { e.launch_pass1(kpos); ++e.launches; }, E::KB_PASS1);
+    site(ST_PASS1, 0, 0, {{wr ? FS_Y1 : FS_Y0, SS_POINTWISE, H_LO}, {wr ? FS_V1 : FS_V0, SS_POINTWISE, H_LO}});
+    if (e0.hc.njobs > 0) {
+      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
+        each([&](Engine<T>& e) { e.launch_select(r); }, E::KB_SELECT);
+        site(ST_SELECT, 0, r, {});
+      }
+      if (e0.has_card()) {
+        each([&](Engine<T>& e) { e.launch_tie(); }, E::KB_TIE);
+        site(ST_TIE, 0, 0, {});
+      }
+    }
+    if (e0.Pr.nglob > 0) {
+      each([&](Engine<T>& e) { e.launch_pass2(kpos); ++e.launches; }, E::KB_PASS2);
+      site(ST_PASS2, 0, 0, {{wr ? FS_Y1 : FS_Y0, SS_GLOBAL, H_LO}, {wr ? FS_V1 : FS_V0, SS_GLOBAL, H_LO}});
+    }
+    each([&](Engine<T>& e) { e.launch_control(); }, E::KB_CTRL);
+  }
+
+  int period() const {
+    const int ce = std::max(1, eng[0]->hc.opt.check_every);
+    return (ce % 2 == 0) ? ce : 2 * ce;
+  }
+
+  void ensure_graph(int iters, int n_cg) {
+    const int ce = eng[0]->hc.opt.check_every;
+    if (gexec && g_iters == iters && g_ncg == n_cg && g_ce == ce && g_prof == eng[0]->prof) return;
+    if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+    cudaGraph_t graph;
+    const long long before = launches;
+    eng[0]->pev_used = 0;
+    eng[0]->pkind.clear();
+    CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) enqueue_iteration(n_cg, i + 1);
+    cudaError_t e = cudaStreamEndCapture(stream, &graph);
+    if (e != cudaSuccess) throw SipError{SIP_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e)};
+    graph_kernels = launches - before;
+    launches = before;
+    CU(cudaGraphInstantiate(&gexec, graph, 0));
+    cudaGraphDestroy(graph);
+    g_iters = iters; g_ncg = n_cg; g_ce = ce; g_prof = eng[0]->prof;
+  }
+
+  void run_iterations(int max_iter, int gi, int n_cg) {
+    const bool poll = !eng[0]->hc.opt.fixed_work;
+    int* d_stop = &eng[0]->d_ctrl->stopped;
+    if (gi <= 0) {
+      for (int it = 0; it < max_iter; ++it) {
+        if (eng[0]->prof) { eng[0]->pev_used = 0; eng[0]->pkind.clear(); }
+        enqueue_iteration(n_cg, it + 1);
+        eng[0]->harvest_profile();
+        if ((it + 1) % std::max(1, eng[0]->hc.opt.check_every) == 0 || it + 1 == max_iter) {
+          CU(cudaMemcpyAsync(h_flag, d_stop, sizeof(int), cudaMemcpyDeviceToHost, stream));
+          CU(cudaStreamSynchronize(stream));
+          if (h_flag[0]) break;
+        }
+      }
+      return;
+    }
+    const int per = period();
+    gi = (gi + per - 1) / per * per;   // the graph must start every launch at the same pattern position
+    ensure_graph(gi, n_cg);
+    const int nlaunch = (max_iter + gi - 1) / gi;
+    for (int l = 0; l < nlaunch; ++l) {
+      CU(cudaGraphLaunch(gexec, stream));
+      launches += graph_kernels;
+      eng[0]->harvest_profile();
+      if (!poll) continue;
+      CU(cudaMemcpyAsync(&h_flag[l & 1], d_stop, sizeof(int), cudaMemcpyDeviceToHost, stream));
+      CU(cudaEventRecord(ev_flag[l & 1], stream));
+      if (l >= 1) {
+        CU(cudaEventSynchronize(ev_flag[(l - 1) & 1]));
+        if (h_flag[(l - 1) & 1]) break;
+      }
+    }
+  }
+
+  // single-level solve on the engines' m slabs (Algorithm 1)
+  void solve(const Options& o, int max_iter, double eps_feas, double eps_evol, int init_x, int init_yv,
+             const double* rho_in, const double* gamma_in) {
+    const double floor_ = o.cg_tol_floor > 0 ? o.cg_tol_floor
+                                             : 10.0 * (sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON);
+    launches = 0;
+    each([&](Engine<T>& e) {
+      e.ensure_log(max_iter);
+      e.fill_ctrl(o, max_iter, eps_feas, eps_evol, floor_, rho_in, gamma_in);
+      e.fill_logs_nan(max_iter);
+    });
+    // halos of m (A m in k_init) and of a given x
+    if (init_x) site(ST_INIT, 0, 0, {{FS_M, 0, H_BOTH}}, false);
+    else site(ST_INIT, 0, 0, {{FS_M, 0, H_BOTH}, {FS_X, 0, H_BOTH}}, false);
+    each([&](Engine<T>& e) { e.run_init(init_x, init_yv); });
+    site(ST_INIT, 0, 0, {{FS_X, 0, H_BOTH}, {FS_Y1, SS_ALL, H_LO}, {FS_V1, SS_ALL, H_LO}});
+    run_iterations(max_iter, o.graph_iters, o.n_cg);
+    each([&](Engine<T>& e) { e.read_ctrl(); e.ran = true; e.scratch_used = false; });
+    ran = true;
+  }
+};
+
 }  // namespace
 
 // ------------------------------------------------------------------ grid
@@ -668,7 +1069,9 @@ struct sip_grid_s {
   int ndim = 2;
   int64_t n[3] = {1, 1, 1};   // nz, ny, nx
   double h[3] = {1, 1, 1};
-  int nranks = 1, rank = 0;
+  int nranks = 1, rank = 0;   // NCCL z-slab decomposition (one rank per process)
+  int vranks = 1;             // option "virtual_ranks": G slabs on this device
+  std::unique_ptr<Comm> comm;
   std::vector<HostSet> sets;
   Options opt;
   std::string err;
@@ -683,6 +1086,8 @@ namespace {
 
 template <class T>
 Engine<T>* engine_of(sip_grid g) {
+  if (g->nranks > 1 || g->vranks > 1)
+    throw SipError{SIP_ERR_CONFIG, "step-level entry points and multilevel are single-rank in this build"};
   if (!g->eng) {
     auto e = std::make_unique<Engine<T>>();
     e->setup(g->ndim, (int)g->n[0], (int)g->n[1], (int)g->n[2], g->h, g->stream, g->sets);
@@ -707,8 +1112,62 @@ double eps_evol_of(const sip_grid g, double tol) {
   return tol > 0 ? 10.0 * tol : 1e-2;
 }
 
+bool is_team(const sip_grid g) { return g->nranks > 1 || g->vranks > 1; }
+
+template <class T>
+Team<T>* team_of(sip_grid g) {
+  if (!g->eng) {
+    const bool nc = g->nranks > 1;
+    const int G = nc ? g->nranks : g->vranks;
+    if (!nc) {
+      auto lc = std::make_unique<LocalComm>();
+      lc->G = G;
+      g->comm = std::move(lc);
+    }
+    auto t = std::make_unique<Team<T>>();
+    t->setup(g->ndim, (int)g->n[0], (int)g->n[1], (int)g->n[2], g->h, g->stream, g->sets, G,
+             nc ? g->rank : 0, nc ? 1 : G, g->comm.get());
+    g->eng = std::move(t);
+  }
+  return static_cast<Team<T>*>(g->eng.get());
+}
+
+// z-slab projection: NCCL ranks (m, x = this rank's slab) or virtual ranks
+// (m, x = the whole grid, slab l at plane offset z0_l)
+template <class T>
+sip_status project_team_T(sip_grid g, const void* m, void* x, int max_iter, double tol, sip_result* res) {
+  Team<T>* t = team_of<T>(g);
+  Engine<T>* e0 = t->eng[0].get();
+  const double eps_feas = tol > 0 ? tol : 1e-3;
+  e0->prof = g->opt.profile != 0;
+  for (int q = 0; q < Engine<T>::NKIND; ++q) { e0->prof_ms[q] = 0; e0->prof_cnt[q] = 0; }
+  CU(cudaEventRecord(e0->ev0, g->stream));
+  const int64_t zoff0 = g->nranks > 1 ? e0->z0 : 0;
+  for (auto& e : t->eng) {
+    const size_t off = (size_t)(e->z0 - zoff0) * e->Pr.g.plane;
+    copy_in(e.get(), (const T*)m + off, const_cast<T*>(e->Pr.m), (size_t)e->Pr.g.N);
+  }
+  t->solve(g->opt, max_iter, eps_feas, eps_evol_of(g, tol), 1, 1, nullptr, nullptr);
+  for (auto& e : t->eng) {
+    const size_t off = (size_t)(e->z0 - zoff0) * e->Pr.g.plane;
+    copy_out(e.get(), e->Pr.x, (T*)x + off, (size_t)e->Pr.g.N);
+  }
+  CU(cudaEventRecord(e0->ev1, g->stream));
+  CU(cudaEventSynchronize(e0->ev1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0->ev0, e0->ev1);
+  e0->fill_result(res, ms);
+  g->have_m = true;
+  g->last_launches = t->launches;
+  g->last = e0;
+  for (auto& e : t->eng)
+    if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, "NaN/Inf in the PARSDMM state"};
+  return e0->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
+}
+
 template <class T>
 sip_status project_T(sip_grid g, const void* m, void* x, int max_iter, double tol, sip_result* res) {
+  if (is_team(g)) return project_team_T<T>(g, m, x, max_iter, tol, res);
   Engine<T>* e = engine_of<T>(g);
   const size_t N = (size_t)e->Pr.g.N;
   const double eps_feas = tol > 0 ? tol : 1e-3;
@@ -1062,6 +1521,30 @@ sip_status get_state_T(sip_grid g, int set_id, int which, void* out) {
   return SIP_OK;
 }
 
+// z slabs: the compact field of set i, block-major, each block the slabs of
+// this process's ranks in rank order (virtual ranks: the whole field)
+template <class T>
+sip_status get_state_team_T(sip_grid g, int set_id, int which, void* out) {
+  Team<T>* t = static_cast<Team<T>*>(g->eng.get());
+  if (!t || !t->ran) throw SipError{SIP_ERR_STATE, "no projection state"};
+  const SetD<T>& S0 = t->eng[0]->Pr.set[set_id];
+  long long off = 0;
+  for (int b = 0; b < S0.nblk; ++b)
+    for (auto& e : t->eng) {
+      const Geo& G = e->Pr.g;
+      const long long len = e->block_len(S0.prim[b]);
+      T* comp = e->template dalloc<T>((size_t)std::max(len, 1ll));
+      T* src = e->final_field(set_id, which) + (int64_t)b * G.ld;
+      k_pack<T, T><<<e->g_small_(), BLOCK, 0, e->stream>>>(G, S0.prim[b], e->d_fmap, 0, src, comp, 0);
+      CU(cudaGetLastError());
+      copy_out(e.get(), comp, (T*)out + off, (size_t)len);
+      CU(cudaStreamSynchronize(e->stream));
+      cudaFree(comp); e->allocs.pop_back();
+      off += len;
+    }
+  return SIP_OK;
+}
+
 template <class T>
 sip_status get_log_T(sip_grid g, int max_iter, int* cg, int* branch, double* rho_t, double* gam_t,
                      double* feas, double* evol) {
@@ -1124,7 +1607,21 @@ const char* sip_last_error(sip_grid g) { return g ? g->err.c_str() : "null grid"
 sip_status sip_comm_unique_id(uint8_t out[128]) {
   if (!out) return SIP_ERR_ARG;
   memset(out, 0, 128);
-  return SIP_ERR_CONFIG;   // multi-rank z-slab path: not in this build
+  NcclApi& A = nccl();
+  if (!A.ok) return SIP_ERR_NCCL;
+  nccl_uid id;
+  if (A.GetUniqueId(&id) != 0) return SIP_ERR_NCCL;
+  memcpy(out, id.internal, 128);
+  return SIP_OK;
+}
+
+sip_status sip_slab(int64_t nz, int nranks, int rank, int64_t* z0, int64_t* nz_local) {
+  if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || !z0 || !nz_local) return SIP_ERR_ARG;
+  int a, b;
+  slab_of((int)nz, nranks, rank, &a, &b);
+  *z0 = a;
+  *nz_local = b;
+  return SIP_OK;
 }
 
 sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtype dtype,
@@ -1133,7 +1630,8 @@ sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtyp
   *out = nullptr;
   for (int a = 0; a < ndim; ++a) if (n[a] < 2) return SIP_ERR_SHAPE;
   if (h) for (int a = 0; a < ndim; ++a) if (!(h[a] > 0)) return SIP_ERR_PARAM;
-  if (comm && comm->nranks > 1) return SIP_ERR_CONFIG;
+  if (comm && (comm->nranks < 1 || comm->rank < 0 || comm->rank >= comm->nranks)) return SIP_ERR_ARG;
+  if (comm && comm->nranks > 1 && (!comm->nccl_unique_id || n[0] < comm->nranks)) return SIP_ERR_ARG;
   int64_t N = 1;
   for (int a = 0; a < ndim; ++a) N *= n[a];
   if (N >= (1ll << 31) - 8) return SIP_ERR_SHAPE;
@@ -1154,6 +1652,19 @@ sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtyp
     g->h[0] = h ? h[0] : 1.0; g->h[1] = 1.0; g->h[2] = h ? h[1] : 1.0;
   } else {
     for (int a = 0; a < 3; ++a) { g->n[a] = n[a]; g->h[a] = h ? h[a] : 1.0; }
+  }
+  if (comm && comm->nranks > 1) {
+    NcclApi& A = nccl();
+    if (!A.ok) { delete g; return SIP_ERR_NCCL; }
+    auto nc = std::make_unique<NcclComm>();
+    nc->G = comm->nranks;
+    nc->rank = comm->rank;
+    nccl_uid id;
+    memcpy(id.internal, comm->nccl_unique_id, 128);
+    if (A.CommInitRank(&nc->comm, comm->nranks, id, comm->rank) != 0) { delete g; return SIP_ERR_NCCL; }
+    g->nranks = comm->nranks;
+    g->rank = comm->rank;
+    g->comm = std::move(nc);
   }
   *out = g;
   return SIP_OK;
@@ -1250,6 +1761,16 @@ sip_status sip_set_option(sip_grid g, const char* key, double value) {
   else if (k == "warm_start") o.warm_start = value != 0;
   else if (k == "graph_iters") { if (value < 0) return SIP_ERR_PARAM; o.graph_iters = (int)value; }
   else if (k == "profile") o.profile = value != 0;
+  else if (k == "virtual_ranks") {
+    const int G = (int)value;
+    if (G < 1 || (double)G != value || G > g->n[0]) return SIP_ERR_PARAM;
+    if (g->nranks > 1) { g->err = "virtual_ranks on an NCCL grid"; return SIP_ERR_CONFIG; }
+    if (G != g->vranks) {
+      if (g->stream) cudaStreamSynchronize(g->stream);
+      g->eng.reset(); g->levels.clear(); g->last = nullptr; g->comm.reset();
+      g->vranks = G;
+    }
+  }
   else { g->err = "unknown option " + k; return SIP_ERR_ARG; }
   return SIP_OK;
 }
@@ -1275,6 +1796,7 @@ sip_status sip_project_multilevel(sip_grid g, const void* m, void* x, int n_leve
     if (a == 1 && g->ndim == 2) continue;
     if (g->n[a] % f != 0 || g->n[a] / f < 2) { g->err = "grid not divisible for the levels"; return SIP_ERR_CONFIG; }
   }
+  if (g->nranks > 1 || g->vranks > 1) { g->err = "multilevel on z slabs: not in this build"; return SIP_ERR_CONFIG; }
   return guarded(g, [&]() -> sip_status {
     return g->dtype == SIP_F32 ? multilevel_T<float>(g, m, x, n_levels, max_iter, tol, per_level)
                                : multilevel_T<double>(g, m, x, n_levels, max_iter, tol, per_level);
@@ -1325,6 +1847,9 @@ sip_status sip_project_set(sip_grid g, int set_id, const void* w, void* y) {
 sip_status sip_get_state(sip_grid g, int set_id, int which, void* out) {
   if (!g || !out || set_id < 0 || set_id > (int)g->sets.size() || (which != 0 && which != 1)) return SIP_ERR_ARG;
   return guarded(g, [&]() -> sip_status {
+    if (is_team(g))
+      return g->dtype == SIP_F32 ? get_state_team_T<float>(g, set_id, which, out)
+                                 : get_state_team_T<double>(g, set_id, which, out);
     return g->dtype == SIP_F32 ? get_state_T<float>(g, set_id, which, out) : get_state_T<double>(g, set_id, which, out);
   });
 }
@@ -1354,7 +1879,7 @@ sip_status sip_get_profile(sip_grid g, int n, double* ms, int64_t* count) {
   return guarded(g, [&]() -> sip_status {
     if (!g->last) throw SipError{SIP_ERR_STATE, "no projection"};
     auto fill = [&](auto* e) {
-      for (int q = 0; q < n && q < 9; ++q) {
+      for (int q = 0; q < n && q < 10; ++q) {
         if (ms) ms[q] = e->prof_ms[q];
         if (count) count[q] = e->prof_cnt[q];
       }

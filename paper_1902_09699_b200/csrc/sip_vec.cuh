@@ -250,19 +250,8 @@ __global__ void __launch_bounds__(BLOCK) k_rhsv(const __grid_constant__ Prob<T> 
     reduce_partials(P.partials, 2, out, sh);
     if (threadIdx.x == 0) {
       *P.counter = 0u;
-      const double bbv = out[0], rrv = out[1];
-      C.bb = bbv; C.rr = rrv; C.rr_prev = rrv; C.beta = 0.0;
-      C.cg_j = 0; C.cg_count = 0;
-      C.zero_x = (bbv == 0.0);
-      double tol = 0.0;
-      if (bbv > 0.0) {
-        tol = 0.1 * sqrt(rrv) / sqrt(bbv);          // Eq. 25
-        if (tol < C.opt.cg_tol_floor) tol = C.opt.cg_tol_floor;
-      }
-      C.tol = tol;
-      int active = (bbv > 0.0) && (rrv > 0.0) && (C.opt.n_cg > 0);
-      if (active && C.opt.eq25 && sqrt(rrv) / sqrt(bbv) < tol) active = 0;
-      C.cg_active = active;
+      if (P.nranks > 1) publish(P, out, 2, 0, 1);
+      else fin_rhs(C, out);
     }
   }
 }
@@ -322,12 +311,8 @@ __global__ void __launch_bounds__(BLOCK) k_cg1v(const __grid_constant__ Prob<T> 
     reduce_partials(P.partials, 1, out, sh);
     if (threadIdx.x == 0) {
       *P.counter = 0u;
-      if (out[0] > 0.0) {
-        C.alpha = C.rr / out[0];
-      } else {               // breakdown: p.q <= 0 (reading L18)
-        C.cg_active = 0;
-        C.breakdown = 1;
-      }
+      if (P.nranks > 1) publish(P, out, 1, 0, 1);
+      else fin_cg1(C, out);
     }
   }
 }
@@ -380,15 +365,8 @@ __global__ void __launch_bounds__(BLOCK) k_cg2v(const __grid_constant__ Prob<T> 
     reduce_partials(P.partials, 1, out, sh);
     if (threadIdx.x == 0) {
       *P.counter = 0u;
-      const double rn = out[0];
-      C.beta = rn / C.rr;
-      C.rr_prev = C.rr;
-      C.rr = rn;
-      C.cg_count += 1;
-      C.cg_j = j + 1;
-      int active = (C.cg_j < C.opt.n_cg) && (rn > 0.0);
-      if (active && C.opt.eq25 && sqrt(rn) / sqrt(C.bb) < C.tol) active = 0;
-      C.cg_active = active;
+      if (P.nranks > 1) publish(P, out, 1, 0, 1);
+      else fin_cg2(C, out, j);
     }
   }
 }

@@ -103,7 +103,7 @@ __device__ __forceinline__ void zapply(const CoefT<T>& cf, const Geo& g, bool hz
                                        int x0, const T* cur, const T* prev, const T* next, const T* ym,
                                        const T* yp, T xl, T xr, T* q) {
   constexpr int W = VT<T>::W;
-  const bool zlo = z >= 1, zhi = z < g.nz - 1;
+  const bool zlo = z + g.z0 >= 1, zhi = z + g.z0 < g.nz_g - 1;
   const bool ylo = y >= 1, yhi = y < g.ny - 1;
   const bool xlo = x0 >= 1, xhi = x0 + W < g.nx;
 #pragma unroll
@@ -148,7 +148,9 @@ __device__ __forceinline__ double zsweep(const Prob<T>& P, const ZGeo& Z, const 
     for (int e = 0; e < W; ++e) v[e] = 0;
   };
   auto fetch_plane = [&](int z, T* o) {
-    if (z >= 0 && z < g.nz) zfetch<T, UP>(g, src_r, p, beta, z, c.y, c.xw0, o); else zero(o);
+    const int gz = z + g.z0;   // planes -1 and nz are ghost planes (the z-slab halo)
+    if (gz >= 0 && gz < g.nz_g && z >= -1 && z <= g.nz) zfetch<T, UP>(g, src_r, p, beta, z, c.y, c.xw0, o);
+    else zero(o);
   };
   auto fetch_halo = [&](int z, int yy, T* o) {
     if (z < g.nz && yy >= 0 && yy < g.ny) zfetch<T, UP>(g, src_r, p, beta, z, yy, c.xw0, o); else zero(o);
@@ -278,12 +280,8 @@ __global__ void __launch_bounds__(BLOCK) k_cg1z(const __grid_constant__ Prob<T> 
     reduce_partials(P.partials, 1, out, sh);
     if (threadIdx.x == 0) {
       *P.counter = 0u;
-      if (out[0] > 0.0) {
-        C.alpha = C.rr / out[0];
-      } else {               // breakdown: p.q <= 0 (reading L18)
-        C.cg_active = 0;
-        C.breakdown = 1;
-      }
+      if (P.nranks > 1) publish(P, out, 1, 0, 1);
+      else fin_cg1(C, out);
     }
   }
 }
@@ -305,15 +303,8 @@ __global__ void __launch_bounds__(BLOCK) k_cg2z(const __grid_constant__ Prob<T> 
     reduce_partials(P.partials, 1, out, sh);
     if (threadIdx.x == 0) {
       *P.counter = 0u;
-      const double rn = out[0];
-      C.beta = rn / C.rr;
-      C.rr_prev = C.rr;
-      C.rr = rn;
-      C.cg_count += 1;
-      C.cg_j = j + 1;
-      int active = (C.cg_j < C.opt.n_cg) && (rn > 0.0);
-      if (active && C.opt.eq25 && sqrt(rn) / sqrt(C.bb) < C.tol) active = 0;
-      C.cg_active = active;
+      if (P.nranks > 1) publish(P, out, 1, 0, 1);
+      else fin_cg2(C, out, j);
     }
   }
 }

@@ -61,9 +61,9 @@ EXPORTS = [
     "sip_comm_unique_id", "sip_create_grid", "sip_add_set", "sip_set_option", "sip_project",
     "sip_project_multilevel", "sip_destroy", "sip_status_string", "sip_last_error",
     "sip_apply_op", "sip_apply_system", "sip_cg", "sip_project_set", "sip_get_state",
-    "sip_get_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile",
+    "sip_get_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
 ]
-KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control"]
+KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm"]
 
 _lib = None
 
@@ -103,6 +103,8 @@ def lib():
                                     C.POINTER(C.c_int64)]
         L.sip_get_launch_count.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
         L.sip_get_profile.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+        L.sip_slab.argtypes = [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.sip_comm_unique_id.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -288,9 +290,10 @@ def _res(r, p):
                 gamma=np.array(r.gamma[: p + 1]))
 
 
-def grid_for(problem, stream=None):
-    """Grid + sets for a sip_inputs.Problem (marshalling convenience)."""
-    g = Grid(problem.shape, problem.h, problem.dtype, stream=stream)
+def grid_for(problem, stream=None, comm=None):
+    """Grid + sets for a sip_inputs.Problem (marshalling convenience); comm:
+    a dist.comm_desc() for the z-slab path (the problem stays whole-grid)."""
+    g = Grid(problem.shape, problem.h, problem.dtype, stream=stream, comm=comm)
     for sd in problem.sets:
         g.add_set(sd)
     return g

@@ -1,0 +1,149 @@
+"""Parity of the z-slab decomposition on one GPU.
+
+The option "virtual_ranks" runs G z slabs on one device with the multi-GPU
+path's per-slab kernels, gather-slot finalisers (sip_team.cuh) and exchange
+schedule; only the transfers are device copies instead of NCCL send/recv.
+Bars: tiny fp64 cases keep the oracle's exact control flow (iterations, CG
+count per iteration, Algorithm-2 branches) and exact cardinality supports,
+including ties that straddle slab boundaries (index-ordered, L6); fp32
+slabs reproduce the single-rank run to 1e-5 and the oracle to 1e-3.
+"""
+import copy
+
+import numpy as np
+import pytest
+
+import oracle as O
+import sip_inputs as G
+from sip_inputs import INF, SetDef
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1902_09699_b200 import grid_for  # noqa: E402
+
+TD = {"f32": torch.float32, "f64": torch.float64}
+
+
+def run(prob, ranks, max_iter=None, want_log=False, states=(), **opts):
+    g = grid_for(prob)
+    if ranks > 1:
+        g.set_option("virtual_ranks", ranks)
+    for k, v in opts.items():
+        g.set_option(k, v)
+    m = torch.tensor(np.ascontiguousarray(prob.m), dtype=TD[prob.dtype], device="cuda")
+    x = torch.empty_like(m)
+    mi = max_iter or prob.options.get("max_iter", 200)
+    res, _ = g.project(m, x, max_iter=mi, tol=1e-3)
+    log = g.get_log(mi) if want_log else None
+    ys = {}
+    for i in states:
+        y = np.zeros(g.m_len(i))
+        g.get_state(i, 0, y)
+        ys[i] = y
+    out = x.double().cpu().numpy().ravel()
+    g.close()
+    return out, res, log, ys
+
+
+SLAB_TINY = [
+    (100, (8, 8), ("bounds", "l1", "slope"), 2),
+    (101, (8, 8), ("bounds", "l1", "slope", "card", "annulus"), 3),
+    (102, (6, 10), ("bounds", "l1", "slope", "dxbox"), 4),
+    (103, (4, 4, 4), ("bounds", "l1", "slope", "dybox"), 2),
+    (104, (6, 10), ("bounds", "card", "l2"), 3),
+    (105, (4, 4, 4), ("bounds", "l1", "cardz", "annulus"), 4),
+    (106, (8, 8), ("bounds", "l1x", "slope"), 5),
+    (107, (9, 8), ("bounds", "l1", "cardz", "slope"), 4),
+]
+
+
+@pytest.mark.parametrize("seed,shape,kinds,ranks", SLAB_TINY)
+def test_slab_tiny_bitexact_control_flow(seed, shape, kinds, ranks):
+    prob = G.tiny(seed, shape, kinds)
+    cards = [i for i, sd in enumerate(prob.sets) if sd.kind == "card"]
+    x, res, log, ys = run(prob, ranks, want_log=True, states=cards)
+    ref = O.parsdmm(prob.shape, prob.sets, prob.m, want_yv=True, **prob.options)
+    it = ref.iterations
+    assert res["iterations"] == it
+    np.testing.assert_array_equal(log["cg"][:it], ref.cg_per_iter)
+    np.testing.assert_array_equal(log["branch"][:it], ref.branch)
+    assert res["converged"] == ref.converged
+    assert O.relres(x, ref.x) < 1e-6
+    for i in cards:   # the final top-k supports (exact)
+        np.testing.assert_array_equal(ys[i] != 0, ref.y[i] != 0)
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 3, 7])
+def test_slab_ties_across_boundaries(ranks):
+    """Integer model and no x-update (n_cg = 0): w = D_z m stays integer, so
+    the k-th largest |w| is shared by many entries on several slabs and the
+    index-ordered tie break (L6) decides across ranks."""
+    rng = np.random.default_rng(7)
+    shape = (14, 6, 8)
+    m = rng.integers(0, 4, size=shape).astype(np.float64)
+    sets = [SetDef("DZ", "card", k=100), SetDef("TV", "card", k=230), SetDef("I", "bounds", lo=0, hi=3)]
+    prob = G.Problem("ties", shape, "f64", m, sets, options=dict(G.DEFAULT_OPTIONS))
+    prob.options["n_cg"] = 0
+    prob.options["max_iter"] = 12
+    x, res, log, ys = run(prob, ranks, want_log=True, states=(0, 1), n_cg=0)
+    ref = O.parsdmm(prob.shape, prob.sets, prob.m, want_yv=True, **prob.options)
+    assert res["iterations"] == ref.iterations
+    for i in (0, 1):
+        a = O.apply_A(shape, sets[i], m)
+        assert len(np.unique(np.abs(a))) < 8                 # heavy ties by construction
+        np.testing.assert_array_equal(ys[i], ref.y[i])        # values and support, exact
+
+
+def mid_problem(dtype="f32"):
+    shape = (20, 12, 64)
+    m = G.tiny_model(11, shape)
+    sets = [SetDef("I", "bounds", lo=1500.0, hi=4500.0), SetDef("TV", "l1", sigma=0.3, relative=True),
+            SetDef("DZ", "bounds", lo=0.0, hi=INF), SetDef("I", "annulus", sigma_lo=0.97, sigma_hi=0.99,
+                                                           relative=True)]
+    return G.Problem("mid", shape, dtype, m, sets, options=dict(G.DEFAULT_OPTIONS))
+
+
+@pytest.mark.parametrize("ranks", [2, 4, 5])
+def test_slab_fp32_matches_single_rank(ranks):
+    prob = mid_problem()
+    x1, r1, _, _ = run(prob, 1, max_iter=30, fixed_work=1, eq25=0)
+    xg, rg, _, _ = run(prob, ranks, max_iter=30, fixed_work=1, eq25=0)
+    assert rg["iterations"] == r1["iterations"] == 30
+    assert O.relres(xg, x1) < 1e-5
+
+
+def test_slab_fp32_natural_mode_vs_oracle():
+    prob = mid_problem()
+    prob.sets.append(SetDef("DZ", "card", k_frac=0.05, relative=True))
+    x, res, _, _ = run(prob, 4)
+    o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps), decide_f32=1)
+    ref = O.parsdmm(prob.shape, prob.sets, prob.m, **o)
+    assert O.relres(x, ref.x) < 1e-3, (res["iterations"], ref.iterations)
+
+
+def test_slab_c4_full_size_fixed_work():
+    """C4 at full size (256 x 256 x 128, z-marching CG on every slab) on 8
+    virtual ranks, 10 fixed-work iterations: the single-rank result to 1e-5."""
+    prob = G.c4()
+    x1, r1, _, _ = run(prob, 1, max_iter=10, fixed_work=1, eq25=0)
+    x8, r8, _, _ = run(prob, 8, max_iter=10, fixed_work=1, eq25=0)
+    assert r8["iterations"] == r1["iterations"] == 10
+    assert O.relres(x8, x1) < 1e-5
+
+
+def test_virtual_ranks_option_errors():
+    prob = G.tiny(100, (8, 8), ("bounds", "l1"))
+    g = grid_for(prob)
+    with pytest.raises(Exception):
+        g.set_option("virtual_ranks", 9)        # more ranks than planes
+    with pytest.raises(Exception):
+        g.set_option("virtual_ranks", 1.5)
+    g.set_option("virtual_ranks", 2)
+    m = torch.tensor(prob.m, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(m)
+    with pytest.raises(Exception):
+        g.project_multilevel(m, x, 2)          # multilevel is single-rank in this build
+    g.close()
