@@ -91,19 +91,25 @@ __device__ __forceinline__ void axis_w(int i, int nf, int nc, int* i0, int* i1, 
 // prolong one block of a field.  The block's real entries form an image of
 // shape (ez, ey, ex) = grid shape minus 1 along the primitive's axis; it is
 // interpolated from the coarse image of the same kind.  Pads are set to 0.
+//
+// z slabs: z is mapped in global plane numbers (nz_g, z0 of each level); the
+// coarse planes a fine slab needs lie within one plane of the coarse slab
+// (the coarse field's ghost planes, filled by the runtime's halo exchange).
 template <class T>
 __global__ void k_prolong(Geo fine, Geo coarse, int prim, const T* c, T* f) {
   const int dz = prim == PRIM_Z, dy = prim == PRIM_Y, dx = prim == PRIM_X;
-  const int cz = coarse.nz - dz, cy = coarse.ny - dy, cx = coarse.nx - dx;
-  const int fz = fine.nz - dz, fy = fine.ny - dy, fx = fine.nx - dx;
+  const int cz = coarse.nz_g - dz, cy = coarse.ny - dy, cx = coarse.nx - dx;
+  const int fz = fine.nz_g - dz, fy = fine.ny - dy, fx = fine.nx - dx;
   for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < fine.N; pt += gridDim.x * blockDim.x) {
     Loc L = locate(fine, pt);
-    if (L.iz >= fz || L.iy >= fy || L.ix >= fx) { f[pt] = (T)0; continue; }
+    if (L.gz >= fz || L.iy >= fy || L.ix >= fx) { f[pt] = (T)0; continue; }
     int z0, z1, y0, y1, x0, x1;
     double tz, ty, tx;
-    axis_w(L.iz, fz, cz, &z0, &z1, &tz);
+    axis_w(L.gz, fz, cz, &z0, &z1, &tz);
     axis_w(L.iy, fy, cy, &y0, &y1, &ty);
     axis_w(L.ix, fx, cx, &x0, &x1, &tx);
+    z0 -= coarse.z0;   // local coarse plane, -1 .. coarse.nz (ghosts)
+    z1 -= coarse.z0;
     auto C_ = [&](int a, int b, int d) {  // coarse padded storage
       return (double)c[((int64_t)a * coarse.ny + b) * coarse.nx + d];
     };

@@ -841,7 +841,7 @@ struct NcclComm : Comm {
 
 // fields whose planes a site exchanges
 enum FieldSel { FS_X, FS_R, FS_P0, FS_P1, FS_M, FS_Y0, FS_Y1, FS_V0, FS_V1 };
-enum SetSel { SS_ALL = 0, SS_POINTWISE = 1, SS_GLOBAL = 2 };
+enum SetSel { SS_ALL = 0, SS_POINTWISE = 1, SS_GLOBAL = 2, SS_ALLBLK = 3 /* every block of every set */ };
 struct HaloReq { int sel, sets, dir; };
 
 // The engines of this process's ranks (1 with NCCL, G with virtual ranks) run
@@ -917,7 +917,7 @@ struct Team : EngineBase {
       if (q.sets == SS_POINTWISE && S.global) continue;
       if (q.sets == SS_GLOBAL && !S.global) continue;
       for (int b = 0; b < S.nblk; ++b)   // only D_z blocks reach across planes (D_z^T in the rhs)
-        if (S.prim[b] == PRIM_Z) push((isy ? S.y[par] : S.v[par]) + (int64_t)b * g.ld);
+        if (S.prim[b] == PRIM_Z || q.sets == SS_ALLBLK) push((isy ? S.y[par] : S.v[par]) + (int64_t)b * g.ld);
     }
   }
 
@@ -1077,6 +1077,7 @@ struct sip_grid_s {
   std::string err;
   std::unique_ptr<EngineBase> eng;                 // single-level engine
   EngineBase* last = nullptr;                      // engine of the last projection (finest level)
+  EngineBase* last_team = nullptr;                 // z slabs: Team of the last projection (finest level)
   std::vector<std::unique_ptr<EngineBase>> levels; // multilevel (index 0 = finest)
   bool have_m = false;
   long long last_launches = 0;
@@ -1119,7 +1120,7 @@ Team<T>* team_of(sip_grid g) {
   if (!g->eng) {
     const bool nc = g->nranks > 1;
     const int G = nc ? g->nranks : g->vranks;
-    if (!nc) {
+    if (!nc && !g->comm) {
       auto lc = std::make_unique<LocalComm>();
       lc->G = G;
       g->comm = std::move(lc);
@@ -1160,6 +1161,7 @@ sip_status project_team_T(sip_grid g, const void* m, void* x, int max_iter, doub
   g->have_m = true;
   g->last_launches = t->launches;
   g->last = e0;
+  g->last_team = t;
   for (auto& e : t->eng)
     if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, "NaN/Inf in the PARSDMM state"};
   return e0->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
@@ -1203,7 +1205,7 @@ sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int ma
   // level grids: each axis halves (y stays 1 in 2D), h doubles (reading L2)
   if ((int)g->levels.size() != n_levels) {
     g->levels.clear();
-    g->last = nullptr;
+    g->last = nullptr; g->last_team = nullptr;
     for (int l = 0; l < n_levels; ++l) {
       auto e = std::make_unique<Engine<T>>();
       const int f = 1 << l;
@@ -1279,6 +1281,116 @@ sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int ma
   g->last_launches = launches;
   g->last = fine;
   return fine->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
+}
+
+// Algorithm 3 on z slabs: every level is a Team of the same G ranks; the
+// slabs of all levels nest (nz divisible by G 2^(L-1)), so the restriction
+// is slab-local; the prolongation reads one coarse ghost plane on each side,
+// filled by a halo exchange of the coarse level's final x, y_i, v_i.
+template <class T>
+sip_status multilevel_team_T(sip_grid g, const void* m, void* x, int n_levels, int max_iter, double tol,
+                             sip_result* per_level) {
+  const bool nc = g->nranks > 1;
+  const int G = nc ? g->nranks : g->vranks;
+  if (g->n[0] % ((int64_t)G << (n_levels - 1)) != 0)
+    throw SipError{SIP_ERR_CONFIG, "multilevel on z slabs needs nz divisible by ranks * 2^(levels-1)"};
+  if ((int)g->levels.size() != n_levels) {
+    g->levels.clear();
+    g->last = nullptr; g->last_team = nullptr;
+    if (!nc && !g->comm) {
+      auto lc = std::make_unique<LocalComm>();
+      lc->G = G;
+      g->comm = std::move(lc);
+    }
+    for (int l = 0; l < n_levels; ++l) {
+      const int f = 1 << l;
+      double hl[3] = {g->h[0] * f, g->ndim == 3 ? g->h[1] * f : 1.0, g->h[2] * f};
+      auto t = std::make_unique<Team<T>>();
+      t->setup(g->ndim, (int)(g->n[0] / f), g->ndim == 3 ? (int)(g->n[1] / f) : 1, (int)(g->n[2] / f), hl,
+               g->stream, g->sets, G, nc ? g->rank : 0, nc ? 1 : G, g->comm.get());
+      g->levels.push_back(std::move(t));
+    }
+  }
+  auto L = [&](int l) { return static_cast<Team<T>*>(g->levels[l].get()); };
+  Team<T>* fine = L(0);
+  const double eps_feas = tol > 0 ? tol : 1e-3;
+  Engine<T>* f0 = fine->eng[0].get();
+  CU(cudaEventRecord(f0->ev0, g->stream));
+  const int64_t zoff0 = nc ? f0->z0 : 0;
+  for (auto& e : fine->eng)
+    copy_in(e.get(), (const T*)m + (size_t)(e->z0 - zoff0) * e->Pr.g.plane, const_cast<T*>(e->Pr.m),
+            (size_t)e->Pr.g.N);
+  long long launches = 0;
+  for (int l = 1; l < n_levels; ++l)
+    for (size_t r = 0; r < fine->eng.size(); ++r) {
+      Engine<T>* ef = L(l - 1)->eng[r].get();
+      Engine<T>* ec = L(l)->eng[r].get();
+      k_restrict<T><<<ec->g_small_(), BLOCK, 0, g->stream>>>(ef->Pr.g, ec->Pr.g, ef->Pr.m, const_cast<T*>(ec->Pr.m));
+      ++launches;
+    }
+  CU(cudaGetLastError());
+  std::vector<double> rho, gam;
+  for (int l = n_levels - 1; l >= 0; --l) {
+    Team<T>* t = L(l);
+    Engine<T>* e0 = t->eng[0].get();
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a)); CU(cudaEventCreate(&b));
+    CU(cudaEventRecord(a, g->stream));
+    if (l == n_levels - 1) {
+      for (auto& e : t->eng)   // coarsest: x = m_L, y_i = v_i = 0 (reading L13)
+        for (int i = 0; i < e->P; ++i) {
+          SetD<T>& S = e->Pr.set[i];
+          CU(cudaMemsetAsync(S.y[1] - (size_t)GHOST * e->Pr.g.plane, 0, (size_t)S.nblk * e->Pr.g.ld * sizeof(T), g->stream));
+          CU(cudaMemsetAsync(S.v[1] - (size_t)GHOST * e->Pr.g.plane, 0, (size_t)S.nblk * e->Pr.g.ld * sizeof(T), g->stream));
+        }
+      t->solve(g->opt, max_iter, eps_feas, eps_evol_of(g, tol), 1, 0, nullptr, nullptr);
+    } else {
+      Team<T>* c = L(l + 1);
+      const int kk = std::min(c->eng[0]->hc.k, c->eng[0]->hc.opt.max_iter);
+      const int par = (kk + 1) & 1;   // parity of the coarse level's final y, v
+      c->site(ST_INIT, 0, 0, {{FS_X, 0, H_BOTH}, {par ? FS_Y1 : FS_Y0, SS_ALLBLK, H_BOTH},
+                              {par ? FS_V1 : FS_V0, SS_ALLBLK, H_BOTH}}, false);
+      for (size_t r = 0; r < t->eng.size(); ++r) {
+        Engine<T>* e = t->eng[r].get();
+        Engine<T>* ec = c->eng[r].get();
+        const int gs = e->g_small_();
+        k_prolong<T><<<gs, BLOCK, 0, g->stream>>>(e->Pr.g, ec->Pr.g, PRIM_I, ec->Pr.x, e->Pr.x);
+        ++launches;
+        for (int i = 0; i < e->P; ++i) {
+          SetD<T>& Sf = e->Pr.set[i];
+          const T* yc = ec->final_field(i, 0);
+          const T* vc = ec->final_field(i, 1);
+          for (int bl = 0; bl < Sf.nblk; ++bl) {
+            k_prolong<T><<<gs, BLOCK, 0, g->stream>>>(e->Pr.g, ec->Pr.g, Sf.prim[bl], yc + (int64_t)bl * ec->Pr.g.ld,
+                                                      Sf.y[1] + (int64_t)bl * e->Pr.g.ld);
+            k_prolong<T><<<gs, BLOCK, 0, g->stream>>>(e->Pr.g, ec->Pr.g, Sf.prim[bl], vc + (int64_t)bl * ec->Pr.g.ld,
+                                                      Sf.v[1] + (int64_t)bl * e->Pr.g.ld);
+            launches += 2;
+          }
+        }
+      }
+      CU(cudaGetLastError());
+      t->solve(g->opt, max_iter, eps_feas, eps_evol_of(g, tol), 0, 0, rho.data(), gam.data());
+    }
+    rho.assign(e0->hc.rho, e0->hc.rho + e0->P);   // rho, gamma carry over (L23)
+    gam.assign(e0->hc.gamma, e0->hc.gamma + e0->P);
+    CU(cudaEventRecord(b, g->stream));
+    CU(cudaEventSynchronize(b));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    if (per_level) e0->fill_result(&per_level[l], ms);
+    launches += t->launches;
+    for (auto& e : t->eng)
+      if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, "NaN/Inf in the PARSDMM state"};
+  }
+  for (auto& e : fine->eng)
+    copy_out(e.get(), e->Pr.x, (T*)x + (size_t)(e->z0 - zoff0) * e->Pr.g.plane, (size_t)e->Pr.g.N);
+  CU(cudaStreamSynchronize(g->stream));
+  g->last_launches = launches;
+  g->last = f0;
+  g->last_team = fine;
+  return f0->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
 }
 
 template <class T>
@@ -1525,7 +1637,7 @@ sip_status get_state_T(sip_grid g, int set_id, int which, void* out) {
 // this process's ranks in rank order (virtual ranks: the whole field)
 template <class T>
 sip_status get_state_team_T(sip_grid g, int set_id, int which, void* out) {
-  Team<T>* t = static_cast<Team<T>*>(g->eng.get());
+  Team<T>* t = static_cast<Team<T>*>(g->last_team);
   if (!t || !t->ran) throw SipError{SIP_ERR_STATE, "no projection state"};
   const SetD<T>& S0 = t->eng[0]->Pr.set[set_id];
   long long off = 0;
@@ -1736,7 +1848,7 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type 
     g->sets.push_back(std::move(hs));
     g->eng.reset();
     g->levels.clear();
-    g->last = nullptr;
+    g->last = nullptr; g->last_team = nullptr;
     if (set_id) *set_id = (int)g->sets.size() - 1;
     return SIP_OK;
   });
@@ -1767,7 +1879,7 @@ sip_status sip_set_option(sip_grid g, const char* key, double value) {
     if (g->nranks > 1) { g->err = "virtual_ranks on an NCCL grid"; return SIP_ERR_CONFIG; }
     if (G != g->vranks) {
       if (g->stream) cudaStreamSynchronize(g->stream);
-      g->eng.reset(); g->levels.clear(); g->last = nullptr; g->comm.reset();
+      g->eng.reset(); g->levels.clear(); g->last = nullptr; g->last_team = nullptr; g->comm.reset();
       g->vranks = G;
     }
   }
@@ -1796,8 +1908,10 @@ sip_status sip_project_multilevel(sip_grid g, const void* m, void* x, int n_leve
     if (a == 1 && g->ndim == 2) continue;
     if (g->n[a] % f != 0 || g->n[a] / f < 2) { g->err = "grid not divisible for the levels"; return SIP_ERR_CONFIG; }
   }
-  if (g->nranks > 1 || g->vranks > 1) { g->err = "multilevel on z slabs: not in this build"; return SIP_ERR_CONFIG; }
   return guarded(g, [&]() -> sip_status {
+    if (is_team(g))
+      return g->dtype == SIP_F32 ? multilevel_team_T<float>(g, m, x, n_levels, max_iter, tol, per_level)
+                                 : multilevel_team_T<double>(g, m, x, n_levels, max_iter, tol, per_level);
     return g->dtype == SIP_F32 ? multilevel_T<float>(g, m, x, n_levels, max_iter, tol, per_level)
                                : multilevel_T<double>(g, m, x, n_levels, max_iter, tol, per_level);
   });

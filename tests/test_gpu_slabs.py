@@ -141,9 +141,52 @@ def test_virtual_ranks_option_errors():
         g.set_option("virtual_ranks", 9)        # more ranks than planes
     with pytest.raises(Exception):
         g.set_option("virtual_ranks", 1.5)
-    g.set_option("virtual_ranks", 2)
+    g.set_option("virtual_ranks", 3)
     m = torch.tensor(prob.m, dtype=torch.float64, device="cuda")
     x = torch.empty_like(m)
     with pytest.raises(Exception):
-        g.project_multilevel(m, x, 2)          # multilevel is single-rank in this build
+        g.project_multilevel(m, x, 2)          # 8 planes do not nest into 3 slabs x 2 levels
+    with pytest.raises(Exception):
+        g.apply_op(0, m, x)                    # step-level entries are single-rank
+    g.close()
+
+
+ML_SLAB = [((16, 16), 2, ("bounds", "l1", "slope"), 4),
+           ((16, 16), 3, ("bounds", "l1", "slope", "card"), 2),
+           ((8, 8, 8), 2, ("bounds", "l1", "slope", "annulus"), 2),
+           ((16, 8, 16), 2, ("bounds", "l1", "cardz"), 4)]
+
+
+@pytest.mark.parametrize("shape,levels,kinds,ranks", ML_SLAB)
+def test_slab_multilevel_matches_oracle(shape, levels, kinds, ranks):
+    """Algorithm 3 on z slabs: restriction slab-local, prolongation through
+    the coarse ghost planes; per-level iteration counts as the oracle's."""
+    prob = G.tiny(120 + len(shape) + levels, shape, kinds)
+    g = grid_for(prob)
+    g.set_option("virtual_ranks", ranks)
+    m = torch.tensor(prob.m, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(m)
+    per, st = g.project_multilevel(m, x, levels, max_iter=200, tol=1e-3)
+    xo, sto, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, levels, **prob.options)
+    all_conv = True
+    for l in range(levels - 1, -1, -1):
+        assert per[l]["iterations"] == logs[l].iterations, (l, per[l]["iterations"], logs[l].iterations)
+        if not logs[l].converged:
+            all_conv = False
+            break
+        assert per[l]["cg_iterations"] == logs[l].cg_total
+    assert O.relres(x.cpu().numpy().ravel(), xo.ravel()) < (1e-6 if all_conv else 1e-3)
+    g.close()
+
+
+def test_slab_multilevel_fp32_c5_like():
+    prob = G.c5(seed=4, shape=(32, 32, 16))
+    o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps), decide_f32=1)
+    x_ref, _, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3, **o)
+    g = grid_for(prob)
+    g.set_option("virtual_ranks", 4)
+    m = torch.tensor(prob.m, dtype=torch.float32, device="cuda")
+    x = torch.empty_like(m)
+    per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
+    assert O.relres(x.double().cpu().numpy().ravel(), x_ref.ravel()) < 1e-3
     g.close()
