@@ -17,6 +17,7 @@ constexpr int NWARP = BLOCK / 32;
 constexpr int MAXJOBS = 2 * MAXP;
 constexpr int MAXTAPS = 81;     // blur kernel up to 9 x 9
 constexpr int GHOST = 2;        // ghost planes on each side of every N-field
+constexpr int MAXCG = 16;       // p-vector ring of the deferred x update (n_cg <= MAXCG)
 
 // primitive operators: every set's operator is a stack of 1..3 primitive blocks
 enum Prim { PRIM_I = 0, PRIM_Z = 1, PRIM_Y = 2, PRIM_X = 3, PRIM_F = 4, NPRIM = 5 };
@@ -133,6 +134,7 @@ struct Ctrl {
   // CG state (Eq. 25, reading L18)
   int cg_j, cg_active, cg_count, cg_total;
   double bb, rr, rr_prev, alpha, beta, tol;
+  double alph[MAXCG];            // alpha_j of this x-update (deferred x += sum alpha_j p_j)
   // merged operator coefficients of C (Eq. 23/24)
   double cI, cz, cy, cx, cF;
   double rho[MAXP], gamma[MAXP];
@@ -254,13 +256,21 @@ __device__ inline bool last_block(unsigned* counter) {
   return s_last != 0;
 }
 
-// last CTA: out[v] = sum over CTAs b of partials[b*nv + v], fixed order
+// last CTA: out[v] = sum over CTAs b of partials[b*nv + v], fixed order.
+// Values are spread over the warps (warp w takes v = w, w + NWARP, ...), each
+// lane sums a strided subset of the CTAs, then a shuffle tree: no block
+// barrier per value, so a wide reduction (pass 1: up to 159 values) costs a
+// few L2 round trips instead of one barrier-separated phase per value.
 __device__ inline void reduce_partials(const double* partials, int nv, double* out, double* sh) {
-  for (int v = 0; v < nv; ++v) {
+  (void)sh;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nb = (int)gridDim.x;
+  for (int v = w; v < nv; v += NWARP) {
     double a = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) a += __ldcg(partials + (size_t)b * nv + v);
-    a = block_sum(a, sh);
-    if (threadIdx.x == 0) out[v] = a;
+#pragma unroll 4
+    for (int b = lane; b < nb; b += 32) a += __ldcg(partials + (size_t)b * nv + v);
+    a = warp_sum(a);
+    if (lane == 0) out[v] = a;
   }
   __syncthreads();
 }

@@ -34,6 +34,12 @@ struct Prob {
   int ntiles_pb;                  // tiles of BLOCK points per block (pass2, ties)
   SetD<T> set[MAXP];
   T* x; const T* m; T* r; T* pb[2]; T* tb;
+  // deferred x update (vectorised path, n_cg <= MAXCG): p_j lives in ring
+  // slot j for the whole CG solve, the CG kernels never touch x, and k_cgx
+  // forms x += alpha_0 p_0 + alpha_1 p_1 + ... in that order afterwards
+  // (the same fp operations, in the same order, as per-step updates)
+  T* pr[MAXCG];
+  int defer_x;
   T* hist[HIST_S];
   T* xs[2];
   Ctrl* ctrl;
@@ -47,9 +53,7 @@ struct Prob {
   // flattened segments (sip_flat.cuh): pass1 = x work + every (set, block);
   // pass2 = every (global set, block)
   int nseg1, nseg2;
-  // fused round 1 of the radix search in pass 1 (fp32): smem histogram per
-  // w-job at dynamic smem offset h1_off (bytes); cand[job] = round-2 survivors
-  int fuse_r1, h1_off;
+  // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32)
   unsigned* cand[MAXJOBS];
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
@@ -90,9 +94,10 @@ __device__ inline void fin_rhs(Ctrl& C, const double* v) {
 }
 
 // after <p_j, C p_j>: alpha, or breakdown (p.q <= 0, reading L18)
-__device__ inline void fin_cg1(Ctrl& C, const double* v) {
+__device__ inline void fin_cg1(Ctrl& C, const double* v, int j) {
   if (v[0] > 0.0) {
     C.alpha = C.rr / v[0];
+    if (j < MAXCG) C.alph[j] = C.alpha;
   } else {
     C.cg_active = 0;
     C.breakdown = 1;
@@ -110,6 +115,12 @@ __device__ inline void fin_cg2(Ctrl& C, const double* v, int j) {
   int active = (C.cg_j < C.opt.n_cg) && (rn > 0.0);
   if (active && C.opt.eq25 && sqrt(rn) / sqrt(C.bb) < C.tol) active = 0;
   C.cg_active = active;
+}
+
+// p_j of the CG solve: ring slot j (deferred x) or the ping-pong pair
+template <class T>
+__device__ __forceinline__ T* p_slot(const Prob<T>& P, int j) {
+  return P.defer_x ? P.pr[j] : P.pb[j & 1];
 }
 
 // rank-local values -> this rank's gather slot (threads of one CTA, strided)

@@ -12,6 +12,7 @@
 // accumulated in fp64 (reading L20).
 #pragma once
 #include "sip_flat.cuh"
+#include "sip_stage.cuh"
 
 namespace sip {
 
@@ -34,177 +35,236 @@ __device__ __forceinline__ IterFlags iter_flags(Ctrl& C) {
   return f;
 }
 
-// A_prim x on a chunk in the storage precision (Eq. 8; pads -> 0)
-template <class T>
-__device__ __forceinline__ void prim_chunkT(const Geo& g, int prim, const T* x, int pt0, int lane,
-                                            const Loc& L, const T* xc, T* s) {
+// ------------------------------------------------------------ pass 1
+// Segment-major over a contiguous chunk range per CTA.  A segment is the x
+// work (history ring, Alg. 2 x snapshot, Eq. 27 sums) or one (set, block)
+// pair; the CTA runs every segment over its range, one thread per chunk of
+// W = 16 / sizeof(T) points, with the set kind, the primitive operator and
+// the iteration type fixed at compile time (no per-element dispatch).  x and
+// its neighbours are re-read per segment from L1 / L2 (x was just written by
+// the CG); y_i, v_i and the outputs stream through DRAM once.  Per-thread
+// fp64 accumulators are reduced once per (warp, segment) into the per-warp
+// shared slots.
+
+// A_prim x at the W points of a chunk in the storage precision (Eq. 8);
+// pad entries come out 0
+template <class T, int PRIM>
+__device__ __forceinline__ void prim_chunk(const Geo& g, const T* x, int pt0, const T* xc, bool lastx, bool padc,
+                                           T* s) {
   constexpr int W = VT<T>::W;
-  if (prim == PRIM_I) {
+  if (PRIM == PRIM_I) {
 #pragma unroll
     for (int e = 0; e < W; ++e) s[e] = xc[e];
-  } else if (prim == PRIM_X) {
-    T xr = __shfl_down_sync(0xffffffffu, xc[0], 1);
-    if (lane == 31) xr = x[pt0 + W];
+  } else if (PRIM == PRIM_X) {
+    const T xr = lastx ? (T)0 : x[pt0 + W];
     const T ih = (T)g.ihx;
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       const T nx_ = e < W - 1 ? xc[e + 1] : xr;
-      s[e] = (L.ix + e < g.nx - 1) ? (nx_ - xc[e]) * ih : (T)0;
+      s[e] = (lastx && e == W - 1) ? (T)0 : (nx_ - xc[e]) * ih;
     }
   } else {
-    const bool z = prim == PRIM_Z;
     T t[W];
-    VT<T>::ldT(x + pt0 + (z ? g.plane : g.nx), t);
-    const bool hi = z ? (L.gz < g.nz_g - 1) : (L.iy < g.ny - 1);
-    const T ih = (T)(z ? g.ihz : g.ihy);
+    VT<T>::ldT(x + pt0 + (PRIM == PRIM_Z ? g.plane : g.nx), t);
+    const T ih = (T)(PRIM == PRIM_Z ? g.ihz : g.ihy);
 #pragma unroll
-    for (int e = 0; e < W; ++e) s[e] = hi ? (t[e] - xc[e]) * ih : (T)0;
+    for (int e = 0; e < W; ++e) s[e] = padc ? (T)0 : (t[e] - xc[e]) * ih;
   }
 }
 
-// chunks per thread per warp group of pass 1 (amortises the per-group setup)
-constexpr int P1_U = 4;
+// chunk location: whole-chunk pad (D_z: last global plane; D_y: last row)
+// and whether the chunk holds the last point of its x row (D_x pad)
+template <int PRIM>
+__device__ __forceinline__ void chunk_pads(const Geo& g, int pt0, int W, bool* padc, bool* lastx) {
+  const int iz = (int)g.dplane.div((uint32_t)pt0);
+  const int r = pt0 - iz * g.plane;
+  const int iy = (int)g.dnx.div((uint32_t)r);
+  const int ix = r - iy * g.nx;
+  *padc = PRIM == PRIM_Z ? (iz + g.z0 >= g.nz_g - 1) : PRIM == PRIM_Y ? (iy >= g.ny - 1) : false;
+  *lastx = PRIM == PRIM_X && (ix + W >= g.nx);
+}
 
-// PU chunks (stride 32) of one (set, block) segment; KIND: 0 box, 1 distance
-// block, 2 global set.  Reductions are summed in T per chunk, in fp64 across
-// chunks, and reduced across the warp once per group.
-template <class T, int KIND>
-__device__ __forceinline__ void p1_seg(const Prob<T>& P, const Ctrl& C, int i, int bl, const IterFlags& f,
-                                       int par, int cbase, int nch, int lane, const T* xs_rd, double* acc,
-                                       int nv, unsigned* h1) {
+// staged arrays of a pass-1 segment (Stage2 slots)
+enum P1Arr { A_X = 0, A_XN, A_Y, A_V, A_M, A_HI, A_VH0, A_XS, A_XSN, A_Y0, A_V0, A_NP1 };
+constexpr int P1_NA_PLAIN = 6;    // x, x+d, y, v, m or lo, hi
+constexpr int P1_NA_ADAPT = A_NP1;
+
+template <class T>
+__device__ __forceinline__ void ld_s(const char* base, int idx, T* o) {   // chunk idx of a staged tile
+  VT<T>::ldT_s(reinterpret_cast<const T*>(base) + idx * VT<T>::W, o);
+}
+
+// one (set, block) segment over chunks [c0, c1).  KIND: 0 box, 1 distance
+// block (Eq. 22), 2 global set (w stored for pass 2)
+template <class T, int KIND, int PRIM, int AD, int CK, int NA>
+__device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, int bl, const IterFlags& f,
+                                       int par, int c0, int c1, const T* xs_rd, double* acc, int nv,
+                                       Stage2<NA>& st) {
   constexpr int W = VT<T>::W;
   const Geo& g = P.g;
   const SetD<T>& S = P.set[i];
-  const int prim = S.prim[bl];
   const bool pointwise = KIND != 2;
-  const T* yr = S.y[par] + (int64_t)bl * g.ld;
-  const T* vr = S.v[par] + (int64_t)bl * g.ld;
-  T* yw = S.y[par ^ 1] + (int64_t)bl * g.ld;
-  T* vw = S.v[par ^ 1] + (int64_t)bl * g.ld;
-  T* vhp = S.vh0 + (int64_t)bl * g.ld;
-  T* wp = S.w ? S.w + (int64_t)bl * g.ld : nullptr;
-  T* sp = S.s ? S.s + (int64_t)bl * g.ld : nullptr;
-  const T* lop = S.lo_vec ? S.lo_vec + (int64_t)bl * g.ld : nullptr;
-  const T* hip = S.hi_vec ? S.hi_vec + (int64_t)bl * g.ld : nullptr;
+  const bool adapt = AD == 2 ? f.adapt : AD == 1;
+  const bool check = CK == 2 ? f.check : CK == 1;
+  const bool dots = NA > A_VH0 && adapt && f.dots;
+  const int64_t bo = (int64_t)bl * g.ld;
+  const T* yr = S.y[par] + bo;
+  const T* vr = S.v[par] + bo;
+  T* yw = S.y[par ^ 1] + bo;
+  T* vw = S.v[par ^ 1] + bo;
+  T* vhp = S.vh0 + bo;
+  T* wp = S.w ? S.w + bo : nullptr;
+  T* sp = (check && S.s) ? S.s + bo : nullptr;
+  const T* lop = S.lo_vec ? S.lo_vec + bo : nullptr;
+  const T* hip = S.hi_vec ? S.hi_vec + bo : nullptr;
+  const bool w2 = KIND == 2 && (S.kind == K_L2 || S.kind == K_ANN);
   const T rho = (T)C.rho[i], gam = (T)C.gamma[i], one = (T)1;
   const T irho = (T)(1.0 / C.rho[i]), i1rho = (T)(1.0 / (1.0 + C.rho[i]));
   const T tlo = (T)S.lo, thi = (T)S.hi;
-  // fused round 1 of the radix search on w (fp32; see k_selectf): smem
-  // histogram of the top 11 key bits, count + significand offset in 10-bit limbs
-  unsigned* hc = (KIND == 2 && h1 && S.job >= 0) ? h1 + (S.job >> 1) * 3 * NBUCK : nullptr;
-  const bool hsum = S.kind == K_L1;
+  const int dn = PRIM == PRIM_Z ? g.plane : g.nx;   // neighbour offset of D_z / D_y
+  const T ih = (T)(PRIM == PRIM_Z ? g.ihz : PRIM == PRIM_Y ? g.ihy : g.ihx);
   double d_w2 = 0, d_hv = 0, d_hh = 0, d_vh = 0, d_gv = 0, d_gg = 0, d_vv = 0, d_fn = 0, d_s2 = 0;
-#pragma unroll 1
-  for (int u = 0; u < P1_U; ++u) {
-    const int c = cbase + u * 32 + lane;
-    const bool valid = c < nch;
-    const int pt0 = (valid ? c : nch - 1) * W;
-    const Loc L = locate(g, pt0);
-    T xc[W], yo[W], vo[W], lo[W], hi[W], mm[W], y0[W], v0[W], vh0[W], xo[W];
-    VT<T>::ldT(P.x + pt0, xc);
-    VT<T>::ldT(yr + pt0, yo);
-    VT<T>::ldT(vr + pt0, vo);
-    if (KIND == 0 && lop) VT<T>::ldT(lop + pt0, lo);
-    if (KIND == 0 && hip) VT<T>::ldT(hip + pt0, hi);
-    if (KIND == 1) VT<T>::ldT(P.m + pt0, mm);
-    if (f.dots) {
-      VT<T>::ldT(vhp + pt0, vh0);
-      VT<T>::ldT(xs_rd + pt0, xo);
+  const int ntile = (c1 - c0 + BLOCK - 1) / BLOCK;
+  auto issue = [&](int t) {
+    const int cs = c0 + t * BLOCK;
+    const unsigned b = (unsigned)min(BLOCK, c1 - cs) * 16u;
+    const unsigned bx = b + (PRIM == PRIM_X ? 16u : 0u);   // + the next chunk (x neighbour)
+    const int64_t o = (int64_t)cs * W;
+    const char* src[NA];
+    unsigned by[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) { src[a] = nullptr; by[a] = 0; }
+    src[A_X] = (const char*)(P.x + o); by[A_X] = bx;
+    if (PRIM == PRIM_Z || PRIM == PRIM_Y) { src[A_XN] = (const char*)(P.x + o + dn); by[A_XN] = b; }
+    src[A_Y] = (const char*)(yr + o); by[A_Y] = b;
+    src[A_V] = (const char*)(vr + o); by[A_V] = b;
+    if (KIND == 1) { src[A_M] = (const char*)(P.m + o); by[A_M] = b; }
+    if (KIND == 0 && lop) { src[A_M] = (const char*)(lop + o); by[A_M] = b; }
+    if (KIND == 0 && hip) { src[A_HI] = (const char*)(hip + o); by[A_HI] = b; }
+    if (NA > A_VH0 && dots) {
+      src[A_VH0] = (const char*)(vhp + o); by[A_VH0] = b;
+      src[A_XS] = (const char*)(xs_rd + o); by[A_XS] = bx;
+      if (PRIM == PRIM_Z || PRIM == PRIM_Y) { src[A_XSN] = (const char*)(xs_rd + o + dn); by[A_XSN] = b; }
       if (pointwise) {
-        VT<T>::ldT(yw + pt0, y0);
-        VT<T>::ldT(vw + pt0, v0);
+        src[A_Y0] = (const char*)(yw + o); by[A_Y0] = b;
+        src[A_V0] = (const char*)(vw + o); by[A_V0] = b;
       }
     }
-    T s[W], s0[W];
-    prim_chunkT<T>(g, prim, P.x, pt0, lane, L, xc, s);
-    if (f.dots) prim_chunkT<T>(g, prim, xs_rd, pt0, lane, L, xo, s0);
-    T a_w2 = 0, a_hv = 0, a_hh = 0, a_vh = 0, a_gv = 0, a_gg = 0, a_vv = 0, a_fn = 0, a_s2 = 0;
-    T yn[W], vn[W], wv[W], vh[W], st_s[W];
+    st.issue(t & 1, NA, src, by);
+  };
+  if (ntile > 0) issue(0);
+  for (int t = 0; t < ntile; ++t) {
+    if (t + 1 < ntile) issue(t + 1);
+    const int s = t & 1;
+    st.wait(s);
+    const int c = c0 + t * BLOCK + (int)threadIdx.x;
+    if (c < c1) {
+      const int pt0 = c * W;
+      const int tid = threadIdx.x;
+      bool padc, lastx;
+      chunk_pads<PRIM>(g, pt0, W, &padc, &lastx);
+      T xc[W], yo[W], vo[W];
+      ld_s<T>(st.at(s, A_X), tid, xc);
+      ld_s<T>(st.at(s, A_Y), tid, yo);
+      ld_s<T>(st.at(s, A_V), tid, vo);
+      // s = A x (Eq. 8), 0 on pads
+      T sv_[W], s0_[W];
+      auto prim_s = [&](int arr, int arrn, const T* c_, T* out) {
+        if (PRIM == PRIM_I) {
 #pragma unroll
-    for (int e = 0; e < W; ++e) {
-      const bool pad = !valid || pad_vec(g, prim, L, e);
-      const T sv = pad ? (T)0 : s[e];
-      st_s[e] = sv;
-      const T xbar = gam * sv + (one - gam) * yo[e];                   // relaxation
-      // fp64 keeps the oracle's exact divisions; fp32 multiplies by reciprocals
-      const T w = xbar - (sizeof(T) == 8 ? vo[e] / rho : vo[e] * irho);
-      wv[e] = pad ? (T)0 : w;
-      if (pointwise) {
-        T y;
-        if (KIND == 1) {
-          y = sizeof(T) == 8 ? (mm[e] + rho * w) / (one + rho) : (mm[e] + rho * w) * i1rho;  // Eq. 22
-        } else {
-          const T l = lop ? lo[e] : tlo;
-          const T h = hip ? hi[e] : thi;
-          y = w < l ? l : (w > h ? h : w);                             // box clamp
-          if (f.check && !pad) {
-            const T cl = sv < l ? l : (sv > h ? h : sv);
-            a_fn += (sv - cl) * (sv - cl);
+          for (int e = 0; e < W; ++e) out[e] = c_[e];
+        } else if (PRIM == PRIM_X) {
+          const T xr = reinterpret_cast<const T*>(st.at(s, arr))[(tid + 1) * W];
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            const T nx_ = e < W - 1 ? c_[e + 1] : xr;
+            out[e] = (lastx && e == W - 1) ? (T)0 : (nx_ - c_[e]) * ih;
           }
+        } else {
+          T tn[W];
+          ld_s<T>(st.at(s, arrn), tid, tn);
+#pragma unroll
+          for (int e = 0; e < W; ++e) out[e] = padc ? (T)0 : (tn[e] - c_[e]) * ih;
         }
-        const T vt = rho * (y - w);                                    // Eq. 21 as rho (y - w), L26
-        yn[e] = pad ? (T)0 : y;
-        vn[e] = pad ? (T)0 : vt;
-        if (f.dots && !pad) {
-          const T dg = y0[e] - y;
-          const T dv = vt - v0[e];
-          a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+      };
+      prim_s(A_X, A_XN, xc, sv_);
+      T lo[W], hi[W], mm[W];
+      if (KIND == 1) ld_s<T>(st.at(s, A_M), tid, mm);
+      if (KIND == 0 && lop) ld_s<T>(st.at(s, A_M), tid, lo);
+      if (KIND == 0 && hip) ld_s<T>(st.at(s, A_HI), tid, hi);
+      T a_w2 = 0, a_hv = 0, a_hh = 0, a_vh = 0, a_gv = 0, a_gg = 0, a_vv = 0, a_fn = 0, a_s2 = 0;
+      T yn[W], vn[W], wv[W], vh[W];
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        const bool pad = padc || (PRIM == PRIM_X && lastx && e == W - 1);
+        const T sv = sv_[e];                                             // 0 on pads
+        const T xbar = gam * sv + (one - gam) * yo[e];                   // relaxation
+        // fp64 keeps the oracle's exact divisions; fp32 multiplies by reciprocals
+        const T w = xbar - (sizeof(T) == 8 ? vo[e] / rho : vo[e] * irho);
+        wv[e] = pad ? (T)0 : w;
+        if (pointwise) {
+          T y;
+          if (KIND == 1) {
+            y = sizeof(T) == 8 ? (mm[e] + rho * w) / (one + rho) : (mm[e] + rho * w) * i1rho;  // Eq. 22
+          } else {
+            const T l = lop ? lo[e] : tlo;
+            const T h = hip ? hi[e] : thi;
+            y = w < l ? l : (w > h ? h : w);                             // box clamp
+            if (check && !pad) {
+              const T cl = sv < l ? l : (sv > h ? h : sv);
+              a_fn += (sv - cl) * (sv - cl);
+            }
+          }
+          const T vt = rho * (y - w);                                    // Eq. 21 as rho (y - w), L26
+          yn[e] = pad ? (T)0 : y;
+          vn[e] = pad ? (T)0 : vt;
+        } else if (w2 && !pad) {
+          a_w2 += w * w;
         }
-      } else if (!pad) {
-        a_w2 += w * w;
+        if (adapt) vh[e] = pad ? (T)0 : vo[e] + rho * (yo[e] - sv);     // Alg. 2 line 1
+        if (check && !pad) a_s2 += sv * sv;
       }
-      if (f.adapt) {                                                   // Alg. 2 line 1
-        const T vht = vo[e] + rho * (yo[e] - sv);
-        vh[e] = pad ? (T)0 : vht;
-        if (f.dots && !pad) {
-          const T dvh = vht - vh0[e];
-          const T dh = sv - s0[e];
+      if (dots) {   // Alg. 2 inner products against the k0 snapshots
+        T xo[W], vh0[W];
+        ld_s<T>(st.at(s, A_XS), tid, xo);
+        ld_s<T>(st.at(s, A_VH0), tid, vh0);
+        prim_s(A_XS, A_XSN, xo, s0_);
+        T y0[W], v0[W];
+        if (pointwise) {
+          ld_s<T>(st.at(s, A_Y0), tid, y0);
+          ld_s<T>(st.at(s, A_V0), tid, v0);
+        }
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+          const bool pad = padc || (PRIM == PRIM_X && lastx && e == W - 1);
+          if (pad) continue;
+          if (pointwise) {
+            const T dg = y0[e] - yn[e];
+            const T dv = vn[e] - v0[e];
+            a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+          }
+          const T dvh = vh[e] - vh0[e];
+          const T dh = sv_[e] - s0_[e];
           a_hv += dh * dvh; a_hh += dh * dh; a_vh += dvh * dvh;
         }
       }
-      if (f.check && !pad) a_s2 += sv * sv;
-    }
-    if (valid) {
       if (pointwise) {
         VT<T>::stT(yw + pt0, yn);
         VT<T>::stT(vw + pt0, vn);
       } else {
         VT<T>::stT(wp + pt0, wv);
-        if (f.check && sp) VT<T>::stT(sp + pt0, st_s);
+        if (sp) VT<T>::stT(sp + pt0, sv_);
       }
-      if (f.adapt) VT<T>::stT(vhp + pt0, vh);
+      if (adapt) VT<T>::stT(vhp + pt0, vh);
+      d_w2 += (double)a_w2; d_hv += (double)a_hv; d_hh += (double)a_hh; d_vh += (double)a_vh;
+      d_gv += (double)a_gv; d_gg += (double)a_gg; d_vv += (double)a_vv; d_fn += (double)a_fn;
+      d_s2 += (double)a_s2;
     }
-    if (sizeof(T) == 4 && KIND == 2 && hc && valid) {
-      int pd = -1;
-      unsigned pc = 0, pa = 0, pb = 0;
-#pragma unroll
-      for (int e = 0; e < W; ++e) {
-        if (pad_vec(g, prim, L, e)) continue;
-        const unsigned key = __float_as_uint((float)wv[e]) & 0x7fffffffu;
-        const int d = (int)(key >> 20);
-        if (d != pd) {
-          if (pd >= 0) {
-            atomicAdd(&hc[pd], pc);
-            if (hsum) { atomicAdd(&hc[NBUCK + pd], pa); atomicAdd(&hc[2 * NBUCK + pd], pb); }
-          }
-          pd = d; pc = 0; pa = 0; pb = 0;
-        }
-        pc += 1;
-        pa += key & 1023u;
-        pb += (key >> 10) & 1023u;
-      }
-      if (pd >= 0) {
-        atomicAdd(&hc[pd], pc);
-        if (hsum) { atomicAdd(&hc[NBUCK + pd], pa); atomicAdd(&hc[2 * NBUCK + pd], pb); }
-      }
-    }
-    d_w2 += (double)a_w2; d_hv += (double)a_hv; d_hh += (double)a_hh; d_vh += (double)a_vh;
-    d_gv += (double)a_gv; d_gg += (double)a_gg; d_vv += (double)a_vv; d_fn += (double)a_fn;
-    d_s2 += (double)a_s2;
+    __syncthreads();   // stage s is refilled by the issue of tile t + 2
   }
   const int base = i * NSLOT;
-  if (KIND == 2 && (S.kind == K_L2 || S.kind == K_ANN)) warp_acc(acc, nv, base + SLOT_W2, d_w2);
-  if (f.dots) {
+  if (w2) warp_acc(acc, nv, base + SLOT_W2, d_w2);
+  if (dots) {
     warp_acc(acc, nv, base + SLOT_HV, d_hv);
     warp_acc(acc, nv, base + SLOT_HH, d_hh);
     warp_acc(acc, nv, base + SLOT_VHVH, d_vh);
@@ -214,9 +274,86 @@ __device__ __forceinline__ void p1_seg(const Prob<T>& P, const Ctrl& C, int i, i
       warp_acc(acc, nv, base + SLOT_VV, d_vv);
     }
   }
-  if (f.check) {
+  if (check) {
     if (KIND == 0) warp_acc(acc, nv, base + SLOT_FN, d_fn);
     warp_acc(acc, nv, base + SLOT_S2, d_s2);
+  }
+}
+
+// the x segment: history ring (Eq. 27), Alg. 2's x snapshot, ||x||^2 and
+// ||x - x^{k-j}||^2 on check iterations
+template <class T, int AD, int CK, int NA>
+__device__ __forceinline__ void p1_xrun(const Prob<T>& P, const Ctrl& C, const IterFlags& f, int c0, int c1,
+                                        T* xs_wr, double* acc, int nv, Stage2<NA>& st) {
+  constexpr int W = VT<T>::W;
+  const Geo& g = P.g;
+  const bool adapt = AD == 2 ? f.adapt : AD == 1;
+  const bool check = CK == 2 ? f.check : CK == 1;
+  const int hcount = C.hist_count, hhead = C.hist_head;
+  const int hslot = (hhead + 1) % HIST_S;
+  double x2 = 0.0, d2[HIST_S] = {0, 0, 0, 0, 0};
+  const int ntile = (c1 - c0 + BLOCK - 1) / BLOCK;
+  auto issue = [&](int t) {
+    const int cs = c0 + t * BLOCK;
+    const unsigned b = (unsigned)min(BLOCK, c1 - cs) * 16u;
+    const int64_t o = (int64_t)cs * W;
+    const char* src[NA];
+    unsigned by[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) { src[a] = nullptr; by[a] = 0; }
+    src[0] = (const char*)(P.x + o); by[0] = b;
+    if (check)
+#pragma unroll
+      for (int js = 0; js < HIST_S; ++js)
+        if ((hhead - js + HIST_S) % HIST_S < hcount) { src[1 + js] = (const char*)(P.hist[js] + o); by[1 + js] = b; }
+    st.issue(t & 1, NA, src, by);
+  };
+  if (ntile > 0) issue(0);
+  for (int t = 0; t < ntile; ++t) {
+    if (t + 1 < ntile) issue(t + 1);
+    const int s = t & 1;
+    st.wait(s);
+    const int c = c0 + t * BLOCK + (int)threadIdx.x;
+    if (c < c1) {
+      const int pt0 = c * W;
+      T xc[W];
+      ld_s<T>(st.at(s, 0), threadIdx.x, xc);
+      if (check) {
+        T t2 = 0;
+#pragma unroll
+        for (int e = 0; e < W; ++e) t2 += xc[e] * xc[e];
+        x2 += (double)t2;
+#pragma unroll
+        for (int js = 0; js < HIST_S; ++js) {
+          if ((hhead - js + HIST_S) % HIST_S >= hcount) continue;
+          T h[W];
+          ld_s<T>(st.at(s, 1 + js), threadIdx.x, h);
+          T tt = 0;
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            const T d = xc[e] - h[e];
+            tt += d * d;
+          }
+          d2[js] += (double)tt;
+        }
+      }
+      VT<T>::stT(P.hist[hslot] + pt0, xc);
+      if (adapt) {
+        VT<T>::stT(xs_wr + pt0, xc);
+        if (pt0 >= g.N - g.plane) {   // the upper ghost plane too (x^{k0} at z+1 on a z slab)
+          T xg_[W];
+          VT<T>::ldT(P.x + pt0 + g.plane, xg_);
+          VT<T>::stT(xs_wr + pt0 + g.plane, xg_);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (check) {
+    warp_acc(acc, nv, P.P * NSLOT, x2);
+#pragma unroll
+    for (int js = 0; js < HIST_S; ++js)
+      if ((hhead - js + HIST_S) % HIST_S < hcount) warp_acc(acc, nv, P.P * NSLOT + 1 + js, d2[js]);
   }
 }
 
@@ -247,13 +384,17 @@ __device__ inline void fin_pass1(const Prob<T>& P, Ctrl& C, const double* stage)
   }
 }
 
+// k_pass1t: s = A x, relaxation, w, pointwise projections + duals, Alg. 2
+// and Eq. 26/27 statistics (Algorithm 1 lines of P:279-288; Alg. 2 line 1)
 template <class T, int AD, int CK>
-__global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Prob<T> P) {
+__global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_constant__ Prob<T> P) {
   constexpr int W = VT<T>::W;
+  constexpr int NA = AD == 0 ? P1_NA_PLAIN : P1_NA_ADAPT;
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
-  extern __shared__ double acc[];
+  extern __shared__ __align__(16) double acc[];
   __shared__ double sh[NWARP + 1];
+  __shared__ uint64_t bars[2];
   const Geo& g = P.g;
   const IterFlags f = iter_flags<AD, CK>(C);
   const int nv = P.P * NSLOT + NEVOL;
@@ -261,97 +402,25 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Pro
   const int a = C.adapt_calls;
   const T* xs_rd = P.xs[(a + 1) & 1];
   T* xs_wr = P.xs[a & 1];
-  const int hcount = C.hist_count, hhead = C.hist_head;
-  const int hslot = (hhead + 1) % HIST_S;
   for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
-  unsigned* h1 = P.fuse_r1 ? reinterpret_cast<unsigned*>(reinterpret_cast<char*>(acc) + P.h1_off) : nullptr;
-  if (h1)
-    for (int v = threadIdx.x; v < P.fuse_r1 * 3 * NBUCK; v += BLOCK) h1[v] = 0u;
-  __syncthreads();
+  Stage2<NA> st;
+  st.init(bars, reinterpret_cast<char*>(acc) + (((size_t)NWARP * nv * sizeof(double) + 127) / 128) * 128, BLOCK);
   const int nch = g.N / W;
-  const int gch = 32 * P1_U;                           // chunks per warp group
-  const int gps = (nch + gch - 1) / gch;               // warp groups per segment
-  const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * NWARP;
-  const int g0 = blockIdx.x * NWARP + (threadIdx.x >> 5);
-  // chunk-major order: the segments of one chunk range are processed by
-  // consecutive warps, so x (and x^{k0}) come from DRAM once
-  const int nseg = P.nseg1;
-  const int total = gps * nseg;
-  for (int grp = g0; grp < total; grp += nw) {
-    const int cg = grp / nseg;
-    const int seg = grp - cg * nseg;
-    const int cbase = cg * gch;
-    if (seg == 0) {   // x history (Eq. 27) and Alg. 2's x snapshot
-      double x2 = 0.0, d2[HIST_S] = {0, 0, 0, 0, 0};
-      for (int u = 0; u < P1_U; ++u) {
-        const int c = cbase + u * 32 + lane;
-        const bool valid = c < nch;
-        const int pt0 = (valid ? c : nch - 1) * W;
-        T xc[W];
-        VT<T>::ldT(P.x + pt0, xc);
-        if (f.check) {
-          T h[HIST_S][W];
-#pragma unroll
-          for (int js = 0; js < HIST_S; ++js)
-            if ((hhead - js + HIST_S) % HIST_S < hcount) VT<T>::ldT(P.hist[js] + pt0, h[js]);
-          T t2 = 0;
-#pragma unroll
-          for (int e = 0; e < W; ++e) t2 += valid ? xc[e] * xc[e] : (T)0;
-          x2 += (double)t2;
-#pragma unroll
-          for (int js = 0; js < HIST_S; ++js) {
-            if ((hhead - js + HIST_S) % HIST_S >= hcount) continue;
-            T t = 0;
-#pragma unroll
-            for (int e = 0; e < W; ++e) {
-              const T d = xc[e] - h[js][e];
-              t += valid ? d * d : (T)0;
-            }
-            d2[js] += (double)t;
-          }
-        }
-        if (valid) {
-          VT<T>::stT(P.hist[hslot] + pt0, xc);
-          if (f.adapt) {
-            VT<T>::stT(xs_wr + pt0, xc);
-            if (pt0 >= g.N - g.plane) {   // the upper ghost plane too (x^{k0} at z+1 on a z slab)
-              T xg_[W];
-              VT<T>::ldT(P.x + pt0 + g.plane, xg_);
-              VT<T>::stT(xs_wr + pt0 + g.plane, xg_);
-            }
-          }
-        }
-      }
-      if (f.check) {
-        warp_acc(acc, nv, P.P * NSLOT, x2);
-#pragma unroll
-        for (int js = 0; js < HIST_S; ++js)
-          if ((hhead - js + HIST_S) % HIST_S < hcount) warp_acc(acc, nv, P.P * NSLOT + 1 + js, d2[js]);
-      }
-    } else {
-      const int i = P.seg_set[seg], bl = P.seg_blk[seg];
-      switch (P.set[i].kind) {
-        case K_BOUNDS: p1_seg<T, 0>(P, C, i, bl, f, par, cbase, nch, lane, xs_rd, acc, nv, h1); break;
-        case K_DIST: p1_seg<T, 1>(P, C, i, bl, f, par, cbase, nch, lane, xs_rd, acc, nv, h1); break;
-        default: p1_seg<T, 2>(P, C, i, bl, f, par, cbase, nch, lane, xs_rd, acc, nv, h1); break;
-      }
-    }
-  }
-  if (h1) {   // flush the round-1 histograms (exact integer sums) to global
-    __syncthreads();
-    for (int jj = 0; jj < P.fuse_r1; ++jj) {
-      const int jb = 2 * jj;
-      const unsigned* hc = h1 + jj * 3 * NBUCK;
-      for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
-        const unsigned cnt = hc[d];
-        if (!cnt) continue;
-        atomicAdd(P.gh_cnt + (size_t)jb * NBUCK + d, cnt);
-        const unsigned long long base = ((d >> 3) ? (1ull << 23) : 0ull) + ((unsigned long long)(d & 7) << 20);
-        const unsigned long long sum = (unsigned long long)cnt * base + hc[NBUCK + d] +
-                                       ((unsigned long long)hc[2 * NBUCK + d] << 10);
-        atomicAdd(P.gh_s0 + (size_t)jb * NBUCK + d, sum);
-      }
+  const int per = (nch + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int c0 = min(nch, (int)blockIdx.x * per), c1 = min(nch, c0 + per);
+  p1_xrun<T, AD, CK, NA>(P, C, f, c0, c1, xs_wr, acc, nv, st);
+  for (int seg = 1; seg < P.nseg1; ++seg) {
+    const int i = P.seg_set[seg], bl = P.seg_blk[seg];
+    const int kd = P.set[i].kind;
+    const int K = kd == K_BOUNDS ? 0 : (kd == K_DIST ? 1 : 2);
+    switch (K * 4 + P.set[i].prim[bl]) {
+#define P1CASE(KK, PP) \
+      case KK * 4 + PP: p1_run<T, KK, PP, AD, CK, NA>(P, C, i, bl, f, par, c0, c1, xs_rd, acc, nv, st); break;
+      P1CASE(0, PRIM_I) P1CASE(0, PRIM_Z) P1CASE(0, PRIM_Y) P1CASE(0, PRIM_X)
+      P1CASE(1, PRIM_I)
+      P1CASE(2, PRIM_I) P1CASE(2, PRIM_Z) P1CASE(2, PRIM_Y) P1CASE(2, PRIM_X)
+#undef P1CASE
+      default: break;   // the distance block is I; blur/mask sets take the scalar kernels
     }
   }
   double* stage = P.partials + (size_t)gridDim.x * nv;
@@ -361,24 +430,13 @@ __global__ void __launch_bounds__(BLOCK, 2) k_pass1t(const __grid_constant__ Pro
       return;
     }
     fin_pass1<T>(P, C, stage);
-    if (h1) {   // resolve round 1 of the w jobs (k_selectf continues at round 2)
-      __syncthreads();
-      for (int jj = 0; jj < P.fuse_r1; ++jj) {
-        const int jb = 2 * jj;
-        Job& J = C.job[jb];
-        if (J.mode == JM_SEARCH && J.round == 0) {
-          resolve_round<T>(P, J, 1, P.gh_cnt + (size_t)jb * NBUCK, P.gh_s0 + (size_t)jb * NBUCK,
-                           P.gh_s1 + (size_t)jb * NBUCK);
-        }
-        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
-          P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;
-          P.gh_s0[(size_t)jb * NBUCK + d] = 0ull;
-          P.gh_s1[(size_t)jb * NBUCK + d] = 0ull;
-        }
-        __syncthreads();
-      }
-    }
   }
+}
+
+// dynamic shared memory of k_pass1t<T, AD, .>: per-warp slots + two stages
+__host__ inline size_t pass1_smem(int P, bool adapt) {
+  const size_t accb = ((size_t)NWARP * (P * NSLOT + NEVOL) * sizeof(double) + 127) / 128 * 128;
+  return accb + (size_t)2 * (adapt ? P1_NA_ADAPT : P1_NA_PLAIN) * (BLOCK + 1) * 16;
 }
 
 // ------------------------------------------------------------ pass 2

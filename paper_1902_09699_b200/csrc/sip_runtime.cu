@@ -117,11 +117,12 @@ struct Engine : EngineBase {
   cudaEvent_t ev_flag[2];
   cudaEvent_t ev0, ev1;
   // launch geometry
-  int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1;
+  int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1, g_p1 = 1, g_p1a = 1;
+  int npr = 0;                   // allocated slots of the p ring (Prob::pr)
   bool vec = false;
   ZGeo zg{};                     // z-marching CG geometry (sip_zmarch.cuh)
   size_t smem_z = 0;
-  size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0;
+  size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0, smem_p1v = 0, smem_p1a = 0;
   // graph
   cudaGraphExec_t gexec = nullptr;
   int g_iters = 0, g_ncg = -1;
@@ -250,6 +251,9 @@ struct Engine : EngineBase {
     Pr.m = field(1);
     Pr.r = field(1);
     Pr.pb[0] = field(1); Pr.pb[1] = field(1);
+    Pr.pr[0] = Pr.pb[0]; Pr.pr[1] = Pr.pb[1];
+    npr = 2;
+    Pr.defer_x = 0;
     Pr.tb = Pr.has[PRIM_F] ? field(1) : nullptr;
     for (int j = 0; j < HIST_S; ++j) Pr.hist[j] = field(1);
     Pr.xs[0] = field(1); Pr.xs[1] = field(1);
@@ -283,15 +287,13 @@ struct Engine : EngineBase {
       }
     }
     const int nv1 = P * NSLOT + NEVOL;
-    smem_p1 = (size_t)NWARP * nv1 * sizeof(double);
-    // fp32 vectorised path: round 1 of the radix search is fused into pass 1
-    // (one smem histogram per w-job) and round 2 compacts its survivors
-    Pr.fuse_r1 = 0;
-    if (vec && sizeof(T) == 4 && njobs > 0 && nranks == 1 && getenv("SIP_FUSE_R1")) {   // measured slower on C4: opt-in
-      Pr.fuse_r1 = njobs / 2;
-      Pr.h1_off = (int)((smem_p1 + 15) / 16 * 16);
-      smem_p1 = (size_t)Pr.h1_off + (size_t)Pr.fuse_r1 * 3 * NBUCK * sizeof(unsigned);
-    }
+    smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
+    smem_p1v = pass1_smem(P, false);                   // k_pass1t: slots + bulk-copy stages
+    smem_p1a = pass1_smem(P, true);
+    // pass 1: segment-major over one contiguous chunk range per CTA
+    // (3 CTAs / SM plain, 2 on adapt iterations: registers + stage buffers)
+    g_p1 = std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * 3));
+    g_p1a = std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * 2));
     if (vec && sizeof(T) == 4)
       for (int i = 0; i < P; ++i) {
         const SetD<T>& S = Pr.set[i];
@@ -302,7 +304,7 @@ struct Engine : EngineBase {
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
     const int gz_ = zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1;
-    const int gmax = std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_);
+    const int gmax = std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1);
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -329,11 +331,11 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1v));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1v));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1a));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1a));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1a));
     memset(&hc, 0, sizeof(hc));
     hc.njobs = njobs;
     for (int i = 0; i < P; ++i) {
@@ -407,7 +409,7 @@ struct Engine : EngineBase {
   // profiling: an event is recorded before the first kernel and after every
   // kernel; consecutive pairs give each kernel's device time (kind list)
   // KB_COMM: a z-slab site's exchange + finalisers (multi-rank only)
-  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, NKIND };
+  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, KB_CGX, NKIND };
   bool prof = false;
   std::vector<cudaEvent_t> pev;      // events of one graph (capture order)
   std::vector<int> pkind;            // kind of the kernel ending at pev[i+1]
@@ -438,11 +440,11 @@ struct Engine : EngineBase {
     const int ad = kpos > 0 ? (kpos % 2 == 1) : 2;
     const int ck = kpos > 0 ? (kpos % hc.opt.check_every == 0) : 2;
     switch (ad * 3 + ck) {
-      case 0: k_pass1t<T, 0, 0><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
-      case 1: k_pass1t<T, 0, 1><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
-      case 3: k_pass1t<T, 1, 0><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
-      case 4: k_pass1t<T, 1, 1><<<g_vec, BLOCK, smem_p1, stream>>>(Pr); break;
-      default: k_pass1t<T, 2, 2><<<g_vec, BLOCK, smem_p1, stream>>>(Pr);
+      case 0: k_pass1t<T, 0, 0><<<g_p1, BLOCK, smem_p1v, stream>>>(Pr); break;
+      case 1: k_pass1t<T, 0, 1><<<g_p1, BLOCK, smem_p1v, stream>>>(Pr); break;
+      case 3: k_pass1t<T, 1, 0><<<g_p1a, BLOCK, smem_p1a, stream>>>(Pr); break;
+      case 4: k_pass1t<T, 1, 1><<<g_p1a, BLOCK, smem_p1a, stream>>>(Pr); break;
+      default: k_pass1t<T, 2, 2><<<g_p1a, BLOCK, smem_p1a, stream>>>(Pr);
     }
   }
   void launch_pass2(int kpos) {
@@ -482,6 +484,13 @@ struct Engine : EngineBase {
     else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
     ++launches;
   }
+  // deferred x update: one ring slot per CG step (vectorised path, n_cg <= MAXCG)
+  void ensure_ring(int n_cg) {
+    if (!vec || n_cg < 1 || n_cg > MAXCG || getenv("SIP_NO_DEFER_X")) { Pr.defer_x = 0; return; }
+    while (npr < n_cg) Pr.pr[npr++] = field(1);
+    Pr.defer_x = 1;
+  }
+  void launch_cgx() { k_cgx<T><<<g_vec, BLOCK, 0, stream>>>(Pr); ++launches; }
   void launch_select(int r) {
     if (vec) k_selectf<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
     else k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
@@ -511,6 +520,7 @@ struct Engine : EngineBase {
       launch_cg1(j); mark(KB_CG1);
       launch_cg2(j); mark(KB_CG2);
     }
+    if (Pr.defer_x && n_cg > 0) { launch_cgx(); mark(KB_CGX); }
     launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
@@ -661,6 +671,7 @@ struct Engine : EngineBase {
   void solve(const Options& o, int max_iter, double eps_feas, double eps_evol, int init_x, int init_yv,
              const double* rho_in, const double* gamma_in) {
     ensure_log(max_iter);
+    ensure_ring(o.n_cg);
     const double floor_ = o.cg_tol_floor > 0 ? o.cg_tol_floor
                                              : 10.0 * (sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON);
     fill_ctrl(o, max_iter, eps_feas, eps_evol, floor_, rho_in, gamma_in);
@@ -840,7 +851,7 @@ struct NcclComm : Comm {
 };
 
 // fields whose planes a site exchanges
-enum FieldSel { FS_X, FS_R, FS_P0, FS_P1, FS_M, FS_Y0, FS_Y1, FS_V0, FS_V1 };
+enum FieldSel { FS_X, FS_R, FS_M, FS_Y0, FS_Y1, FS_V0, FS_V1, FS_PRING /* + slot: p ring (pr) */ };
 enum SetSel { SS_ALL = 0, SS_POINTWISE = 1, SS_GLOBAL = 2, SS_ALLBLK = 3 /* every block of every set */ };
 struct HaloReq { int sel, sets, dir; };
 
@@ -905,11 +916,10 @@ struct Team : EngineBase {
     switch (q.sel) {
       case FS_X: push(e.Pr.x); return;
       case FS_R: push(e.Pr.r); return;
-      case FS_P0: push(e.Pr.pb[0]); return;
-      case FS_P1: push(e.Pr.pb[1]); return;
       case FS_M: push(const_cast<T*>(e.Pr.m)); return;
       default: break;
     }
+    if (q.sel >= FS_PRING) { push(e.Pr.pr[q.sel - FS_PRING]); return; }
     const bool isy = q.sel == FS_Y0 || q.sel == FS_Y1;
     const int par = (q.sel == FS_Y1 || q.sel == FS_V1) ? 1 : 0;
     for (int i = 0; i < e.P; ++i) {
@@ -953,10 +963,14 @@ struct Team : EngineBase {
     site(ST_RHS, 0, 0, {{FS_R, 0, H_BOTH}});
     for (int j = 0; j < n_cg; ++j) {
       each([&](Engine<T>& e) { e.launch_cg1(j); }, E::KB_CG1);
-      site(ST_CG1, j, 0, {{(j & 1) ? FS_P1 : FS_P0, 0, H_BOTH}});
+      site(ST_CG1, j, 0, {{FS_PRING + (e0.Pr.defer_x ? j : (j & 1)), 0, H_BOTH}});
       each([&](Engine<T>& e) { e.launch_cg2(j); }, E::KB_CG2);
-      if (j == n_cg - 1) site(ST_CG2, j, 0, {{FS_X, 0, H_BOTH}});   // x^{k+1} for pass 1 and the next rhs
+      if (j == n_cg - 1 && !e0.Pr.defer_x) site(ST_CG2, j, 0, {{FS_X, 0, H_BOTH}});   // x^{k+1} for pass 1, next rhs
       else site(ST_CG2, j, 0, {{FS_R, 0, H_BOTH}});
+    }
+    if (e0.Pr.defer_x && n_cg > 0) {
+      each([&](Engine<T>& e) { e.launch_cgx(); }, E::KB_CGX);
+      site(ST_CG2, 0, 0, {{FS_X, 0, H_BOTH}}, false);
     }
     each([&](Engine<T>& e) { e.launch_pass1(kpos); ++e.launches; }, E::KB_PASS1);
     site(ST_PASS1, 0, 0, {{wr ? FS_Y1 : FS_Y0, SS_POINTWISE, H_LO}, {wr ? FS_V1 : FS_V0, SS_POINTWISE, H_LO}});
@@ -1043,6 +1057,7 @@ struct Team : EngineBase {
     launches = 0;
     each([&](Engine<T>& e) {
       e.ensure_log(max_iter);
+      e.ensure_ring(o.n_cg);
       e.fill_ctrl(o, max_iter, eps_feas, eps_evol, floor_, rho_in, gamma_in);
       e.fill_logs_nan(max_iter);
     });
@@ -1466,6 +1481,7 @@ sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg,
                                                 : 10.0 * (sizeof(T) == 4 ? (double)FLT_EPSILON : DBL_EPSILON);
   Options o = g->opt;
   o.n_cg = n_cg; o.eq25 = eq25;
+  e->ensure_ring(n_cg);
   e->fill_ctrl(o, 1, 1e-3, 1e-2, floor_, rho, nullptr);
   T* bb = e->Pr.hist[1];
   copy_in(e, b, bb, G.N);
@@ -1500,6 +1516,7 @@ sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg,
       k_cg2<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
     }
   }
+  if (e->Pr.defer_x && n_cg > 0) e->launch_cgx();
   CU(cudaGetLastError());
   e->read_ctrl();
   copy_out(e, e->Pr.x, x, G.N);
@@ -1587,7 +1604,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
       CU(cudaMemsetAsync(S.v[0] + (int64_t)b * G.ld, 0, G.N * sizeof(T), e->stream));
       boff += e->block_len(S.prim[b]);
     }
-    if (e->vec) k_pass1t<T, 2, 2><<<e->g_vec, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
+    if (e->vec) k_pass1t<T, 2, 2><<<e->g_p1a, BLOCK, e->smem_p1a, e->stream>>>(e->Pr);
     else k_pass1<T><<<e->g_pts, BLOCK, e->smem_p1, e->stream>>>(e->Pr);
   }
   CU(cudaGetLastError());
@@ -1993,7 +2010,7 @@ sip_status sip_get_profile(sip_grid g, int n, double* ms, int64_t* count) {
   return guarded(g, [&]() -> sip_status {
     if (!g->last) throw SipError{SIP_ERR_STATE, "no projection"};
     auto fill = [&](auto* e) {
-      for (int q = 0; q < n && q < 10; ++q) {
+      for (int q = 0; q < n && q < 11; ++q) {
         if (ms) ms[q] = e->prof_ms[q];
         if (count) count[q] = e->prof_cnt[q];
       }

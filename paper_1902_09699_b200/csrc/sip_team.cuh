@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(BLOCK) k_fin(const __grid_constant__ Prob<T> P
     case ST_CG1:
       if (C.stopped || (j == 0 && C.zero_x) || !C.cg_active) return;
       gsum(1);
-      if (threadIdx.x == 0) fin_cg1(C, v);
+      if (threadIdx.x == 0) fin_cg1(C, v, j);
       break;
     case ST_CG2:
       if (C.stopped || !C.cg_active) return;

@@ -31,6 +31,10 @@ template <> struct VT<float> {
   __device__ static void stT(float* p, const float* o) {
     *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
   }
+  __device__ static void ldT_s(const float* p, float* o) {   // shared memory
+    float4 a = *reinterpret_cast<const float4*>(p);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+  }
   // double helpers (used by the set passes where the math stays in fp64)
   __device__ static void ld(const float* p, double* o) {
     float t[4]; ldT(p, t);
@@ -53,6 +57,10 @@ template <> struct VT<double> {
   }
   __device__ static void stT(double* p, const double* o) {
     *reinterpret_cast<double2*>(p) = make_double2(o[0], o[1]);
+  }
+  __device__ static void ldT_s(const double* p, double* o) {   // shared memory
+    double2 a = *reinterpret_cast<const double2*>(p);
+    o[0] = a.x; o[1] = a.y;
   }
   __device__ static void ld(const double* p, double* o) { ldT(p, o); }
   __device__ static void st(double* p, const double* o) { stT(p, o); }
@@ -277,8 +285,8 @@ __global__ void __launch_bounds__(BLOCK) k_cg1v(const __grid_constant__ Prob<T> 
   __shared__ double out[1];
   const T beta = (T)C.beta;
   const CoefT<T> cf(C);
-  const T* pold = P.pb[(j + 1) & 1];
-  T* pw = P.pb[j & 1];
+  const T* pold = j > 0 ? p_slot(P, j - 1) : nullptr;
+  T* pw = p_slot(P, j);
   const bool hz = P.has[PRIM_Z], hy = P.has[PRIM_Y], hx = P.has[PRIM_X];
   const int lane = threadIdx.x & 31;
   double pq = 0.0;
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(BLOCK) k_cg1v(const __grid_constant__ Prob<T> 
     if (threadIdx.x == 0) {
       *P.counter = 0u;
       if (P.nranks > 1) publish(P, out, 1, 0, 1);
-      else fin_cg1(C, out);
+      else fin_cg1(C, out, j);
     }
   }
 }
@@ -327,8 +335,9 @@ __global__ void __launch_bounds__(BLOCK) k_cg2v(const __grid_constant__ Prob<T> 
   __shared__ double out[1];
   const Geo& g = P.g;
   const int nch = g.N / W;
-  const T* pv = P.pb[j & 1];
+  const T* pv = p_slot(P, j);
   const T alpha = (T)C.alpha;
+  const bool upx = !P.defer_x;
   const CoefT<T> cf(C);
   const bool hz = P.has[PRIM_Z], hy = P.has[PRIM_Y], hx = P.has[PRIM_X];
   const int lane = threadIdx.x & 31;
@@ -339,7 +348,7 @@ __global__ void __launch_bounds__(BLOCK) k_cg2v(const __grid_constant__ Prob<T> 
     const int pt0 = (valid ? c : nch - 1) * W;
     const Loc L = locate(g, pt0);
     T xv[W], rv[W];
-    VT<T>::ldcs(P.x + pt0, xv);
+    if (upx) VT<T>::ldcs(P.x + pt0, xv);
     VT<T>::ldcs(P.r + pt0, rv);
     Nbr<T> n;
     fetch5<T, false>(g, pv, nullptr, (T)0, pt0, hy, n);
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(BLOCK) k_cg2v(const __grid_constant__ Prob<T> 
       s += rv[e] * rv[e];
     }
     if (valid) {
-      VT<T>::stT(P.x + pt0, xv);
+      if (upx) VT<T>::stT(P.x + pt0, xv);
       VT<T>::stT(P.r + pt0, rv);
       rr += (double)s;
     }
@@ -368,6 +377,35 @@ __global__ void __launch_bounds__(BLOCK) k_cg2v(const __grid_constant__ Prob<T> 
       if (P.nranks > 1) publish(P, out, 1, 0, 1);
       else fin_cg2(C, out, j);
     }
+  }
+}
+
+// k_cgx: the deferred x update after the CG loop, x += sum_j alpha_j p_j
+// over the cg_count completed steps, in step order (Eq. 21 line 1's CG)
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_cgx(const __grid_constant__ Prob<T> P) {
+  constexpr int W = VT<T>::W;
+  const Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  const int n = C.cg_count;
+  if (n == 0) return;
+  T al[MAXCG];
+#pragma unroll
+  for (int j = 0; j < MAXCG; ++j) al[j] = (T)C.alph[j];
+  const int nch = P.g.N / W;
+  for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
+    const int pt0 = c * W;
+    T xv[W];
+    VT<T>::ldcs(P.x + pt0, xv);
+#pragma unroll
+    for (int j = 0; j < MAXCG; ++j) {
+      if (j >= n) break;
+      T pv[W];
+      VT<T>::ldcs(P.pr[j] + pt0, pv);
+#pragma unroll
+      for (int e = 0; e < W; ++e) xv[e] = xv[e] + al[j] * pv[e];
+    }
+    VT<T>::stT(P.x + pt0, xv);
   }
 }
 

@@ -270,8 +270,8 @@ __global__ void __launch_bounds__(BLOCK) k_cg1z(const __grid_constant__ Prob<T> 
   __shared__ double out[1];
   const CoefT<T> cf(C);
   const T beta = (T)C.beta;
-  const T* pold = P.pb[(j + 1) & 1];
-  T* pw = P.pb[j & 1];
+  const T* pold = j > 0 ? p_slot(P, j - 1) : nullptr;
+  T* pw = p_slot(P, j);
   double pq = j > 0 ? zsweep<T, 1, true, Y3D, ZSMEM>(P, Z, cf, P.r, pold, beta, (T)0, pw, (T*)zsm)
                     : zsweep<T, 1, false, Y3D, ZSMEM>(P, Z, cf, P.r, pold, beta, (T)0, pw, (T*)zsm);
   pq = block_sum(pq, sh);
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(BLOCK) k_cg1z(const __grid_constant__ Prob<T> 
     if (threadIdx.x == 0) {
       *P.counter = 0u;
       if (P.nranks > 1) publish(P, out, 1, 0, 1);
-      else fin_cg1(C, out);
+      else fin_cg1(C, out, j);
     }
   }
 }

@@ -153,7 +153,7 @@ def test_virtual_ranks_option_errors():
 
 ML_SLAB = [((16, 16), 2, ("bounds", "l1", "slope"), 4),
            ((16, 16), 3, ("bounds", "l1", "slope", "card"), 2),
-           ((8, 8, 8), 2, ("bounds", "l1", "slope", "annulus"), 2),
+           ((8, 8, 8), 2, ("bounds", "l1", "dybox", "annulus"), 2),
            ((16, 8, 16), 2, ("bounds", "l1", "cardz"), 4)]
 
 
