@@ -19,6 +19,7 @@
 #include "../../include/sip.h"
 #include "sip_aux_kernels.cuh"
 #include "sip_team.cuh"
+#include "sip_cgs.cuh"
 
 using namespace sip;
 
@@ -121,6 +122,8 @@ struct Engine : EngineBase {
   int npr = 0;                   // allocated slots of the p ring (Prob::pr)
   bool vec = false;
   ZGeo zg{};                     // z-marching CG geometry (sip_zmarch.cuh)
+  SGeo sg{};                     // staged z-marching CG geometry (sip_cgs.cuh)
+  size_t smem_s1 = 0, smem_s2 = 0;
   size_t smem_z = 0;
   size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0, smem_p1v = 0, smem_p1a = 0;
   // graph
@@ -286,6 +289,34 @@ struct Engine : EngineBase {
         smem_z = (size_t)2 * (zg.tyw + 2) * zg.row_pts * sizeof(T);
       }
     }
+    // staged z-marching CG (sip_cgs.cuh): tile = ty rows x tx chunks = BLOCK
+    // threads; whole-row tiles when they are at least 8 rows deep
+    sg.on = 0;
+    if (vec && !getenv("SIP_NO_CGS")) {
+      const int nxc = g.nx / W;
+      int tx = 0, ty = 0, full = 0;
+      if (ndim == 3) {
+        if (BLOCK % nxc == 0 && BLOCK / nxc >= 8 && g.ny % (BLOCK / nxc) == 0) { tx = nxc; ty = BLOCK / nxc; full = 1; }
+        else if (nxc % 32 == 0 && g.ny % 8 == 0) { tx = 32; ty = 8; }
+      } else if (nxc % BLOCK == 0) {
+        tx = BLOCK; ty = 1; full = (nxc == BLOCK);
+      }
+      if (tx) {
+        sg.tx = tx; sg.ty = ty; sg.full = full;
+        sg.hrow = ndim == 3 ? 1 : 0;
+        sg.rows = ty + 2 * sg.hrow;
+        sg.tiles_x = nxc / tx;
+        sg.tiles_y = g.ny / ty;
+        const int tiles = sg.tiles_x * sg.tiles_y;
+        const int want = nsm * 2;   // ~2 CTAs per SM; each keeps 3-4 planes in flight
+        const int nzc = std::max(1, std::min(g.nz, (want + tiles - 1) / tiles));
+        sg.zc = (g.nz + nzc - 1) / nzc;
+        sg.nzc = (g.nz + sg.zc - 1) / sg.zc;
+        smem_s1 = cgs_smem<T>(sg, g.nx, true);
+        smem_s2 = cgs_smem<T>(sg, g.nx, false);
+        if (smem_s1 <= 200 * 1024 && smem_s2 <= 200 * 1024) sg.on = 1;
+      }
+    }
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
     smem_p1v = pass1_smem(P, false);                   // k_pass1t: slots + bulk-copy stages
@@ -305,7 +336,8 @@ struct Engine : EngineBase {
       }
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
-    const int gz_ = zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1;
+    const int gz_ = std::max(zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1,
+                             sg.on ? sg.tiles_x * sg.tiles_y * sg.nzc : 1);
     const int gmax = std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1);
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
@@ -333,6 +365,10 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
+    if (sg.on) {
+      CU(cudaFuncSetAttribute(k_cg1s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s1));
+      CU(cudaFuncSetAttribute(k_cg2s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s2));
+    }
     CU(cudaFuncSetAttribute(k_pass1t<T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1v));
     CU(cudaFuncSetAttribute(k_pass1t<T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1v));
     CU(cudaFuncSetAttribute(k_pass1t<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1a));
@@ -470,7 +506,9 @@ struct Engine : EngineBase {
     ++launches;
   }
   void launch_cg1(int j) {
-    if (zg.on) {
+    if (sg.on) {
+      k_cg1s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s1, stream>>>(Pr, sg, j);
+    } else if (zg.on) {
       // measured on C4: z-marching wins for k_cg1 (operand recomputed from
       // two arrays at 5 positions), the flat sweep for k_cg2 (profiles/)
       k_cg1z<T, true><<<zg.tiles_x * zg.tiles_y * zg.nzc, BLOCK, smem_z, stream>>>(Pr, zg, j);
@@ -482,7 +520,8 @@ struct Engine : EngineBase {
     ++launches;
   }
   void launch_cg2(int j) {
-    if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
+    if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
+    else if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
     else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
     ++launches;
   }
@@ -1507,13 +1546,9 @@ sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg,
   k_rhs<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2);
   for (int j = 0; j < n_cg; ++j) {
     if (e->Pr.has[PRIM_F]) k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, 1, j);
-    if (e->zg.on) {   // the same kernels as the hot path
-      const int gz = e->zg.tiles_x * e->zg.tiles_y * e->zg.nzc;
-      k_cg1z<T, true><<<gz, BLOCK, e->smem_z, e->stream>>>(e->Pr, e->zg, j);
-      k_cg2v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
-    } else if (e->vec) {
-      k_cg1v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
-      k_cg2v<T><<<e->g_vec, BLOCK, 0, e->stream>>>(e->Pr, j);
+    if (e->vec) {   // the same kernels as the hot path
+      e->launch_cg1(j);
+      e->launch_cg2(j);
     } else {
       k_cg1<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
       k_cg2<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
