@@ -70,34 +70,56 @@ struct SIdx {
 template <class T>
 __device__ __forceinline__ void lds(const T* p, T* o) { VT<T>::ldT_s(p, o); }
 
-// q = C p at the W points of my chunk from a 3-plane ring (prev, cur, next)
+// C = cI I + cz Dz'Dz + cy Dy'Dy + cx Dx'Dx (Eq. 23) written per point as
+// q = diag p0 - sum_n c_n p_n over the present neighbours n: the boundary
+// rows of D'D (reading L3) drop a neighbour together with its diagonal
+// share.  Coefficients of absent neighbours are 0 (so a missing primitive
+// costs nothing), y and x masks are per thread, the z mask per plane.
 template <class T>
-__device__ __forceinline__ void stencil_s(const CoefT<T>& cf, const Geo& g, bool hz, bool hy, bool hx,
-                                          bool zlo, bool zhi, bool ylo, bool yhi, int ix0, const T* pm,
-                                          const T* pc, const T* pp, const SIdx<T>& I, int r, int c, T* p0out,
-                                          T* q) {
+struct SCo {
+  T cI, cz, cyl, cyh, cxl0, cxh, cx, cxhW, d0, d1, dW;   // d*: diagonal without the z part
+  __device__ SCo(const Ctrl& C, const Prob<T>& P, bool ylo, bool yhi, int ix0) {
+    constexpr int W = VT<T>::W;
+    const Geo& g = P.g;
+    cI = (T)C.cI;
+    cz = P.has[PRIM_Z] ? (T)C.cz : (T)0;
+    const T cy = P.has[PRIM_Y] ? (T)C.cy : (T)0;
+    cx = P.has[PRIM_X] ? (T)C.cx : (T)0;
+    cyl = ylo ? cy : (T)0;
+    cyh = yhi ? cy : (T)0;
+    cxl0 = ix0 >= 1 ? cx : (T)0;               // left neighbour of lane 0
+    cxhW = ix0 + W < g.nx ? cx : (T)0;         // right neighbour of lane W-1
+    cxh = cx;
+    const T dy = cI + cyl + cyh;
+    d0 = dy + cxl0 + cx;                        // lane 0
+    d1 = dy + cx + cx;                          // inner lanes
+    dW = dy + cx + cxhW;                        // lane W-1
+  }
+};
+
+template <class T, bool HY>
+__device__ __forceinline__ void stencil_s(const SCo<T>& k, T czl, T czh, const T* pm, const T* pc, const T* pp,
+                                          int o, int rs, T* p0out, T* q) {
   constexpr int W = VT<T>::W;
   T cur[W], zm[W], zp[W], ym[W], yp[W];
-  lds<T>(pc + I.at(r, c), cur);
-  lds<T>(pm + I.at(r, c), zm);
-  lds<T>(pp + I.at(r, c), zp);
-  if (hy) {
-    lds<T>(pc + I.at(r - 1, c), ym);
-    lds<T>(pc + I.at(r + 1, c), yp);
+  lds<T>(pc + o, cur);
+  lds<T>(pm + o, zm);
+  lds<T>(pp + o, zp);
+  if (HY) {
+    lds<T>(pc + o - rs, ym);
+    lds<T>(pc + o + rs, yp);
   }
-  const T xl = pc[I.at(r, c) - 1], xr = pc[I.at(r, c) + W];
-  const bool xlo = ix0 >= 1, xhi = ix0 + W < g.nx;
+  const T xl = pc[o - 1], xr = pc[o + W];
+  const T dz = czl + czh;
 #pragma unroll
   for (int e = 0; e < W; ++e) {
     const T p0 = cur[e];
-    T v = cf.cI * p0;
-    if (hz) v += cf.cz * ((p0 - (zlo ? zm[e] : p0)) - ((zhi ? zp[e] : p0) - p0));
-    if (hy) v += cf.cy * ((p0 - (ylo ? ym[e] : p0)) - ((yhi ? yp[e] : p0) - p0));
-    if (hx) {
-      const T left = e > 0 ? cur[e - 1] : (xlo ? xl : p0);
-      const T right = e < W - 1 ? cur[e + 1] : (xhi ? xr : p0);
-      v += cf.cx * ((p0 - left) - (right - p0));
-    }
+    const T de = (e == 0 ? k.d0 : (e == W - 1 ? k.dW : k.d1)) + dz;
+    T v = de * p0 - czl * zm[e] - czh * zp[e];
+    if (HY) v = v - k.cyl * ym[e] - k.cyh * yp[e];
+    const T left = e > 0 ? cur[e - 1] : xl;
+    const T right = e < W - 1 ? cur[e + 1] : xr;
+    v = v - (e == 0 ? k.cxl0 : k.cx) * left - (e == W - 1 ? k.cxhW : k.cx) * right;
     q[e] = v;
     p0out[e] = p0;
   }
@@ -153,10 +175,9 @@ __global__ void __launch_bounds__(BLOCK) k_cg1s(const __grid_constant__ Prob<T> 
   T* pn = sq + CG1_RS * PLa;                       // [3][PLa] p_j ring
   const bool usep = j > 0;
   const T beta = (T)C.beta;
-  const CoefT<T> cf(C);
   const T* pold = usep ? p_slot(P, j - 1) : nullptr;
   T* pw = p_slot(P, j);
-  const bool hz = P.has[PRIM_Z], hy = P.has[PRIM_Y], hx = P.has[PRIM_X];
+  const bool hy = P.has[PRIM_Y] && g.ny > 1;
   const STile t(g, Z);
   const SIdx<T> I(g, Z);
   if (threadIdx.x == 0) {
@@ -176,6 +197,14 @@ __global__ void __launch_bounds__(BLOCK) k_cg1s(const __grid_constant__ Prob<T> 
   };
   // p_j = r + beta p_{j-1} on every staged position of plane z -> ring slot
   const int nchk = Z.rows * (Z.tx + 2);
+  constexpr int MPN = 3;             // staged chunks per thread (<= (ty + 2)(tx + 2) / BLOCK + 1)
+  int mo[MPN];
+#pragma unroll
+  for (int u = 0; u < MPN; ++u) {
+    const int kk = threadIdx.x + u * BLOCK;
+    const int r = kk / (Z.tx + 2), c = kk - r * (Z.tx + 2);
+    mo[u] = kk < nchk ? I.at(r, c) : -1;
+  }
   auto make_pn = [&](int z) {
     const int s = (z + CG1_RS) % CG1_RS;
     mbar_wait(&bar[s], (ph >> s) & 1u);
@@ -183,9 +212,10 @@ __global__ void __launch_bounds__(BLOCK) k_cg1s(const __grid_constant__ Prob<T> 
     T* dst = pn + ((z + 3) % 3) * PLa;
     const T* a = sr + s * PLa;
     const T* q = sq + s * PLa;
-    for (int k = threadIdx.x; k < nchk; k += BLOCK) {
-      const int r = k / (Z.tx + 2), c = k - r * (Z.tx + 2);
-      const int o = I.at(r, c);
+#pragma unroll
+    for (int u = 0; u < MPN; ++u) {
+      const int o = mo[u];
+      if (o < 0) continue;
       T av[W];
       lds<T>(a + o, av);
       if (usep) {
@@ -203,17 +233,22 @@ __global__ void __launch_bounds__(BLOCK) k_cg1s(const __grid_constant__ Prob<T> 
   __syncthreads();
   issue(t.zb + 3);                   // into the slot of zb - 1
   const int iy = t.y0 + t.ty;
-  const bool ylo = iy >= 1, yhi = iy < g.ny - 1;
   const int ix0 = (t.x0c + t.tx) * W;
+  const SCo<T> k(C, P, iy >= 1, iy < g.ny - 1, ix0);
+  const int om = I.at(t.ty + Z.hrow, t.tx + 1);
   double pq = 0.0;
   for (int z = t.zb; z < t.ze; ++z) {
     make_pn(z + 1);
     __syncthreads();                 // ring holds z-1, z, z+1; the staging slot of plane z is free
     issue(z + 4);                    // planes z+2 .. z+4 in flight
     const int gz = z + g.z0;
+    const T czl = gz >= 1 ? k.cz : (T)0, czh = gz < g.nz_g - 1 ? k.cz : (T)0;
     T p0[W], qv[W];
-    stencil_s<T>(cf, g, hz, hy, hx, gz >= 1, gz < g.nz_g - 1, ylo, yhi, ix0, pn + ((z + 2) % 3) * PLa,
-                 pn + (z % 3) * PLa, pn + ((z + 1) % 3) * PLa, I, t.ty + Z.hrow, t.tx + 1, p0, qv);
+    const T* r0 = pn + ((z + 2) % 3) * PLa;
+    const T* r1 = pn + (z % 3) * PLa;
+    const T* r2 = pn + ((z + 1) % 3) * PLa;
+    if (hy) stencil_s<T, true>(k, czl, czh, r0, r1, r2, om, I.rs, p0, qv);
+    else stencil_s<T, false>(k, czl, czh, r0, r1, r2, om, I.rs, p0, qv);
     VT<T>::stT(pw + ((int64_t)z * g.ny + iy) * g.nx + ix0, p0);
     T s = 0;
 #pragma unroll
@@ -253,8 +288,7 @@ __global__ void __launch_bounds__(BLOCK) k_cg2s(const __grid_constant__ Prob<T> 
   T* srr = sp + CG2_RP * PLa;                      // [CG2_RR][RL] staged r
   const T* pv = p_slot(P, j);
   const T alpha = (T)C.alpha;
-  const CoefT<T> cf(C);
-  const bool hz = P.has[PRIM_Z], hy = P.has[PRIM_Y], hx = P.has[PRIM_X];
+  const bool hy = P.has[PRIM_Y] && g.ny > 1;
   const STile t(g, Z);
   const SIdx<T> I(g, Z);
   if (threadIdx.x == 0) {
@@ -298,8 +332,10 @@ __global__ void __launch_bounds__(BLOCK) k_cg2s(const __grid_constant__ Prob<T> 
   wait_p(t.zb - 1);
   wait_p(t.zb);
   const int iy = t.y0 + t.ty;
-  const bool ylo = iy >= 1, yhi = iy < g.ny - 1;
   const int ix0 = (t.x0c + t.tx) * W;
+  const SCo<T> k(C, P, iy >= 1, iy < g.ny - 1, ix0);
+  const int om = I.at(t.ty + Z.hrow, t.tx + 1);
+  const int orr = (t.ty * Z.tx + t.tx) * W;
   double rr = 0.0;
   for (int z = t.zb; z < t.ze; ++z) {
     issue_p(z + CG2_PD);             // slot of z + PD - RP <= z - 2: free since the last step's barrier
@@ -307,11 +343,14 @@ __global__ void __launch_bounds__(BLOCK) k_cg2s(const __grid_constant__ Prob<T> 
     wait_p(z + 1);
     wait_r(z);
     const int gz = z + g.z0;
+    const T czl = gz >= 1 ? k.cz : (T)0, czh = gz < g.nz_g - 1 ? k.cz : (T)0;
     T p0[W], qv[W], rv[W];
-    stencil_s<T>(cf, g, hz, hy, hx, gz >= 1, gz < g.nz_g - 1, ylo, yhi, ix0,
-                 sp + ((z - 1 + CG2_RP) % CG2_RP) * PLa, sp + (z % CG2_RP) * PLa, sp + ((z + 1) % CG2_RP) * PLa, I,
-                 t.ty + Z.hrow, t.tx + 1, p0, qv);
-    lds<T>(srr + (z % CG2_RR) * RL + (t.ty * Z.tx + t.tx) * W, rv);
+    const T* r0 = sp + ((z - 1 + CG2_RP) % CG2_RP) * PLa;
+    const T* r1 = sp + (z % CG2_RP) * PLa;
+    const T* r2 = sp + ((z + 1) % CG2_RP) * PLa;
+    if (hy) stencil_s<T, true>(k, czl, czh, r0, r1, r2, om, I.rs, p0, qv);
+    else stencil_s<T, false>(k, czl, czh, r0, r1, r2, om, I.rs, p0, qv);
+    lds<T>(srr + (z % CG2_RR) * RL + orr, rv);
     T s = 0;
 #pragma unroll
     for (int e = 0; e < W; ++e) {

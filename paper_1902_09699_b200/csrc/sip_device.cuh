@@ -125,9 +125,6 @@ struct Job {
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
   unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
-  unsigned c1_n;                 // keys of the round-1 window compacted by round 1 (fp32)
-  int wlo, whi;                  // round-1 digit window (from the last iteration's digit; -1: none)
-  int r2c;                       // round 2 reads the window's keys instead of all of w
 };
 
 struct Ctrl {
@@ -158,7 +155,6 @@ struct Ctrl {
   Opts opt;
   Job job[MAXJOBS];
   int njobs;
-  int hint[MAXJOBS];             // last resolved round-1 digit per job (-1: none)
   // log
   int* log_cg; int* log_branch; double* log_rho; double* log_gamma;
   double* log_feas; double* log_evol;

@@ -359,17 +359,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     // fp32 candidate compaction: round 2 appends the keys of the round-1
     // bucket (its survivors), rounds >= 3 read only those
     unsigned* cand = (sizeof(T) == 4) ? P.cand[jb] : nullptr;
-    // round 1 also compacts the keys whose digit lies in the window around
-    // the last iteration's digit; when the new digit falls inside, round 2
-    // reads those keys instead of all of w (post_round1)
-    unsigned* cand1 = (sizeof(T) == 4) ? P.cand1[jb] : nullptr;
-    const bool win1 = cand1 && round == 1 && J.wlo >= 0;
-    const bool from1 = cand1 && round == 2 && J.r2c;
     const bool make_cand = cand && round == 2;
-    const bool use_cand = (cand && round >= 3) || from1;
-    const unsigned* csrc = from1 ? cand1 : cand;
-    const int ntot = use_cand ? (int)(from1 ? J.c1_n : J.cand_n) : tot;
-    const unsigned wlo = (unsigned)J.wlo, whi = (unsigned)J.whi;
+    const bool use_cand = cand && round >= 3;
+    const int ntot = use_cand ? (int)J.cand_n : tot;
     int pd = -1;
     unsigned pc = 0, pl[LB::N];
     auto hflush = [&]() {
@@ -407,23 +399,11 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
         for (int u = 0; u < SEL_U; ++u) {
           const int q = q0 + u * BLOCK;
           ok[u] = q < ntot;
-          kk[u] = ok[u] ? (U)__ldcg(csrc + q) : (U)0;
+          kk[u] = ok[u] ? (U)__ldcg(cand + q) : (U)0;
         }
-        unsigned mine = 0;
 #pragma unroll
         for (int u = 0; u < SEL_U; ++u)
-          if (ok[u] && (U)(kk[u] >> plo) == prefix) { hkey(kk[u]); mine |= 1u << u; }
-        if (make_cand) {   // round 2 from the window: keep the chosen bucket's keys
-          const int cnt = __popc(mine);
-          const int before = block_excl_count(cnt, s_wc);
-          if (threadIdx.x == BLOCK - 1) s_base = atomicAdd(&C.job[jb].cand_n, (unsigned)(before + cnt));
-          __syncthreads();
-          unsigned pos = s_base + before;
-#pragma unroll
-          for (int u = 0; u < SEL_U; ++u)
-            if (mine & (1u << u)) cand[pos++] = (unsigned)kk[u];
-          __syncthreads();
-        }
+          if (ok[u] && (U)(kk[u] >> plo) == prefix) hkey(kk[u]);
       } else {
         T v[SEL_U][W];
         bool ok[SEL_U];
@@ -442,24 +422,8 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
           for (int e = 0; e < W; ++e) {
             const U key = K::key(v[u][e]);
             const bool in = ok[u] && (round == 1 || (U)(key >> plo) == prefix);
-            if (in) hkey(key);
-            const unsigned dg = (unsigned)(key >> lo);
-            const bool keep = win1 ? (ok[u] && dg >= wlo && dg <= whi) : in;
-            if (keep) mine |= 1u << (u * W + e);
+            if (in) { hkey(key); mine |= 1u << (u * W + e); }
           }
-        }
-        if (win1) {   // round 1: the window's keys (CTA-aggregated append)
-          const int cnt = __popc(mine);
-          const int before = block_excl_count(cnt, s_wc);
-          if (threadIdx.x == BLOCK - 1) s_base = atomicAdd(&C.job[jb].c1_n, (unsigned)(before + cnt));
-          __syncthreads();
-          unsigned pos = s_base + before;
-#pragma unroll
-          for (int u = 0; u < SEL_U; ++u)
-#pragma unroll
-            for (int e = 0; e < W; ++e)
-              if (mine & (1u << (u * W + e))) cand1[pos++] = (unsigned)K::key(v[u][e]);
-          __syncthreads();
         }
         if (make_cand) {   // CTA-aggregated append: one global atomic per CTA iteration
           const int cnt = __popc(mine);
@@ -488,12 +452,8 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
       unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
       unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
       unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
-      if (P.nranks > 1) {
-        publish_hist(P, jb, gc, g0, g1);
-      } else {
-        resolve_round<T>(P, J, round, gc, g0, g1);
-        if (round == 1 && threadIdx.x == 0) post_round1(C, J, jb);
-      }
+      if (P.nranks > 1) publish_hist(P, jb, gc, g0, g1);
+      else resolve_round<T>(P, J, round, gc, g0, g1);
       __syncthreads();
       for (int d = threadIdx.x; d < NBUCK; d += BLOCK) { gc[d] = 0u; g0[d] = 0ull; g1[d] = 0ull; }
       __syncthreads();

@@ -53,10 +53,8 @@ struct Prob {
   // flattened segments (sip_flat.cuh): pass1 = x work + every (set, block);
   // pass2 = every (global set, block)
   int nseg1, nseg2;
-  // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32);
-  // cand1[job]: keys whose round-1 digit is in the job's window (round 1)
+  // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32)
   unsigned* cand[MAXJOBS];
-  unsigned* cand1[MAXJOBS];
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)
@@ -69,17 +67,6 @@ struct Prob {
   double* xg;
   int xslot;
 };
-
-constexpr int SEL_WIN = 3;      // round-1 digit window half-width (buckets of 1/8 octave)
-
-// after round 1 of a job: remember its digit for the next iteration's window
-// and decide whether round 2 can read the window's compacted keys (exact:
-// every key with the chosen digit is in the window's list)
-__device__ inline void post_round1(Ctrl& C, Job& J, int jb) {
-  const bool found = J.mode == JM_SEARCH && J.round == 1;
-  C.hint[jb] = found ? (int)J.prefix : -1;
-  J.r2c = found && J.wlo >= 0 && (int)J.prefix >= J.wlo && (int)J.prefix <= J.whi;
-}
 
 __device__ __forceinline__ bool is_adapt_it(int k, int every) {
   return every <= 1 || (k % every) == 1;   // mod(k, update-frequency) = 1
@@ -1035,10 +1022,7 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
   for (int jb = 0; jb < C.njobs; ++jb) {
     Job& J = C.job[jb];
     const int i = J.set;
-    J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u; J.c1_n = 0u;
-    J.r2c = 0;
-    J.wlo = C.hint[jb] >= 0 ? max(0, C.hint[jb] - SEL_WIN) : -1;   // round-1 window around the last digit
-    J.whi = C.hint[jb] >= 0 ? min(NBUCK - 1, C.hint[jb] + SEL_WIN) : -1;
+    J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u;
     J.theta = 0.0; J.tau = 0ull; J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0.0;
     J.sigma = C.sigma[i];
     J.k = C.kcard[i];

@@ -314,7 +314,7 @@ struct Engine : EngineBase {
         sg.nzc = (g.nz + sg.zc - 1) / sg.zc;
         smem_s1 = cgs_smem<T>(sg, g.nx, true);
         smem_s2 = cgs_smem<T>(sg, g.nx, false);
-        if (smem_s1 <= 200 * 1024 && smem_s2 <= 200 * 1024) sg.on = 1;
+        if (smem_s1 <= 200 * 1024 && smem_s2 <= 200 * 1024 && sg.rows * (tx + 2) <= 3 * BLOCK) sg.on = 1;
       }
     }
     const int nv1 = P * NSLOT + NEVOL;
@@ -331,8 +331,6 @@ struct Engine : EngineBase {
         if (S.job < 0) continue;
         Pr.cand[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
         Pr.cand[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
-        Pr.cand1[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
-        Pr.cand1[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
       }
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
@@ -364,16 +362,16 @@ struct Engine : EngineBase {
     CU(cudaEventCreateWithFlags(&ev_flag[1], cudaEventDisableTiming));
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
-    CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1));
-    if (sg.on) {
-      CU(cudaFuncSetAttribute(k_cg1s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s1));
-      CU(cudaFuncSetAttribute(k_cg2s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s2));
+    CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (sg.on) {   // the attribute is per function: use the largest any engine may launch with
+      CU(cudaFuncSetAttribute(k_cg1s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      CU(cudaFuncSetAttribute(k_cg2s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     }
-    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1v));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1v));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1a));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1a));
-    CU(cudaFuncSetAttribute(k_pass1t<T, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p1a));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CU(cudaFuncSetAttribute(k_pass1t<T, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     memset(&hc, 0, sizeof(hc));
     hc.njobs = njobs;
     for (int i = 0; i < P; ++i) {
@@ -630,7 +628,6 @@ struct Engine : EngineBase {
     c.hist_head = 0; c.hist_count = 1; c.breakdown = 0; c.numeric_err = 0; c.zero_x = 0;
     c.cg_j = 0; c.cg_active = 0; c.cg_count = 0; c.cg_total = 0;
     c.P = P; c.p = p;
-    for (int jb = 0; jb < MAXJOBS; ++jb) c.hint[jb] = -1;
     c.opt.n_cg = o.n_cg; c.opt.eq25 = o.eq25; c.opt.fixed_work = o.fixed_work;
     c.opt.adapt_every = o.adapt_every; c.opt.check_every = o.check_every; c.opt.max_iter = max_iter;
     c.opt.eps_evol = eps_evol; c.opt.eps_feas = eps_feas; c.opt.eps_corr = o.eps_corr;
@@ -1586,7 +1583,6 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     const int i = J.set;
     J.round = 0; J.prefix = 0; J.cnt_above = 0; J.sum_above = 0; J.theta = 0; J.tau = 0;
     J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0; J.cand_n = 0;
-    J.c1_n = 0; J.wlo = J.whi = -1; J.r2c = 0;
     J.sigma = c.sigma[i]; J.k = c.kcard[i];
     J.mode = (J.on_s || i != set_id) ? JM_OFF : JM_SEARCH;
     if (J.mode == JM_SEARCH && J.kind == K_CARD) {
