@@ -126,10 +126,11 @@ __device__ __forceinline__ void stencil_s(const SCo<T>& k, T czl, T czh, const T
 }
 
 // ring sizes (planes) and prefetch distances
-constexpr int CG1_RS = 4;    // staged (r, p_{j-1}) planes: 3 planes in flight beyond the one consumed
-constexpr int CG2_RP = 8;    // staged p_j planes: z-1 .. z+1 in use, PD2 ahead
-constexpr int CG2_PD = 4;
-constexpr int CG2_RR = 4;    // staged r tiles (no halo)
+// (one or two CTAs per SM each keep ~60 KB of plane tiles in flight)
+constexpr int CG1_RS = 8;    // staged (r, p_{j-1}) planes: RS - 1 planes in flight beyond the one consumed
+constexpr int CG2_RP = 12;   // staged p_j planes: z-1 .. z+1 in use, up to z + PD in flight
+constexpr int CG2_PD = 8;
+constexpr int CG2_RR = 8;    // staged r tiles (no halo): z .. z + RR - 1
 
 // tile and z range of this CTA
 struct STile {
@@ -227,11 +228,11 @@ __global__ void __launch_bounds__(BLOCK) k_cg1s(const __grid_constant__ Prob<T> 
       VT<T>::stT(dst + o, av);   // generic store to shared
     }
   };
-  for (int z = t.zb - 1; z < t.zb - 1 + CG1_RS; ++z) issue(z);   // zb-1 .. zb+2
+  for (int z = t.zb - 1; z < t.zb - 1 + CG1_RS; ++z) issue(z);   // zb-1 .. zb+RS-2
   make_pn(t.zb - 1);
   make_pn(t.zb);
   __syncthreads();
-  issue(t.zb + 3);                   // into the slot of zb - 1
+  issue(t.zb + CG1_RS - 1);          // into the slot of zb - 1
   const int iy = t.y0 + t.ty;
   const int ix0 = (t.x0c + t.tx) * W;
   const SCo<T> k(C, P, iy >= 1, iy < g.ny - 1, ix0);
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(BLOCK) k_cg1s(const __grid_constant__ Prob<T> 
   for (int z = t.zb; z < t.ze; ++z) {
     make_pn(z + 1);
     __syncthreads();                 // ring holds z-1, z, z+1; the staging slot of plane z is free
-    issue(z + 4);                    // planes z+2 .. z+4 in flight
+    issue(z + CG1_RS);               // into the slot of plane z: planes z+2 .. z+RS in flight
     const int gz = z + g.z0;
     const T czl = gz >= 1 ? k.cz : (T)0, czh = gz < g.nz_g - 1 ? k.cz : (T)0;
     T p0[W], qv[W];
