@@ -308,13 +308,22 @@ struct Engine : EngineBase {
         sg.tiles_x = nxc / tx;
         sg.tiles_y = g.ny / ty;
         const int tiles = sg.tiles_x * sg.tiles_y;
-        const int want = nsm * 2;   // ~2 CTAs per SM; each keeps 3-4 planes in flight
-        const int nzc = std::max(1, std::min(g.nz, (want + tiles - 1) / tiles));
-        sg.zc = (g.nz + nzc - 1) / nzc;
-        sg.nzc = (g.nz + sg.zc - 1) / sg.zc;
         smem_s1 = cgs_smem<T>(sg, g.nx, true);
         smem_s2 = cgs_smem<T>(sg, g.nx, false);
-        if (smem_s1 <= 200 * 1024 && smem_s2 <= 200 * 1024 && sg.rows * (tx + 2) <= 3 * BLOCK) sg.on = 1;
+        if (smem_s1 <= 200 * 1024 && smem_s2 <= 200 * 1024 && sg.rows * (tx + 2) <= 3 * BLOCK) {
+          // one wave: tiles x z-chunks <= resident CTAs (a second partial wave
+          // would double the kernel time)
+          CU(cudaFuncSetAttribute(k_cg1s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          CU(cudaFuncSetAttribute(k_cg2s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          int o1 = 0, o2 = 0;
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cg1s<T>, BLOCK, smem_s1));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cg2s<T>, BLOCK, smem_s2));
+          const int slots = nsm * std::max(1, std::min(o1, o2));
+          const int nzc = std::max(1, std::min(g.nz, slots / tiles));
+          sg.zc = (g.nz + nzc - 1) / nzc;
+          sg.nzc = (g.nz + sg.zc - 1) / sg.zc;
+          sg.on = 1;
+        }
       }
     }
     const int nv1 = P * NSLOT + NEVOL;
