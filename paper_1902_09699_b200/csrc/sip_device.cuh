@@ -8,7 +8,7 @@
 namespace sip {
 
 constexpr int MAXP = 17;        // p <= 16 sets + the distance block
-constexpr int NSLOT = 13;       // per-set reduction slots (see SLOT_*)
+constexpr int NSLOT = 9;        // per-set reduction slots (see SLOT_*)
 constexpr int NEVOL = 6;        // ||x||^2 and ||x - x_hist[j]||^2, j < 5 (Eq. 27)
 constexpr int HIST_S = 5;       // s = 5
 constexpr int NBUCK = 2048;     // radix digits of 11 bits
@@ -34,11 +34,7 @@ enum Slot {
   SLOT_GG = 5,    // dg . dg
   SLOT_VV = 6,    // dv . dv
   SLOT_FN = 7,    // ||s - P(s)||^2               (Eq. 26 numerator)
-  SLOT_S2 = 8,    // ||s||^2                      (Eq. 26 denominator)
-  SLOT_CHI = 9,   // window search (fp32): count of |w| above the window
-  SLOT_SHI = 10,  //   and their sum of |w|
-  SLOT_CW = 11,   //   count of |w| inside the window (compacted as candidates)
-  SLOT_SW = 12    //   and their sum
+  SLOT_S2 = 8     // ||s||^2                      (Eq. 26 denominator)
 };
 
 // select-job modes
@@ -129,9 +125,6 @@ struct Job {
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
   unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
-  unsigned win_lo, win_hi;       // key window from the last iteration's threshold (win_hi = 0: none)
-  int win;                        // 1: the threshold lies in the window; every round reads the
-                                  // window's keys compacted by pass 1 (cnt/sum_above = above it)
 };
 
 struct Ctrl {
@@ -162,7 +155,6 @@ struct Ctrl {
   Opts opt;
   Job job[MAXJOBS];
   int njobs;
-  float hint[MAXJOBS];            // last resolved threshold value per job (0: none)
   // log
   int* log_cg; int* log_branch; double* log_rho; double* log_gamma;
   double* log_feas; double* log_evol;

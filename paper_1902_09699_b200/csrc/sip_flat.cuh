@@ -359,9 +359,8 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     // fp32 candidate compaction: round 2 appends the keys of the round-1
     // bucket (its survivors), rounds >= 3 read only those
     unsigned* cand = (sizeof(T) == 4) ? P.cand[jb] : nullptr;
-    const bool winm = cand && J.win;              // every round on the window's keys (pass 1)
-    const bool make_cand = cand && round == 2 && !winm;
-    const bool use_cand = cand && (round >= 3 || winm);
+    const bool make_cand = cand && round == 2;
+    const bool use_cand = cand && round >= 3;
     const int ntot = use_cand ? (int)J.cand_n : tot;
     int pd = -1;
     unsigned pc = 0, pl[LB::N];
@@ -404,7 +403,7 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
         }
 #pragma unroll
         for (int u = 0; u < SEL_U; ++u)
-          if (ok[u] && (round == 1 || (U)(kk[u] >> plo) == prefix)) hkey(kk[u]);
+          if (ok[u] && (U)(kk[u] >> plo) == prefix) hkey(kk[u]);
       } else {
         T v[SEL_U][W];
         bool ok[SEL_U];

@@ -68,8 +68,6 @@ struct Prob {
   int xslot;
 };
 
-constexpr float WIN_F = 1.5f;   // warm-start window half-width (factor) of the threshold search
-
 __device__ __forceinline__ bool is_adapt_it(int k, int every) {
   return every <= 1 || (k % every) == 1;   // mod(k, update-frequency) = 1
 }
@@ -671,7 +669,7 @@ __device__ void resolve_round(const Prob<T>& P, Job& J, int round, const unsigne
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (J.kind == K_L1 && round == 1 && !J.win && s_stot <= J.sigma) {
+    if (J.kind == K_L1 && round == 1 && s_stot <= J.sigma) {
       J.mode = JM_INSIDE;          // ||w||_1 <= sigma: w is in the ball (L5)
     } else if (J.kind == K_L1 && round == 1 && J.sigma <= 0.0) {
       J.mode = JM_ZERO;            // sigma = 0: the ball is {0}
@@ -1025,15 +1023,6 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
     Job& J = C.job[jb];
     const int i = J.set;
     J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u;
-    // warm start: the window [h / WIN_F, h * WIN_F] around the last threshold h
-    // (fp32 w-jobs); pass 1 counts / sums what lies above it and compacts
-    // what lies inside, fin_pass1 checks that the new threshold is inside
-    J.win = 0;
-    J.win_lo = J.win_hi = 0u;
-    if (sizeof(T) == 4 && !J.on_s && C.hint[jb] > 0.0f) {
-      J.win_lo = __float_as_uint(C.hint[jb] / WIN_F);
-      J.win_hi = __float_as_uint(C.hint[jb] * WIN_F);
-    }
     J.theta = 0.0; J.tau = 0ull; J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0.0;
     J.sigma = C.sigma[i];
     J.k = C.kcard[i];
@@ -1144,12 +1133,6 @@ __global__ void k_control(const __grid_constant__ Prob<T> P) {
     }
   for (int i = 0; i < Pn; ++i)
     for (int q = 0; q < NSLOT; ++q) C.sums[i][q] = 0.0;
-  for (int jb = 0; jb < C.njobs; ++jb) {   // warm start of the next threshold search
-    const Job& J = C.job[jb];
-    float h = 0.0f;
-    if (J.mode == JM_DONE) h = J.kind == K_L1 ? (float)J.theta : __uint_as_float((unsigned)J.tau);
-    C.hint[jb] = (h > 0.0f && h < 1e30f) ? h : 0.0f;
-  }
   reset_jobs(P, C);
   C.k = k + 1;
   if (C.k > C.opt.max_iter) C.stopped = 1;

@@ -124,14 +124,6 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
   const int dn = PRIM == PRIM_Z ? g.plane : g.nx;   // neighbour offset of D_z / D_y
   const T ih = (T)(PRIM == PRIM_Z ? g.ihz : PRIM == PRIM_Y ? g.ihy : g.ihx);
   double d_w2 = 0, d_hv = 0, d_hh = 0, d_vh = 0, d_gv = 0, d_gg = 0, d_vv = 0, d_fn = 0, d_s2 = 0;
-  // warm-started threshold search (fp32 l1 / cardinality on w): the window
-  // around the last threshold -- count and sum above it, compact inside it
-  Job* Jw = (KIND == 2 && sizeof(T) == 4 && S.job >= 0) ? &const_cast<Ctrl&>(C).job[S.job] : nullptr;
-  const bool win = Jw && Jw->win_hi != 0u && Jw->mode == JM_SEARCH;
-  const unsigned wlo = win ? Jw->win_lo : 0u, whi = win ? Jw->win_hi : 0u;
-  unsigned* wcand = win ? P.cand[S.job] : nullptr;
-  double d_chi = 0, d_shi = 0, d_cw = 0, d_sw = 0;
-  const int lane = threadIdx.x & 31;
   const int ntile = (c1 - c0 + BLOCK - 1) / BLOCK;
   auto issue = [&](int t) {
     const int cs = c0 + t * BLOCK;
@@ -166,7 +158,6 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
     const int s = t & 1;
     st.wait(s);
     const int c = c0 + t * BLOCK + (int)threadIdx.x;
-    unsigned wmsk = 0u, wkey[W];
     if (c < c1) {
       const int pt0 = c * W;
       const int tid = threadIdx.x;
@@ -263,53 +254,16 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
       } else {
         VT<T>::stT(wp + pt0, wv);
         if (sp) VT<T>::stT(sp + pt0, sv_);
-        if (win) {
-          T chi = 0, shi = 0, cw = 0, sw = 0;
-#pragma unroll
-          for (int e = 0; e < W; ++e) {
-            const bool pad = padc || (PRIM == PRIM_X && lastx && e == W - 1);
-            const T a = wv[e] < (T)0 ? -wv[e] : wv[e];
-            const unsigned key = __float_as_uint((float)a);
-            wkey[e] = key;
-            if (pad) continue;
-            if (key > whi) { chi += (T)1; shi += a; }
-            else if (key >= wlo) { cw += (T)1; sw += a; wmsk |= 1u << e; }
-          }
-          d_chi += (double)chi; d_shi += (double)shi; d_cw += (double)cw; d_sw += (double)sw;
-        }
       }
       if (adapt) VT<T>::stT(vhp + pt0, vh);
       d_w2 += (double)a_w2; d_hv += (double)a_hv; d_hh += (double)a_hh; d_vh += (double)a_vh;
       d_gv += (double)a_gv; d_gg += (double)a_gg; d_vv += (double)a_vv; d_fn += (double)a_fn;
       d_s2 += (double)a_s2;
     }
-    if (win) {   // warp-aggregated append of the window's keys (one global atomic per warp)
-      const int cnt = __popc(wmsk);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int tot = __shfl_sync(0xffffffffu, incl, 31);
-      unsigned base_ = 0u;
-      if (lane == 31 && tot > 0) base_ = atomicAdd(&Jw->cand_n, (unsigned)tot);
-      base_ = __shfl_sync(0xffffffffu, base_, 31);
-      unsigned pos = base_ + (unsigned)(incl - cnt);
-#pragma unroll
-      for (int e = 0; e < W; ++e)
-        if (wmsk & (1u << e)) wcand[pos++] = wkey[e];
-    }
     __syncthreads();   // stage s is refilled by the issue of tile t + 2
   }
   const int base = i * NSLOT;
   if (w2) warp_acc(acc, nv, base + SLOT_W2, d_w2);
-  if (win) {
-    warp_acc(acc, nv, base + SLOT_CHI, d_chi);
-    warp_acc(acc, nv, base + SLOT_SHI, d_shi);
-    warp_acc(acc, nv, base + SLOT_CW, d_cw);
-    warp_acc(acc, nv, base + SLOT_SW, d_sw);
-  }
   if (dots) {
     warp_acc(acc, nv, base + SLOT_HV, d_hv);
     warp_acc(acc, nv, base + SLOT_HH, d_hh);
@@ -426,32 +380,6 @@ __device__ inline void fin_pass1(const Prob<T>& P, Ctrl& C, const double* stage)
       else if (n < C.sig_lo[i]) fct = C.sig_lo[i] / n;
       C.ann_scale[i] = fct;
       C.ann_zero[i] = z;
-    }
-    // warm-started threshold search: keep the window if the new threshold is
-    // inside it (f(theta_lo) >= sigma > f(theta_hi) for l1, C_hi < k <= C_hi +
-    // C_win for cardinality), else search all of w (the rounds' fallback)
-    for (int i = 0; i < P.P; ++i) {
-      const SetD<T>& S = P.set[i];
-      if (!S.global || S.job < 0 || sizeof(T) != 4) continue;
-      Job& J = C.job[S.job];
-      if (J.win_hi == 0u || J.mode != JM_SEARCH) continue;
-      const double chi = stage[i * NSLOT + SLOT_CHI], shi = stage[i * NSLOT + SLOT_SHI];
-      const double cw = stage[i * NSLOT + SLOT_CW], sw = stage[i * NSLOT + SLOT_SW];
-      bool ok;
-      if (J.kind == K_L1) {
-        const double tlo = (double)__uint_as_float(J.win_lo), thi = (double)__uint_as_float(J.win_hi);
-        ok = ((shi + sw) - tlo * (chi + cw) >= J.sigma) && (shi - thi * chi < J.sigma);
-      } else {
-        ok = (chi < (double)J.k) && ((double)J.k <= chi + cw);
-      }
-      if (ok) {
-        J.win = 1;
-        J.cnt_above = (long long)chi;
-        J.sum_above = shi;
-      } else {
-        J.win = 0;
-        J.cand_n = 0u;
-      }
     }
   }
 }

@@ -637,7 +637,6 @@ struct Engine : EngineBase {
     c.hist_head = 0; c.hist_count = 1; c.breakdown = 0; c.numeric_err = 0; c.zero_x = 0;
     c.cg_j = 0; c.cg_active = 0; c.cg_count = 0; c.cg_total = 0;
     c.P = P; c.p = p;
-    for (int jb = 0; jb < MAXJOBS; ++jb) c.hint[jb] = 0.0f;   // no warm start across solves
     c.opt.n_cg = o.n_cg; c.opt.eq25 = o.eq25; c.opt.fixed_work = o.fixed_work;
     c.opt.adapt_every = o.adapt_every; c.opt.check_every = o.check_every; c.opt.max_iter = max_iter;
     c.opt.eps_evol = eps_evol; c.opt.eps_feas = eps_feas; c.opt.eps_corr = o.eps_corr;
@@ -1593,7 +1592,6 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     const int i = J.set;
     J.round = 0; J.prefix = 0; J.cnt_above = 0; J.sum_above = 0; J.theta = 0; J.tau = 0;
     J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0; J.cand_n = 0;
-    J.win = 0; J.win_lo = J.win_hi = 0u;
     J.sigma = c.sigma[i]; J.k = c.kcard[i];
     J.mode = (J.on_s || i != set_id) ? JM_OFF : JM_SEARCH;
     if (J.mode == JM_SEARCH && J.kind == K_CARD) {
