@@ -63,7 +63,7 @@ struct Geo {
   int64_t ld;            // element stride between blocks of a multi-block field
   double ihz, ihy, ihx;  // 1/h (reading L2)
   int kh, kw;            // blur kernel size (0 if none)
-  FastDiv dplane, dnx;
+  FastDiv dplane, dnx, dny;
   const uint8_t* mask;   // blur observation mask (N, local) or null
 };
 

@@ -66,6 +66,7 @@ struct Prob {
   int nranks, rank;
   double* xg;
   int xslot;
+  FastDiv dncr;                   // division by the chunks per x row (lean CG kernels)
 };
 
 __device__ __forceinline__ bool is_adapt_it(int k, int every) {

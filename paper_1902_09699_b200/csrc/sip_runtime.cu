@@ -120,6 +120,7 @@ struct Engine : EngineBase {
   // launch geometry
   int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1, g_p1 = 1, g_p1a = 1;
   int npr = 0;                   // allocated slots of the p ring (Prob::pr)
+  int g_cgf = 1;                 // grid of the lean CG kernels
   bool vec = false;
   ZGeo zg{};                     // z-marching CG geometry (sip_zmarch.cuh)
   SGeo sg{};                     // staged z-marching CG geometry (sip_cgs.cuh)
@@ -188,6 +189,8 @@ struct Engine : EngineBase {
     g.ihz = 1.0 / h[0]; g.ihy = 1.0 / h[1]; g.ihx = 1.0 / h[2];
     g.dplane.init((uint32_t)g.plane);
     g.dnx.init((uint32_t)g.nx);
+    g.dny.init((uint32_t)g.ny);
+    Pr.dncr.init((uint32_t)std::max(1, g.nx / VT<T>::W));
     Pr.P = P; Pr.p = p;
     Pr.nranks = nranks; Pr.rank = rank;
     Pr.rounds = KeyT<T>::ROUNDS;
@@ -270,6 +273,7 @@ struct Engine : EngineBase {
     constexpr int W = VT<T>::W;
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
+    g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));   // 4 CTAs / SM resident
     // z-marching CG: 3D grids whose rows split into whole warps of W-chunks
     zg.on = 0;
     if (vec && ndim == 3 && g.nx % (32 * W) == 0 && !getenv("SIP_NO_ZMARCH")) {
@@ -345,7 +349,7 @@ struct Engine : EngineBase {
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
     const int gz_ = std::max(zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1,
                              sg.on ? sg.tiles_x * sg.tiles_y * sg.nzc : 1);
-    const int gmax = std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1);
+    const int gmax = std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf);
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -512,8 +516,14 @@ struct Engine : EngineBase {
     else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
+  // lean flat CG kernels (sip_vec.cuh k_cg1f / k_cg2f); SIP_OLD_CG=1 keeps the
+  // z-marching / shuffle kernels for A/B measurements
+  bool lean_cg() const { return vec && !getenv("SIP_OLD_CG"); }
   void launch_cg1(int j) {
-    if (sg.on) {
+    if (lean_cg() && !sg.on) {
+      if (ndim == 3) k_cg1f<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+      else k_cg1f<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+    } else if (sg.on) {
       k_cg1s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s1, stream>>>(Pr, sg, j);
     } else if (zg.on) {
       // measured on C4: z-marching wins for k_cg1 (operand recomputed from
@@ -527,7 +537,10 @@ struct Engine : EngineBase {
     ++launches;
   }
   void launch_cg2(int j) {
-    if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
+    if (lean_cg() && !sg.on && Pr.defer_x) {
+      if (ndim == 3) k_cg2f<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+      else k_cg2f<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+    } else if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
     else if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
     else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
     ++launches;

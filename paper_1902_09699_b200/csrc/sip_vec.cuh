@@ -409,4 +409,181 @@ __global__ void __launch_bounds__(BLOCK) k_cgx(const __grid_constant__ Prob<T> P
   }
 }
 
+// ------------------------------------------------------------ lean flat CG
+// One thread per chunk, grid-stride.  C p at the chunk is written in
+// diagonal form, q = d p0 - sum_n c_n p_n over the present neighbours
+// (Eq. 23; the boundary rows of D'D drop a neighbour together with its
+// diagonal share, reading L3), with the neighbour masks folded into the
+// coefficients once per chunk: no per-element predicates, no shuffles.
+template <class T>
+struct CGLoc {   // chunk location and its masked coefficients
+  T d0, d1, dW, czl, czh, cyl, cyh, cxl, cxh, cx;
+  __device__ __forceinline__ CGLoc(const Geo& g, const CoefT<T>& k, int c, int ncr, const FastDiv& dncr) {
+    const int row = (int)dncr.div((uint32_t)c);
+    const int xc = c - row * ncr;
+    const int iz = g.ny > 1 ? (int)g.dny.div((uint32_t)row) : row;
+    const int iy = row - iz * g.ny;
+    const int gz = iz + g.z0;
+    czl = gz >= 1 ? k.cz : (T)0;
+    czh = gz < g.nz_g - 1 ? k.cz : (T)0;
+    cyl = iy >= 1 ? k.cy : (T)0;
+    cyh = iy < g.ny - 1 ? k.cy : (T)0;
+    cx = k.cx;
+    cxl = xc > 0 ? k.cx : (T)0;
+    cxh = xc < ncr - 1 ? k.cx : (T)0;
+    const T dd = k.cI + czl + czh + cyl + cyh;
+    d0 = dd + cxl + cx;
+    d1 = dd + cx + cx;
+    dW = dd + cx + cxh;
+  }
+  template <int W>
+  __device__ __forceinline__ void apply(const T* cur, const T* zm, const T* zp, const T* ym, const T* yp, T xl,
+                                        T xr, bool hy, T* q) const {
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      const T de = e == 0 ? d0 : (e == W - 1 ? dW : d1);
+      T v = de * cur[e] - czl * zm[e] - czh * zp[e];
+      if (hy) v = v - cyl * ym[e] - cyh * yp[e];
+      const T left = e > 0 ? cur[e - 1] : xl;
+      const T right = e < W - 1 ? cur[e + 1] : xr;
+      v = v - (e == 0 ? cxl : cx) * left - (e == W - 1 ? cxh : cx) * right;
+      q[e] = v;
+    }
+  }
+};
+
+template <class T>
+__device__ __forceinline__ CoefT<T> coefs_present(const Prob<T>& P, const Ctrl& C) {
+  CoefT<T> k(C);
+  if (!P.has[PRIM_Z]) k.cz = (T)0;
+  if (!P.has[PRIM_Y] || P.g.ny == 1) k.cy = (T)0;
+  if (!P.has[PRIM_X]) k.cx = (T)0;
+  return k;
+}
+
+// k_cg1f(j): p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j>; p_j -> slot j
+template <class T, bool HY>
+__global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
+  constexpr int W = VT<T>::W;
+  Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  const Geo& g = P.g;
+  const int nch = g.N / W;
+  if (j == 0 && C.zero_x) {   // b = 0 gives x = 0
+    for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
+      T z[W] = {};
+      VT<T>::stT(P.x + c * W, z);
+    }
+    return;
+  }
+  if (!C.cg_active) return;
+  __shared__ double sh[NWARP + 1];
+  __shared__ double out[1];
+  const CoefT<T> k = coefs_present(P, C);
+  const T beta = (T)C.beta;
+  const bool usep = j > 0;
+  const T* r = P.r;
+  const T* po = usep ? p_slot(P, j - 1) : P.r;
+  T* pw = p_slot(P, j);
+  const int ncr = g.nx / W;
+  FastDiv dncr;
+  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
+  const int pl = g.plane, nx = g.nx;
+  double pq = 0.0;
+  for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
+    const int pt0 = c * W;
+    const CGLoc<T> L(g, k, c, ncr, dncr);
+    T a0[W], a1[W], a2[W], a3[W], a4[W], b0[W], b1[W], b2[W], b3[W], b4[W];
+    VT<T>::ldT(r + pt0, a0);
+    VT<T>::ldT(r + pt0 - pl, a1);
+    VT<T>::ldT(r + pt0 + pl, a2);
+    if (HY) { VT<T>::ldT(r + pt0 - nx, a3); VT<T>::ldT(r + pt0 + nx, a4); }
+    T rl = r[pt0 - 1], rr_ = r[pt0 + W];
+    if (usep) {
+      VT<T>::ldT(po + pt0, b0);
+      VT<T>::ldT(po + pt0 - pl, b1);
+      VT<T>::ldT(po + pt0 + pl, b2);
+      if (HY) { VT<T>::ldT(po + pt0 - nx, b3); VT<T>::ldT(po + pt0 + nx, b4); }
+      const T bl = po[pt0 - 1], br = po[pt0 + W];
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        a0[e] = a0[e] + beta * b0[e];
+        a1[e] = a1[e] + beta * b1[e];
+        a2[e] = a2[e] + beta * b2[e];
+        if (HY) { a3[e] = a3[e] + beta * b3[e]; a4[e] = a4[e] + beta * b4[e]; }
+      }
+      rl = rl + beta * bl;
+      rr_ = rr_ + beta * br;
+    }
+    T q[W];
+    L.template apply<W>(a0, a1, a2, a3, a4, rl, rr_, HY, q);
+    VT<T>::stT(pw + pt0, a0);
+    T s = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) s += a0[e] * q[e];
+    pq += (double)s;
+  }
+  pq = block_sum(pq, sh);
+  if (threadIdx.x == 0) P.partials[blockIdx.x] = pq;
+  if (last_block(P.counter)) {
+    reduce_partials(P.partials, 1, out, sh);
+    if (threadIdx.x == 0) {
+      *P.counter = 0u;
+      if (P.nranks > 1) publish(P, out, 1, 0, 1);
+      else fin_cg1(C, out, j);
+    }
+  }
+}
+
+// k_cg2f(j): r -= alpha C p_j and <r, r> (the x update is deferred to k_cgx)
+template <class T, bool HY>
+__global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
+  constexpr int W = VT<T>::W;
+  Ctrl& C = *P.ctrl;
+  if (C.stopped || !C.cg_active) return;
+  __shared__ double sh[NWARP + 1];
+  __shared__ double out[1];
+  const Geo& g = P.g;
+  const int nch = g.N / W;
+  const CoefT<T> k = coefs_present(P, C);
+  const T alpha = (T)C.alpha;
+  const T* p = p_slot(P, j);
+  const int ncr = g.nx / W;
+  FastDiv dncr;
+  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
+  const int pl = g.plane, nx = g.nx;
+  double rr = 0.0;
+  for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
+    const int pt0 = c * W;
+    const CGLoc<T> L(g, k, c, ncr, dncr);
+    T a0[W], a1[W], a2[W], a3[W], a4[W], rv[W];
+    VT<T>::ldT(p + pt0, a0);
+    VT<T>::ldT(p + pt0 - pl, a1);
+    VT<T>::ldT(p + pt0 + pl, a2);
+    if (HY) { VT<T>::ldT(p + pt0 - nx, a3); VT<T>::ldT(p + pt0 + nx, a4); }
+    const T xl = p[pt0 - 1], xr = p[pt0 + W];
+    VT<T>::ldcs(P.r + pt0, rv);
+    T q[W];
+    L.template apply<W>(a0, a1, a2, a3, a4, xl, xr, HY, q);
+    T s = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      rv[e] = rv[e] - alpha * q[e];
+      s += rv[e] * rv[e];
+    }
+    VT<T>::stT(P.r + pt0, rv);
+    rr += (double)s;
+  }
+  rr = block_sum(rr, sh);
+  if (threadIdx.x == 0) P.partials[blockIdx.x] = rr;
+  if (last_block(P.counter)) {
+    reduce_partials(P.partials, 1, out, sh);
+    if (threadIdx.x == 0) {
+      *P.counter = 0u;
+      if (P.nranks > 1) publish(P, out, 1, 0, 1);
+      else fin_cg2(C, out, j);
+    }
+  }
+}
+
 }  // namespace sip
