@@ -191,6 +191,7 @@ struct Engine : EngineBase {
     g.dnx.init((uint32_t)g.nx);
     g.dny.init((uint32_t)g.ny);
     Pr.dncr.init((uint32_t)std::max(1, g.nx / VT<T>::W));
+    Pr.sel_match = getenv("SIP_SEL_MATCH") ? 1 : 0;
     Pr.P = P; Pr.p = p;
     Pr.nranks = nranks; Pr.rank = rank;
     Pr.rounds = KeyT<T>::ROUNDS;
