@@ -416,44 +416,13 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
           VT<T>::ldT(buf + (int64_t)bl * g.ld + (int64_t)(qq - bl * nch) * W, v[u]);
         }
         unsigned mine = 0;   // survivors of this thread (bit u*W+e)
-        if (sizeof(T) == 4 && P.sel_match) {
-          // warp aggregation: one shared atomic per distinct digit per warp
-          // slot; the warp's significand sum (<= 32 * 2^24) fits in 32 bits
-          const int lane = threadIdx.x & 31;
 #pragma unroll
-          for (int u = 0; u < SEL_U; ++u) {
+        for (int u = 0; u < SEL_U; ++u) {
 #pragma unroll
-            for (int e = 0; e < W; ++e) {
-              const U key = K::key(v[u][e]);
-              const bool in = ok[u] && (round == 1 || (U)(key >> plo) == prefix);
-              const int d = in ? (int)((key >> lo) & dmask) : -1;
-              const unsigned peers = __match_any_sync(0xffffffffu, d);
-              unsigned sg = 0u;
-              if (sums) {
-                const uint32_t k32 = (uint32_t)key;
-                const uint32_t ex = k32 >> 23;
-                sg = in ? ((ex ? (1u << 23) : 0u) | (k32 & 0x7fffffu)) : 0u;
-                sg = __reduce_add_sync(peers, sg);
-              }
-              if (in && lane == __ffs(peers) - 1) {
-                atomicAdd(&h_cnt[d], (unsigned)__popc(peers));
-                if (sums) {
-                  atomicAdd(&h_l[0][d], sg & 0xffffu);
-                  if (sg >> 16) atomicAdd(&h_l[1][d], sg >> 16);
-                }
-              }
-              if (in) mine |= 1u << (u * W + e);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < SEL_U; ++u) {
-#pragma unroll
-            for (int e = 0; e < W; ++e) {
-              const U key = K::key(v[u][e]);
-              const bool in = ok[u] && (round == 1 || (U)(key >> plo) == prefix);
-              if (in) { hkey(key); mine |= 1u << (u * W + e); }
-            }
+          for (int e = 0; e < W; ++e) {
+            const U key = K::key(v[u][e]);
+            const bool in = ok[u] && (round == 1 || (U)(key >> plo) == prefix);
+            if (in) { hkey(key); mine |= 1u << (u * W + e); }
           }
         }
         if (make_cand) {   // CTA-aggregated append: one global atomic per CTA iteration

@@ -67,7 +67,6 @@ struct Prob {
   double* xg;
   int xslot;
   FastDiv dncr;                   // division by the chunks per x row (lean CG kernels)
-  int sel_match;                  // radix histogram: warp-aggregated by __match_any_sync (fp32)
 };
 
 __device__ __forceinline__ bool is_adapt_it(int k, int every) {

@@ -20,6 +20,7 @@
 #include "sip_aux_kernels.cuh"
 #include "sip_team.cuh"
 #include "sip_cgs.cuh"
+#include "sip_cgt.cuh"
 
 using namespace sip;
 
@@ -121,6 +122,8 @@ struct Engine : EngineBase {
   int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1, g_p1 = 1, g_p1a = 1;
   int npr = 0;                   // allocated slots of the p ring (Prob::pr)
   int g_cgf = 1;                 // grid of the lean CG kernels
+  int g_cgt1 = 0, g_cgt2 = 0;    // grids of the tile-staged CG kernels (0: unused)
+  size_t smem_t1 = 0, smem_t2 = 0;
   bool vec = false;
   ZGeo zg{};                     // z-marching CG geometry (sip_zmarch.cuh)
   SGeo sg{};                     // staged z-marching CG geometry (sip_cgs.cuh)
@@ -191,7 +194,6 @@ struct Engine : EngineBase {
     g.dnx.init((uint32_t)g.nx);
     g.dny.init((uint32_t)g.ny);
     Pr.dncr.init((uint32_t)std::max(1, g.nx / VT<T>::W));
-    Pr.sel_match = getenv("SIP_SEL_MATCH") ? 1 : 0;
     Pr.P = P; Pr.p = p;
     Pr.nranks = nranks; Pr.rank = rank;
     Pr.rounds = KeyT<T>::ROUNDS;
@@ -331,6 +333,30 @@ struct Engine : EngineBase {
         }
       }
     }
+    // tile-staged flat CG (sip_cgt.cuh): one wave of resident CTAs
+    g_cgt1 = g_cgt2 = 0;
+    if (vec) {
+      const bool hy = ndim == 3;
+      smem_t1 = cgt_smem<T>(g.nx, hy, true);
+      smem_t2 = cgt_smem<T>(g.nx, hy, false);
+      if (smem_t1 <= 200 * 1024 && (!hy || g.plane >= g.nx + W)) {
+        int o1 = 0, o2 = 0;
+        if (hy) {
+          CU(cudaFuncSetAttribute(k_cg1t<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          CU(cudaFuncSetAttribute(k_cg2t<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cg1t<T, true>, BLOCK, smem_t1));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cg2t<T, true>, BLOCK, smem_t2));
+        } else {
+          CU(cudaFuncSetAttribute(k_cg1t<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          CU(cudaFuncSetAttribute(k_cg2t<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cg1t<T, false>, BLOCK, smem_t1));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cg2t<T, false>, BLOCK, smem_t2));
+        }
+        const int tiles = (g.N / W + BLOCK - 1) / BLOCK;
+        g_cgt1 = std::max(1, std::min(tiles, nsm * std::max(1, o1)));
+        g_cgt2 = std::max(1, std::min(tiles, nsm * std::max(1, o2)));
+      }
+    }
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
     smem_p1v = pass1_smem(P, false);                   // k_pass1t: slots + bulk-copy stages
@@ -350,7 +376,8 @@ struct Engine : EngineBase {
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
     const int gz_ = std::max(zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1,
                              sg.on ? sg.tiles_x * sg.tiles_y * sg.nzc : 1);
-    const int gmax = std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf);
+    const int gmax = std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
+                              std::max(g_cgt1, g_cgt2));
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -520,8 +547,13 @@ struct Engine : EngineBase {
   // lean flat CG kernels (sip_vec.cuh k_cg1f / k_cg2f); SIP_OLD_CG=1 keeps the
   // z-marching / shuffle kernels for A/B measurements
   bool lean_cg() const { return vec && !getenv("SIP_OLD_CG"); }
+  bool tiled_cg() const { return lean_cg() && !sg.on && g_cgt1 > 0 && !getenv("SIP_CGF"); }
   void launch_cg1(int j) {
-    if (lean_cg() && !sg.on) {
+    if (tiled_cg()) {
+      const bool hy = ndim == 3;
+      if (hy) k_cg1t<T, true><<<g_cgt1, BLOCK, smem_t1, stream>>>(Pr, j);
+      else k_cg1t<T, false><<<g_cgt1, BLOCK, smem_t1, stream>>>(Pr, j);
+    } else if (lean_cg() && !sg.on) {
       if (ndim == 3) k_cg1f<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
       else k_cg1f<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
     } else if (sg.on) {
@@ -538,7 +570,10 @@ struct Engine : EngineBase {
     ++launches;
   }
   void launch_cg2(int j) {
-    if (lean_cg() && !sg.on && Pr.defer_x) {
+    if (tiled_cg() && Pr.defer_x) {
+      if (ndim == 3) k_cg2t<T, true><<<g_cgt2, BLOCK, smem_t2, stream>>>(Pr, j);
+      else k_cg2t<T, false><<<g_cgt2, BLOCK, smem_t2, stream>>>(Pr, j);
+    } else if (lean_cg() && !sg.on && Pr.defer_x) {
       if (ndim == 3) k_cg2f<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
       else k_cg2f<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
     } else if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
