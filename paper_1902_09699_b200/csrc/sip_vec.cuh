@@ -410,43 +410,38 @@ __global__ void __launch_bounds__(BLOCK) k_cgx(const __grid_constant__ Prob<T> P
 }
 
 // ------------------------------------------------------------ lean flat CG
-// One thread per chunk, grid-stride.  C p at the chunk is written in
-// diagonal form, q = d p0 - sum_n c_n p_n over the present neighbours
-// (Eq. 23; the boundary rows of D'D drop a neighbour together with its
-// diagonal share, reading L3), with the neighbour masks folded into the
-// coefficients once per chunk: no per-element predicates, no shuffles.
+// One thread per chunk, grid-stride, no shuffles.  C p at the chunk in the
+// difference form of apply_C_vec / zapply: per axis a = (p0 - m) - (n - p0)
+// with an absent neighbour replaced by p0 (its difference is exactly 0), so
+// no large terms cancel (fp32 fields of ~10^3 keep their digits); the masks
+// are computed once per chunk.
 template <class T>
-struct CGLoc {   // chunk location and its masked coefficients
-  T d0, d1, dW, czl, czh, cyl, cyh, cxl, cxh, cx;
+struct CGLoc {   // chunk location: which neighbours exist
+  bool zlo, zhi, ylo, yhi, xlo, xhi;
+  T cI, cz, cy, cx;
   __device__ __forceinline__ CGLoc(const Geo& g, const CoefT<T>& k, int c, int ncr, const FastDiv& dncr) {
     const int row = (int)dncr.div((uint32_t)c);
     const int xc = c - row * ncr;
     const int iz = g.ny > 1 ? (int)g.dny.div((uint32_t)row) : row;
     const int iy = row - iz * g.ny;
     const int gz = iz + g.z0;
-    czl = gz >= 1 ? k.cz : (T)0;
-    czh = gz < g.nz_g - 1 ? k.cz : (T)0;
-    cyl = iy >= 1 ? k.cy : (T)0;
-    cyh = iy < g.ny - 1 ? k.cy : (T)0;
-    cx = k.cx;
-    cxl = xc > 0 ? k.cx : (T)0;
-    cxh = xc < ncr - 1 ? k.cx : (T)0;
-    const T dd = k.cI + czl + czh + cyl + cyh;
-    d0 = dd + cxl + cx;
-    d1 = dd + cx + cx;
-    dW = dd + cx + cxh;
+    zlo = gz >= 1; zhi = gz < g.nz_g - 1;
+    ylo = iy >= 1; yhi = iy < g.ny - 1;
+    xlo = xc > 0; xhi = xc < ncr - 1;
+    cI = k.cI; cz = k.cz; cy = k.cy; cx = k.cx;
   }
   template <int W>
   __device__ __forceinline__ void apply(const T* cur, const T* zm, const T* zp, const T* ym, const T* yp, T xl,
                                         T xr, bool hy, T* q) const {
 #pragma unroll
     for (int e = 0; e < W; ++e) {
-      const T de = e == 0 ? d0 : (e == W - 1 ? dW : d1);
-      T v = de * cur[e] - czl * zm[e] - czh * zp[e];
-      if (hy) v = v - cyl * ym[e] - cyh * yp[e];
-      const T left = e > 0 ? cur[e - 1] : xl;
-      const T right = e < W - 1 ? cur[e + 1] : xr;
-      v = v - (e == 0 ? cxl : cx) * left - (e == W - 1 ? cxh : cx) * right;
+      const T p0 = cur[e];
+      T v = cI * p0;
+      v += cz * ((p0 - (zlo ? zm[e] : p0)) - ((zhi ? zp[e] : p0) - p0));
+      if (hy) v += cy * ((p0 - (ylo ? ym[e] : p0)) - ((yhi ? yp[e] : p0) - p0));
+      const T left = e > 0 ? cur[e - 1] : (xlo ? xl : p0);
+      const T right = e < W - 1 ? cur[e + 1] : (xhi ? xr : p0);
+      v += cx * ((p0 - left) - (right - p0));
       q[e] = v;
     }
   }
