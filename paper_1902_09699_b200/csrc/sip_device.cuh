@@ -125,6 +125,8 @@ struct Job {
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
   unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
+  unsigned cut;                  // round 1 histograms only keys >= cut (warm start; 0: all)
+  int cutfail;                   // the cut was too high: round 1 is redone on all keys (pass 1)
 };
 
 struct Ctrl {
@@ -155,6 +157,7 @@ struct Ctrl {
   Opts opt;
   Job job[MAXJOBS];
   int njobs;
+  float hint[MAXJOBS];           // last resolved threshold per job (0: none), warm start of the cut
   // log
   int* log_cg; int* log_branch; double* log_rho; double* log_gamma;
   double* log_feas; double* log_evol;
@@ -262,9 +265,31 @@ __device__ inline bool last_block(unsigned* counter) {
 // barrier per value, so a wide reduction (pass 1: up to 159 values) costs a
 // few L2 round trips instead of one barrier-separated phase per value.
 __device__ inline void reduce_partials(const double* partials, int nv, double* out, double* sh) {
-  (void)sh;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nb = (int)gridDim.x;
+  if (nv <= 2) {
+    // one or two values (the CG scalars): all warps split the CTAs, then the
+    // NWARP warp sums are added in order -- one L2 round trip per lane
+    __shared__ double ws[2][NWARP];
+    const int per = (nb + NWARP - 1) / NWARP;
+    const int b0 = w * per, b1 = min(nb, b0 + per);
+    for (int v = 0; v < nv; ++v) {
+      double a = 0.0;
+#pragma unroll 4
+      for (int b = b0 + lane; b < b1; b += 32) a += __ldcg(partials + (size_t)b * nv + v);
+      a = warp_sum(a);
+      if (lane == 0) ws[v][w] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < nv) {
+      double t = 0.0;
+      for (int i = 0; i < NWARP; ++i) t += ws[threadIdx.x][i];
+      out[threadIdx.x] = t;
+    }
+    __syncthreads();
+    return;
+  }
+  (void)sh;
   for (int v = w; v < nv; v += NWARP) {
     double a = 0.0;
 #pragma unroll 4

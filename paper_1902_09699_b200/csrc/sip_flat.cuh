@@ -294,7 +294,8 @@ __device__ inline void publish_hist(const Prob<T>& P, int jb, const unsigned* gc
 }
 
 template <class T>
-__global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<T> P, int round) {
+// pass 1 (round 1 only): redo round 1 on all keys for the jobs whose cut failed
+__global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<T> P, int round, int pass) {
   using K = KeyT<T>;
   using U = typename K::U;
   using LB = Limbs<T>;
@@ -303,8 +304,6 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
   if (C.stopped) return;
   __shared__ unsigned h_cnt[NBUCK];
   __shared__ unsigned h_l[LB::N][NBUCK];
-  __shared__ int s_wc[NWARP];
-  __shared__ unsigned s_base;
   const Geo& g = P.g;
   const bool check = (C.k % C.opt.check_every) == 0;
   int lo, nb, plo = 0, pnb = 0;
@@ -317,7 +316,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
   for (int jb = 0; jb < C.njobs; ++jb) {
     const Job& J = C.job[jb];
     if (J.mode != JM_SEARCH || J.round != round - 1 || (J.on_s && !check)) continue;
+    if (pass == 1 && !J.cutfail) continue;
     any = true;
+    const U cut = (round == 1 && pass == 0) ? (U)J.cut : (U)0;
     unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
     unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
     unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
@@ -421,22 +422,28 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
 #pragma unroll
           for (int e = 0; e < W; ++e) {
             const U key = K::key(v[u][e]);
-            const bool in = ok[u] && (round == 1 || (U)(key >> plo) == prefix);
+            const bool in = ok[u] && (round == 1 ? key >= cut : (U)(key >> plo) == prefix);
             if (in) { hkey(key); mine |= 1u << (u * W + e); }
           }
         }
-        if (make_cand) {   // CTA-aggregated append: one global atomic per CTA iteration
+        if (make_cand) {   // warp-aggregated append: one global atomic per warp, no block barrier
+          const int lane = threadIdx.x & 31;
           const int cnt = __popc(mine);
-          const int before = block_excl_count(cnt, s_wc);
-          if (threadIdx.x == BLOCK - 1) s_base = atomicAdd(&C.job[jb].cand_n, (unsigned)(before + cnt));
-          __syncthreads();
-          unsigned pos = s_base + before;
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t_ = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t_;
+          }
+          const int tot = __shfl_sync(0xffffffffu, incl, 31);
+          unsigned base_ = 0u;
+          if (lane == 31 && tot > 0) base_ = atomicAdd(&C.job[jb].cand_n, (unsigned)tot);
+          unsigned pos = __shfl_sync(0xffffffffu, base_, 31) + (unsigned)(incl - cnt);
 #pragma unroll
           for (int u = 0; u < SEL_U; ++u)
 #pragma unroll
             for (int e = 0; e < W; ++e)
               if (mine & (1u << (u * W + e))) cand[pos++] = (unsigned)K::key(v[u][e]);
-          __syncthreads();
         }
       }
       hflush();
@@ -449,6 +456,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     for (int jb = 0; jb < C.njobs; ++jb) {
       Job& J = C.job[jb];
       if (J.mode != JM_SEARCH || J.round != round - 1 || (J.on_s && !check)) continue;
+      if (pass == 1 && !J.cutfail) continue;
+      if (pass == 1 && P.nranks == 1 && threadIdx.x == 0) { J.cut = 0u; J.cutfail = 0; }   // k_fin's, else
+      __syncthreads();
       unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
       unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
       unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;

@@ -669,7 +669,15 @@ __device__ void resolve_round(const Prob<T>& P, Job& J, int round, const unsigne
     s_sab = sm;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && round == 1 && J.cut != 0u) {
+    // a cut round 1 is conclusive only if its digit lies strictly above the
+    // cut's bucket (all keys >= that edge were counted) and, for l1, the
+    // ball is active (the skipped keys could hold the rest of ||w||_1)
+    const int dcut = (int)((U)J.cut >> lo);
+    if (dstar <= dcut || (J.kind == K_L1 && s_stot <= J.sigma)) J.cutfail = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && !J.cutfail) {
     if (J.kind == K_L1 && round == 1 && s_stot <= J.sigma) {
       J.mode = JM_INSIDE;          // ||w||_1 <= sigma: w is in the ball (L5)
     } else if (J.kind == K_L1 && round == 1 && J.sigma <= 0.0) {
@@ -1024,6 +1032,11 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
     Job& J = C.job[jb];
     const int i = J.set;
     J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u;
+    // warm start (fp32 jobs on w): keys below half the last threshold cannot
+    // decide the new one unless it fell by more than 2x; round 1 skips them
+    // and falls back to all keys when its digit lands at or below the cut
+    J.cutfail = 0;
+    J.cut = (sizeof(T) == 4 && !J.on_s && C.hint[jb] > 0.0f) ? __float_as_uint(0.5f * C.hint[jb]) : 0u;
     J.theta = 0.0; J.tau = 0ull; J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0.0;
     J.sigma = C.sigma[i];
     J.k = C.kcard[i];
@@ -1134,6 +1147,12 @@ __global__ void k_control(const __grid_constant__ Prob<T> P) {
     }
   for (int i = 0; i < Pn; ++i)
     for (int q = 0; q < NSLOT; ++q) C.sums[i][q] = 0.0;
+  for (int jb = 0; jb < C.njobs; ++jb) {   // the next iteration's warm start
+    const Job& J = C.job[jb];
+    float h = 0.0f;
+    if (J.mode == JM_DONE) h = J.kind == K_L1 ? (float)J.theta : __uint_as_float((unsigned)J.tau);
+    C.hint[jb] = (h > 0.0f && h < 1e30f) ? h : 0.0f;
+  }
   reset_jobs(P, C);
   C.k = k + 1;
   if (C.k > C.opt.max_iter) C.stopped = 1;
