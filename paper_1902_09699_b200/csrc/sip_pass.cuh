@@ -450,12 +450,19 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
   constexpr int W = VT<T>::W;
   const Geo& g = P.g;
   const SetD<T>& S = P.set[i];
-  const int prim = S.prim[bl];
   const int nch = g.N / W;
   const int c = lt * BLOCK + threadIdx.x;
   const bool valid = c < nch;
   const int pt0 = (valid ? c : nch - 1) * W;
-  const Loc L = locate(g, pt0);
+  const int prim = S.prim[bl];
+  bool padc, lastx;   // once per chunk (no per-element operator dispatch)
+  {
+    const int iz = (int)g.dplane.div((uint32_t)pt0);
+    const int r = pt0 - iz * g.plane;
+    const int iy = (int)g.dnx.div((uint32_t)r);
+    padc = prim == PRIM_Z ? (iz + g.z0 >= g.nz_g - 1) : (prim == PRIM_Y ? iy >= g.ny - 1 : false);
+    lastx = prim == PRIM_X && (r - iy * g.nx + W >= g.nx);
+  }
   const int64_t off = (int64_t)bl * g.ld + pt0;
   T wv[W], y0[W], v0[W];
   VT<T>::ldT(S.w + off, wv);
@@ -465,7 +472,7 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
   }
   bool pad[W];
 #pragma unroll
-  for (int e = 0; e < W; ++e) pad[e] = !valid || pad_vec(g, prim, L, e);
+  for (int e = 0; e < W; ++e) pad[e] = !valid || padc || (lastx && e == W - 1);
   T y[W];
   if (KIND == 0) {
     const Job& J = C.job[S.job];
@@ -556,7 +563,7 @@ __device__ inline void fin_pass2(const Prob<T>& P, Ctrl& C, const double* stage)
 }
 
 template <class T, int AD, int CK>
-__global__ void __launch_bounds__(BLOCK) k_pass2t(const __grid_constant__ Prob<T> P) {
+__global__ void __launch_bounds__(BLOCK, 4) k_pass2t(const __grid_constant__ Prob<T> P) {
   using K = KeyT<T>;
   using U = typename K::U;
   constexpr int W = VT<T>::W;

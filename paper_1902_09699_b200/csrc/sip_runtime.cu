@@ -540,7 +540,10 @@ struct Engine : EngineBase {
   // ---- phase launchers (one rank's part of each step) -------------------
   void launch_blur(int mode, int j) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, mode, j); ++launches; }
   void launch_rhs() {
-    if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
+    if (lean_cg()) {
+      if (ndim == 3) k_rhsf<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr);
+      else k_rhsf<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr);
+    } else if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
     else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
