@@ -121,7 +121,8 @@ struct Engine : EngineBase {
   // launch geometry
   int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1, g_p1 = 1, g_p1a = 1;
   int npr = 0;                   // allocated slots of the p ring (Prob::pr)
-  int g_cgf = 1;                 // grid of the lean CG kernels
+  int g_cgf = 1, g_cgf3 = 1;     // grids of the lean CG kernels (4 / 3 CTAs per SM)
+  bool u2 = false;               // lean CG unrolled by 2 (SIP_CG_U2)
   int g_cgt1 = 0, g_cgt2 = 0;    // grids of the tile-staged CG kernels (0: unused)
   size_t smem_t1 = 0, smem_t2 = 0;
   bool vec = false;
@@ -277,6 +278,8 @@ struct Engine : EngineBase {
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
     g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));   // 4 CTAs / SM resident
+    g_cgf3 = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 3));
+    u2 = getenv("SIP_CG_U2") != nullptr;
     // z-marching CG: 3D grids whose rows split into whole warps of W-chunks
     zg.on = 0;
     if (vec && ndim == 3 && g.nx % (32 * W) == 0 && !getenv("SIP_NO_ZMARCH")) {
@@ -557,8 +560,13 @@ struct Engine : EngineBase {
       if (hy) k_cg1t<T, true><<<g_cgt1, BLOCK, smem_t1, stream>>>(Pr, j);
       else k_cg1t<T, false><<<g_cgt1, BLOCK, smem_t1, stream>>>(Pr, j);
     } else if (lean_cg() && !sg.on) {
-      if (ndim == 3) k_cg1f<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
-      else k_cg1f<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+      if (u2) {
+        if (ndim == 3) k_cg1f<T, true, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
+        else k_cg1f<T, false, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
+      } else {
+        if (ndim == 3) k_cg1f<T, true, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+        else k_cg1f<T, false, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+      }
     } else if (sg.on) {
       k_cg1s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s1, stream>>>(Pr, sg, j);
     } else if (zg.on) {
@@ -577,8 +585,13 @@ struct Engine : EngineBase {
       if (ndim == 3) k_cg2t<T, true><<<g_cgt2, BLOCK, smem_t2, stream>>>(Pr, j);
       else k_cg2t<T, false><<<g_cgt2, BLOCK, smem_t2, stream>>>(Pr, j);
     } else if (lean_cg() && !sg.on && Pr.defer_x) {
-      if (ndim == 3) k_cg2f<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
-      else k_cg2f<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+      if (u2) {
+        if (ndim == 3) k_cg2f<T, true, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
+        else k_cg2f<T, false, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
+      } else {
+        if (ndim == 3) k_cg2f<T, true, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+        else k_cg2f<T, false, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+      }
     } else if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
     else if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
     else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);

