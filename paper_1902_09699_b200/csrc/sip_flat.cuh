@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
           const int q = q0 + u * BLOCK;
           ok[u] = q < tot;
           const int qq = ok[u] ? q : tot - 1;
-          const int bl = qq / nch;
+          const int bl = (qq >= nch) + (qq >= 2 * nch);   // nblk <= 3: no integer division
           VT<T>::ldT(buf + (int64_t)bl * g.ld + (int64_t)(qq - bl * nch) * W, v[u]);
         }
         unsigned mine = 0;   // survivors of this thread (bit u*W+e)
@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(BLOCK) k_pass2f(const __grid_constant__ Prob<T
       if (Js.mode == JM_DONE) {
         const int tot = S.nblk * nch;
         for (int q = blockIdx.x * BLOCK + threadIdx.x; q < tot; q += gridDim.x * BLOCK) {
-          const int bl = q / nch, c = q - bl * nch;
+          const int bl = (q >= nch) + (q >= 2 * nch), c = q - bl * nch;   // nblk <= 3
           T sv[W];
           VT<T>::ldT(S.s + (int64_t)bl * g.ld + (int64_t)c * W, sv);
 #pragma unroll

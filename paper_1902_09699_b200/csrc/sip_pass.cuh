@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_pass2t(const __grid_constant__ Pro
       if (Js.mode == JM_DONE) {
         const int tot = S.nblk * nch;
         for (int q = blockIdx.x * BLOCK + threadIdx.x; q < tot; q += gridDim.x * BLOCK) {
-          const int bl = q / nch, c = q - bl * nch;
+          const int bl = (q >= nch) + (q >= 2 * nch), c = q - bl * nch;   // nblk <= 3
           T sv[W];
           VT<T>::ldT(S.s + (int64_t)bl * g.ld + (int64_t)c * W, sv);
           T a2 = 0;
