@@ -121,6 +121,11 @@ struct Engine : EngineBase {
   // launch geometry
   int g_pts = 1, g_sel = 1, g_p2 = 1, g_small = 1, g_vec = 1, g_p1 = 1, g_p1a = 1;
   int npr = 0;                   // allocated slots of the p ring (Prob::pr)
+  bool l2_window = false;        // an L2 persisting window on r (set on the stream before capture)
+  cudaStreamAttrValue l2av;
+  void apply_l2_window() {
+    if (l2_window) CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &l2av));
+  }
   int g_cgf = 1, g_cgf3 = 1;     // grids of the lean CG kernels (4 / 3 CTAs per SM)
   bool u2 = false;               // lean CG unrolled by 2 (SIP_CG_U2)
   int g_cgt1 = 0, g_cgt2 = 0;    // grids of the tile-staged CG kernels (0: unused)
@@ -260,6 +265,32 @@ struct Engine : EngineBase {
     Pr.x = field(1);
     Pr.m = field(1);
     Pr.r = field(1);
+    // keep the CG residual r resident in L2 (persisting access window on the
+    // work stream): every CG step reads it (k_cg1 stencil) and reads + writes
+    // it (k_cg2); with r in L2 a step moves ~4N words from DRAM instead of 6N.
+    // The window is captured into the iteration graph's kernel nodes.
+    if (!getenv("SIP_NO_L2_PERSIST")) {
+      int maxp = 0, maxw = 0, dev = 0;
+      CU(cudaGetDevice(&dev));
+      CU(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+      CU(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+      const size_t rb = (size_t)g.ld * sizeof(T);
+      if (maxp > 0 && maxw > 0) {
+        size_t cur = 0;
+        CU(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+        const size_t want = std::min((size_t)maxp, rb);
+        if (cur < want) CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+        cudaStreamAttrValue av;
+        memset(&av, 0, sizeof(av));
+        av.accessPolicyWindow.base_ptr = (void*)(Pr.r - (size_t)GHOST * g.plane);
+        av.accessPolicyWindow.num_bytes = std::min(rb, (size_t)maxw);
+        av.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)want / (double)av.accessPolicyWindow.num_bytes);
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        l2av = av;
+        l2_window = true;
+      }
+    }
     Pr.pb[0] = field(1); Pr.pb[1] = field(1);
     Pr.pr[0] = Pr.pb[0]; Pr.pr[1] = Pr.pb[1];
     npr = 2;
@@ -671,6 +702,7 @@ struct Engine : EngineBase {
     long long before = launches;
     pev_used = 0;
     pkind.clear();
+    apply_l2_window();   // captured into the kernel nodes
     CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     // the adapt / check pattern repeats every lcm(2, check_every) iterations
     const int ce = std::max(1, hc.opt.check_every);
@@ -1128,6 +1160,7 @@ struct Team : EngineBase {
     const long long before = launches;
     eng[0]->pev_used = 0;
     eng[0]->pkind.clear();
+    eng[0]->apply_l2_window();
     CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     for (int i = 0; i < iters; ++i) enqueue_iteration(n_cg, i + 1);
     cudaError_t e = cudaStreamEndCapture(stream, &graph);
