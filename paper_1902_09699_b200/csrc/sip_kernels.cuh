@@ -53,8 +53,10 @@ struct Prob {
   // flattened segments (sip_flat.cuh): pass1 = x work + every (set, block);
   // pass2 = every (global set, block)
   int nseg1, nseg2;
-  // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32)
+  // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32);
+  // cand1[job]: keys whose round-1 digit lies in the warm-start window
   unsigned* cand[MAXJOBS];
+  unsigned* cand1[MAXJOBS];
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)
@@ -68,6 +70,13 @@ struct Prob {
   int xslot;
   FastDiv dncr;                   // division by the chunks per x row (lean CG kernels)
 };
+
+// after round 1 of a job: can round 2 read the window's compacted keys?
+// (exact: every key with the chosen digit is in the list iff the digit is
+// inside the window)
+__device__ inline void post_round1(Job& J) {
+  J.r2c = J.mode == JM_SEARCH && J.round == 1 && J.wlo >= 0 && (int)J.prefix >= J.wlo && (int)J.prefix <= J.whi;
+}
 
 __device__ __forceinline__ bool is_adapt_it(int k, int every) {
   return every <= 1 || (k % every) == 1;   // mod(k, update-frequency) = 1
@@ -1037,6 +1046,15 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
     // and falls back to all keys when its digit lands at or below the cut
     J.cutfail = 0;
     J.cut = (sizeof(T) == 4 && !J.on_s && C.hint[jb] > 0.0f) ? __float_as_uint(0.5f * C.hint[jb]) : 0u;
+    // ... and compacts the keys whose digit is within one of the last one's,
+    // so that round 2 usually reads a few percent of w (post_round1)
+    J.c1_n = 0u; J.r2c = 0;
+    J.wlo = J.whi = -1;
+    if (J.cut != 0u) {
+      const int hd = (int)(__float_as_uint(C.hint[jb]) >> 20);
+      J.wlo = max(0, hd - 1);
+      J.whi = min(NBUCK - 1, hd + 1);
+    }
     J.theta = 0.0; J.tau = 0ull; J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0.0;
     J.sigma = C.sigma[i];
     J.k = C.kcard[i];

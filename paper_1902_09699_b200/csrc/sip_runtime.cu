@@ -405,6 +405,8 @@ struct Engine : EngineBase {
         if (S.job < 0) continue;
         Pr.cand[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
         Pr.cand[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
+        Pr.cand1[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
+        Pr.cand1[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
       }
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
@@ -1702,6 +1704,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     J.round = 0; J.prefix = 0; J.cnt_above = 0; J.sum_above = 0; J.theta = 0; J.tau = 0;
     J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0; J.cand_n = 0;
     J.cut = 0u; J.cutfail = 0;
+    J.wlo = J.whi = -1; J.r2c = 0; J.c1_n = 0u;
     J.sigma = c.sigma[i]; J.k = c.kcard[i];
     J.mode = (J.on_s || i != set_id) ? JM_OFF : JM_SEARCH;
     if (J.mode == JM_SEARCH && J.kind == K_CARD) {

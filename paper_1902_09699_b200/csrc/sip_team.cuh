@@ -61,6 +61,7 @@ __device__ inline void fin_select(const Prob<T>& P, Ctrl& C, int round, int pass
     }
     __syncthreads();
     resolve_round<T>(P, J, round, gc, g0, g1);
+    if (round == 1 && threadIdx.x == 0) post_round1(J);
     __syncthreads();
     for (int d = threadIdx.x; d < NBUCK; d += BLOCK) { gc[d] = 0u; g0[d] = 0ull; g1[d] = 0ull; }
     __syncthreads();
