@@ -125,11 +125,6 @@ struct Job {
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
   unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
-  unsigned cut;                  // round 1 histograms only keys >= cut (warm start; 0: all)
-  int cutfail;                   // the cut was too high: round 1 is redone on all keys (pass 1)
-  int wlo, whi;                  // round-1 digit window around the last threshold's digit (-1: none)
-  int r2c;                       // round 2 reads the window's keys (the new digit is inside it)
-  unsigned c1_n;                 // keys compacted by round 1 (digit in [wlo, whi])
 };
 
 struct Ctrl {
@@ -160,7 +155,6 @@ struct Ctrl {
   Opts opt;
   Job job[MAXJOBS];
   int njobs;
-  float hint[MAXJOBS];           // last resolved threshold per job (0: none), warm start of the cut
   // log
   int* log_cg; int* log_branch; double* log_rho; double* log_gamma;
   double* log_feas; double* log_evol;

@@ -294,8 +294,7 @@ __device__ inline void publish_hist(const Prob<T>& P, int jb, const unsigned* gc
 }
 
 template <class T>
-// pass 1 (round 1 only): redo round 1 on all keys for the jobs whose cut failed
-__global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<T> P, int round, int pass) {
+__global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<T> P, int round) {
   using K = KeyT<T>;
   using U = typename K::U;
   using LB = Limbs<T>;
@@ -316,9 +315,7 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
   for (int jb = 0; jb < C.njobs; ++jb) {
     const Job& J = C.job[jb];
     if (J.mode != JM_SEARCH || J.round != round - 1 || (J.on_s && !check)) continue;
-    if (pass == 1 && !J.cutfail) continue;
     any = true;
-    const U cut = (round == 1 && pass == 0) ? (U)J.cut : (U)0;
     unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
     unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
     unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
@@ -360,14 +357,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     // fp32 candidate compaction: round 2 appends the keys of the round-1
     // bucket (its survivors), rounds >= 3 read only those
     unsigned* cand = (sizeof(T) == 4) ? P.cand[jb] : nullptr;
-    unsigned* cand1 = (sizeof(T) == 4) ? P.cand1[jb] : nullptr;
-    const bool win1 = cand1 && round == 1 && pass == 0 && J.wlo >= 0;   // round 1 compacts the window
-    const bool from1 = cand1 && round == 2 && J.r2c;                     // round 2 reads it
     const bool make_cand = cand && round == 2;
-    const bool use_cand = (cand && round >= 3) || from1;
-    const unsigned* csrc = from1 ? cand1 : cand;
-    const int ntot = use_cand ? (int)(from1 ? J.c1_n : J.cand_n) : tot;
-    const unsigned wlo = (unsigned)J.wlo, whi = (unsigned)J.whi;
+    const bool use_cand = cand && round >= 3;
+    const int ntot = use_cand ? (int)J.cand_n : tot;
     int pd = -1;
     unsigned pc = 0, pl[LB::N];
     auto hflush = [&]() {
@@ -405,29 +397,11 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
         for (int u = 0; u < SEL_U; ++u) {
           const int q = q0 + u * BLOCK;
           ok[u] = q < ntot;
-          kk[u] = ok[u] ? (U)__ldcg(csrc + q) : (U)0;
+          kk[u] = ok[u] ? (U)__ldcg(cand + q) : (U)0;
         }
-        unsigned mine = 0;
 #pragma unroll
         for (int u = 0; u < SEL_U; ++u)
-          if (ok[u] && (U)(kk[u] >> plo) == prefix) { hkey(kk[u]); mine |= 1u << u; }
-        if (make_cand) {   // round 2 from the window: keep the chosen bucket's keys
-          const int lane = threadIdx.x & 31;
-          const int cnt = __popc(mine);
-          int incl = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t_ = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t_;
-          }
-          const int tot_ = __shfl_sync(0xffffffffu, incl, 31);
-          unsigned base_ = 0u;
-          if (lane == 31 && tot_ > 0) base_ = atomicAdd(&C.job[jb].cand_n, (unsigned)tot_);
-          unsigned pos = __shfl_sync(0xffffffffu, base_, 31) + (unsigned)(incl - cnt);
-#pragma unroll
-          for (int u = 0; u < SEL_U; ++u)
-            if (mine & (1u << u)) cand[pos++] = (unsigned)kk[u];
-        }
+          if (ok[u] && (U)(kk[u] >> plo) == prefix) hkey(kk[u]);
       } else {
         T v[SEL_U][W];
         bool ok[SEL_U];
@@ -445,30 +419,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
 #pragma unroll
           for (int e = 0; e < W; ++e) {
             const U key = K::key(v[u][e]);
-            const bool in = ok[u] && (round == 1 ? key >= cut : (U)(key >> plo) == prefix);
-            if (in) hkey(key);
-            const unsigned dg = (unsigned)(key >> lo);
-            if (win1 ? (ok[u] && dg >= wlo && dg <= whi) : in) mine |= 1u << (u * W + e);
+            const bool in = ok[u] && (round == 1 || (U)(key >> plo) == prefix);
+            if (in) { hkey(key); mine |= 1u << (u * W + e); }
           }
-        }
-        if (win1) {   // round 1: the window's keys (warp-aggregated append)
-          const int lane = threadIdx.x & 31;
-          const int cnt = __popc(mine);
-          int incl = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int t_ = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t_;
-          }
-          const int tot_ = __shfl_sync(0xffffffffu, incl, 31);
-          unsigned base_ = 0u;
-          if (lane == 31 && tot_ > 0) base_ = atomicAdd(&C.job[jb].c1_n, (unsigned)tot_);
-          unsigned pos = __shfl_sync(0xffffffffu, base_, 31) + (unsigned)(incl - cnt);
-#pragma unroll
-          for (int u = 0; u < SEL_U; ++u)
-#pragma unroll
-            for (int e = 0; e < W; ++e)
-              if (mine & (1u << (u * W + e))) cand1[pos++] = (unsigned)K::key(v[u][e]);
         }
         if (make_cand) {   // warp-aggregated append: one global atomic per warp, no block barrier
           const int lane = threadIdx.x & 31;
@@ -479,9 +432,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
             const int t_ = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += t_;
           }
-          const int tot = __shfl_sync(0xffffffffu, incl, 31);
+          const int tot_ = __shfl_sync(0xffffffffu, incl, 31);
           unsigned base_ = 0u;
-          if (lane == 31 && tot > 0) base_ = atomicAdd(&C.job[jb].cand_n, (unsigned)tot);
+          if (lane == 31 && tot_ > 0) base_ = atomicAdd(&C.job[jb].cand_n, (unsigned)tot_);
           unsigned pos = __shfl_sync(0xffffffffu, base_, 31) + (unsigned)(incl - cnt);
 #pragma unroll
           for (int u = 0; u < SEL_U; ++u)
@@ -500,18 +453,11 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     for (int jb = 0; jb < C.njobs; ++jb) {
       Job& J = C.job[jb];
       if (J.mode != JM_SEARCH || J.round != round - 1 || (J.on_s && !check)) continue;
-      if (pass == 1 && !J.cutfail) continue;
-      if (pass == 1 && P.nranks == 1 && threadIdx.x == 0) { J.cut = 0u; J.cutfail = 0; }   // k_fin's, else
-      __syncthreads();
       unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
       unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
       unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
-      if (P.nranks > 1) {
-        publish_hist(P, jb, gc, g0, g1);
-      } else {
-        resolve_round<T>(P, J, round, gc, g0, g1);
-        if (round == 1 && threadIdx.x == 0) post_round1(J);
-      }
+      if (P.nranks > 1) publish_hist(P, jb, gc, g0, g1);
+      else resolve_round<T>(P, J, round, gc, g0, g1);
       __syncthreads();
       for (int d = threadIdx.x; d < NBUCK; d += BLOCK) { gc[d] = 0u; g0[d] = 0ull; g1[d] = 0ull; }
       __syncthreads();

@@ -53,10 +53,8 @@ struct Prob {
   // flattened segments (sip_flat.cuh): pass1 = x work + every (set, block);
   // pass2 = every (global set, block)
   int nseg1, nseg2;
-  // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32);
-  // cand1[job]: keys whose round-1 digit lies in the warm-start window
+  // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32)
   unsigned* cand[MAXJOBS];
-  unsigned* cand1[MAXJOBS];
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)
@@ -70,13 +68,6 @@ struct Prob {
   int xslot;
   FastDiv dncr;                   // division by the chunks per x row (lean CG kernels)
 };
-
-// after round 1 of a job: can round 2 read the window's compacted keys?
-// (exact: every key with the chosen digit is in the list iff the digit is
-// inside the window)
-__device__ inline void post_round1(Job& J) {
-  J.r2c = J.mode == JM_SEARCH && J.round == 1 && J.wlo >= 0 && (int)J.prefix >= J.wlo && (int)J.prefix <= J.whi;
-}
 
 __device__ __forceinline__ bool is_adapt_it(int k, int every) {
   return every <= 1 || (k % every) == 1;   // mod(k, update-frequency) = 1
@@ -678,15 +669,7 @@ __device__ void resolve_round(const Prob<T>& P, Job& J, int round, const unsigne
     s_sab = sm;
   }
   __syncthreads();
-  if (threadIdx.x == 0 && round == 1 && J.cut != 0u) {
-    // a cut round 1 is conclusive only if its digit lies strictly above the
-    // cut's bucket (all keys >= that edge were counted) and, for l1, the
-    // ball is active (the skipped keys could hold the rest of ||w||_1)
-    const int dcut = (int)((U)J.cut >> lo);
-    if (dstar <= dcut || (J.kind == K_L1 && s_stot <= J.sigma)) J.cutfail = 1;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && !J.cutfail) {
+  if (threadIdx.x == 0) {
     if (J.kind == K_L1 && round == 1 && s_stot <= J.sigma) {
       J.mode = JM_INSIDE;          // ||w||_1 <= sigma: w is in the ball (L5)
     } else if (J.kind == K_L1 && round == 1 && J.sigma <= 0.0) {
@@ -1041,20 +1024,6 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
     Job& J = C.job[jb];
     const int i = J.set;
     J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u;
-    // warm start (fp32 jobs on w): keys below half the last threshold cannot
-    // decide the new one unless it fell by more than 2x; round 1 skips them
-    // and falls back to all keys when its digit lands at or below the cut
-    J.cutfail = 0;
-    J.cut = (sizeof(T) == 4 && !J.on_s && C.hint[jb] > 0.0f) ? __float_as_uint(0.5f * C.hint[jb]) : 0u;
-    // ... and compacts the keys whose digit is within one of the last one's,
-    // so that round 2 usually reads a few percent of w (post_round1)
-    J.c1_n = 0u; J.r2c = 0;
-    J.wlo = J.whi = -1;
-    if (J.cut != 0u) {
-      const int hd = (int)(__float_as_uint(C.hint[jb]) >> 20);
-      J.wlo = max(0, hd - 1);
-      J.whi = min(NBUCK - 1, hd + 1);
-    }
     J.theta = 0.0; J.tau = 0ull; J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0.0;
     J.sigma = C.sigma[i];
     J.k = C.kcard[i];
@@ -1165,12 +1134,6 @@ __global__ void k_control(const __grid_constant__ Prob<T> P) {
     }
   for (int i = 0; i < Pn; ++i)
     for (int q = 0; q < NSLOT; ++q) C.sums[i][q] = 0.0;
-  for (int jb = 0; jb < C.njobs; ++jb) {   // the next iteration's warm start
-    const Job& J = C.job[jb];
-    float h = 0.0f;
-    if (J.mode == JM_DONE) h = J.kind == K_L1 ? (float)J.theta : __uint_as_float((unsigned)J.tau);
-    C.hint[jb] = (h > 0.0f && h < 1e30f) ? h : 0.0f;
-  }
   reset_jobs(P, C);
   C.k = k + 1;
   if (C.k > C.opt.max_iter) C.stopped = 1;

@@ -405,8 +405,6 @@ struct Engine : EngineBase {
         if (S.job < 0) continue;
         Pr.cand[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
         Pr.cand[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
-        Pr.cand1[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
-        Pr.cand1[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
       }
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
@@ -637,11 +635,8 @@ struct Engine : EngineBase {
     Pr.defer_x = 1;
   }
   void launch_cgx() { k_cgx<T><<<g_vec, BLOCK, 0, stream>>>(Pr); ++launches; }
-  // round 1 of the fp32 radix search is split: pass 0 skips keys below the
-  // warm-start cut, pass 1 redoes the round on all keys where that failed
-  bool split_r1() const { return vec && sizeof(T) == 4; }
-  void launch_select(int r, int pass = 0) {
-    if (vec) k_selectf<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r, pass);
+  void launch_select(int r) {
+    if (vec) k_selectf<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
     else k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
     ++launches;
   }
@@ -673,10 +668,7 @@ struct Engine : EngineBase {
     launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
-      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
-        launch_select(r); mark(KB_SELECT);
-        if (r == 1 && split_r1()) { launch_select(1, 1); mark(KB_SELECT); }
-      }
+      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
       if (has_card()) { launch_tie(); mark(KB_TIE); }
     }
     if (Pr.nglob > 0) {
@@ -742,7 +734,6 @@ struct Engine : EngineBase {
     c.hist_head = 0; c.hist_count = 1; c.breakdown = 0; c.numeric_err = 0; c.zero_x = 0;
     c.cg_j = 0; c.cg_active = 0; c.cg_count = 0; c.cg_total = 0;
     c.P = P; c.p = p;
-    for (int jb = 0; jb < MAXJOBS; ++jb) c.hint[jb] = 0.0f;   // no warm start across solves
     c.opt.n_cg = o.n_cg; c.opt.eq25 = o.eq25; c.opt.fixed_work = o.fixed_work;
     c.opt.adapt_every = o.adapt_every; c.opt.check_every = o.check_every; c.opt.max_iter = max_iter;
     c.opt.eps_evol = eps_evol; c.opt.eps_feas = eps_feas; c.opt.eps_corr = o.eps_corr;
@@ -1132,10 +1123,6 @@ struct Team : EngineBase {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
         each([&](Engine<T>& e) { e.launch_select(r); }, E::KB_SELECT);
         site(ST_SELECT, 0, r, {});
-        if (r == 1 && e0.split_r1()) {
-          each([&](Engine<T>& e) { e.launch_select(1, 1); }, E::KB_SELECT);
-          site(ST_SELECT, 1, 1, {});
-        }
       }
       if (e0.has_card()) {
         each([&](Engine<T>& e) { e.launch_tie(); }, E::KB_TIE);
@@ -1703,8 +1690,6 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     const int i = J.set;
     J.round = 0; J.prefix = 0; J.cnt_above = 0; J.sum_above = 0; J.theta = 0; J.tau = 0;
     J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0; J.cand_n = 0;
-    J.cut = 0u; J.cutfail = 0;
-    J.wlo = J.whi = -1; J.r2c = 0; J.c1_n = 0u;
     J.sigma = c.sigma[i]; J.k = c.kcard[i];
     J.mode = (J.on_s || i != set_id) ? JM_OFF : JM_SEARCH;
     if (J.mode == JM_SEARCH && J.kind == K_CARD) {
@@ -1738,10 +1723,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
     if (S.job >= 0) {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
-        if (e->vec) {
-          e->launch_select(r);
-          if (r == 1 && e->split_r1()) e->launch_select(1, 1);
-        }
+        if (e->vec) e->launch_select(r);
         else k_select<T><<<e->g_sel, BLOCK, 0, e->stream>>>(e->Pr, r);
       }
       if (S.kind == K_CARD) {

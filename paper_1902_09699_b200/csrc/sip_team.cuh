@@ -36,14 +36,11 @@ __host__ inline int site_payload(int site, int P, int njobs) {
 
 // radix round `round` of every active job on the summed histograms
 template <class T>
-__device__ inline void fin_select(const Prob<T>& P, Ctrl& C, int round, int pass) {
+__device__ inline void fin_select(const Prob<T>& P, Ctrl& C, int round) {
   const bool check = (C.k % C.opt.check_every) == 0;
   for (int jb = 0; jb < C.njobs; ++jb) {
     Job& J = C.job[jb];
     if (J.mode != JM_SEARCH || J.round != round - 1 || (J.on_s && !check)) continue;
-    if (pass == 1 && !J.cutfail) continue;
-    if (pass == 1 && threadIdx.x == 0) { J.cut = 0u; J.cutfail = 0; }
-    __syncthreads();
     unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
     unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
     unsigned long long* g1 = P.gh_s1 + (size_t)jb * NBUCK;
@@ -61,7 +58,6 @@ __device__ inline void fin_select(const Prob<T>& P, Ctrl& C, int round, int pass
     }
     __syncthreads();
     resolve_round<T>(P, J, round, gc, g0, g1);
-    if (round == 1 && threadIdx.x == 0) post_round1(J);
     __syncthreads();
     for (int d = threadIdx.x; d < NBUCK; d += BLOCK) { gc[d] = 0u; g0[d] = 0ull; g1[d] = 0ull; }
     __syncthreads();
@@ -145,7 +141,7 @@ __global__ void __launch_bounds__(BLOCK) k_fin(const __grid_constant__ Prob<T> P
       break;
     case ST_SELECT:
       if (C.stopped) return;
-      fin_select<T>(P, C, round, j);
+      fin_select<T>(P, C, round);
       break;
     case ST_TIE:
       if (C.stopped) return;

@@ -177,3 +177,4 @@ def test_c5_full_size_gpu_properties():
     fg = feas_of(prob, xh)
     for r_gpu, r_dev in zip(fg, per[0]["r_feas"]):
         assert abs(r_gpu - r_dev) <= 1e-3 + 1e-2 * abs(r_gpu)
+
