@@ -152,6 +152,18 @@ def sum_over_ranks(v, world, device=None):
     return float(t.item())
 
 
+def workload_config(prob, args, world=None):
+    """the `config` object of both arms (same workload, same keys)"""
+    world = world if world is not None else args.gpus
+    return {"workload": f"{prob.name} {'x'.join(map(str, prob.shape))} "
+                        f"{', '.join(sd.op + ':' + sd.kind for sd in prob.sets)}",
+            "grid": list(prob.shape), "sets": len(prob.sets), "iters_per_step": args.iters_per_step,
+            "n_cg": args.n_cg, "mode": "fixed_work (Eq.25 off, stop test not acted on)",
+            "l2": "flushed (256 MiB write) between timed steps",
+            "parallelism": ("1 GPU" if world == 1 else f"z-slab x{world} (NCCL halos + gathered reductions)")
+                           + (f", {args.virtual_ranks} virtual z-slabs on the GPU" if args.virtual_ranks > 1 else "")}
+
+
 # ------------------------------------------------------------------ oracle arm
 def oracle_sample(prob, iters, reps=1):
     """the CPU oracle (fixed-work PARSDMM) on the same workload; seconds/iteration"""
@@ -171,8 +183,11 @@ def run_reference(args, prob):
     if rank != 0:
         return 0
     ips = args.ref_iters
+    # warm-up steps (untimed): the plain C oracle has no JIT or caches to warm;
+    # a small case keeps the whole --steps K --warmup W run within minutes
+    small = G.tiny(100, (8, 8), ("bounds", "l1", "slope"))
     for _ in range(args.warmup):
-        oracle_sample(prob, 1)
+        oracle_sample(small, 1)
     ts = []
     for _ in range(args.steps):
         ts += oracle_sample(prob, ips)
@@ -183,8 +198,7 @@ def run_reference(args, prob):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": prob.name, "grid": list(prob.shape), "sets": len(prob.sets),
-                   "iters_per_step": ips, "mode": "fixed_work"},
+        "config": workload_config(prob, args),
         "pts_sets_per_s": val * prob.N * len(prob.sets),
         "cpu_baseline": {"value": val, "unit": "it/s", "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} steps x {ips} fixed-work iterations of {prob.name} "
@@ -302,15 +316,7 @@ def run_cuda(args, prob):
             "ms_per_step": t_total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prob.dtype == "f32" else "f64",
             "data": "synthetic",
-            "config": {"workload": f"{prob.name} {'x'.join(map(str, prob.shape))} "
-                                   f"{', '.join(sd.op + ':' + sd.kind for sd in prob.sets)}",
-                       "grid": list(prob.shape), "sets": len(prob.sets), "iters_per_step": ips,
-                       "n_cg": args.n_cg, "mode": "fixed_work (Eq.25 off, stop test not acted on)",
-                       "l2": "flushed (256 MiB write) between timed steps",
-                       "parallelism": ("1 GPU" if world == 1 else
-                                       f"z-slab x{world} (NCCL halos + gathered reductions)")
-                                      + (f", {args.virtual_ranks} virtual z-slabs on the GPU"
-                                         if args.virtual_ranks > 1 else "")},
+            "config": workload_config(prob, args, world),
             "pts_sets_per_s": value_job * prob.N * len(prob.sets),
             "iteration_model_gbs": it_model_gbs,
             "comm_ms_per_step": prof.get("comm", (0.0, 0))[0],
