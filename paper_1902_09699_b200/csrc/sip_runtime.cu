@@ -126,7 +126,7 @@ struct Engine : EngineBase {
   void apply_l2_window() {
     if (l2_window) CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &l2av));
   }
-  int g_cgf = 1, g_cgf3 = 1;     // grids of the lean CG kernels (4 / 3 CTAs per SM)
+  int g_cgf = 1, g_cgf3 = 1, g_cg2f = 1;   // grids of the lean CG kernels (CTAs per SM: 5 / 3 / 6)
   bool u2 = false;               // lean CG unrolled by 2 (SIP_CG_U2)
   int g_cgt1 = 0, g_cgt2 = 0;    // grids of the tile-staged CG kernels (0: unused)
   size_t smem_t1 = 0, smem_t2 = 0;
@@ -308,7 +308,9 @@ struct Engine : EngineBase {
     constexpr int W = VT<T>::W;
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
-    g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));   // 4 CTAs / SM resident
+    // lean CG / rhs: one wave of resident CTAs (launch bounds: cg1 / rhs 5, cg2 6 per SM)
+    g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 5));
+    g_cg2f = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 6));
     g_cgf3 = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 3));
     u2 = getenv("SIP_CG_U2") != nullptr;
     // z-marching CG: 3D grids whose rows split into whole warps of W-chunks
@@ -411,7 +413,7 @@ struct Engine : EngineBase {
     const int gz_ = std::max(zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1,
                              sg.on ? sg.tiles_x * sg.tiles_y * sg.nzc : 1);
     const int gmax = std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
-                              std::max(g_cgt1, g_cgt2));
+                              std::max(std::max(g_cgt1, g_cgt2), g_cg2f));
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -620,8 +622,8 @@ struct Engine : EngineBase {
         if (ndim == 3) k_cg2f<T, true, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
         else k_cg2f<T, false, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
       } else {
-        if (ndim == 3) k_cg2f<T, true, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
-        else k_cg2f<T, false, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+        if (ndim == 3) k_cg2f<T, true, false><<<g_cg2f, BLOCK, 0, stream>>>(Pr, j);
+        else k_cg2f<T, false, false><<<g_cg2f, BLOCK, 0, stream>>>(Pr, j);
       }
     } else if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
     else if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
