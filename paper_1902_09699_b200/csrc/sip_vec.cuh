@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 6) k_cg2f(const __grid_constan
 // the transposed differences need no masks: D^T u at a point is u(point - 1
 // step) - u(point), whose absent terms read those zeros (reading L3).
 template <class T, bool HY>
-__global__ void __launch_bounds__(BLOCK, 5) k_rhsf(const __grid_constant__ Prob<T> P) {
+__global__ void __launch_bounds__(BLOCK, 4) k_rhsf(const __grid_constant__ Prob<T> P) {
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
