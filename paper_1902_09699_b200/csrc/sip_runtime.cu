@@ -126,7 +126,7 @@ struct Engine : EngineBase {
   void apply_l2_window() {
     if (l2_window) CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &l2av));
   }
-  int g_cgf = 1, g_cgf3 = 1, g_cg2f = 1;   // grids of the lean CG kernels (CTAs per SM: 5 / 3 / 6)
+  int g_cgf = 1, g_cgf3 = 1, g_cg2f = 1, g_rhsf = 1;   // lean CG / rhs grids (CTAs per SM: 5 / 3 / 6 / 4)
   bool u2 = false;               // lean CG unrolled by 2 (SIP_CG_U2)
   int g_cgt1 = 0, g_cgt2 = 0;    // grids of the tile-staged CG kernels (0: unused)
   size_t smem_t1 = 0, smem_t2 = 0;
@@ -311,6 +311,7 @@ struct Engine : EngineBase {
     // lean CG / rhs: one wave of resident CTAs (launch bounds: cg1 / rhs 5, cg2 6 per SM)
     g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 5));
     g_cg2f = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 6));
+    g_rhsf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
     g_cgf3 = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 3));
     u2 = getenv("SIP_CG_U2") != nullptr;
     // z-marching CG: 3D grids whose rows split into whole warps of W-chunks
@@ -577,8 +578,8 @@ struct Engine : EngineBase {
   void launch_blur(int mode, int j) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, mode, j); ++launches; }
   void launch_rhs() {
     if (lean_cg()) {
-      if (ndim == 3) k_rhsf<T, true><<<g_cgf, BLOCK, 0, stream>>>(Pr);
-      else k_rhsf<T, false><<<g_cgf, BLOCK, 0, stream>>>(Pr);
+      if (ndim == 3) k_rhsf<T, true><<<g_rhsf, BLOCK, 0, stream>>>(Pr);
+      else k_rhsf<T, false><<<g_rhsf, BLOCK, 0, stream>>>(Pr);
     } else if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
     else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
     ++launches;
