@@ -1036,9 +1036,8 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
 }
 
 template <class T>
-__global__ void k_control(const __grid_constant__ Prob<T> P) {
-  Ctrl& C = *P.ctrl;
-  if (threadIdx.x != 0 || C.stopped) return;
+__device__ void control_body(const Prob<T>& P, Ctrl& C) {
+  if (C.stopped) return;
   if (C.numeric_err) { C.stopped = 1; return; }   // set by a kernel (variant mismatch)
   const int k = C.k;
   const int Pn = P.P, p = P.p;
@@ -1137,6 +1136,24 @@ __global__ void k_control(const __grid_constant__ Prob<T> P) {
   reset_jobs(P, C);
   C.k = k + 1;
   if (C.k > C.opt.max_iter) C.stopped = 1;
+}
+
+// k_control: one thread runs Algorithm 2 / Eq. 26-28 on a shared-memory copy
+// of the control block (its ~9 KB moved in and out by the whole CTA), so the
+// long chain of dependent reads and writes stays on chip
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_control(const __grid_constant__ Prob<T> P) {
+  __shared__ Ctrl Cs;
+  static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied in 8-byte words");
+  constexpr int NW8 = (int)(sizeof(Ctrl) / 8);
+  const unsigned long long* g = reinterpret_cast<const unsigned long long*>(P.ctrl);
+  unsigned long long* sm = reinterpret_cast<unsigned long long*>(&Cs);
+  for (int i = threadIdx.x; i < NW8; i += BLOCK) sm[i] = g[i];
+  __syncthreads();
+  if (threadIdx.x == 0) control_body<T>(P, Cs);
+  __syncthreads();
+  unsigned long long* gw = reinterpret_cast<unsigned long long*>(P.ctrl);
+  for (int i = threadIdx.x; i < NW8; i += BLOCK) gw[i] = sm[i];
 }
 
 // init finaliser (one thread): relative parameters from the norms of A_i m

@@ -652,7 +652,7 @@ struct Engine : EngineBase {
     else k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
-  void launch_control() { k_control<T><<<1, 32, 0, stream>>>(Pr); ++launches; }
+  void launch_control() { k_control<T><<<1, BLOCK, 0, stream>>>(Pr); ++launches; }
   void launch_fin(int site, int j, int round) {
     k_fin<T><<<1, BLOCK, 0, stream>>>(Pr, site, j, round);
     ++launches;
