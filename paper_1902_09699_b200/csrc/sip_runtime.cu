@@ -308,9 +308,9 @@ struct Engine : EngineBase {
     constexpr int W = VT<T>::W;
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
-    // lean CG / rhs: one wave of resident CTAs (launch bounds: cg1 / rhs 5, cg2 6 per SM)
-    g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 5));
-    g_cg2f = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 6));
+    // lean CG / rhs: one wave of resident CTAs (4 per SM)
+    g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
+    g_cg2f = g_cgf;   // 5-6 CTAs / SM measured no faster (latency per chunk, not occupancy)
     g_rhsf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
     g_cgf3 = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 3));
     u2 = getenv("SIP_CG_U2") != nullptr;

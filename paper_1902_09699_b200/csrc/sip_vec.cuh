@@ -458,7 +458,7 @@ __device__ __forceinline__ CoefT<T> coefs_present(const Prob<T>& P, const Ctrl& 
 
 // k_cg1f(j): p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j>; p_j -> slot j
 template <class T, bool HY, bool U2>
-__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 5) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
+__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 5) k_cg1f(const __grid_constan
 
 // k_cg2f(j): r -= alpha C p_j and <r, r> (the x update is deferred to k_cgx)
 template <class T, bool HY, bool U2>
-__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 6) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
+__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped || !C.cg_active) return;
