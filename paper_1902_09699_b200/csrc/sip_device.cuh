@@ -217,6 +217,19 @@ template <> struct SigT<double> {
   }
 };
 
+// ---------------------------------------------------------------- launch overlap
+// Programmatic dependent launch: the runtime launches the hot kernels with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so kernel n+1 may be
+// scheduled while kernel n drains (its last-CTA reduction, its tail CTAs).
+// Every such kernel starts with pdl_begin(): wait until the previous kernel
+// has completed and its memory is visible, then allow the next kernel to
+// launch once all of this kernel's CTAs are running.  Without the launch
+// attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 // ---------------------------------------------------------------- reductions
 // fixed-order block sum (warp shuffle tree, then warps in order): deterministic
 __device__ __forceinline__ double warp_sum(double v) {

@@ -295,6 +295,7 @@ __device__ inline void publish_hist(const Prob<T>& P, int jb, const unsigned* gc
 
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<T> P, int round) {
+  pdl_begin();
   using K = KeyT<T>;
   using U = typename K::U;
   using LB = Limbs<T>;
@@ -469,6 +470,7 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
 // ------------------------------------------------------------ ties / pass2 (CTA tiles)
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_tiecountf(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
   using K = KeyT<T>;
   using U = typename K::U;
   constexpr int W = VT<T>::W;

@@ -1143,6 +1143,7 @@ __device__ void control_body(const Prob<T>& P, Ctrl& C) {
 // long chain of dependent reads and writes stays on chip
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_control(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
   __shared__ Ctrl Cs;
   static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied in 8-byte words");
   constexpr int NW8 = (int)(sizeof(Ctrl) / 8);

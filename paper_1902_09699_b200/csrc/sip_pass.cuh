@@ -388,6 +388,7 @@ __device__ inline void fin_pass1(const Prob<T>& P, Ctrl& C, const double* stage)
 // and Eq. 26/27 statistics (Algorithm 1 lines of P:279-288; Alg. 2 line 1)
 template <class T, int AD, int CK>
 __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
   constexpr int W = VT<T>::W;
   constexpr int NA = AD == 0 ? P1_NA_PLAIN : P1_NA_ADAPT;
   Ctrl& C = *P.ctrl;
@@ -564,6 +565,7 @@ __device__ inline void fin_pass2(const Prob<T>& P, Ctrl& C, const double* stage)
 
 template <class T, int AD, int CK>
 __global__ void __launch_bounds__(BLOCK, 4) k_pass2t(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
   using K = KeyT<T>;
   using U = typename K::U;
   constexpr int W = VT<T>::W;

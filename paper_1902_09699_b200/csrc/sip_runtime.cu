@@ -202,6 +202,7 @@ struct Engine : EngineBase {
     Pr.dncr.init((uint32_t)std::max(1, g.nx / VT<T>::W));
     Pr.P = P; Pr.p = p;
     Pr.nranks = nranks; Pr.rank = rank;
+    pdl = nranks == 1 && !getenv("SIP_NO_PDL");
     Pr.rounds = KeyT<T>::ROUNDS;
     Pr.ntiles_pb = (g.N + BLOCK - 1) / BLOCK;
     Pr.nseg1 = 0;   // counts (set, block) segments below; +1 for the x segment after
@@ -547,6 +548,24 @@ struct Engine : EngineBase {
     ++pev_used;
   }
 
+  // launch with programmatic dependent launch (single rank; pdl_begin() in
+  // the kernels): the next kernel is scheduled while this one drains
+  bool pdl = false;
+  template <typename... KA, typename... A>
+  void lk(void (*kern)(KA...), int grid, int block, size_t smem, A&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? at : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CU(cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...));
+  }
+
   // kernel variants by iteration type: kpos = k (1-based) when the launch
   // position fixes it, 0 = decide on the device (see sip_pass.cuh)
   void launch_pass1(int kpos) {
@@ -554,11 +573,11 @@ struct Engine : EngineBase {
     const int ad = kpos > 0 ? (kpos % 2 == 1) : 2;
     const int ck = kpos > 0 ? (kpos % hc.opt.check_every == 0) : 2;
     switch (ad * 3 + ck) {
-      case 0: k_pass1t<T, 0, 0><<<g_p1, BLOCK, smem_p1v, stream>>>(Pr); break;
-      case 1: k_pass1t<T, 0, 1><<<g_p1, BLOCK, smem_p1v, stream>>>(Pr); break;
-      case 3: k_pass1t<T, 1, 0><<<g_p1a, BLOCK, smem_p1a, stream>>>(Pr); break;
-      case 4: k_pass1t<T, 1, 1><<<g_p1a, BLOCK, smem_p1a, stream>>>(Pr); break;
-      default: k_pass1t<T, 2, 2><<<g_p1a, BLOCK, smem_p1a, stream>>>(Pr);
+      case 0: lk(k_pass1t<T, 0, 0>, g_p1, BLOCK, smem_p1v, Pr); break;
+      case 1: lk(k_pass1t<T, 0, 1>, g_p1, BLOCK, smem_p1v, Pr); break;
+      case 3: lk(k_pass1t<T, 1, 0>, g_p1a, BLOCK, smem_p1a, Pr); break;
+      case 4: lk(k_pass1t<T, 1, 1>, g_p1a, BLOCK, smem_p1a, Pr); break;
+      default: lk(k_pass1t<T, 2, 2>, g_p1a, BLOCK, smem_p1a, Pr);
     }
   }
   void launch_pass2(int kpos) {
@@ -566,11 +585,11 @@ struct Engine : EngineBase {
     const int ad = kpos > 0 ? (kpos % 2 == 1) : 2;
     const int ck = kpos > 0 ? (kpos % hc.opt.check_every == 0) : 2;
     switch (ad * 3 + ck) {
-      case 0: k_pass2t<T, 0, 0><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
-      case 1: k_pass2t<T, 0, 1><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
-      case 3: k_pass2t<T, 1, 0><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
-      case 4: k_pass2t<T, 1, 1><<<g_p2, BLOCK, smem_p2, stream>>>(Pr); break;
-      default: k_pass2t<T, 2, 2><<<g_p2, BLOCK, smem_p2, stream>>>(Pr);
+      case 0: lk(k_pass2t<T, 0, 0>, g_p2, BLOCK, smem_p2, Pr); break;
+      case 1: lk(k_pass2t<T, 0, 1>, g_p2, BLOCK, smem_p2, Pr); break;
+      case 3: lk(k_pass2t<T, 1, 0>, g_p2, BLOCK, smem_p2, Pr); break;
+      case 4: lk(k_pass2t<T, 1, 1>, g_p2, BLOCK, smem_p2, Pr); break;
+      default: lk(k_pass2t<T, 2, 2>, g_p2, BLOCK, smem_p2, Pr);
     }
   }
 
@@ -578,8 +597,8 @@ struct Engine : EngineBase {
   void launch_blur(int mode, int j) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, mode, j); ++launches; }
   void launch_rhs() {
     if (lean_cg()) {
-      if (ndim == 3) k_rhsf<T, true><<<g_rhsf, BLOCK, 0, stream>>>(Pr);
-      else k_rhsf<T, false><<<g_rhsf, BLOCK, 0, stream>>>(Pr);
+      if (ndim == 3) lk(k_rhsf<T, true>, g_rhsf, BLOCK, 0, Pr);
+      else lk(k_rhsf<T, false>, g_rhsf, BLOCK, 0, Pr);
     } else if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
     else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
     ++launches;
@@ -595,11 +614,11 @@ struct Engine : EngineBase {
       else k_cg1t<T, false><<<g_cgt1, BLOCK, smem_t1, stream>>>(Pr, j);
     } else if (lean_cg() && !sg.on) {
       if (u2) {
-        if (ndim == 3) k_cg1f<T, true, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
-        else k_cg1f<T, false, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
+        if (ndim == 3) lk(k_cg1f<T, true, true>, g_cgf3, BLOCK, 0, Pr, j);
+        else lk(k_cg1f<T, false, true>, g_cgf3, BLOCK, 0, Pr, j);
       } else {
-        if (ndim == 3) k_cg1f<T, true, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
-        else k_cg1f<T, false, false><<<g_cgf, BLOCK, 0, stream>>>(Pr, j);
+        if (ndim == 3) lk(k_cg1f<T, true, false>, g_cgf, BLOCK, 0, Pr, j);
+        else lk(k_cg1f<T, false, false>, g_cgf, BLOCK, 0, Pr, j);
       }
     } else if (sg.on) {
       k_cg1s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s1, stream>>>(Pr, sg, j);
@@ -620,11 +639,11 @@ struct Engine : EngineBase {
       else k_cg2t<T, false><<<g_cgt2, BLOCK, smem_t2, stream>>>(Pr, j);
     } else if (lean_cg() && !sg.on && Pr.defer_x) {
       if (u2) {
-        if (ndim == 3) k_cg2f<T, true, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
-        else k_cg2f<T, false, true><<<g_cgf3, BLOCK, 0, stream>>>(Pr, j);
+        if (ndim == 3) lk(k_cg2f<T, true, true>, g_cgf3, BLOCK, 0, Pr, j);
+        else lk(k_cg2f<T, false, true>, g_cgf3, BLOCK, 0, Pr, j);
       } else {
-        if (ndim == 3) k_cg2f<T, true, false><<<g_cg2f, BLOCK, 0, stream>>>(Pr, j);
-        else k_cg2f<T, false, false><<<g_cg2f, BLOCK, 0, stream>>>(Pr, j);
+        if (ndim == 3) lk(k_cg2f<T, true, false>, g_cg2f, BLOCK, 0, Pr, j);
+        else lk(k_cg2f<T, false, false>, g_cg2f, BLOCK, 0, Pr, j);
       }
     } else if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
     else if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
@@ -637,9 +656,9 @@ struct Engine : EngineBase {
     while (npr < n_cg) Pr.pr[npr++] = field(1);
     Pr.defer_x = 1;
   }
-  void launch_cgx() { k_cgx<T><<<g_vec, BLOCK, 0, stream>>>(Pr); ++launches; }
+  void launch_cgx() { lk(k_cgx<T>, g_vec, BLOCK, 0, Pr); ++launches; }
   void launch_select(int r) {
-    if (vec) k_selectf<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
+    if (vec) lk(k_selectf<T>, g_sel, BLOCK, 0, Pr, r);
     else k_select<T><<<g_sel, BLOCK, 0, stream>>>(Pr, r);
     ++launches;
   }
@@ -648,11 +667,11 @@ struct Engine : EngineBase {
     return false;
   }
   void launch_tie() {
-    if (vec) k_tiecountf<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
+    if (vec) lk(k_tiecountf<T>, g_p2, BLOCK, 0, Pr);
     else k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
-  void launch_control() { k_control<T><<<1, BLOCK, 0, stream>>>(Pr); ++launches; }
+  void launch_control() { lk(k_control<T>, 1, BLOCK, 0, Pr); ++launches; }
   void launch_fin(int site, int j, int round) {
     k_fin<T><<<1, BLOCK, 0, stream>>>(Pr, site, j, round);
     ++launches;

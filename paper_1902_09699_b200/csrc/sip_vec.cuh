@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(BLOCK) k_cg2v(const __grid_constant__ Prob<T> 
 // over the cg_count completed steps, in step order (Eq. 21 line 1's CG)
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_cgx(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
   constexpr int W = VT<T>::W;
   const Ctrl& C = *P.ctrl;
   if (C.stopped) return;
@@ -459,6 +460,7 @@ __device__ __forceinline__ CoefT<T> coefs_present(const Prob<T>& P, const Ctrl& 
 // k_cg1f(j): p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j>; p_j -> slot j
 template <class T, bool HY, bool U2>
 __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
+  pdl_begin();
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
@@ -534,6 +536,7 @@ __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg1f(const __grid_constan
 // k_cg2f(j): r -= alpha C p_j and <r, r> (the x update is deferred to k_cgx)
 template <class T, bool HY, bool U2>
 __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
+  pdl_begin();
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped || !C.cg_active) return;
@@ -590,6 +593,7 @@ __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg2f(const __grid_constan
 // step) - u(point), whose absent terms read those zeros (reading L3).
 template <class T, bool HY>
 __global__ void __launch_bounds__(BLOCK, 4) k_rhsf(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
