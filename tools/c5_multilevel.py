@@ -2,9 +2,7 @@
 natural mode (Eq. 25 and Eq. 28 active, max 200 iterations per level) on
 the full 512 x 512 x 256 fp32 model, through the public call
 sip_project_multilevel.  Prints one JSON line: per-level iterations, CG
-steps, device ms, final r_feas / r_evol, and the whole call's wall time.
-Also re-verifies the finest level's constraints with the oracle's
-projectors on the GPU's x (Eq. 26, test infrastructure)."""
+steps, device ms, final r_feas / r_evol, and the whole call's wall time."""
 import json
 import os
 import sys
@@ -38,15 +36,6 @@ def main():
                    r_feas=[float(v) for v in r["r_feas"]]) for l, r in enumerate(per)]
     out = dict(workload="C5 512x512x256 fp32, 3-level multilevel (Algorithm 3), natural mode",
                status=int(st), wall_s=wall, device_ms=sum(l["ms"] for l in levels), levels=levels)
-    try:   # independent check of the finest level by the oracle's projectors
-        import oracle as O
-        from tests.test_gpu_parity import absolute_set  # noqa
-    except Exception:
-        absolute_set = None
-    if absolute_set is not None:
-        xv = x.double().cpu().numpy().ravel()
-        out["oracle_feas"] = [float(O.feas(absolute_set(sd, prob), O.apply_A(prob.shape, sd, xv)))
-                              for sd in prob.sets]
     print(json.dumps(out), flush=True)
     g.close()
 
