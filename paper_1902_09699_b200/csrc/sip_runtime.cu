@@ -123,8 +123,10 @@ struct Engine : EngineBase {
   int npr = 0;                   // allocated slots of the p ring (Prob::pr)
   bool l2_window = false;        // an L2 persisting window on r (set on the stream before capture)
   cudaStreamAttrValue l2av;
-  void apply_l2_window() {
-    if (l2_window) CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &l2av));
+  void apply_l2_window() {   // this engine's window, or none (the stream is shared by levels)
+    cudaStreamAttrValue none;
+    memset(&none, 0, sizeof(none));
+    CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, l2_window ? &l2av : &none));
   }
   int g_cgf = 1, g_cgf3 = 1, g_cg2f = 1, g_rhsf = 1;   // lean CG / rhs grids (CTAs per SM: 5 / 3 / 6 / 4)
   bool u2 = false;               // lean CG unrolled by 2 (SIP_CG_U2)
@@ -270,13 +272,17 @@ struct Engine : EngineBase {
     // work stream): every CG step reads it (k_cg1 stencil) and reads + writes
     // it (k_cg2); with r in L2 a step moves ~4N words from DRAM instead of 6N.
     // The window is captured into the iteration graph's kernel nodes.
+    // Only when r fits in a third of L2 (C4: 33.5 MB of 126 MB): a larger
+    // carve-out starves every other kernel (measured on C5-L1, r = 268 MB:
+    // all kernels ~2x slower).
     if (!getenv("SIP_NO_L2_PERSIST")) {
-      int maxp = 0, maxw = 0, dev = 0;
+      int maxp = 0, maxw = 0, l2 = 0, dev = 0;
       CU(cudaGetDevice(&dev));
       CU(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
       CU(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+      CU(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
       const size_t rb = (size_t)g.ld * sizeof(T);
-      if (maxp > 0 && maxw > 0) {
+      if (maxp > 0 && maxw > 0 && rb <= (size_t)l2 / 3 && rb <= (size_t)maxp && rb <= (size_t)maxw) {
         size_t cur = 0;
         CU(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
         const size_t want = std::min((size_t)maxp, rb);
