@@ -54,6 +54,7 @@ class Set(C.Structure):
         ("k", C.c_int64), ("relative", C.c_int), ("k_frac", C.c_double),
         ("kernel", C.POINTER(C.c_double)), ("kh", C.c_int), ("kw", C.c_int),
         ("mask", C.POINTER(C.c_ubyte)), ("key_f32", C.c_int),
+        ("app_mode", C.c_int), ("fib_len", C.c_int64),
     ]
 
 
@@ -90,6 +91,7 @@ def lib():
         _lib = C.CDLL(build())
         _lib.sipref_npts.restype = C.c_int64
         _lib.sipref_op_len.restype = C.c_int64
+        _lib.sipref_fiber_len.restype = C.c_int64
         _lib.sipref_feas.restype = C.c_double
     return _lib
 
@@ -140,6 +142,7 @@ class _SetHolder:
         s.k = int(sd.k)
         s.relative = int(bool(sd.relative))
         s.k_frac = float(sd.k_frac)
+        s.app_mode = APP_MODES[getattr(sd, "app_mode", "") or ""]
         if sd.kernel is not None:
             kk = _f64(sd.kernel); self.keep.append(kk)
             s.kernel = _dp(kk); s.kh, s.kw = kk.shape
@@ -203,8 +206,20 @@ def apply_C(shape, setdefs, rho, p_vec, h=None):
     return q
 
 
-def project(sd, w):
+APP_MODES = {"": 0, "x": 1, "z": 2}
+
+
+def fiber_len(shape, sd, h=None) -> int:
+    g = make_grid(shape, h)
     hold = _SetHolder(sd)
+    return int(lib().sipref_fiber_len(C.byref(g), C.byref(hold.s)))
+
+
+def project(sd, w, shape=None):
+    """Table 1 projector; shape is needed for per-fiber sets (app_mode)"""
+    hold = _SetHolder(sd)
+    if shape is not None:
+        hold.s.fib_len = fiber_len(shape, sd)
     w = _f64(w).ravel()
     y = np.zeros_like(w)
     lib().sipref_project(C.byref(hold.s), C.c_int64(w.size), _dp(w), _dp(y))
@@ -218,8 +233,10 @@ def prox_dist(m, rho, w):
     return y
 
 
-def feas(sd, s_vec):
+def feas(sd, s_vec, shape=None):
     hold = _SetHolder(sd)
+    if shape is not None:
+        hold.s.fib_len = fiber_len(shape, sd)
     s_vec = _f64(s_vec).ravel()
     return float(lib().sipref_feas(C.byref(hold.s), C.c_int64(s_vec.size), _dp(s_vec)))
 

@@ -312,7 +312,35 @@ static void proj_card(int64_t M, const double *w, int64_t k, int key_f32, double
   free(t);
 }
 
+static void project_whole(const sipref_set *s, int64_t M, const double *w, double *y);
+
+int64_t sipref_fiber_len(const sipref_grid *g, const sipref_set *s) {
+  if (s->app_mode == 1) return s->op == SIPREF_OP_DX ? g->n[2] - 1 : g->n[2];
+  if (s->app_mode == 2) return s->op == SIPREF_OP_DZ ? g->n[0] - 1 : g->n[0];
+  return 0;
+}
+
+/* Table 1 projector of set s on w (length M).  app_mode 1 / 2: the output
+   field of the (single-block) operator is split into its x-fibers, which are
+   consecutive runs of fib_len entries of the compact layout, or its
+   z-fibers, fib_len entries at stride M / fib_len; each fiber is projected
+   on its own with the set's parameters (k, sigma per fiber). */
 void sipref_project(const sipref_set *s, int64_t M, const double *w, double *y) {
+  if (s->app_mode == 0 || s->fib_len <= 0) { project_whole(s, M, w, y); return; }
+  const int64_t L = s->fib_len, nf = M / L;
+  const int64_t stride = s->app_mode == 1 ? 1 : nf;
+  double *a = dalloc(L), *b = dalloc(L);
+  for (int64_t f = 0; f < nf; ++f) {
+    const int64_t base = s->app_mode == 1 ? f * L : f;
+    for (int64_t t = 0; t < L; ++t) a[t] = w[base + t * stride];
+    project_whole(s, L, a, b);
+    for (int64_t t = 0; t < L; ++t) y[base + t * stride] = b[t];
+  }
+  free(a);
+  free(b);
+}
+
+static void project_whole(const sipref_set *s, int64_t M, const double *w, double *y) {
   switch (s->type) {
     case SIPREF_BOUNDS: /* l[i] <= (Am)[i] <= u[i]: clamp */
       for (int64_t i = 0; i < M; ++i) {
@@ -489,6 +517,7 @@ int sipref_adapt_rho_gamma(int64_t M, const double *v_hat, const double *v_hat0,
 static void resolve_set(const sipref_grid *g, const sipref_set *in, const double *m,
                         sipref_set *out) {
   *out = *in;
+  out->fib_len = sipref_fiber_len(g, in);
   if (!in->relative) return;
   int64_t M = sipref_op_len(g, in);
   double *a = dalloc(M);
@@ -503,7 +532,8 @@ static void resolve_set(const sipref_grid *g, const sipref_set *in, const double
     out->sigma_lo = in->sigma_lo * n2;
     out->sigma_hi = in->sigma_hi * n2;
   }
-  if (in->type == SIPREF_CARD) out->k = (int64_t)floor(in->k_frac * (double)M);
+  if (in->type == SIPREF_CARD)   /* per fiber: a fraction of the fiber length */
+    out->k = (int64_t)floor(in->k_frac * (double)(in->app_mode ? out->fib_len : M));
   out->relative = 0;
 }
 

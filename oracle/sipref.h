@@ -51,6 +51,12 @@ typedef struct {
   const unsigned char *mask;         /* BLUR_MASK: N bytes, 1 = observed     */
   int key_f32;                       /* CARD: rank |w| rounded to fp32 (set by
                                         the solver from options.decide_f32)  */
+  int app_mode;      /* 0: the whole vector A m; 1: each x-fiber (row) of the
+                        operator's grid-shaped output; 2: each z-fiber
+                        (column) -- the projector is applied to every fiber
+                        independently ("each row/column
+                        independently"; NEXT-1).  Single-block operators.   */
+  int64_t fib_len;   /* fiber length (set by sipref_fiber_len)               */
 } sipref_set;
 
 typedef struct {
@@ -85,6 +91,10 @@ void sipref_default_options(sipref_options *o);
 /* number of grid points; M of an operator (compact) */
 int64_t sipref_npts(const sipref_grid *g);
 int64_t sipref_op_len(const sipref_grid *g, const sipref_set *s);
+/* length of one fiber of the operator's output (app_mode 1: the x extent of
+   the output field, nx - 1 for D_x; app_mode 2: its z extent, nz - 1 for
+   D_z); 0 for app_mode 0 */
+int64_t sipref_fiber_len(const sipref_grid *g, const sipref_set *s);
 
 /* y = A x  and  x = A^T y  (compact layouts) */
 void sipref_apply_A(const sipref_grid *g, const sipref_set *s, const double *x, double *y);

@@ -37,6 +37,7 @@ class SetDef:
     relative: bool = False        # sigma*, k relative to A m (reading L4, L23)
     kernel: np.ndarray | None = None   # BLUR_MASK kernel (kh x kw)
     mask: np.ndarray | None = None     # BLUR_MASK observation mask, grid shape, uint8
+    app_mode: str = ""            # '' whole vector, 'x' each row (x-fiber), 'z' each column
 
 
 @dataclass

@@ -526,3 +526,78 @@ def test_multilevel_converges_and_is_cheaper():
     assert logs[0].converged
     assert O.relres(x, _box_mono_exact(m, 1500.0, 4500.0)) < 1e-2
     assert logs[0].cg_total < single.cg_total
+
+
+# ------------------------------------------------------------ per-fiber sets (NEXT-1)
+def test_fiber_worked_example():
+    """per-row cardinality k = 1 on [[1, 2], [4, 3]] -> [[0, 2], [4, 0]]
+    ("applied to each row/column independently"); per column -> [[0, 0], [4, 3]]"""
+    np.testing.assert_array_equal(O.project(SetDef("I", "card", k=1, app_mode="x"), [1, 2, 4, 3], shape=(2, 2)),
+                                  [0, 2, 4, 0])
+    np.testing.assert_array_equal(O.project(SetDef("I", "card", k=1, app_mode="z"), [1, 2, 4, 3], shape=(2, 2)),
+                                  [0, 0, 4, 3])
+
+
+@pytest.mark.parametrize("op,mode,shape", [("I", "x", (5, 4)), ("I", "z", (5, 4)), ("DX", "x", (5, 6)),
+                                           ("DX", "z", (5, 6)), ("DZ", "z", (6, 5)), ("DZ", "x", (6, 5)),
+                                           ("DY", "x", (3, 4, 5)), ("DX", "z", (4, 3, 5))])
+@pytest.mark.parametrize("kind", ["card", "l1"])
+def test_fiber_projection_vs_explicit_loop(op, mode, shape, kind):
+    """the fiber projector equals an explicit loop over the rows /
+    columns of the operator's output field, each projected by the
+    whole-vector projector (itself pinned by brute force above)"""
+    r = np.random.default_rng(21)
+    sd = SetDef(op, kind, k=2, sigma=1.5, app_mode=mode)
+    M = O.op_len(shape, sd)
+    L = O.fiber_len(shape, sd)
+    nz = shape[0]
+    ny = shape[1] if len(shape) == 3 else 1
+    nx = shape[-1]
+    fz = nz - (op == "DZ")
+    fy = ny - (op == "DY")
+    fx = nx - (op == "DX")
+    assert M == fz * fy * fx and L == (fx if mode == "x" else fz)
+    w = r.normal(size=M)
+    W = w.reshape(fz, fy, fx)
+    ref = np.zeros_like(W)
+    whole = SetDef("I", kind, k=2, sigma=1.5)
+    if mode == "x":
+        for a in range(fz):
+            for b in range(fy):
+                ref[a, b, :] = O.project(whole, W[a, b, :])
+    else:
+        for b in range(fy):
+            for c in range(fx):
+                ref[:, b, c] = O.project(whole, W[:, b, c])
+    np.testing.assert_allclose(O.project(sd, w, shape=shape), ref.ravel(), rtol=0, atol=1e-14)
+
+
+def test_fiber_bounds_is_separable_and_feasibility():
+    """per-row bounds == whole-field bounds (separable set); Eq. 26 of a
+    fiber set measures the distance to the per-fiber projection"""
+    r = np.random.default_rng(22)
+    w = r.normal(size=20)
+    a = O.project(SetDef("I", "bounds", lo=-0.3, hi=0.5, app_mode="x"), w, shape=(4, 5))
+    b = O.project(SetDef("I", "bounds", lo=-0.3, hi=0.5), w)
+    np.testing.assert_array_equal(a, b)
+    sd = SetDef("I", "card", k=1, app_mode="x")
+    s = np.array([1.0, 2.0, 4.0, 3.0])
+    expect = np.linalg.norm([1.0, 0.0, 0.0, 3.0]) / np.linalg.norm(s)
+    assert O.feas(sd, s, shape=(2, 2)) == pytest.approx(expect, rel=1e-15)
+
+
+def test_parsdmm_fiber_l1_vs_dykstra():
+    """convex per-row l1 balls (A = I) with bounds: PARSDMM run tightly equals
+    Dykstra's algorithm (Algorithm 4) with the exact per-row projector"""
+    shape = (6, 8)
+    m = tiny_model(33, shape)
+    sig = 0.4 * np.abs(m - 3000.0).sum(axis=1).min()
+    c0 = np.full(shape, 3000.0)
+    row = SetDef("I", "l1", sigma=sig, app_mode="x")
+    projs = [lambda z: np.clip(z, 1500.0 - 3000.0, 4500.0 - 3000.0),
+             lambda z: O.project(row, z.ravel(), shape=shape).reshape(shape)]
+    ref = _dykstra(m - c0, projs)
+    sets = [SetDef("I", "bounds", lo=1500.0 - 3000.0, hi=4500.0 - 3000.0), row]
+    t = O.parsdmm(shape, sets, m - c0, eps_evol=1e-10, eps_feas=1e-10, n_cg=200, max_iter=50000)
+    assert O.relres(t.x, ref.ravel()) < 1e-6
+    assert all(np.abs(t.x.reshape(shape)).sum(axis=1) <= sig * (1 + 1e-6))
