@@ -97,7 +97,18 @@ typedef struct {
                              norm of A m (l1 norm for L1_BALL, l2 otherwise),
                              re-derived from the m of every projection and every
                              multilevel level (readings L4, L23)               */
+  int app_mode;           /* SIP_APPLY_*: the projector acts on the whole vector
+                             A m (0), or on each x-fiber (row) / z-fiber
+                             (column) of the operator's output field on its own
+                             (NEXT-1): CARDINALITY (k per fiber; relative:
+                             k = floor(k_frac * fiber length)) and L1_BALL
+                             (absolute sigma per fiber), single-block operators
+                             (not TV / BLUR_MASK), fibers of <= 4096 entries,
+                             one rank; BOUNDS accepts it (separable).  Else
+                             SIP_ERR_CONFIG; L1_BALL relative: SIP_ERR_PARAM.  */
 } sip_set_params;
+
+enum { SIP_APPLY_WHOLE = 0, SIP_APPLY_X_FIBERS = 1, SIP_APPLY_Z_FIBERS = 2 };
 
 typedef struct {
   const double *kernel;   /* host, kh*kw taps, row major (z rows, x columns)    */

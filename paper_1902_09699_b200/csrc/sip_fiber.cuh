@@ -1,0 +1,224 @@
+// sip_fiber.cuh -- per-fiber projections (NEXT-1; "the projection
+// onto a simple set is now applied to each row/column independently").
+//
+// A fiber set's operator output field (single block, grid-shaped, pads 0) is
+// split into x-fibers (rows: fixed z, y) or z-fibers (columns: fixed y, x);
+// every fiber is projected on its own: cardinality keeps its k largest |w|
+// (ties to the lowest index, reading L6), the l1 ball soft-thresholds it at
+// the Duchi threshold of its sorted magnitudes (reading L5).  One CTA per
+// fiber: the fiber's keys are sorted in shared memory by a bitonic network
+// (<= 4096 entries), so the selection is exact and local -- no global
+// histogram.  The kernel also forms Algorithm 2's beta-side products and,
+// on check iterations, the Eq. 26 numerator ||s - P(s)||^2 of these sets.
+#pragma once
+#include "sip_pass.cuh"
+
+namespace sip {
+
+constexpr int FIB_MAX = 4096;
+
+// location of entry t of fiber f in the padded field; fibers that are pads
+// (D_z x-fibers in the last global plane, D_y x-fibers in the last row,
+// D_x z-fibers in the last column) are skipped by the caller
+__device__ __forceinline__ int64_t fib_pt(const Geo& g, int mode, int f, int t) {
+  if (mode == 1) return (int64_t)f * g.nx + t;                       // f = iz * ny + iy
+  const int iy = f / g.nx, ix = f - iy * g.nx;                       // f = iy * nx + ix
+  return ((int64_t)t * g.ny + iy) * g.nx + ix;
+}
+__device__ __forceinline__ bool fib_is_pad(const Geo& g, int mode, int prim, int f) {
+  if (mode == 1) {
+    const int iz = f / g.ny, iy = f - iz * g.ny;
+    return (prim == PRIM_Z && iz + g.z0 >= g.nz_g - 1) || (prim == PRIM_Y && iy >= g.ny - 1);
+  }
+  const int iy = f / g.nx, ix = f - iy * g.nx;
+  return (prim == PRIM_X && ix >= g.nx - 1) || (prim == PRIM_Y && iy >= g.ny - 1);
+}
+
+// bitonic sort of n2 (power of 2) (key, index) pairs in shared memory into
+// descending key order, equal keys by ascending index (reading L6)
+__device__ inline void bitonic_desc(unsigned long long* k, short* ix, int n2) {
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < n2 / 2; t += BLOCK) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool desc = ((lo & size) == 0);
+        const unsigned long long a = k[lo], b = k[hi];
+        const short ia = ix[lo], ib = ix[hi];
+        const bool b_first = b > a || (b == a && ib < ia);   // b ranks before a
+        if (b_first == desc) { k[lo] = b; k[hi] = a; ix[lo] = ib; ix[hi] = ia; }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// inclusive prefix sums of u[0..L) in place (fp64): per-thread contiguous
+// runs, then an exclusive scan of the run totals across the CTA
+__device__ inline void block_prefix(double* u, int L, double* sh /* >= NWARP */) {
+  const int per = (L + BLOCK - 1) / BLOCK;
+  const int b = threadIdx.x * per, e = min(L, b + per);
+  double run = 0.0;
+  for (int t = b; t < e; ++t) run += u[t];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double inc = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double n = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += n;
+  }
+  __syncthreads();
+  if (lane == 31) sh[w] = inc;
+  __syncthreads();
+  double off = inc - run;
+  for (int q = 0; q < w; ++q) off += sh[q];
+  for (int t = b; t < e; ++t) { off += u[t]; u[t] = off; }
+  __syncthreads();
+}
+
+// projection of one fiber held in v[0..L) (storage precision) into y[0..L);
+// keys / ix / sums are scratch.  Exact: cardinality by sorting (|w|, index)
+// -- |w| in the field's precision (reading L27) -- and the l1 ball by
+// Duchi's sorted prefix sums in fp64 (reading L5).
+template <class T>
+__device__ void fib_project(int kind, int L, const T* v, T* y, long long k, double sigma,
+                            unsigned long long* keys, short* ix, double* sums, double* sh) {
+  using K = KeyT<T>;
+  int n2 = 1;
+  while (n2 < L) n2 <<= 1;
+  if (kind == K_CARD && k >= L) {
+    for (int t = threadIdx.x; t < L; t += BLOCK) y[t] = v[t];
+    __syncthreads();
+    return;
+  }
+  // the bit pattern of |w| orders magnitudes; padding sorts last (key 0, index >= L)
+  for (int t = threadIdx.x; t < n2; t += BLOCK) {
+    keys[t] = t < L ? (unsigned long long)K::key(v[t]) : 0ull;
+    ix[t] = (short)t;
+  }
+  bitonic_desc(keys, ix, n2);
+  if (kind == K_CARD) {   // keep the first k in (|w| desc, index asc) order
+    for (int t = threadIdx.x; t < L; t += BLOCK) y[t] = (T)0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < L && j < k; j += BLOCK) y[ix[j]] = v[ix[j]];
+    __syncthreads();
+    return;
+  }
+  // l1 ball: u = sorted |w|, S_j = u_1 + ... + u_j
+  for (int t = threadIdx.x; t < L; t += BLOCK) sums[t] = (double)K::val((typename K::U)keys[t]);
+  __syncthreads();
+  block_prefix(sums, L, sh);
+  __shared__ int s_rho;
+  __shared__ double s_theta;
+  if (threadIdx.x == 0) s_rho = 0;
+  __syncthreads();
+  const double tot = L > 0 ? sums[L - 1] : 0.0;
+  const bool inside = tot <= sigma;
+  if (!inside && sigma > 0.0) {   // largest j with u_j - (S_j - sigma) / j > 0 (Duchi)
+    for (int t = threadIdx.x; t < L; t += BLOCK) {
+      const double u = (double)K::val((typename K::U)keys[t]);
+      if (u - (sums[t] - sigma) / (double)(t + 1) > 0.0) atomicMax(&s_rho, t + 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s_theta = s_rho > 0 ? (sums[s_rho - 1] - sigma) / (double)s_rho : 0.0;
+  __syncthreads();
+  const double th = s_theta;
+  for (int t = threadIdx.x; t < L; t += BLOCK) {
+    const T w = v[t];
+    if (inside) { y[t] = w; continue; }
+    if (sigma <= 0.0) { y[t] = (T)0; continue; }
+    const double a = fabs((double)w) - th;
+    y[t] = a > 0.0 ? (T)(w > (T)0 ? a : -a) : (T)0;
+  }
+  __syncthreads();
+}
+
+// k_fiber: y = P(w) per fiber, v = rho (y - w) (L26), Alg. 2 beta-side sums,
+// Eq. 26 numerator on s (check iterations); sums land in C.sums like pass 2's
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
+  Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  unsigned long long* keys = reinterpret_cast<unsigned long long*>(fsm);        // [FIB_MAX]
+  double* sums = reinterpret_cast<double*>(keys + FIB_MAX);                      // [FIB_MAX]
+  T* vin = reinterpret_cast<T*>(sums + FIB_MAX);                                 // [FIB_MAX]
+  T* vout = vin + FIB_MAX;                                                       // [FIB_MAX]
+  short* ix = reinterpret_cast<short*>(vout + FIB_MAX);                          // [FIB_MAX]
+  __shared__ double sh[NWARP + 1];
+  __shared__ double out[4 * MAXP];
+  const Geo& g = P.g;
+  const IterFlags f = iter_flags<2, 2>(C);
+  const int par = C.k & 1;
+  double acc[4] = {0, 0, 0, 0};
+  __shared__ double accs[4 * MAXP];
+  for (int v = threadIdx.x; v < 4 * MAXP; v += BLOCK) accs[v] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < P.P; ++i) {
+    const SetD<T>& S = P.set[i];
+    if (!S.fib) continue;
+    const int prim = S.prim[0];
+    const int nfib = S.fib == 1 ? g.nz * g.ny : g.ny * g.nx;
+    const int L = S.flen;
+    const T rho = (T)C.rho[i];
+    const long long kk = C.kcard[i];
+    const double sg = C.sigma[i];
+    T* yw = S.y[par ^ 1];
+    T* vw = S.v[par ^ 1];
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+    for (int fb = blockIdx.x; fb < nfib; fb += gridDim.x) {
+      if (fib_is_pad(g, S.fib, prim, fb)) continue;
+      for (int t = threadIdx.x; t < L; t += BLOCK) vin[t] = S.w[fib_pt(g, S.fib, fb, t)];
+      __syncthreads();
+      fib_project<T>(S.kind, L, vin, vout, kk, sg, keys, ix, sums, sh);
+      for (int t = threadIdx.x; t < L; t += BLOCK) {
+        const int64_t pt = fib_pt(g, S.fib, fb, t);
+        const T y = vout[t];
+        const T vt = rho * (y - vin[t]);                 // Eq. 21 as rho (y - w), L26
+        if (f.dots) {
+          const T dg = yw[pt] - y, dv = vt - vw[pt];
+          acc[0] += (double)(dg * dv); acc[1] += (double)(dg * dg); acc[2] += (double)(dv * dv);
+        }
+        yw[pt] = y;
+        vw[pt] = vt;
+      }
+      __syncthreads();
+      if (f.check && S.s) {   // Eq. 26 numerator: the per-fiber projection of s
+        for (int t = threadIdx.x; t < L; t += BLOCK) vin[t] = S.s[fib_pt(g, S.fib, fb, t)];
+        __syncthreads();
+        fib_project<T>(S.kind, L, vin, vout, kk, sg, keys, ix, sums, sh);
+        for (int t = threadIdx.x; t < L; t += BLOCK) {
+          const double d = (double)vin[t] - (double)vout[t];
+          acc[3] += d * d;
+        }
+        __syncthreads();
+      }
+    }
+    for (int q = 0; q < 4; ++q) {
+      const double a = block_sum(acc[q], sh);
+      if (threadIdx.x == 0) accs[4 * i + q] = a;
+    }
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < 4 * P.P; v += BLOCK) P.partials[(size_t)blockIdx.x * 4 * P.P + v] = accs[v];
+  if (last_block(P.counter)) {
+    reduce_partials(P.partials, 4 * P.P, out, sh);
+    if (threadIdx.x == 0) {
+      *P.counter = 0u;
+      for (int i = 0; i < P.P; ++i) {
+        if (!P.set[i].fib) continue;
+        C.sums[i][SLOT_GV] = out[4 * i + 0];
+        C.sums[i][SLOT_GG] = out[4 * i + 1];
+        C.sums[i][SLOT_VV] = out[4 * i + 2];
+        C.sums[i][SLOT_FN] = out[4 * i + 3];
+      }
+    }
+  }
+}
+
+__host__ inline size_t fiber_smem(int dsize) { return (size_t)FIB_MAX * (8 + 8 + 2 * dsize + 2); }
+
+}  // namespace sip

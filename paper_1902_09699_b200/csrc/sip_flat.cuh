@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(BLOCK) k_tiecountf(const __grid_constant__ Pro
   bool any = false;
   for (int i = 0; i < P.P; ++i) {
     const SetD<T>& S = P.set[i];
-    if (S.kind != K_CARD) continue;
+    if (S.kind != K_CARD || S.job < 0) continue;
     const Job& J = C.job[S.job];
     if (J.mode != JM_DONE || !J.ties) continue;
     any = true;
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(BLOCK) k_tiecountf(const __grid_constant__ Pro
   if (last_block(P.counter)) {
     for (int i = 0; i < P.P; ++i) {
       const SetD<T>& S = P.set[i];
-      if (S.kind != K_CARD) continue;
+      if (S.kind != K_CARD || S.job < 0) continue;
       const Job& J = C.job[S.job];
       if (J.mode != JM_DONE || !J.ties) continue;
       int* tc = P.tiecnt + (size_t)S.job * P.ntiles_max;

@@ -1056,7 +1056,7 @@ __device__ void control_body(const Prob<T>& P, Ctrl& C) {
       const int kd = P.set[i].kind;
       const double s2 = C.sums[i][SLOT_S2];
       double fn = C.sums[i][SLOT_FN];
-      if (kd == K_L1 || kd == K_CARD) {
+      if ((kd == K_L1 || kd == K_CARD) && P.set[i].sjob >= 0) {   // fiber sets: k_fiber's FN
         const Job& J = C.job[P.set[i].sjob];
         if (J.mode == JM_INSIDE || J.mode == JM_ALL) fn = 0.0;
         else if (J.mode == JM_ZERO) fn = s2;

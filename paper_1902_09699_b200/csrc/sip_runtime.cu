@@ -21,6 +21,7 @@
 #include "sip_team.cuh"
 #include "sip_cgs.cuh"
 #include "sip_cgt.cuh"
+#include "sip_fiber.cuh"
 
 using namespace sip;
 
@@ -48,6 +49,8 @@ struct HostSet {
   std::vector<uint8_t> mask;
   int64_t M = 0;
   int zero_in = 1;
+  int fib = 0;          // 0 whole vector; 1 x-fibers; 2 z-fibers (app_mode)
+  int64_t flen = 0;     // fiber length
 };
 
 struct Options {
@@ -103,6 +106,9 @@ struct Engine : EngineBase {
   double h[3];
   cudaStream_t stream;
   int nsm = 148;
+  int nfib_sets = 0;             // sets applied per fiber (k_fiber)
+  int g_fib = 0;
+  size_t smem_fib = 0;
   const std::vector<HostSet>* sets;
   int p, P;
   // device state
@@ -226,12 +232,17 @@ struct Engine : EngineBase {
       }
       S.global = (S.kind == K_L1 || S.kind == K_L2 || S.kind == K_ANN || S.kind == K_CARD);
       S.job = S.sjob = -1;
-      if (S.kind == K_L1 || S.kind == K_CARD) { S.job = njobs++; S.sjob = njobs++; }
+      S.fib = (i < p) ? s[i].fib : 0;
+      // fiber length on this engine's own grid (multilevel levels differ)
+      S.flen = !S.fib ? 0 : S.fib == 1 ? g.nx - (S.prim[0] == PRIM_X ? 1 : 0)
+                                       : nz_g - (S.prim[0] == PRIM_Z ? 1 : 0);
+      if ((S.kind == K_L1 || S.kind == K_CARD) && !S.fib) { S.job = njobs++; S.sjob = njobs++; }
+      if (S.fib) nfib_sets++;
       for (int b = 0; b < S.nblk; ++b) Pr.has[S.prim[b]] = 1;
       if (S.global) Pr.nglob++;
       for (int b = 0; b < S.nblk; ++b) {
         Pr.seg_set[1 + Pr.nseg1] = (short)i; Pr.seg_blk[1 + Pr.nseg1] = (short)b; Pr.nseg1++;
-        if (S.global) { Pr.seg2_set[Pr.nseg2] = (short)i; Pr.seg2_blk[Pr.nseg2] = (short)b; Pr.nseg2++; }
+        if (S.global && !S.fib) { Pr.seg2_set[Pr.nseg2] = (short)i; Pr.seg2_blk[Pr.nseg2] = (short)b; Pr.nseg2++; }
       }
     }
     Pr.nseg1 += 1;   // segment 0: the per-point x work
@@ -314,6 +325,8 @@ struct Engine : EngineBase {
     // vectorised CG kernels: W = 16/sizeof(T) points per thread along x
     constexpr int W = VT<T>::W;
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
+    if (nfib_sets && !vec)
+      throw SipError{SIP_ERR_CONFIG, "per-fiber sets need nx % (16 / sizeof(dtype)) == 0 and no blur/mask operator"};
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
     // lean CG / rhs: one wave of resident CTAs (4 per SM)
     g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
@@ -420,8 +433,19 @@ struct Engine : EngineBase {
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
     const int gz_ = std::max(zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1,
                              sg.on ? sg.tiles_x * sg.tiles_y * sg.nzc : 1);
+    // per-fiber sets (sip_fiber.cuh): one CTA per fiber, a single wave
+    if (nfib_sets) {
+      int nf = 1;
+      for (int i = 0; i < p; ++i)
+        if (Pr.set[i].fib) nf = std::max(nf, Pr.set[i].fib == 1 ? g.nz * g.ny : g.ny * g.nx);
+      smem_fib = fiber_smem((int)sizeof(T));
+      CU(cudaFuncSetAttribute(k_fiber<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fib));
+      int per = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fiber<T>, BLOCK, smem_fib));
+      g_fib = std::max(1, std::min(nf, nsm * std::max(per, 1)));
+    }
     const int gmax = std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
-                              std::max(std::max(g_cgt1, g_cgt2), g_cg2f));
+                              std::max(std::max(std::max(g_cgt1, g_cgt2), g_cg2f), g_fib));
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -669,7 +693,7 @@ struct Engine : EngineBase {
     ++launches;
   }
   bool has_card() const {
-    for (int i = 0; i < p; ++i) if (Pr.set[i].kind == K_CARD) return true;
+    for (int i = 0; i < p; ++i) if (Pr.set[i].kind == K_CARD && Pr.set[i].job >= 0) return true;
     return false;
   }
   void launch_tie() {
@@ -699,8 +723,12 @@ struct Engine : EngineBase {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
       if (has_card()) { launch_tie(); mark(KB_TIE); }
     }
-    if (Pr.nglob > 0) {
+    if (Pr.nseg2 > 0) {
       launch_pass2(kpos);
+      ++launches; mark(KB_PASS2);
+    }
+    if (nfib_sets) {   // per-fiber projections, after pass 2's sums
+      lk(k_fiber<T>, g_fib, BLOCK, smem_fib, Pr);
       ++launches; mark(KB_PASS2);
     }
     launch_control(); mark(KB_CTRL);
@@ -779,7 +807,7 @@ struct Engine : EngineBase {
       c.u_k[i] = hs.prm.k;
       c.rel[i] = hs.prm.relative;
       c.zin[i] = hs.zero_in;
-      c.mreal[i] = set_len_global(i);   // compact M on this level's grid (k = floor(k_frac M_l), L23)
+      c.mreal[i] = Pr.set[i].fib ? Pr.set[i].flen : set_len_global(i);   // per fiber for fiber sets
     }
     c.mreal[p] = (long long)nz_g * Pr.g.plane;
     make_coeffs(Pr, c.rho, &c.cI, &c.cz, &c.cy, &c.cx, &c.cF);
@@ -1055,6 +1083,8 @@ struct Team : EngineBase {
   void setup(int ndim, int nz_g, int ny, int nx, const double* h, cudaStream_t st, const std::vector<HostSet>& s,
              int G_, int r0, int nlocal, Comm* c) {
     G = G_; comm = c; stream = st;
+    for (const HostSet& hs : s)
+      if (hs.fib) throw SipError{SIP_ERR_CONFIG, "per-fiber sets on z slabs: not in this build"};
     for (const HostSet& hs : s)
       if (!hs.lo_vec.empty() || !hs.hi_vec.empty())
         throw SipError{SIP_ERR_CONFIG, "per-entry bounds on z slabs: not in this build"};
@@ -1749,7 +1779,9 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     }
     e->hc = c;
     CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
-    if (S.job >= 0) {
+    if (S.fib) {   // per-fiber projection: k_fiber writes y[1]
+      k_fiber<T><<<e->g_fib, BLOCK, e->smem_fib, e->stream>>>(e->Pr);
+    } else if (S.job >= 0) {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
         if (e->vec) e->launch_select(r);
         else k_select<T><<<e->g_sel, BLOCK, 0, e->stream>>>(e->Pr, r);
@@ -1759,7 +1791,8 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
         else k_tiecount<T><<<e->g_p2, BLOCK, 0, e->stream>>>(e->Pr);
       }
     }
-    if (e->vec) k_pass2t<T, 2, 2><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
+    if (S.fib) {
+    } else if (e->vec) k_pass2t<T, 2, 2><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
     else k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
   } else {
     // pointwise: gamma = 0 and v = 0 make x-bar = y_old and w = y_old, so
@@ -2031,6 +2064,19 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type 
     } else if (type == SIP_SET_CARDINALITY) {
       if (prm->relative) { if (!(prm->k_frac >= 0 && prm->k_frac <= 1)) return SIP_ERR_PARAM; }
       else if (prm->k < 0 || prm->k > hs.M) return SIP_ERR_PARAM;
+    }
+    // per-fiber application (NEXT-1)
+    if (prm->app_mode < SIP_APPLY_WHOLE || prm->app_mode > SIP_APPLY_Z_FIBERS) return SIP_ERR_ARG;
+    hs.fib = 0;
+    hs.flen = 0;
+    if (prm->app_mode != SIP_APPLY_WHOLE && type != SIP_SET_BOUNDS) {   // bounds: separable, same set
+      if (type != SIP_SET_CARDINALITY && type != SIP_SET_L1_BALL) { g->err = "per-fiber sets: cardinality and l1 ball only"; return SIP_ERR_CONFIG; }
+      if (op == SIP_OP_TV || op == SIP_OP_BLUR_MASK) { g->err = "per-fiber sets need a single-block operator"; return SIP_ERR_CONFIG; }
+      if (type == SIP_SET_L1_BALL && prm->relative) return SIP_ERR_PARAM;
+      hs.fib = prm->app_mode;
+      hs.flen = prm->app_mode == SIP_APPLY_X_FIBERS ? nx - (op == SIP_OP_DX ? 1 : 0) : nz - (op == SIP_OP_DZ ? 1 : 0);
+      if (hs.flen > 4096) { g->err = "per-fiber sets: fibers longer than 4096"; return SIP_ERR_CONFIG; }
+      if (type == SIP_SET_CARDINALITY && !prm->relative && prm->k > hs.flen) return SIP_ERR_PARAM;
     }
     g->sets.push_back(std::move(hs));
     g->eng.reset();

@@ -75,7 +75,7 @@ __device__ inline void fin_tie(const Prob<T>& P, Ctrl& C) {
   const int tpb = (nch + BLOCK - 1) / BLOCK;
   for (int i = 0; i < P.P; ++i) {
     const SetD<T>& S = P.set[i];
-    if (S.kind != K_CARD) continue;
+    if (S.kind != K_CARD || S.job < 0) continue;
     const Job& J = C.job[S.job];
     if (J.mode != JM_DONE || !J.ties) continue;
     if (threadIdx.x == 0) {

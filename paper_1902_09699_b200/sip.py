@@ -37,6 +37,7 @@ class SetParams(C.Structure):
         ("lo_vec", C.c_void_p), ("hi_vec", C.c_void_p),
         ("sigma", C.c_double), ("sigma_lo", C.c_double), ("sigma_hi", C.c_double),
         ("k", C.c_int64), ("k_frac", C.c_double), ("relative", C.c_int),
+        ("app_mode", C.c_int),
     ]
 
 
@@ -205,6 +206,7 @@ class Grid:
         prm.k = int(sd.k)
         prm.k_frac = float(sd.k_frac)
         prm.relative = int(bool(sd.relative))
+        prm.app_mode = {"": 0, "x": 1, "z": 2}[getattr(sd, "app_mode", "") or ""]
         desc = None
         if sd.op == "BLUR_MASK":
             K = np.ascontiguousarray(sd.kernel, dtype=np.float64)

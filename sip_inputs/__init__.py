@@ -269,6 +269,15 @@ def tiny(seed=100, shape=(8, 8), kinds=("bounds", "l1", "slope")) -> Problem:
             sets.append(SetDef("DZ", "l2", sigma=0.5, relative=True))
         elif k == "l1x":
             sets.append(SetDef("DX", "l1", sigma=0.4, relative=True))
+        # per-fiber sets (NEXT-1): x-fibers are rows, z-fibers columns
+        elif k == "card_rows":
+            sets.append(SetDef("DX", "card", k_frac=0.3, relative=True, app_mode="x"))
+        elif k == "card_cols":
+            sets.append(SetDef("DZ", "card", k_frac=0.3, relative=True, app_mode="z"))
+        elif k == "l1_rows":
+            sets.append(SetDef("DX", "l1", sigma=120.0 * (shape[-1] - 1), app_mode="x"))
+        elif k == "l1_cols":
+            sets.append(SetDef("I", "l1", sigma=2500.0 * shape[0], app_mode="z"))
         else:
             raise KeyError(k)
     return Problem(f"tiny{seed}", tuple(shape), "f64", m, sets,
