@@ -255,8 +255,10 @@ sip_status sip_get_sizes(sip_grid g, int *p, int64_t *n_local, int set_id, int64
 /* Device time per kernel kind of the last sip_project run with option
    "profile" = 1 (CUDA event nodes between consecutive kernels, captured in
    the graph).  Kinds, in order: 0 blur (S G p), 1 rhs, 2 cg1, 3 cg2,
-   4 pass1, 5 select, 6 tiecount, 7 pass2, 8 control.  ms[q] is the summed
-   milliseconds, count[q] the number of launches (arrays of n <= 9). */
+   4 pass1, 5 select, 6 tiecount, 7 pass2, 8 control, 9 comm (z-slab
+   exchanges), 10 cgx (deferred CG x update), 11 fiber (per-fiber
+   projections).  ms[q] is the summed milliseconds, count[q] the number of
+   launches (arrays of n <= 12). */
 sip_status sip_get_profile(sip_grid g, int n, double *ms, int64_t *count);
 
 /* Number of kernel launches enqueued by the last sip_project (bench evidence). */

@@ -97,6 +97,7 @@ struct SetD {
   int job, sjob;          // select jobs on w (every iteration) / on s (check)
   int first_real;         // point index of the first entry (annulus at 0, L7)
   int fib, flen;          // per-fiber application (0 whole; 1 x-, 2 z-fibers) and fiber length
+  int fpath;              // 1: warp kernel k_fiberw; 0: CTA-per-fiber sort kernel k_fiber
   T* y[2];                // ping-pong y_i (parity k & 1), nblk blocks of ld
   T* v[2];
   T* vh0;                 // Alg. 2 snapshot v-hat^{k0}

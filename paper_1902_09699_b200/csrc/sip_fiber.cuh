@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T>
   __syncthreads();
   for (int i = 0; i < P.P; ++i) {
     const SetD<T>& S = P.set[i];
-    if (!S.fib) continue;
+    if (!S.fib || S.fpath) continue;
     const int prim = S.prim[0];
     const int nfib = S.fib == 1 ? g.nz * g.ny : g.ny * g.nx;
     const int L = S.flen;
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T>
     if (threadIdx.x == 0) {
       *P.counter = 0u;
       for (int i = 0; i < P.P; ++i) {
-        if (!P.set[i].fib) continue;
+        if (!P.set[i].fib || P.set[i].fpath) continue;
         C.sums[i][SLOT_GV] = out[4 * i + 0];
         C.sums[i][SLOT_GG] = out[4 * i + 1];
         C.sums[i][SLOT_VV] = out[4 * i + 2];
@@ -220,5 +220,294 @@ __global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T>
 }
 
 __host__ inline size_t fiber_smem(int dsize) { return (size_t)FIB_MAX * (8 + 8 + 2 * dsize + 2); }
+
+// ---------------------------------------------------------------------------
+// k_fiberw: one warp per fiber, the fiber in registers (E entries per lane,
+// entry t = e * 32 + lane, fibers of <= 32 * FW_E entries).  No sort: both
+// projections are found by a bitwise search over the |w| key space with
+// warp-wide counts / sums (BITS steps, 31 fp32 / 63 fp64):
+//  - cardinality: tau = the k-th largest key, the largest key with
+//    #{key >= tau} >= k; keep key > tau and the first k - #{key > tau}
+//    entries equal to tau in index order (ballot prefix, reading L6);
+//  - l1 ball (Duchi, reading L5): g(t) = sum max(|w| - t, 0) decreases in t
+//    and Duchi's condition u_j - (S_j - sigma)/j > 0 is g(u_j) < sigma, so
+//    rho = #{|w| > t'} for the largest key t' with g(t') >= sigma and
+//    theta = (sum_{|w| > t'} |w| - sigma) / rho -- the sorted algorithm's
+//    theta without the sort.
+// x-fibers are contiguous rows: each warp reads its row straight from HBM;
+// z-fibers (stride ny*nx) go through a shared tile of 32 adjacent columns
+// x L planes so every HBM access is a coalesced row segment.
+constexpr int FW_E = 16;
+constexpr int FW_TP = 33;   // tile pitch (32 columns + 1: conflict-free column reads)
+
+__device__ __forceinline__ double fw_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int fw_cnt(int v) { return __reduce_add_sync(0xffffffffu, v); }
+
+template <class T, int E>
+__device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long long k, double sigma, int L,
+                                             int lane) {
+  using K = KeyT<T>;
+  using U = typename K::U;
+  if (kind == K_CARD) {
+    if (k >= L) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) y[e] = w[e];
+      return;
+    }
+    if (k <= 0) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) y[e] = (T)0;
+      return;
+    }
+    U tau = 0;   // entries past L are 0: key 0 never reaches a candidate >= 1
+    for (int b = K::BITS - 1; b >= 0; --b) {
+      const U cand = tau | ((U)1 << b);
+      int c = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) c += K::key(w[e]) >= cand ? 1 : 0;
+      if (fw_cnt(c) >= k) tau = cand;
+    }
+    if (tau == 0) {   // fewer than k nonzeros: every nonzero kept, the rest is 0 = w
+#pragma unroll
+      for (int e = 0; e < E; ++e) y[e] = w[e];
+      return;
+    }
+    int gt = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) gt += K::key(w[e]) > tau ? 1 : 0;
+    const long long need = k - fw_cnt(gt);
+    const unsigned lt = (1u << lane) - 1u;
+    int run = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const U key = K::key(w[e]);
+      const unsigned tie = __ballot_sync(0xffffffffu, key == tau);
+      const bool keep = key > tau || (key == tau && run + __popc(tie & lt) < need);
+      run += __popc(tie);
+      y[e] = keep ? w[e] : (T)0;
+    }
+    return;
+  }
+  double a1 = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) a1 += fabs((double)w[e]);
+  const double tot = fw_sum(a1);
+  if (tot <= sigma) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) y[e] = w[e];
+    return;
+  }
+  if (sigma <= 0.0) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) y[e] = (T)0;
+    return;
+  }
+  U tp = 0;   // g(0) = tot > sigma
+  for (int b = K::BITS - 1; b >= 0; --b) {
+    const U cand = tp | ((U)1 << b);
+    const double v = (double)K::val(cand);   // NaN patterns: no term counts, g = 0
+    double gs = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double a = fabs((double)w[e]);
+      gs += a > v ? a - v : 0.0;
+    }
+    if (fw_sum(gs) >= sigma) tp = cand;
+  }
+  int c = 0;
+  double sa = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (K::key(w[e]) > tp) { ++c; sa += fabs((double)w[e]); }
+  const double th = (fw_sum(sa) - sigma) / (double)fw_cnt(c);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const double a = fabs((double)w[e]) - th;
+    y[e] = a > 0.0 ? (T)(w[e] > (T)0 ? a : -a) : (T)0;
+  }
+}
+
+// shared bytes of the z-fiber tiles (w and y, L x 33 each)
+__host__ __device__ inline size_t fiberw_smem(int L, int dsize) { return (size_t)2 * L * FW_TP * dsize; }
+// entries per lane for a fiber length (the kernel instantiation)
+__host__ __device__ inline int fiberw_e(int L) { return L <= 128 ? 4 : L <= 256 ? 8 : 16; }
+
+// one launch per fiber set i; E = fiberw_e(flen).  The previous y / v (Alg. 2
+// products) are loaded before the threshold search so their latency hides
+// behind it; z tiles move through shared memory in batches of FW_U rows.
+constexpr int FW_U = 8;
+
+template <class T, int E>
+__global__ void __launch_bounds__(BLOCK) k_fiberw(const __grid_constant__ Prob<T> P, int i) {
+  pdl_begin();
+  Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  extern __shared__ __align__(16) unsigned char fsm[];
+  __shared__ double sh[NWARP + 1];
+  __shared__ double out[4];
+  const Geo& g = P.g;
+  const IterFlags f = iter_flags<2, 2>(C);
+  const int par = C.k & 1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const SetD<T>& S = P.set[i];
+  const int prim = S.prim[0];
+  const int L = S.flen;
+  const T rho = (T)C.rho[i];
+  const long long kk = C.kcard[i];
+  const double sg = C.sigma[i];
+  T* yw = S.y[par ^ 1];
+  T* vw = S.v[par ^ 1];
+  const bool chk = f.check && S.s;
+  double acc[4] = {0, 0, 0, 0};
+  T w[E], y[E];
+  if (S.fib == 1) {   // x-fibers: a warp per row, straight from HBM
+    const int nf = g.nz * g.ny;
+    for (int fb = blockIdx.x * NWARP + wid; fb < nf; fb += gridDim.x * NWARP) {
+      if (fib_is_pad(g, 1, prim, fb)) continue;
+      const int64_t base = (int64_t)fb * g.nx;
+      T y0[E], v0[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int t = e * 32 + lane;
+        w[e] = t < L ? S.w[base + t] : (T)0;
+        y0[e] = (f.dots && t < L) ? yw[base + t] : (T)0;
+        v0[e] = (f.dots && t < L) ? vw[base + t] : (T)0;
+      }
+      fw_project_e<T, E>(S.kind, w, y, kk, sg, L, lane);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int t = e * 32 + lane;
+        if (t >= L) continue;
+        const T vt = rho * (y[e] - w[e]);                  // Eq. 21 as rho (y - w), L26
+        if (f.dots) {
+          const T dg = y0[e] - y[e], dv = vt - v0[e];
+          acc[0] += (double)(dg * dv); acc[1] += (double)(dg * dg); acc[2] += (double)(dv * dv);
+        }
+        yw[base + t] = y[e];
+        vw[base + t] = vt;
+      }
+      if (chk) {   // Eq. 26 numerator of this fiber
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int t = e * 32 + lane;
+          w[e] = t < L ? S.s[base + t] : (T)0;
+        }
+        fw_project_e<T, E>(S.kind, w, y, kk, sg, L, lane);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const double d = (double)w[e] - (double)y[e];   // 0 past L (w = y = 0 there)
+          acc[3] += d * d;
+        }
+      }
+    }
+  } else {   // z-fibers: tiles of 32 adjacent columns staged in shared memory
+    T* tw = reinterpret_cast<T*>(fsm);
+    T* ty = tw + (size_t)L * FW_TP;
+    const int ntx = (g.nx + 31) / 32;
+    const int ntile = g.ny * ntx;
+    const int64_t pl = (int64_t)g.plane;
+    const int nq = L * 32;
+    for (int tl = blockIdx.x; tl < ntile; tl += gridDim.x) {
+      const int iy = tl / ntx, ix0 = (tl - iy * ntx) * 32;
+      const int64_t b0 = (int64_t)iy * g.nx + ix0;
+      const int c_ = threadIdx.x & 31;
+      const bool colok = ix0 + c_ < g.nx && !fib_is_pad(g, 2, prim, iy * g.nx + ix0 + c_);
+      for (int ph = 0; ph < (chk ? 2 : 1); ++ph) {
+        const T* src = ph == 0 ? S.w : S.s;
+        for (int q0 = threadIdx.x; q0 < nq; q0 += BLOCK * FW_U) {   // batched coalesced loads
+          T r[FW_U];
+#pragma unroll
+          for (int u = 0; u < FW_U; ++u) {
+            const int q = q0 + u * BLOCK;
+            r[u] = (q < nq && ix0 + c_ < g.nx) ? src[(q >> 5) * pl + b0 + c_] : (T)0;
+          }
+#pragma unroll
+          for (int u = 0; u < FW_U; ++u) {
+            const int q = q0 + u * BLOCK;
+            if (q < nq) tw[(q >> 5) * FW_TP + c_] = r[u];
+          }
+        }
+        __syncthreads();
+        for (int c = wid; c < 32; c += NWARP) {
+          const int ix = ix0 + c;
+          if (ix >= g.nx || fib_is_pad(g, 2, prim, iy * g.nx + ix)) continue;   // warp-uniform
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int t = e * 32 + lane;
+            w[e] = t < L ? tw[t * FW_TP + c] : (T)0;
+          }
+          fw_project_e<T, E>(S.kind, w, y, kk, sg, L, lane);
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int t = e * 32 + lane;
+            if (ph == 0) {
+              if (t < L) ty[t * FW_TP + c] = y[e];
+            } else {
+              const double d = (double)w[e] - (double)y[e];
+              acc[3] += d * d;
+            }
+          }
+        }
+        __syncthreads();
+        if (ph == 0) {   // y, v = rho (y - w) and the Alg. 2 sums, coalesced
+          for (int q0 = threadIdx.x; q0 < nq; q0 += BLOCK * FW_U) {
+            T a0[FW_U], b0v[FW_U];
+#pragma unroll
+            for (int u = 0; u < FW_U; ++u) {
+              const int q = q0 + u * BLOCK;
+              const bool ok = q < nq && colok && f.dots;
+              a0[u] = ok ? yw[(q >> 5) * pl + b0 + c_] : (T)0;
+              b0v[u] = ok ? vw[(q >> 5) * pl + b0 + c_] : (T)0;
+            }
+#pragma unroll
+            for (int u = 0; u < FW_U; ++u) {
+              const int q = q0 + u * BLOCK;
+              if (q >= nq || !colok) continue;
+              const int t = q >> 5;
+              const int64_t pt = t * pl + b0 + c_;
+              const T wt = tw[t * FW_TP + c_], yt = ty[t * FW_TP + c_];
+              const T vt = rho * (yt - wt);
+              if (f.dots) {
+                const T dg = a0[u] - yt, dv = vt - b0v[u];
+                acc[0] += (double)(dg * dv); acc[1] += (double)(dg * dg); acc[2] += (double)(dv * dv);
+              }
+              yw[pt] = yt;
+              vw[pt] = vt;
+            }
+          }
+          __syncthreads();
+        }
+      }
+    }
+  }
+  double part[4];
+  for (int q = 0; q < 4; ++q) part[q] = block_sum(acc[q], sh);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) P.partials[(size_t)blockIdx.x * 4 + q] = part[q];
+  if (last_block(P.counter)) {
+    reduce_partials(P.partials, 4, out, sh);
+    if (threadIdx.x == 0) {
+      *P.counter = 0u;
+      C.sums[i][SLOT_GV] = out[0];
+      C.sums[i][SLOT_GG] = out[1];
+      C.sums[i][SLOT_VV] = out[2];
+      C.sums[i][SLOT_FN] = out[3];
+    }
+  }
+}
+
+// the warp kernel instantiation for a fiber length
+template <class T>
+struct FiberW {
+  using F = void (*)(Prob<T>, int);
+  static F of(int L) {
+    const int E = fiberw_e(L);
+    return E == 4 ? k_fiberw<T, 4> : E == 8 ? k_fiberw<T, 8> : k_fiberw<T, 16>;
+  }
+};
 
 }  // namespace sip

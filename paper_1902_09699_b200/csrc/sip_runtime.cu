@@ -107,8 +107,9 @@ struct Engine : EngineBase {
   cudaStream_t stream;
   int nsm = 148;
   int nfib_sets = 0;             // sets applied per fiber (k_fiber)
-  int g_fib = 0;
-  size_t smem_fib = 0;
+  int g_fib = 0, g_fibw = 0, nfib_sort = 0, nfib_warp = 0;
+  int g_fw[MAXP] = {0};
+  size_t smem_fib = 0, smem_fw[MAXP] = {0};
   const std::vector<HostSet>* sets;
   int p, P;
   // device state
@@ -238,6 +239,10 @@ struct Engine : EngineBase {
                                        : nz_g - (S.prim[0] == PRIM_Z ? 1 : 0);
       if ((S.kind == K_L1 || S.kind == K_CARD) && !S.fib) { S.job = njobs++; S.sjob = njobs++; }
       if (S.fib) nfib_sets++;
+      // warp kernel for fibers of <= 32 FW_E entries (z-fibers: tiles that
+      // fit in shared memory); SIP_FIBER_SORT=1 keeps the sort kernel (A/B)
+      S.fpath = S.fib && S.flen <= 32 * FW_E && !getenv("SIP_FIBER_SORT") &&
+                (S.fib == 1 || fiberw_smem(S.flen, (int)sizeof(T)) <= 200 * 1024);
       for (int b = 0; b < S.nblk; ++b) Pr.has[S.prim[b]] = 1;
       if (S.global) Pr.nglob++;
       for (int b = 0; b < S.nblk; ++b) {
@@ -436,16 +441,33 @@ struct Engine : EngineBase {
     // per-fiber sets (sip_fiber.cuh): one CTA per fiber, a single wave
     if (nfib_sets) {
       int nf = 1;
-      for (int i = 0; i < p; ++i)
-        if (Pr.set[i].fib) nf = std::max(nf, Pr.set[i].fib == 1 ? g.nz * g.ny : g.ny * g.nx);
-      smem_fib = fiber_smem((int)sizeof(T));
-      CU(cudaFuncSetAttribute(k_fiber<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fib));
+      for (int i = 0; i < p; ++i) {
+        const SetD<T>& S = Pr.set[i];
+        if (!S.fib) continue;
+        if (!S.fpath) { nfib_sort++; nf = std::max(nf, S.fib == 1 ? g.nz * g.ny : g.ny * g.nx); continue; }
+        nfib_warp++;
+      }
       int per = 0;
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fiber<T>, BLOCK, smem_fib));
-      g_fib = std::max(1, std::min(nf, nsm * std::max(per, 1)));
+      if (nfib_sort) {
+        smem_fib = fiber_smem((int)sizeof(T));
+        CU(cudaFuncSetAttribute(k_fiber<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fib));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fiber<T>, BLOCK, smem_fib));
+        g_fib = std::max(1, std::min(nf, nsm * std::max(per, 1)));
+      }
+      for (int i = 0; i < p; ++i) {   // warp kernel: one launch per set, its own single-wave grid
+        const SetD<T>& S = Pr.set[i];
+        if (!S.fib || !S.fpath) continue;
+        auto kern = FiberW<T>::of(S.flen);
+        smem_fw[i] = S.fib == 2 ? fiberw_smem(S.flen, (int)sizeof(T)) : 0;
+        CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, BLOCK, smem_fw[i]));
+        const int units = S.fib == 1 ? (g.nz * g.ny + NWARP - 1) / NWARP : g.ny * ((g.nx + 31) / 32);
+        g_fw[i] = std::max(1, std::min(units, nsm * std::max(per, 1)));
+        g_fibw = std::max(g_fibw, g_fw[i]);
+      }
     }
     const int gmax = std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
-                              std::max(std::max(std::max(g_cgt1, g_cgt2), g_cg2f), g_fib));
+                              std::max(std::max(std::max(g_cgt1, g_cgt2), g_cg2f), std::max(g_fib, g_fibw)));
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -554,7 +576,7 @@ struct Engine : EngineBase {
   // profiling: an event is recorded before the first kernel and after every
   // kernel; consecutive pairs give each kernel's device time (kind list)
   // KB_COMM: a z-slab site's exchange + finalisers (multi-rank only)
-  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, KB_CGX, NKIND };
+  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, KB_CGX, KB_FIBER, NKIND };
   bool prof = false;
   std::vector<cudaEvent_t> pev;      // events of one graph (capture order)
   std::vector<int> pkind;            // kind of the kernel ending at pev[i+1]
@@ -727,9 +749,14 @@ struct Engine : EngineBase {
       launch_pass2(kpos);
       ++launches; mark(KB_PASS2);
     }
-    if (nfib_sets) {   // per-fiber projections, after pass 2's sums
+    for (int i = 0; nfib_warp && i < p; ++i) {   // per-fiber projections, after pass 2's sums
+      if (!Pr.set[i].fib || !Pr.set[i].fpath) continue;
+      lk(FiberW<T>::of(Pr.set[i].flen), g_fw[i], BLOCK, smem_fw[i], Pr, i);
+      ++launches; mark(KB_FIBER);
+    }
+    if (nfib_sort) {
       lk(k_fiber<T>, g_fib, BLOCK, smem_fib, Pr);
-      ++launches; mark(KB_PASS2);
+      ++launches; mark(KB_FIBER);
     }
     launch_control(); mark(KB_CTRL);
   }
@@ -1779,8 +1806,9 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     }
     e->hc = c;
     CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
-    if (S.fib) {   // per-fiber projection: k_fiber writes y[1]
-      k_fiber<T><<<e->g_fib, BLOCK, e->smem_fib, e->stream>>>(e->Pr);
+    if (S.fib) {   // per-fiber projection: k_fiberw / k_fiber write y[1]
+      if (S.fpath) FiberW<T>::of(S.flen)<<<e->g_fw[set_id], BLOCK, e->smem_fw[set_id], e->stream>>>(e->Pr, set_id);
+      else k_fiber<T><<<e->g_fib, BLOCK, e->smem_fib, e->stream>>>(e->Pr);
     } else if (S.job >= 0) {
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) {
         if (e->vec) e->launch_select(r);
@@ -2226,7 +2254,7 @@ sip_status sip_get_profile(sip_grid g, int n, double* ms, int64_t* count) {
   return guarded(g, [&]() -> sip_status {
     if (!g->last) throw SipError{SIP_ERR_STATE, "no projection"};
     auto fill = [&](auto* e) {
-      for (int q = 0; q < n && q < 11; ++q) {
+      for (int q = 0; q < n && q < Engine<float>::NKIND; ++q) {
         if (ms) ms[q] = e->prof_ms[q];
         if (count) count[q] = e->prof_cnt[q];
       }

@@ -64,7 +64,7 @@ EXPORTS = [
     "sip_apply_op", "sip_apply_system", "sip_cg", "sip_project_set", "sip_get_state",
     "sip_get_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
 ]
-KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm", "cgx"]
+KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm", "cgx", "fiber"]
 
 _lib = None
 

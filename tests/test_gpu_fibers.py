@@ -38,6 +38,10 @@ def host(t):
 # DY rows, DX columns) and 2D / 3D
 CASES = [
     ((24, 64), "DX", "x"),
+    ((5, 4, 32), "DX", "x"),       # 31-entry fibers: one entry per lane
+    ((4, 8, 200), "DZ", "x"),      # E = 8 lanes' entries
+    ((300, 40), "DZ", "z"),        # 299-entry columns (E = 16), ragged column tile
+    ((64, 3, 36), "I", "z"),
     ((24, 64), "DZ", "x"),
     ((24, 64), "I", "z"),
     ((37, 100), "DZ", "z"),
@@ -69,10 +73,16 @@ def _case(shape, op, mode, kind, dtype, seed, ties=False):
     return sd, w
 
 
+@pytest.mark.parametrize("path", ["warp", "sort"])
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("kind", ["card", "card_ties", "l1"])
 @pytest.mark.parametrize("shape,op,mode", CASES)
-def test_project_set_per_fiber(shape, op, mode, kind, dtype):
+def test_project_set_per_fiber(shape, op, mode, kind, dtype, path, monkeypatch):
+    """path "warp": k_fiberw (bitwise threshold search, fibers <= 512);
+    "sort": k_fiber (bitonic sort, SIP_FIBER_SORT=1); fibers longer than
+    512 take the sort kernel on both"""
+    if path == "sort":
+        monkeypatch.setenv("SIP_FIBER_SORT", "1")
     base = "card" if kind.startswith("card") else "l1"
     sd, w = _case(shape, op, mode, base, dtype, 7 + len(shape) + len(op), ties=kind == "card_ties")
     g = Grid(shape, None, dtype)
@@ -120,8 +130,11 @@ FIBER_TINY = [
 ]
 
 
+@pytest.mark.parametrize("path", ["warp", "sort"])
 @pytest.mark.parametrize("seed,shape,kinds", FIBER_TINY)
-def test_tiny_fiber_control_flow(seed, shape, kinds):
+def test_tiny_fiber_control_flow(seed, shape, kinds, path, monkeypatch):
+    if path == "sort":
+        monkeypatch.setenv("SIP_FIBER_SORT", "1")
     prob = G.tiny(seed, shape, kinds)
     g = grid_for(prob)
     m = dev(prob.m, "f64")
