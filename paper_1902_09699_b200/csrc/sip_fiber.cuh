@@ -223,17 +223,19 @@ __host__ inline size_t fiber_smem(int dsize) { return (size_t)FIB_MAX * (8 + 8 +
 
 // ---------------------------------------------------------------------------
 // k_fiberw: one warp per fiber, the fiber in registers (E entries per lane,
-// entry t = e * 32 + lane, fibers of <= 32 * FW_E entries).  No sort: both
-// projections are found by a bitwise search over the |w| key space with
-// warp-wide counts / sums (BITS steps, 31 fp32 / 63 fp64):
-//  - cardinality: tau = the k-th largest key, the largest key with
-//    #{key >= tau} >= k; keep key > tau and the first k - #{key > tau}
-//    entries equal to tau in index order (ballot prefix, reading L6);
-//  - l1 ball (Duchi, reading L5): g(t) = sum max(|w| - t, 0) decreases in t
-//    and Duchi's condition u_j - (S_j - sigma)/j > 0 is g(u_j) < sigma, so
-//    rho = #{|w| > t'} for the largest key t' with g(t') >= sigma and
-//    theta = (sum_{|w| > t'} |w| - sigma) / rho -- the sorted algorithm's
-//    theta without the sort.
+// entry t = e * 32 + lane, fibers of <= 32 * FW_E entries).  No sort; every
+// step is a warp-wide count / sum:
+//  - cardinality: a bitwise search over the |w| key space (<= 31 steps fp32,
+//    63 fp64) for tau = the k-th largest key, the largest key with
+//    #{key >= tau} >= k.  A candidate with #{key >= cand} == k exactly ends
+//    the search ({key >= cand} is the top k, nothing to break); otherwise
+//    keep key > tau and the first k - #{key > tau} entries equal to tau in
+//    index order (ballot prefix, reading L6);
+//  - l1 ball: Michelot's fixed point theta = (sum_{|w| > theta} |w| - sigma)
+//    / #{|w| > theta}, started from theta = (||w||_1 - sigma) / L.  theta
+//    grows and the active set shrinks monotonically, and the fixed point is
+//    the theta of Duchi's sorted algorithm (reading L5): the same active set
+//    (rho entries) and the same sum; it usually settles in a few steps.
 // x-fibers are contiguous rows: each warp reads its row straight from HBM;
 // z-fibers (stride ny*nx) go through a shared tile of 32 adjacent columns
 // x L planes so every HBM access is a coalesced row segment.
@@ -264,12 +266,22 @@ __device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long lo
       return;
     }
     U tau = 0;   // entries past L are 0: key 0 never reaches a candidate >= 1
+    bool exact = false;
     for (int b = K::BITS - 1; b >= 0; --b) {
       const U cand = tau | ((U)1 << b);
       int c = 0;
 #pragma unroll
       for (int e = 0; e < E; ++e) c += K::key(w[e]) >= cand ? 1 : 0;
-      if (fw_cnt(c) >= k) tau = cand;
+      c = fw_cnt(c);
+      if (c >= k) {
+        tau = cand;
+        if (c == k) { exact = true; break; }   // {key >= tau} is the top k: no tie to break
+      }
+    }
+    if (exact) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) y[e] = K::key(w[e]) >= tau ? w[e] : (T)0;
+      return;
     }
     if (tau == 0) {   // fewer than k nonzeros: every nonzero kept, the rest is 0 = w
 #pragma unroll
@@ -306,24 +318,27 @@ __device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long lo
     for (int e = 0; e < E; ++e) y[e] = (T)0;
     return;
   }
-  U tp = 0;   // g(0) = tot > sigma
-  for (int b = K::BITS - 1; b >= 0; --b) {
-    const U cand = tp | ((U)1 << b);
-    const double v = (double)K::val(cand);   // NaN patterns: no term counts, g = 0
-    double gs = 0.0;
+  // Michelot's fixed point: theta = (sum of the active |w| - sigma) / #active
+  // over the active set {|w| > theta}; theta only grows, the active set only
+  // shrinks, and the fixed point is Duchi's theta (same rho, same sum).
+  double th = (tot - sigma) / (double)L;
+  int na = L;
+  double sa = tot;
+  for (;;) {
+    int c = 0;
+    double s1 = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const double a = fabs((double)w[e]);
-      gs += a > v ? a - v : 0.0;
+      if (a > th) { ++c; s1 += a; }
     }
-    if (fw_sum(gs) >= sigma) tp = cand;
+    c = fw_cnt(c);
+    if (c == na) break;   // warp-uniform
+    s1 = fw_sum(s1);
+    na = c;
+    sa = s1;
+    th = (sa - sigma) / (double)na;
   }
-  int c = 0;
-  double sa = 0.0;
-#pragma unroll
-  for (int e = 0; e < E; ++e)
-    if (K::key(w[e]) > tp) { ++c; sa += fabs((double)w[e]); }
-  const double th = (fw_sum(sa) - sigma) / (double)fw_cnt(c);
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const double a = fabs((double)w[e]) - th;
@@ -339,10 +354,10 @@ __host__ __device__ inline int fiberw_e(int L) { return L <= 128 ? 4 : L <= 256 
 // one launch per fiber set i; E = fiberw_e(flen).  The previous y / v (Alg. 2
 // products) are loaded before the threshold search so their latency hides
 // behind it; z tiles move through shared memory in batches of FW_U rows.
-constexpr int FW_U = 8;
+constexpr int FW_U = 16;
 
 template <class T, int E>
-__global__ void __launch_bounds__(BLOCK) k_fiberw(const __grid_constant__ Prob<T> P, int i) {
+__global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_constant__ Prob<T> P, int i) {
   pdl_begin();
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
