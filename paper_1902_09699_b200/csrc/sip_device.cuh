@@ -127,6 +127,8 @@ struct Job {
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
   unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
+  unsigned mich_passes;          // l1: Michelot passes of this iteration (k_mich)
+  double theta_w;                // l1: last threshold of this job, the next warm start (k_mich)
 };
 
 struct Ctrl {

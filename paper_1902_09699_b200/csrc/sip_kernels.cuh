@@ -55,6 +55,8 @@ struct Prob {
   int nseg1, nseg2;
   // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32)
   unsigned* cand[MAXJOBS];
+  unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
+  int dbg;                        // SIP_DEBUG_MICH: k_mich prints its passes
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)

@@ -22,6 +22,7 @@
 #include "sip_cgs.cuh"
 #include "sip_cgt.cuh"
 #include "sip_fiber.cuh"
+#include "sip_mich.cuh"
 
 using namespace sip;
 
@@ -108,6 +109,8 @@ struct Engine : EngineBase {
   int nsm = 148;
   int nfib_sets = 0;             // sets applied per fiber (k_fiber)
   int g_fib = 0, g_fibw = 0, nfib_sort = 0, nfib_warp = 0;
+  bool mich = false;   // l1 thresholds by k_mich before the radix rounds
+  int g_mich = 0;
   int g_fw[MAXP] = {0};
   size_t smem_fib = 0, smem_fw[MAXP] = {0};
   const std::vector<HostSet>* sets;
@@ -466,8 +469,23 @@ struct Engine : EngineBase {
         g_fibw = std::max(g_fibw, g_fw[i]);
       }
     }
-    const int gmax = std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
-                              std::max(std::max(std::max(g_cgt1, g_cgt2), g_cg2f), std::max(g_fib, g_fibw)));
+    // k_mich (l1 thresholds by Michelot's fixed point): one resident wave
+    mich = nranks == 1 && getenv("SIP_MICH");   // opt-in: measured slower than the radix rounds on C4
+    if (mich) {
+      bool any_l1 = false;
+      for (int i = 0; i < p; ++i) any_l1 |= (Pr.set[i].kind == K_L1 && Pr.set[i].job >= 0);
+      mich = any_l1;
+    }
+    if (mich) {
+      int per = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mich<T>, BLOCK, 0));
+      g_mich = nsm * std::max(1, std::min(per, getenv("SIP_MICH_CTAS") ? atoi(getenv("SIP_MICH_CTAS")) : 3));   // few CTAs: cheap barriers, 8 loads in flight each
+    }
+    Pr.dbg = getenv("SIP_DEBUG_MICH") ? 1 : 0;
+    Pr.gbar = dalloc<unsigned>(2);
+    CU(cudaMemsetAsync(Pr.gbar, 0, 2 * sizeof(unsigned), stream));
+    const int gmax = std::max(2 * g_mich, std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
+                              std::max(std::max(std::max(g_cgt1, g_cgt2), g_cg2f), std::max(g_fib, g_fibw))));
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -742,6 +760,7 @@ struct Engine : EngineBase {
     launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
+      if (mich) { lk(k_mich<T>, g_mich, BLOCK, 0, Pr); ++launches; mark(KB_SELECT); }
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
       if (has_card()) { launch_tie(); mark(KB_TIE); }
     }
