@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T>
       *P.counter = 0u;
       for (int i = 0; i < P.P; ++i) {
         if (!P.set[i].fib || P.set[i].fpath) continue;
+        if (P.nranks > 1) {   // z slabs: rank-local, summed with pass 2's values
+          for (int q = 0; q < 4; ++q) P.fibv[4 * i + q] = out[4 * i + q];
+          continue;
+        }
         C.sums[i][SLOT_GV] = out[4 * i + 0];
         C.sums[i][SLOT_GG] = out[4 * i + 1];
         C.sums[i][SLOT_VV] = out[4 * i + 2];
@@ -507,10 +511,14 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
     reduce_partials(P.partials, 4, out, sh);
     if (threadIdx.x == 0) {
       *P.counter = 0u;
-      C.sums[i][SLOT_GV] = out[0];
-      C.sums[i][SLOT_GG] = out[1];
-      C.sums[i][SLOT_VV] = out[2];
-      C.sums[i][SLOT_FN] = out[3];
+      if (P.nranks > 1) {   // z slabs: rank-local, summed with pass 2's values
+        for (int q = 0; q < 4; ++q) P.fibv[4 * i + q] = out[q];
+      } else {
+        C.sums[i][SLOT_GV] = out[0];
+        C.sums[i][SLOT_GG] = out[1];
+        C.sums[i][SLOT_VV] = out[2];
+        C.sums[i][SLOT_FN] = out[3];
+      }
     }
   }
 }

@@ -57,6 +57,7 @@ struct Prob {
   unsigned* cand[MAXJOBS];
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
   int dbg;                        // SIP_DEBUG_MICH: k_mich prints its passes
+  double* fibv;                   // z slabs: this rank's fiber-set sums (4 per set), added to pass 2's
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
   double taps[MAXTAPS];           // blur kernel (row major kh x kw)

@@ -559,7 +559,7 @@ __device__ inline void fin_pass2(const Prob<T>& P, Ctrl& C, const double* stage)
     if (q == 0) C.sums[i][SLOT_GV] = val;
     if (q == 1) C.sums[i][SLOT_GG] = val;
     if (q == 2) C.sums[i][SLOT_VV] = val;
-    if (q == 3 && P.set[i].sjob >= 0) C.sums[i][SLOT_FN] = val;
+    if (q == 3 && (P.set[i].sjob >= 0 || P.set[i].fib)) C.sums[i][SLOT_FN] = val;
   }
 }
 
@@ -626,8 +626,16 @@ __global__ void __launch_bounds__(BLOCK, 4) k_pass2t(const __grid_constant__ Pro
   }
   double* stage = P.partials + (size_t)gridDim.x * nv;
   if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
-    if (P.nranks > 1) publish(P, stage, nv, threadIdx.x, BLOCK);
-    else fin_pass2<T>(P, C, stage);
+    if (P.nranks > 1) {
+      __syncthreads();
+      if (P.fibv)   // per-fiber sets: this rank's sums from the fiber kernels (run before pass 2)
+        for (int v = threadIdx.x; v < nv; v += BLOCK)
+          if (P.set[v / 4].fib) stage[v] += P.fibv[v];
+      __syncthreads();
+      publish(P, stage, nv, threadIdx.x, BLOCK);
+    } else {
+      fin_pass2<T>(P, C, stage);
+    }
   }
 }
 

@@ -482,6 +482,7 @@ struct Engine : EngineBase {
       g_mich = nsm * std::max(1, std::min(per, getenv("SIP_MICH_CTAS") ? atoi(getenv("SIP_MICH_CTAS")) : 3));   // few CTAs: cheap barriers, 8 loads in flight each
     }
     Pr.dbg = getenv("SIP_DEBUG_MICH") ? 1 : 0;
+    Pr.fibv = (nfib_sets && nranks > 1) ? dalloc<double>(4 * MAXP) : nullptr;
     Pr.gbar = dalloc<unsigned>(2);
     CU(cudaMemsetAsync(Pr.gbar, 0, 2 * sizeof(unsigned), stream));
     const int gmax = std::max(2 * g_mich, std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
@@ -741,6 +742,15 @@ struct Engine : EngineBase {
     else k_tiecount<T><<<g_p2, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
+  // per-fiber sets: one warp-kernel launch per set, the sort kernel for the rest
+  void launch_fiber() {
+    for (int i = 0; nfib_warp && i < p; ++i) {
+      if (!Pr.set[i].fib || !Pr.set[i].fpath) continue;
+      lk(FiberW<T>::of(Pr.set[i].flen), g_fw[i], BLOCK, smem_fw[i], Pr, i);
+      ++launches;
+    }
+    if (nfib_sort) { lk(k_fiber<T>, g_fib, BLOCK, smem_fib, Pr); ++launches; }
+  }
   void launch_control() { lk(k_control<T>, 1, BLOCK, 0, Pr); ++launches; }
   void launch_fin(int site, int j, int round) {
     k_fin<T><<<1, BLOCK, 0, stream>>>(Pr, site, j, round);
@@ -768,15 +778,7 @@ struct Engine : EngineBase {
       launch_pass2(kpos);
       ++launches; mark(KB_PASS2);
     }
-    for (int i = 0; nfib_warp && i < p; ++i) {   // per-fiber projections, after pass 2's sums
-      if (!Pr.set[i].fib || !Pr.set[i].fpath) continue;
-      lk(FiberW<T>::of(Pr.set[i].flen), g_fw[i], BLOCK, smem_fw[i], Pr, i);
-      ++launches; mark(KB_FIBER);
-    }
-    if (nfib_sort) {
-      lk(k_fiber<T>, g_fib, BLOCK, smem_fib, Pr);
-      ++launches; mark(KB_FIBER);
-    }
+    if (nfib_sets) { launch_fiber(); mark(KB_FIBER); }   // per-fiber projections, after pass 2's sums
     launch_control(); mark(KB_CTRL);
   }
 
@@ -1129,8 +1131,8 @@ struct Team : EngineBase {
   void setup(int ndim, int nz_g, int ny, int nx, const double* h, cudaStream_t st, const std::vector<HostSet>& s,
              int G_, int r0, int nlocal, Comm* c) {
     G = G_; comm = c; stream = st;
-    for (const HostSet& hs : s)
-      if (hs.fib) throw SipError{SIP_ERR_CONFIG, "per-fiber sets on z slabs: not in this build"};
+    for (const HostSet& hs : s)   // x-fibers lie in a plane, z-fibers cross the slabs
+      if (hs.fib == SIP_APPLY_Z_FIBERS) throw SipError{SIP_ERR_CONFIG, "z-fiber sets on z slabs: not in this build"};
     for (const HostSet& hs : s)
       if (!hs.lo_vec.empty() || !hs.hi_vec.empty())
         throw SipError{SIP_ERR_CONFIG, "per-entry bounds on z slabs: not in this build"};
@@ -1233,6 +1235,8 @@ struct Team : EngineBase {
         site(ST_TIE, 0, 0, {});
       }
     }
+    if (e0.nfib_sets)   // before pass 2: its finaliser adds the fiber sums (Prob::fibv)
+      each([&](Engine<T>& e) { e.launch_fiber(); }, E::KB_FIBER);
     if (e0.Pr.nglob > 0) {
       each([&](Engine<T>& e) { e.launch_pass2(kpos); ++e.launches; }, E::KB_PASS2);
       site(ST_PASS2, 0, 0, {{wr ? FS_Y1 : FS_Y0, SS_GLOBAL, H_LO}, {wr ? FS_V1 : FS_V0, SS_GLOBAL, H_LO}});

@@ -193,3 +193,67 @@ def test_fiber_refused_configurations():
     with pytest.raises(SipError):
         g = Grid((8, 8), None, "f64")
         g.add_set(SetDef("DX", "l1", sigma=0.5, relative=True, app_mode="x"))
+
+
+# ---------------------------------------------------------------- z slabs
+# x-fibers lie in one plane, so they shard with the z slabs (option
+# "virtual_ranks": G slabs on one device through the multi-GPU code path);
+# each rank's fiber sums join pass 2's gathered reduction.
+SLAB_FIBER = [
+    (100, (8, 12), ("bounds", "card_rows", "l1_rows"), 3),
+    (100, (12, 8), ("bounds", "l1_rows", "slope"), 2),
+    (100, (4, 4, 8), ("bounds", "card_rows"), 2),
+    (100, (8, 8), ("bounds", "card_rows"), 4),
+]
+
+
+@pytest.mark.parametrize("seed,shape,kinds,ranks", SLAB_FIBER)
+def test_slab_x_fibers_control_flow(seed, shape, kinds, ranks):
+    prob = G.tiny(seed, shape, kinds)
+    ref = O.parsdmm(prob.shape, prob.sets, prob.m, **prob.options)
+    g = grid_for(prob)
+    g.set_option("virtual_ranks", ranks)
+    m = dev(prob.m, "f64")
+    x = torch.empty_like(m)
+    res, st = g.project(m, x, max_iter=200, tol=1e-3)
+    log = g.get_log(200)
+    it = ref.iterations
+    assert res["iterations"] == it
+    lim = it if ref.converged else 100   # see test_tiny_fiber_control_flow
+    np.testing.assert_array_equal(log["cg"][:lim], ref.cg_per_iter[:lim])
+    np.testing.assert_array_equal(log["branch"][:lim], ref.branch[:lim])
+    if ref.converged:
+        assert O.relres(host(x), ref.x) < 1e-6
+    g.close()
+
+
+def test_slab_x_fibers_fp32_matches_single_rank():
+    shape = (40, 24, 64)
+    m = G.tiny_model(21, shape)
+    sets = [SetDef("I", "bounds", lo=1500.0, hi=4500.0),
+            SetDef("DZ", "bounds", lo=0.0, hi=G.INF),
+            SetDef("DX", "card", k_frac=0.5, relative=True, app_mode="x"),
+            SetDef("DY", "l1", sigma=150.0 * shape[2], app_mode="x")]
+    prob = G.Problem("fibslab", shape, "f32", m, sets, options=dict(G.DEFAULT_OPTIONS))
+    xs = []
+    for ranks in (1, 4):
+        g = grid_for(prob)
+        if ranks > 1:
+            g.set_option("virtual_ranks", ranks)
+        g.set_option("fixed_work", 1)
+        md = dev(m, "f32")
+        x = torch.empty_like(md)
+        g.project(md, x, max_iter=20, tol=1e-3)
+        xs.append(host(x))
+        g.close()
+    assert O.relres(xs[1], xs[0]) < 1e-5
+
+
+def test_slab_z_fibers_refused():
+    prob = G.tiny(100, (8, 8), ("bounds", "card_cols"))
+    g = grid_for(prob)
+    g.set_option("virtual_ranks", 2)
+    m = dev(prob.m, "f64")
+    with pytest.raises(SipError):
+        g.project(m, torch.empty_like(m), max_iter=5, tol=1e-3)
+    g.close()
