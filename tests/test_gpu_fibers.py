@@ -257,3 +257,30 @@ def test_slab_z_fibers_refused():
     with pytest.raises(SipError):
         g.project(m, torch.empty_like(m), max_iter=5, tol=1e-3)
     g.close()
+
+
+# ---------------------------------------------------------------- multilevel
+@pytest.mark.parametrize("shape,kinds", [
+    ((16, 16), ("bounds", "card_rows", "l1_rows")),
+    ((16, 16), ("bounds", "l1_cols", "slope")),
+    ((8, 8, 16), ("bounds", "card_rows", "slope")),
+])
+def test_multilevel_with_fibers(shape, kinds):
+    """Algorithm 3 with per-fiber sets: each level's fibers have that
+    level's length (relative k from it, reading L28); per-level iteration
+    and CG counts equal the oracle's while the levels converge"""
+    prob = G.tiny(120, shape, kinds)
+    g = grid_for(prob)
+    m = dev(prob.m, "f64")
+    x = torch.empty_like(m)
+    per, st = g.project_multilevel(m, x, 2, max_iter=200, tol=1e-3)
+    xo, sto, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 2, **prob.options)
+    all_conv = True
+    for l in (1, 0):
+        assert per[l]["iterations"] == logs[l].iterations, (l, per[l]["iterations"], logs[l].iterations)
+        if not logs[l].converged:
+            all_conv = False
+            break
+        assert per[l]["cg_iterations"] == logs[l].cg_total
+    assert O.relres(host(x), xo) < (1e-6 if all_conv else 1e-3)
+    g.close()
