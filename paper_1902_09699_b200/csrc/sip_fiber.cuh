@@ -241,10 +241,12 @@ __host__ inline size_t fiber_smem(int dsize) { return (size_t)FIB_MAX * (8 + 8 +
 //    the theta of Duchi's sorted algorithm (reading L5): the same active set
 //    (rho entries) and the same sum; it usually settles in a few steps.
 // x-fibers are contiguous rows: each warp reads its row straight from HBM;
-// z-fibers (stride ny*nx) go through a shared tile of 32 adjacent columns
+// z-fibers (stride ny*nx) go through a shared tile of FW_TC adjacent columns
 // x L planes so every HBM access is a coalesced row segment.
 constexpr int FW_E = 16;
-constexpr int FW_TP = 33;   // tile pitch (32 columns + 1: conflict-free column reads)
+constexpr int FW_TS = 4;                 // z tiles: 2^FW_TS adjacent columns (64-byte fp32 row segments)
+constexpr int FW_TC = 1 << FW_TS;
+constexpr int FW_TP = FW_TC + 1;         // tile pitch (+1: conflict-free column reads)
 
 __device__ __forceinline__ double fw_sum(double v) {
 #pragma unroll
@@ -269,13 +271,16 @@ __device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long lo
       for (int e = 0; e < E; ++e) y[e] = (T)0;
       return;
     }
+    U key[E];   // |w| bit patterns, formed once
+#pragma unroll
+    for (int e = 0; e < E; ++e) key[e] = K::key(w[e]);
     U tau = 0;   // entries past L are 0: key 0 never reaches a candidate >= 1
     bool exact = false;
     for (int b = K::BITS - 1; b >= 0; --b) {
       const U cand = tau | ((U)1 << b);
       int c = 0;
 #pragma unroll
-      for (int e = 0; e < E; ++e) c += K::key(w[e]) >= cand ? 1 : 0;
+      for (int e = 0; e < E; ++e) c += key[e] >= cand ? 1 : 0;
       c = fw_cnt(c);
       if (c >= k) {
         tau = cand;
@@ -284,7 +289,7 @@ __device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long lo
     }
     if (exact) {
 #pragma unroll
-      for (int e = 0; e < E; ++e) y[e] = K::key(w[e]) >= tau ? w[e] : (T)0;
+      for (int e = 0; e < E; ++e) y[e] = key[e] >= tau ? w[e] : (T)0;
       return;
     }
     if (tau == 0) {   // fewer than k nonzeros: every nonzero kept, the rest is 0 = w
@@ -294,23 +299,23 @@ __device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long lo
     }
     int gt = 0;
 #pragma unroll
-    for (int e = 0; e < E; ++e) gt += K::key(w[e]) > tau ? 1 : 0;
+    for (int e = 0; e < E; ++e) gt += key[e] > tau ? 1 : 0;
     const long long need = k - fw_cnt(gt);
     const unsigned lt = (1u << lane) - 1u;
     int run = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const U key = K::key(w[e]);
-      const unsigned tie = __ballot_sync(0xffffffffu, key == tau);
-      const bool keep = key > tau || (key == tau && run + __popc(tie & lt) < need);
+      const unsigned tie = __ballot_sync(0xffffffffu, key[e] == tau);
+      const bool keep = key[e] > tau || (key[e] == tau && run + __popc(tie & lt) < need);
       run += __popc(tie);
       y[e] = keep ? w[e] : (T)0;
     }
     return;
   }
+  double a[E];   // |w| in fp64, formed once
   double a1 = 0.0;
 #pragma unroll
-  for (int e = 0; e < E; ++e) a1 += fabs((double)w[e]);
+  for (int e = 0; e < E; ++e) { a[e] = fabs((double)w[e]); a1 += a[e]; }
   const double tot = fw_sum(a1);
   if (tot <= sigma) {
 #pragma unroll
@@ -327,30 +332,26 @@ __device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long lo
   // shrinks, and the fixed point is Duchi's theta (same rho, same sum).
   double th = (tot - sigma) / (double)L;
   int na = L;
-  double sa = tot;
   for (;;) {
     int c = 0;
     double s1 = 0.0;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const double a = fabs((double)w[e]);
-      if (a > th) { ++c; s1 += a; }
-    }
+    for (int e = 0; e < E; ++e)
+      if (a[e] > th) { ++c; s1 += a[e]; }
     c = fw_cnt(c);
     if (c == na) break;   // warp-uniform
     s1 = fw_sum(s1);
     na = c;
-    sa = s1;
-    th = (sa - sigma) / (double)na;
+    th = (s1 - sigma) / (double)na;
   }
 #pragma unroll
   for (int e = 0; e < E; ++e) {
-    const double a = fabs((double)w[e]) - th;
-    y[e] = a > 0.0 ? (T)(w[e] > (T)0 ? a : -a) : (T)0;
+    const double d = a[e] - th;
+    y[e] = d > 0.0 ? (T)(w[e] > (T)0 ? d : -d) : (T)0;
   }
 }
 
-// shared bytes of the z-fiber tiles (w and y, L x 33 each)
+// shared bytes of the z-fiber tiles (w and y, L x FW_TP each)
 __host__ __device__ inline size_t fiberw_smem(int L, int dsize) { return (size_t)2 * L * FW_TP * dsize; }
 // entries per lane for a fiber length (the kernel instantiation)
 __host__ __device__ inline int fiberw_e(int L) { return L <= 128 ? 4 : L <= 256 ? 8 : 16; }
@@ -423,17 +424,17 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
         }
       }
     }
-  } else {   // z-fibers: tiles of 32 adjacent columns staged in shared memory
+  } else {   // z-fibers: tiles of FW_TC adjacent columns staged in shared memory
     T* tw = reinterpret_cast<T*>(fsm);
     T* ty = tw + (size_t)L * FW_TP;
-    const int ntx = (g.nx + 31) / 32;
+    const int ntx = (g.nx + FW_TC - 1) / FW_TC;
     const int ntile = g.ny * ntx;
     const int64_t pl = (int64_t)g.plane;
-    const int nq = L * 32;
+    const int nq = L * FW_TC;
     for (int tl = blockIdx.x; tl < ntile; tl += gridDim.x) {
-      const int iy = tl / ntx, ix0 = (tl - iy * ntx) * 32;
+      const int iy = tl / ntx, ix0 = (tl - iy * ntx) * FW_TC;
       const int64_t b0 = (int64_t)iy * g.nx + ix0;
-      const int c_ = threadIdx.x & 31;
+      const int c_ = threadIdx.x & (FW_TC - 1);
       const bool colok = ix0 + c_ < g.nx && !fib_is_pad(g, 2, prim, iy * g.nx + ix0 + c_);
       for (int ph = 0; ph < (chk ? 2 : 1); ++ph) {
         const T* src = ph == 0 ? S.w : S.s;
@@ -442,16 +443,16 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
 #pragma unroll
           for (int u = 0; u < FW_U; ++u) {
             const int q = q0 + u * BLOCK;
-            r[u] = (q < nq && ix0 + c_ < g.nx) ? src[(q >> 5) * pl + b0 + c_] : (T)0;
+            r[u] = (q < nq && ix0 + c_ < g.nx) ? src[(q >> FW_TS) * pl + b0 + c_] : (T)0;
           }
 #pragma unroll
           for (int u = 0; u < FW_U; ++u) {
             const int q = q0 + u * BLOCK;
-            if (q < nq) tw[(q >> 5) * FW_TP + c_] = r[u];
+            if (q < nq) tw[(q >> FW_TS) * FW_TP + c_] = r[u];
           }
         }
         __syncthreads();
-        for (int c = wid; c < 32; c += NWARP) {
+        for (int c = wid; c < FW_TC; c += NWARP) {
           const int ix = ix0 + c;
           if (ix >= g.nx || fib_is_pad(g, 2, prim, iy * g.nx + ix)) continue;   // warp-uniform
 #pragma unroll
@@ -479,14 +480,14 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
             for (int u = 0; u < FW_U; ++u) {
               const int q = q0 + u * BLOCK;
               const bool ok = q < nq && colok && f.dots;
-              a0[u] = ok ? yw[(q >> 5) * pl + b0 + c_] : (T)0;
-              b0v[u] = ok ? vw[(q >> 5) * pl + b0 + c_] : (T)0;
+              a0[u] = ok ? yw[(q >> FW_TS) * pl + b0 + c_] : (T)0;
+              b0v[u] = ok ? vw[(q >> FW_TS) * pl + b0 + c_] : (T)0;
             }
 #pragma unroll
             for (int u = 0; u < FW_U; ++u) {
               const int q = q0 + u * BLOCK;
               if (q >= nq || !colok) continue;
-              const int t = q >> 5;
+              const int t = q >> FW_TS;
               const int64_t pt = t * pl + b0 + c_;
               const T wt = tw[t * FW_TP + c_], yt = ty[t * FW_TP + c_];
               const T vt = rho * (yt - wt);

@@ -464,7 +464,7 @@ struct Engine : EngineBase {
         smem_fw[i] = S.fib == 2 ? fiberw_smem(S.flen, (int)sizeof(T)) : 0;
         CU(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, BLOCK, smem_fw[i]));
-        const int units = S.fib == 1 ? (g.nz * g.ny + NWARP - 1) / NWARP : g.ny * ((g.nx + 31) / 32);
+        const int units = S.fib == 1 ? (g.nz * g.ny + NWARP - 1) / NWARP : g.ny * ((g.nx + FW_TC - 1) / FW_TC);
         g_fw[i] = std::max(1, std::min(units, nsm * std::max(per, 1)));
         g_fibw = std::max(g_fibw, g_fw[i]);
       }
