@@ -314,13 +314,16 @@ static void proj_card(int64_t M, const double *w, int64_t k, int key_f32, double
 
 static void project_whole(const sipref_set *s, int64_t M, const double *w, double *y);
 
+/* fiber length (reading L28): nx (nx - 1 for D_x) for x-fibers, nz
+   (nz - 1 for D_z) for z-fibers -- the forward differences of Eq. 8 */
 int64_t sipref_fiber_len(const sipref_grid *g, const sipref_set *s) {
   if (s->app_mode == 1) return s->op == SIPREF_OP_DX ? g->n[2] - 1 : g->n[2];
   if (s->app_mode == 2) return s->op == SIPREF_OP_DZ ? g->n[0] - 1 : g->n[0];
   return 0;
 }
 
-/* Table 1 projector of set s on w (length M).  app_mode 1 / 2: the output
+/* Table 1 projector of set s on w (length M).  app_mode 1 / 2 (P:418, S:202-
+   210, reading L28 of DESIGN.md): the output
    field of the (single-block) operator is split into its x-fibers, which are
    consecutive runs of fib_len entries of the compact layout, or its
    z-fibers, fib_len entries at stride M / fib_len; each fiber is projected
