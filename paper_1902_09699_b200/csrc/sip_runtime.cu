@@ -676,8 +676,11 @@ struct Engine : EngineBase {
   }
   // lean flat CG kernels (sip_vec.cuh k_cg1f / k_cg2f); SIP_OLD_CG=1 keeps the
   // z-marching / shuffle kernels for A/B measurements
-  bool lean_cg() const { return vec && !getenv("SIP_OLD_CG"); }
-  bool tiled_cg() const { return lean_cg() && !sg.on && g_cgt1 > 0 && getenv("SIP_CGT"); }   // opt-in: measured equal to the flat kernels
+  // A/B switches read once per engine (launchers run per kernel when graphs are off)
+  const bool env_old_cg = getenv("SIP_OLD_CG") != nullptr;
+  const bool env_cgt = getenv("SIP_CGT") != nullptr;
+  bool lean_cg() const { return vec && !env_old_cg; }
+  bool tiled_cg() const { return lean_cg() && !sg.on && g_cgt1 > 0 && env_cgt; }   // opt-in: measured equal to the flat kernels
   void launch_cg1(int j) {
     if (tiled_cg()) {
       const bool hy = ndim == 3;
