@@ -101,11 +101,13 @@ typedef struct {
                              A m (0), or on each x-fiber (row) / z-fiber
                              (column) of the operator's output field on its own
                              (NEXT-1): CARDINALITY (k per fiber; relative:
-                             k = floor(k_frac * fiber length)) and L1_BALL
-                             (absolute sigma per fiber), single-block operators
-                             (not TV / BLUR_MASK), fibers of <= 4096 entries,
-                             one rank; BOUNDS accepts it (separable).  Else
-                             SIP_ERR_CONFIG; L1_BALL relative: SIP_ERR_PARAM.  */
+                             k = floor(k_frac * fiber length)), L1_BALL, L2_BALL
+                             and ANNULUS (absolute radii per fiber; relative:
+                             SIP_ERR_PARAM), single-block operators (not TV /
+                             BLUR_MASK), fibers of <= 4096 entries, nx a
+                             multiple of 16 / sizeof(dtype); on z slabs x-fibers
+                             only.  BOUNDS accepts it (separable).  Else
+                             SIP_ERR_CONFIG.                                    */
 } sip_set_params;
 
 enum { SIP_APPLY_WHOLE = 0, SIP_APPLY_X_FIBERS = 1, SIP_APPLY_Z_FIBERS = 2 };

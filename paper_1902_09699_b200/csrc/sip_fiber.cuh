@@ -82,9 +82,21 @@ __device__ inline void block_prefix(double* u, int L, double* sh /* >= NWARP */)
 // -- |w| in the field's precision (reading L27) -- and the l1 ball by
 // Duchi's sorted prefix sums in fp64 (reading L5).
 template <class T>
-__device__ void fib_project(int kind, int L, const T* v, T* y, long long k, double sigma,
+__device__ void fib_project(int kind, int L, const T* v, T* y, long long k, double sigma, double lo, double hi,
                             unsigned long long* keys, short* ix, double* sums, double* sh) {
   using K = KeyT<T>;
+  if (kind == K_L2 || kind == K_ANN) {   // radial scaling into [lo, hi] (Table 1; L2: lo = 0; L7 at 0)
+    double a = 0.0;
+    for (int t = threadIdx.x; t < L; t += BLOCK) a += (double)v[t] * (double)v[t];
+    const double n = sqrt(block_sum(a, sh));
+    double f = 1.0;
+    if (n > hi) f = hi / n;
+    else if (n < lo && n > 0.0) f = lo / n;
+    for (int t = threadIdx.x; t < L; t += BLOCK)
+      y[t] = n == 0.0 ? ((t == 0 && lo > 0.0) ? (T)lo : (T)0) : (T)((double)v[t] * f);
+    __syncthreads();
+    return;
+  }
   int n2 = 1;
   while (n2 < L) n2 <<= 1;
   if (kind == K_CARD && k >= L) {
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T>
     const int L = S.flen;
     const T rho = (T)C.rho[i];
     const long long kk = C.kcard[i];
-    const double sg = C.sigma[i];
+    const double sg = C.sigma[i], slo = C.sig_lo[i], shi = C.sig_hi[i];
     T* yw = S.y[par ^ 1];
     T* vw = S.v[par ^ 1];
     acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
@@ -173,7 +185,7 @@ __global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T>
       if (fib_is_pad(g, S.fib, prim, fb)) continue;
       for (int t = threadIdx.x; t < L; t += BLOCK) vin[t] = S.w[fib_pt(g, S.fib, fb, t)];
       __syncthreads();
-      fib_project<T>(S.kind, L, vin, vout, kk, sg, keys, ix, sums, sh);
+      fib_project<T>(S.kind, L, vin, vout, kk, sg, slo, shi, keys, ix, sums, sh);
       for (int t = threadIdx.x; t < L; t += BLOCK) {
         const int64_t pt = fib_pt(g, S.fib, fb, t);
         const T y = vout[t];
@@ -189,7 +201,7 @@ __global__ void __launch_bounds__(BLOCK) k_fiber(const __grid_constant__ Prob<T>
       if (f.check && S.s) {   // Eq. 26 numerator: the per-fiber projection of s
         for (int t = threadIdx.x; t < L; t += BLOCK) vin[t] = S.s[fib_pt(g, S.fib, fb, t)];
         __syncthreads();
-        fib_project<T>(S.kind, L, vin, vout, kk, sg, keys, ix, sums, sh);
+        fib_project<T>(S.kind, L, vin, vout, kk, sg, slo, shi, keys, ix, sums, sh);
         for (int t = threadIdx.x; t < L; t += BLOCK) {
           const double d = (double)vin[t] - (double)vout[t];
           acc[3] += d * d;
@@ -256,10 +268,23 @@ __device__ __forceinline__ double fw_sum(double v) {
 __device__ __forceinline__ int fw_cnt(int v) { return __reduce_add_sync(0xffffffffu, v); }
 
 template <class T, int E>
-__device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long long k, double sigma, int L,
-                                             int lane) {
+__device__ __forceinline__ void fw_project_e(int kind, const T* w, T* y, long long k, double sigma, double lo,
+                                             double hi, int L, int lane) {
   using K = KeyT<T>;
   using U = typename K::U;
+  if (kind == K_L2 || kind == K_ANN) {   // radial scaling into [lo, hi] (Table 1; L2: lo = 0; L7 at 0)
+    double a = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) a += (double)w[e] * (double)w[e];
+    const double n = sqrt(fw_sum(a));
+    double f = 1.0;
+    if (n > hi) f = hi / n;
+    else if (n < lo && n > 0.0) f = lo / n;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      y[e] = n == 0.0 ? ((e == 0 && lane == 0 && lo > 0.0) ? (T)lo : (T)0) : (T)((double)w[e] * f);
+    return;
+  }
   if (kind == K_CARD) {
     if (k >= L) {
 #pragma unroll
@@ -378,7 +403,7 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
   const int L = S.flen;
   const T rho = (T)C.rho[i];
   const long long kk = C.kcard[i];
-  const double sg = C.sigma[i];
+  const double sg = C.sigma[i], slo = C.sig_lo[i], shi = C.sig_hi[i];
   T* yw = S.y[par ^ 1];
   T* vw = S.v[par ^ 1];
   const bool chk = f.check && S.s;
@@ -397,7 +422,7 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
         y0[e] = (f.dots && t < L) ? yw[base + t] : (T)0;
         v0[e] = (f.dots && t < L) ? vw[base + t] : (T)0;
       }
-      fw_project_e<T, E>(S.kind, w, y, kk, sg, L, lane);
+      fw_project_e<T, E>(S.kind, w, y, kk, sg, slo, shi, L, lane);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const int t = e * 32 + lane;
@@ -416,7 +441,7 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
           const int t = e * 32 + lane;
           w[e] = t < L ? S.s[base + t] : (T)0;
         }
-        fw_project_e<T, E>(S.kind, w, y, kk, sg, L, lane);
+        fw_project_e<T, E>(S.kind, w, y, kk, sg, slo, shi, L, lane);
 #pragma unroll
         for (int e = 0; e < E; ++e) {
           const double d = (double)w[e] - (double)y[e];   // 0 past L (w = y = 0 there)
@@ -460,7 +485,7 @@ __global__ void __launch_bounds__(BLOCK, E <= 8 ? 3 : 1) k_fiberw(const __grid_c
             const int t = e * 32 + lane;
             w[e] = t < L ? tw[t * FW_TP + c] : (T)0;
           }
-          fw_project_e<T, E>(S.kind, w, y, kk, sg, L, lane);
+          fw_project_e<T, E>(S.kind, w, y, kk, sg, slo, shi, L, lane);
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int t = e * 32 + lane;

@@ -1059,7 +1059,9 @@ __device__ void control_body(const Prob<T>& P, Ctrl& C) {
       const int kd = P.set[i].kind;
       const double s2 = C.sums[i][SLOT_S2];
       double fn = C.sums[i][SLOT_FN];
-      if ((kd == K_L1 || kd == K_CARD) && P.set[i].sjob >= 0) {   // fiber sets: k_fiber's FN
+      if (P.set[i].fib) {
+        // per-fiber sets: the fiber kernels' sum of per-fiber ||s - P(s)||^2
+      } else if ((kd == K_L1 || kd == K_CARD) && P.set[i].sjob >= 0) {
         const Job& J = C.job[P.set[i].sjob];
         if (J.mode == JM_INSIDE || J.mode == JM_ALL) fn = 0.0;
         else if (J.mode == JM_ZERO) fn = s2;

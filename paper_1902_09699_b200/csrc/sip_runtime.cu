@@ -2124,9 +2124,12 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type 
     hs.fib = 0;
     hs.flen = 0;
     if (prm->app_mode != SIP_APPLY_WHOLE && type != SIP_SET_BOUNDS) {   // bounds: separable, same set
-      if (type != SIP_SET_CARDINALITY && type != SIP_SET_L1_BALL) { g->err = "per-fiber sets: cardinality and l1 ball only"; return SIP_ERR_CONFIG; }
+      if (type != SIP_SET_CARDINALITY && type != SIP_SET_L1_BALL && type != SIP_SET_L2_BALL && type != SIP_SET_ANNULUS) {
+        g->err = "per-fiber sets: cardinality, l1 ball, l2 ball, annulus";
+        return SIP_ERR_CONFIG;
+      }
       if (op == SIP_OP_TV || op == SIP_OP_BLUR_MASK) { g->err = "per-fiber sets need a single-block operator"; return SIP_ERR_CONFIG; }
-      if (type == SIP_SET_L1_BALL && prm->relative) return SIP_ERR_PARAM;
+      if (type != SIP_SET_CARDINALITY && prm->relative) return SIP_ERR_PARAM;   // norm radii per fiber: absolute (L28)
       hs.fib = prm->app_mode;
       hs.flen = prm->app_mode == SIP_APPLY_X_FIBERS ? nx - (op == SIP_OP_DX ? 1 : 0) : nz - (op == SIP_OP_DZ ? 1 : 0);
       if (hs.flen > 4096) { g->err = "per-fiber sets: fibers longer than 4096"; return SIP_ERR_CONFIG; }

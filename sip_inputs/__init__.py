@@ -278,6 +278,11 @@ def tiny(seed=100, shape=(8, 8), kinds=("bounds", "l1", "slope")) -> Problem:
             sets.append(SetDef("DX", "l1", sigma=120.0 * (shape[-1] - 1), app_mode="x"))
         elif k == "l1_cols":
             sets.append(SetDef("I", "l1", sigma=2500.0 * shape[0], app_mode="z"))
+        elif k == "l2_rows":
+            sets.append(SetDef("DX", "l2", sigma=150.0 * np.sqrt(shape[-1] - 1), app_mode="x"))
+        elif k == "ann_cols":
+            sets.append(SetDef("I", "annulus", sigma_lo=2400.0 * np.sqrt(shape[0]),
+                               sigma_hi=3200.0 * np.sqrt(shape[0]), app_mode="z"))
         else:
             raise KeyError(k)
     return Problem(f"tiny{seed}", tuple(shape), "f64", m, sets,

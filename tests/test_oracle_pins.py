@@ -541,13 +541,13 @@ def test_fiber_worked_example():
 @pytest.mark.parametrize("op,mode,shape", [("I", "x", (5, 4)), ("I", "z", (5, 4)), ("DX", "x", (5, 6)),
                                            ("DX", "z", (5, 6)), ("DZ", "z", (6, 5)), ("DZ", "x", (6, 5)),
                                            ("DY", "x", (3, 4, 5)), ("DX", "z", (4, 3, 5))])
-@pytest.mark.parametrize("kind", ["card", "l1"])
+@pytest.mark.parametrize("kind", ["card", "l1", "l2", "annulus"])
 def test_fiber_projection_vs_explicit_loop(op, mode, shape, kind):
     """the fiber projector equals an explicit loop over the rows /
     columns of the operator's output field, each projected by the
     whole-vector projector (itself pinned by brute force above)"""
     r = np.random.default_rng(21)
-    sd = SetDef(op, kind, k=2, sigma=1.5, app_mode=mode)
+    sd = SetDef(op, kind, k=2, sigma=1.5, sigma_lo=1.0, sigma_hi=1.5, app_mode=mode)
     M = O.op_len(shape, sd)
     L = O.fiber_len(shape, sd)
     nz = shape[0]
@@ -560,7 +560,7 @@ def test_fiber_projection_vs_explicit_loop(op, mode, shape, kind):
     w = r.normal(size=M)
     W = w.reshape(fz, fy, fx)
     ref = np.zeros_like(W)
-    whole = SetDef("I", kind, k=2, sigma=1.5)
+    whole = SetDef("I", kind, k=2, sigma=1.5, sigma_lo=1.0, sigma_hi=1.5)
     if mode == "x":
         for a in range(fz):
             for b in range(fy):
