@@ -621,8 +621,13 @@ __global__ void __launch_bounds__(BLOCK, 4) k_rhsf(const __grid_constant__ Prob<
         const T* y = S.y[par] + (int64_t)bl * g.ld + pt0;
         const T* v = S.v[par] + (int64_t)bl * g.ld + pt0;
         T yy[W], vv[W], u[W];
-        VT<T>::ldcs(y, yy);
-        VT<T>::ldcs(v, vv);
+        if (prim == PRIM_Z || prim == PRIM_Y) {   // read again as the z / y neighbour: keep in L2
+          VT<T>::ldT(y, yy);
+          VT<T>::ldT(v, vv);
+        } else {
+          VT<T>::ldcs(y, yy);
+          VT<T>::ldcs(v, vv);
+        }
 #pragma unroll
         for (int e = 0; e < W; ++e) u[e] = rho * yy[e] + vv[e];
         if (prim == PRIM_I) {
