@@ -57,6 +57,8 @@ struct Prob {
   unsigned* cand[MAXJOBS];
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
   int dbg;                        // SIP_DEBUG_MICH: k_mich prints its passes
+  int poison;                     // SIP_POISON: k_init writes NaN into fields that are written before read
+  int init_zero;                  // k_init zeroes every state field (scalar kernels)
   double* fibv;                   // z slabs: this rank's fiber-set sums (4 per set), added to pass 2's
   short seg_set[64], seg_blk[64];
   short seg2_set[64], seg2_blk[64];
@@ -1202,7 +1204,13 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Prob<T> 
       L = locate(g, pt);
       if (init_x) P.x[pt] = P.m[pt];
       P.hist[0][pt] = P.x[pt];
-      P.xs[0][pt] = (T)0; P.xs[1][pt] = (T)0;
+      // the Alg. 2 snapshots (xs, vh0), the other y / v parity and the
+      // global sets' w / s are written before any read, pads included, by
+      // the vectorised pass kernels; the scalar kernels and the fiber
+      // kernels leave pads alone, so they get zeros (P.init_zero, per set
+      // S.fib).  SIP_POISON=1 fills the skipped ones with NaN to prove it.
+      if (P.init_zero) { P.xs[0][pt] = (T)0; P.xs[1][pt] = (T)0; }
+      else if (P.poison) { P.xs[0][pt] = (T)NAN; P.xs[1][pt] = (T)NAN; }
     }
     for (int i = 0; i < P.P; ++i) {
       const SetD<T>& S = P.set[i];
@@ -1215,9 +1223,15 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Prob<T> 
         n1 += fabs(am);
         n2 += am * am;
         if (init_yv) { S.y[1][off] = (T)am; S.v[1][off] = (T)0; }
-        S.y[0][off] = (T)0; S.v[0][off] = (T)0; S.vh0[off] = (T)0;
-        if (S.w) S.w[off] = (T)0;
-        if (S.s) S.s[off] = (T)0;
+        if (P.init_zero || S.fib) {
+          S.y[0][off] = (T)0; S.v[0][off] = (T)0; S.vh0[off] = (T)0;
+          if (S.w) S.w[off] = (T)0;
+          if (S.s) S.s[off] = (T)0;
+        } else if (P.poison) {
+          S.y[0][off] = (T)NAN; S.v[0][off] = (T)NAN; S.vh0[off] = (T)NAN;
+          if (S.w) S.w[off] = (T)NAN;
+          if (S.s) S.s[off] = (T)NAN;
+        }
       }
       warp_acc(acc, nv, 2 * i, n1);
       warp_acc(acc, nv, 2 * i + 1, n2);

@@ -482,6 +482,8 @@ struct Engine : EngineBase {
       g_mich = nsm * std::max(1, std::min(per, getenv("SIP_MICH_CTAS") ? atoi(getenv("SIP_MICH_CTAS")) : 3));   // few CTAs: cheap barriers, 8 loads in flight each
     }
     Pr.dbg = getenv("SIP_DEBUG_MICH") ? 1 : 0;
+    Pr.poison = getenv("SIP_POISON") ? 1 : 0;
+    Pr.init_zero = vec ? 0 : 1;
     Pr.fibv = (nfib_sets && nranks > 1) ? dalloc<double>(4 * MAXP) : nullptr;
     Pr.gbar = dalloc<unsigned>(2);
     CU(cudaMemsetAsync(Pr.gbar, 0, 2 * sizeof(unsigned), stream));

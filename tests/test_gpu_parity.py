@@ -324,3 +324,23 @@ def test_multilevel_fp32_small_c5_like():
         fg = O.feas(sda, O.apply_A(prob.shape, sd, host(x).ravel()))
         fo = O.feas(sda, O.apply_A(prob.shape, sd, x_ref.ravel()))
         assert fg <= 1.5 * fo + 1e-4, (sd.op, sd.kind, fg, fo)
+
+
+# ------------------------------------------------------------ no read before write
+@pytest.mark.parametrize("path", ["vec", "scalar"])
+@pytest.mark.parametrize("seed,shape,kinds", [TINY[1], TINY[4], TINY[5]])
+def test_state_written_before_read(seed, shape, kinds, path, monkeypatch):
+    """k_init leaves the Alg. 2 snapshots, the other y / v parity and the
+    global sets' w / s unwritten on the vectorised path (the pass kernels
+    write them, pads included, before any read).  SIP_POISON=1 fills them
+    with NaN: the run must still equal the oracle's exactly."""
+    monkeypatch.setenv("SIP_POISON", "1")
+    if path == "scalar":
+        monkeypatch.setenv("SIP_NO_VEC", "1")
+    prob = G.tiny(seed, shape, kinds)
+    x, res, log, g = run_gpu(prob, want_log=True)
+    ref = O.parsdmm(prob.shape, prob.sets, prob.m, **prob.options)
+    assert res["iterations"] == ref.iterations
+    np.testing.assert_array_equal(log["cg"][:ref.iterations], ref.cg_per_iter)
+    assert rel(x, ref.x) < 1e-6
+    g.close()
