@@ -84,6 +84,83 @@ __device__ __forceinline__ void chunk_pads(const Geo& g, int pt0, int W, bool* p
   *lastx = PRIM == PRIM_X && (ix + W >= g.nx);
 }
 
+// ------------------------------------------------------------ init (vectorised)
+// k_initv: k_init for the vectorised path, one thread per chunk: x = m
+// (unless warm), the history ring's first x, y_i = A_i m, v_i = 0 (reading
+// L13), and the l1 / l2 norms of A_i m for the relative parameters (L4).
+// Fiber sets' other parity, snapshots and w / s get zeros (the fiber kernels
+// leave pads alone); SIP_POISON fills the fields the pass kernels write
+// before reading with NaN.
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_initv(const __grid_constant__ Prob<T> P, int init_x, int init_yv) {
+  constexpr int W = VT<T>::W;
+  Ctrl& C = *P.ctrl;
+  extern __shared__ double acc[];
+  __shared__ double sh[NWARP + 1];
+  const Geo& g = P.g;
+  const int nv = P.P * 2;
+  for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
+  __syncthreads();
+  const int nch = g.N / W;
+  const T zero[W] = {};
+  T nan_[W];
+#pragma unroll
+  for (int e = 0; e < W; ++e) nan_[e] = (T)NAN;
+  double n1[MAXP], n2[MAXP];
+  for (int i = 0; i < MAXP; ++i) { n1[i] = 0.0; n2[i] = 0.0; }
+  for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
+    const int pt0 = c * W;
+    T mc[W];
+    VT<T>::ldT(P.m + pt0, mc);
+    if (init_x) VT<T>::stT(P.x + pt0, mc);
+    T xc[W];
+    if (init_x) {
+#pragma unroll
+      for (int e = 0; e < W; ++e) xc[e] = mc[e];
+    } else {
+      VT<T>::ldT(P.x + pt0, xc);
+    }
+    VT<T>::stT(P.hist[0] + pt0, xc);
+    if (P.poison) { VT<T>::stT(P.xs[0] + pt0, nan_); VT<T>::stT(P.xs[1] + pt0, nan_); }
+    for (int i = 0; i < P.P; ++i) {
+      const SetD<T>& S = P.set[i];
+      for (int bl = 0; bl < S.nblk; ++bl) {
+        const int prim = S.prim[bl];
+        bool padc = false, lastx = false;
+        T sv[W];
+        switch (prim) {
+          case PRIM_Z: chunk_pads<PRIM_Z>(g, pt0, W, &padc, &lastx); prim_chunk<T, PRIM_Z>(g, P.m, pt0, mc, lastx, padc, sv); break;
+          case PRIM_Y: chunk_pads<PRIM_Y>(g, pt0, W, &padc, &lastx); prim_chunk<T, PRIM_Y>(g, P.m, pt0, mc, lastx, padc, sv); break;
+          case PRIM_X: chunk_pads<PRIM_X>(g, pt0, W, &padc, &lastx); prim_chunk<T, PRIM_X>(g, P.m, pt0, mc, lastx, padc, sv); break;
+          default: prim_chunk<T, PRIM_I>(g, P.m, pt0, mc, false, false, sv); break;
+        }
+        T a1 = 0, a2 = 0;
+#pragma unroll
+        for (int e = 0; e < W; ++e) { a1 += sv[e] < (T)0 ? -sv[e] : sv[e]; a2 += sv[e] * sv[e]; }
+        n1[i] += (double)a1;
+        n2[i] += (double)a2;
+        const int64_t off = (int64_t)bl * g.ld + pt0;
+        if (init_yv) { VT<T>::stT(S.y[1] + off, sv); VT<T>::stT(S.v[1] + off, zero); }
+        if (S.fib || P.poison) {
+          const T* f = S.fib ? zero : nan_;
+          VT<T>::stT(S.y[0] + off, f); VT<T>::stT(S.v[0] + off, f); VT<T>::stT(S.vh0 + off, f);
+          if (S.w) VT<T>::stT(S.w + off, f);
+          if (S.s) VT<T>::stT(S.s + off, f);
+        }
+      }
+    }
+  }
+  for (int i = 0; i < P.P; ++i) {
+    warp_acc(acc, nv, 2 * i, n1[i]);
+    warp_acc(acc, nv, 2 * i + 1, n2[i]);
+  }
+  double* stage = P.partials + (size_t)gridDim.x * nv;
+  if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
+    if (P.nranks > 1) publish(P, stage, nv, threadIdx.x, BLOCK);
+    else if (threadIdx.x == 0) fin_init<T>(P, C, stage);
+  }
+}
+
 // staged arrays of a pass-1 segment (Stage2 slots)
 enum P1Arr { A_X = 0, A_XN, A_Y, A_V, A_M, A_HI, A_VH0, A_XS, A_XSN, A_Y0, A_V0, A_NP1 };
 constexpr int P1_NA_PLAIN = 6;    // x, x+d, y, v, m or lo, hi

@@ -879,7 +879,8 @@ struct Engine : EngineBase {
 
   // init_yv: 1 = y_i = A_i m, v_i = 0; 0 = keep Y[1]/V[1] (prolonged / warm)
   void run_init(int init_x, int init_yv) {
-    k_init<T><<<g_pts, BLOCK, smem_init, stream>>>(Pr, init_x, init_yv);
+    if (vec && !getenv("SIP_SCALAR_INIT")) k_initv<T><<<g_vec, BLOCK, smem_init, stream>>>(Pr, init_x, init_yv);
+    else k_init<T><<<g_pts, BLOCK, smem_init, stream>>>(Pr, init_x, init_yv);
     ++launches;
   }
 
