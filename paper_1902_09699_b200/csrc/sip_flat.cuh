@@ -361,36 +361,19 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
     const bool make_cand = cand && round == 2;
     const bool use_cand = cand && round >= 3;
     const int ntot = use_cand ? (int)J.cand_n : tot;
-    int pd = -1;
-    unsigned pc = 0, pl[LB::N];
-    auto hflush = [&]() {
-      if (pd >= 0) {
-        atomicAdd(&h_cnt[pd], pc);
-        if (sums)
-#pragma unroll
-          for (int q = 0; q < LB::N; ++q) if (pl[q]) atomicAdd(&h_l[q][pd], pl[q]);
-      }
-    };
-    auto hkey = [&](U key) {   // merge runs of equal buckets inside the thread
+    auto hkey = [&](U key) {   // one shared reduction per entry and counter (measured faster than run merging)
       const int d = (int)((key >> lo) & dmask);
-      if (d != pd) {
-        hflush();
-        pd = d; pc = 0;
-#pragma unroll
-        for (int q = 0; q < LB::N; ++q) pl[q] = 0u;
-      }
-      pc += 1;
+      atomicAdd(&h_cnt[d], 1u);
       if (sums) {
         unsigned l[LB::N];
         LB::split(key, l);
 #pragma unroll
-        for (int q = 0; q < LB::N; ++q) pl[q] += l[q];
+        for (int q = 0; q < LB::N; ++q) atomicAdd(&h_l[q][d], l[q]);
       }
     };
     // block-uniform trip count (the periodic flush synchronises the CTA)
     for (int b0 = blockIdx.x * BLOCK * SEL_U; b0 < ntot; b0 += stride) {
       const int q0 = b0 + threadIdx.x;
-      pd = -1; pc = 0;
       if (use_cand) {
         U kk[SEL_U];
         bool ok[SEL_U];
@@ -444,7 +427,6 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
               if (mine & (1u << (u * W + e))) cand[pos++] = (unsigned)K::key(v[u][e]);
         }
       }
-      hflush();
       if (++it == SEL_FLUSH_IT) { it = 0; flush(); }
     }
     flush();
