@@ -304,6 +304,7 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
   if (C.stopped) return;
   __shared__ unsigned h_cnt[NBUCK];
   __shared__ unsigned h_l[LB::N][NBUCK];
+  __shared__ unsigned s_cn;   // candidates appended by this CTA (round 2)
   const Geo& g = P.g;
   const bool check = (C.k % C.opt.check_every) == 0;
   int lo, nb, plo = 0, pnb = 0;
@@ -352,15 +353,20 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
       __syncthreads();
     };
     clear();
+    if (threadIdx.x == 0) s_cn = 0u;
     __syncthreads();
     const int stride = gridDim.x * BLOCK * SEL_U;
     int it = 0;
     // fp32 candidate compaction: round 2 appends the keys of the round-1
     // bucket (its survivors), rounds >= 3 read only those
-    unsigned* cand = (sizeof(T) == 4) ? P.cand[jb] : nullptr;
+    // each CTA appends to its own region (a shared counter, no global
+    // contention) and round >= 3 reads back its own region: rounds 2 and 3
+    // run on the same grid
+    unsigned* cand = (sizeof(T) == 4) ? P.cand[jb] + (size_t)blockIdx.x * P.cand_per : nullptr;
     const bool make_cand = cand && round == 2;
     const bool use_cand = cand && round >= 3;
-    const int ntot = use_cand ? (int)J.cand_n : tot;
+    unsigned* ccnt = P.ccnt + (size_t)jb * gridDim.x + blockIdx.x;
+    const int ntot = use_cand ? (int)__ldcg(ccnt) : tot;
     auto hkey = [&](U key) {   // one shared reduction per entry and counter (measured faster than run merging)
       const int d = (int)((key >> lo) & dmask);
       atomicAdd(&h_cnt[d], 1u);
@@ -372,7 +378,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
       }
     };
     // block-uniform trip count (the periodic flush synchronises the CTA)
-    for (int b0 = blockIdx.x * BLOCK * SEL_U; b0 < ntot; b0 += stride) {
+    const int b_first = use_cand ? 0 : blockIdx.x * BLOCK * SEL_U;
+    const int b_step = use_cand ? BLOCK * SEL_U : stride;
+    for (int b0 = b_first; b0 < ntot; b0 += b_step) {
       const int q0 = b0 + threadIdx.x;
       if (use_cand) {
         U kk[SEL_U];
@@ -418,7 +426,7 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
           }
           const int tot_ = __shfl_sync(0xffffffffu, incl, 31);
           unsigned base_ = 0u;
-          if (lane == 31 && tot_ > 0) base_ = atomicAdd(&C.job[jb].cand_n, (unsigned)tot_);
+          if (lane == 31 && tot_ > 0) base_ = atomicAdd(&s_cn, (unsigned)tot_);
           unsigned pos = __shfl_sync(0xffffffffu, base_, 31) + (unsigned)(incl - cnt);
 #pragma unroll
           for (int u = 0; u < SEL_U; ++u)
@@ -430,6 +438,7 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
       if (++it == SEL_FLUSH_IT) { it = 0; flush(); }
     }
     flush();
+    if (make_cand && threadIdx.x == 0) *ccnt = s_cn;
   }
   if (!any) return;
   if (last_block(P.counter)) {

@@ -55,6 +55,8 @@ struct Prob {
   int nseg1, nseg2;
   // cand[job]: keys of the radix round-1 bucket, compacted by round 2 (fp32)
   unsigned* cand[MAXJOBS];
+  unsigned* ccnt;                 // [MAXJOBS][select grid]: candidates per CTA region
+  long long cand_per;             // candidate region per select CTA (entries)
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
   int dbg;                        // SIP_DEBUG_MICH: k_mich prints its passes
   int poison;                     // SIP_POISON: k_init writes NaN into fields that are written before read

@@ -430,13 +430,23 @@ struct Engine : EngineBase {
     // (3 CTAs / SM plain, 2 on adapt iterations: registers + stage buffers)
     g_p1 = std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * 3));
     g_p1a = std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * 2));
-    if (vec && sizeof(T) == 4)
+    if (vec && sizeof(T) == 4) {
+      // per-CTA candidate regions of the select grid: a CTA visits at most
+      // ceil(chunks / (grid * BLOCK * SEL_U)) iterations of BLOCK * SEL_U chunks
+      int nbmax = 1;
+      for (int i = 0; i < P; ++i) if (Pr.set[i].job >= 0) nbmax = std::max(nbmax, Pr.set[i].nblk);
+      const long long chunks = (long long)nbmax * (g.N / VT<T>::W);
+      const long long per_it = (long long)BLOCK * SEL_U;
+      const long long its = (chunks + (long long)g_sel * per_it - 1) / ((long long)g_sel * per_it);
+      Pr.cand_per = its * per_it * VT<T>::W;
       for (int i = 0; i < P; ++i) {
         const SetD<T>& S = Pr.set[i];
         if (S.job < 0) continue;
-        Pr.cand[S.job] = dalloc<unsigned>((size_t)S.nblk * g.N);
-        Pr.cand[S.sjob] = dalloc<unsigned>((size_t)S.nblk * g.N);
+        Pr.cand[S.job] = dalloc<unsigned>((size_t)g_sel * Pr.cand_per);
+        Pr.cand[S.sjob] = dalloc<unsigned>((size_t)g_sel * Pr.cand_per);
       }
+    }
+    Pr.ccnt = dalloc<unsigned>((size_t)MAXJOBS * std::max(g_sel, 1));
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
     const int gz_ = std::max(zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1,
