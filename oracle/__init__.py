@@ -53,7 +53,7 @@ class Set(C.Structure):
         ("sigma", C.c_double), ("sigma_lo", C.c_double), ("sigma_hi", C.c_double),
         ("k", C.c_int64), ("relative", C.c_int), ("k_frac", C.c_double),
         ("kernel", C.POINTER(C.c_double)), ("kh", C.c_int), ("kw", C.c_int),
-        ("mask", C.POINTER(C.c_ubyte)), ("key_f32", C.c_int),
+        ("mask", C.POINTER(C.c_ubyte)),
         ("app_mode", C.c_int), ("fib_len", C.c_int64),
     ]
 
@@ -66,7 +66,6 @@ class Options(C.Structure):
         ("adapt_every", C.c_int), ("check_every", C.c_int), ("hist_s", C.c_int),
         ("rho_ratio_cap", C.c_double), ("gamma_max", C.c_double),
         ("eq25", C.c_int), ("fixed_work", C.c_int), ("cg_tol_floor", C.c_double),
-        ("decide_f32", C.c_int),
     ]
 
 
@@ -77,6 +76,7 @@ class Log(C.Structure):
         ("cg_per_iter", C.POINTER(C.c_int)), ("branch", C.POINTER(C.c_int)),
         ("rho_trace", C.POINTER(C.c_double)), ("gamma_trace", C.POINTER(C.c_double)),
         ("r_feas_trace", C.POINTER(C.c_double)), ("r_evol_trace", C.POINTER(C.c_double)),
+        ("supp_hash", C.POINTER(C.c_uint64)),
         ("r_feas", C.POINTER(C.c_double)), ("rho", C.POINTER(C.c_double)),
         ("gamma", C.POINTER(C.c_double)),
     ]
@@ -93,6 +93,8 @@ def lib():
         _lib.sipref_op_len.restype = C.c_int64
         _lib.sipref_fiber_len.restype = C.c_int64
         _lib.sipref_feas.restype = C.c_double
+        _lib.sipref_supp_key.restype = C.c_uint64
+        _lib.sipref_supp_key.argtypes = [C.POINTER(Grid), C.c_int, C.c_int64]
     return _lib
 
 
@@ -279,6 +281,7 @@ class Result:
     gamma_trace: np.ndarray
     r_feas_trace: np.ndarray
     r_evol_trace: np.ndarray
+    supp_hash: np.ndarray = None
     y: list = field(default_factory=list)
     v: list = field(default_factory=list)
 
@@ -291,10 +294,12 @@ def _make_log(p, max_iter):
         rho_trace=np.zeros(max_iter * P), gamma_trace=np.zeros(max_iter * P),
         r_feas_trace=np.full(max(1, max_iter * p), np.nan),
         r_evol_trace=np.full(max_iter, np.nan),
+        supp_hash=np.zeros(max(1, max_iter * p), dtype=np.uint64),
         r_feas=np.zeros(max(1, p)), rho=np.zeros(P), gamma=np.zeros(P),
     )
     lg = Log()
     lg.cg_per_iter = _ip(bufs["cg_per_iter"]); lg.branch = _ip(bufs["branch"])
+    lg.supp_hash = bufs["supp_hash"].ctypes.data_as(C.POINTER(C.c_uint64))
     for k in ("rho_trace", "gamma_trace", "r_feas_trace", "r_evol_trace", "r_feas", "rho", "gamma"):
         setattr(lg, k, _dp(bufs[k]))
     return lg, bufs
@@ -314,6 +319,8 @@ def _result(x, st, lg, bufs, p, max_iter, ys=None, vs=None):
         r_feas_trace=bufs["r_feas_trace"][: max_iter * p].reshape(max_iter, p)[:it].copy()
         if p else np.zeros((it, 0)),
         r_evol_trace=bufs["r_evol_trace"][:it].copy(),
+        supp_hash=bufs["supp_hash"][: max_iter * p].reshape(max_iter, p)[:it].copy()
+        if p else np.zeros((it, 0), dtype=np.uint64),
         y=ys or [], v=vs or [],
     )
 
@@ -398,6 +405,20 @@ def interp(c, fshape):
     lib().sipref_interp(C.c_int64(cs[0]), C.c_int64(cs[1]), C.c_int64(cs[2]), _dp(c.ravel()),
                         C.c_int64(fs[0]), C.c_int64(fs[1]), C.c_int64(fs[2]), _dp(f))
     return f.reshape(fshape)
+
+
+def supp_key(shape, op, j, h=None) -> int:
+    """support fingerprint key of compact entry j of operator op's output"""
+    g = make_grid(shape, h)
+    return int(lib().sipref_supp_key(C.byref(g), OPS[op], int(j)))
+
+
+def supp_hash(shape, op, y, h=None) -> int:
+    """sum (mod 2^64) of the keys of the non-zero entries of y (compact)"""
+    s = 0
+    for j in np.flatnonzero(np.asarray(y).ravel() != 0.0):
+        s = (s + supp_key(shape, op, int(j), h)) & 0xFFFFFFFFFFFFFFFF
+    return s
 
 
 def relres(a, b):

@@ -55,7 +55,6 @@ void sipref_default_options(sipref_options *o) {
   o->eq25 = 1;
   o->fixed_work = 0;
   o->cg_tol_floor = 10.0 * DBL_EPSILON; /* reading L18 (fp32 runs: 10*FLT_EPSILON) */
-  o->decide_f32 = 0;
 }
 
 /* ------------------------------------------------------------------ */
@@ -297,13 +296,11 @@ static int cmp_keyidx(const void *pa, const void *pb) {
   if (a->a < b->a) return 1;
   return (a->i > b->i) - (a->i < b->i);
 }
-/* key_f32 (reading L27): the ranking is taken on |w| rounded to fp32, the
-   precision in which an fp32 run takes the same integer decision */
-static void proj_card(int64_t M, const double *w, int64_t k, int key_f32, double *y) {
+static void proj_card(int64_t M, const double *w, int64_t k, double *y) {
   if (k >= M) { memcpy(y, w, (size_t)M * sizeof(double)); return; }
   keyidx *t = (keyidx *)malloc((size_t)(M > 0 ? M : 1) * sizeof(keyidx));
   for (int64_t i = 0; i < M; ++i) {
-    t[i].a = key_f32 ? (double)(float)fabs(w[i]) : fabs(w[i]);
+    t[i].a = fabs(w[i]);
     t[i].i = i;
   }
   qsort(t, (size_t)M, sizeof(keyidx), cmp_keyidx);
@@ -373,7 +370,7 @@ static void project_whole(const sipref_set *s, int64_t M, const double *w, doubl
       for (int64_t i = 0; i < M; ++i) y[i] = w[i] * f;
       break;
     }
-    case SIPREF_CARD: proj_card(M, w, s->k, s->key_f32, y); break;
+    case SIPREF_CARD: proj_card(M, w, s->k, y); break;
   }
 }
 
@@ -541,6 +538,43 @@ static void resolve_set(const sipref_grid *g, const sipref_set *in, const double
 }
 
 /* ------------------------------------------------------------------ */
+/* support fingerprint of a cardinality set (test instrument, not part of */
+/* the method): entry j of A x (compact layout) belongs to block b at     */
+/* grid point (iz, iy, ix); its key is splitmix64(b N + grid index).       */
+/* ------------------------------------------------------------------ */
+static uint64_t splitmix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+static int64_t owner_point(const sipref_grid *g, int blk_op, int64_t j) {
+  int64_t ny = g->n[1], nx = g->n[2];
+  switch (blk_op) {
+    case SIPREF_OP_DY: { int64_t iz = j / ((ny - 1) * nx), r = j % ((ny - 1) * nx);
+                         return (iz * ny + r / nx) * nx + r % nx; }
+    case SIPREF_OP_DX: return (j / (nx - 1)) * nx + j % (nx - 1);
+    default: return j;  /* I and D_z: compact index = grid index */
+  }
+}
+uint64_t sipref_supp_key(const sipref_grid *g, int op, int64_t j) {
+  int64_t N = sipref_npts(g);
+  if (op == SIPREF_OP_TV) {
+    int b = 0;
+    if (j >= len_dz(g)) {
+      j -= len_dz(g); b = 1;
+      if (g->ndim == 3) {
+        if (j < len_dy(g)) return splitmix64((uint64_t)(N + owner_point(g, SIPREF_OP_DY, j)));
+        j -= len_dy(g); b = 2;
+      }
+      return splitmix64((uint64_t)(b * N + owner_point(g, SIPREF_OP_DX, j)));
+    }
+    return splitmix64((uint64_t)j);
+  }
+  return splitmix64((uint64_t)owner_point(g, op, j));
+}
+
+/* ------------------------------------------------------------------ */
 /* Algorithm 1, PARSDMM                                                 */
 /* ------------------------------------------------------------------ */
 static int parsdmm_run(const sipref_grid *g, int p, const sipref_set *in_sets,
@@ -554,7 +588,6 @@ static int parsdmm_run(const sipref_grid *g, int p, const sipref_set *in_sets,
   int64_t *M = (int64_t *)calloc((size_t)P, sizeof(int64_t));
   for (int i = 0; i < p; ++i) {
     resolve_set(g, &in_sets[i], m, &sets[i]);
-    sets[i].key_f32 = o->decide_f32;
     M[i] = sipref_op_len(g, &sets[i]);
   }
   sets[p].op = SIPREF_OP_I;
@@ -638,6 +671,15 @@ static int parsdmm_run(const sipref_grid *g, int p, const sipref_set *in_sets,
         y[i][j] = yn[j];
       }
     }
+
+    if (log && log->supp_hash)
+      for (int i = 0; i < p; ++i) {
+        uint64_t hsum = 0;
+        if (sets[i].type == SIPREF_CARD)
+          for (int64_t j = 0; j < M[i]; ++j)
+            if (y[i][j] != 0.0) hsum += sipref_supp_key(g, sets[i].op, j);
+        log->supp_hash[(size_t)(k - 1) * p + i] = hsum;
+      }
 
     /* stopping conditions, Eqs. 26-28, every check_every iterations */
     if (o->check_every > 0 && k % o->check_every == 0) {

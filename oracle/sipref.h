@@ -49,8 +49,6 @@ typedef struct {
   double k_frac;
   const double *kernel; int kh, kw;  /* BLUR_MASK: kh x kw kernel, row major */
   const unsigned char *mask;         /* BLUR_MASK: N bytes, 1 = observed     */
-  int key_f32;                       /* CARD: rank |w| rounded to fp32 (set by
-                                        the solver from options.decide_f32)  */
   int app_mode;      /* 0: the whole vector A m; 1: each x-fiber (row) of the
                         operator's grid-shaped output; 2: each z-fiber
                         (column) -- the projector is applied to every fiber
@@ -67,8 +65,6 @@ typedef struct {
   int eq25;        /* 1: CG stops by Eq. 25; 0: exactly n_cg iterations    */
   int fixed_work;  /* 1: stop test evaluated but never acted on            */
   double cg_tol_floor; /* floor of the Eq. 25 target (10*eps of the dtype)  */
-  int decide_f32;      /* 1: integer decisions (cardinality support) taken on
-                          fp32-rounded keys, as an fp32 run takes them (L27) */
 } sipref_options;
 
 typedef struct {
@@ -81,12 +77,20 @@ typedef struct {
   double *gamma_trace;  /* [max_iter * (p+1)]                              */
   double *r_feas_trace; /* [max_iter * p], NaN when not a check iteration  */
   double *r_evol_trace; /* [max_iter]                                      */
+  uint64_t *supp_hash;  /* [max_iter * p] CARD sets: sum (mod 2^64) of
+                           sipref_supp_key over the support {j : y_j != 0}
+                           after iteration k; 0 for other sets            */
   /* final values (caller-allocated, may be NULL) */
   double *r_feas;       /* [p]   */
   double *rho, *gamma;  /* [p+1] */
 } sipref_log;
 
 void sipref_default_options(sipref_options *o);
+
+/* support fingerprint key of entry j (compact layout) of operator op's
+   output: splitmix64(b N + grid index of the owning point), b the block of
+   a TV stack.  A test instrument (per-iteration support comparison). */
+uint64_t sipref_supp_key(const sipref_grid *g, int op, int64_t j);
 
 /* number of grid points; M of an operator (compact) */
 int64_t sipref_npts(const sipref_grid *g);

@@ -58,7 +58,6 @@ struct Prob {
   unsigned* ccnt;                 // [MAXJOBS][select grid]: candidates per CTA region
   long long cand_per;             // candidate region per select CTA (entries)
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
-  int dbg;                        // SIP_DEBUG_MICH: k_mich prints its passes
   int poison;                     // SIP_POISON: k_init writes NaN into fields that are written before read
   int init_zero;                  // k_init zeroes every state field (scalar kernels)
   double* fibv;                   // z slabs: this rank's fiber-set sums (4 per set), added to pass 2's

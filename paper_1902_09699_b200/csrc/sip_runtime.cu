@@ -19,10 +19,7 @@
 #include "../../include/sip.h"
 #include "sip_aux_kernels.cuh"
 #include "sip_team.cuh"
-#include "sip_cgs.cuh"
-#include "sip_cgt.cuh"
 #include "sip_fiber.cuh"
-#include "sip_mich.cuh"
 
 using namespace sip;
 
@@ -109,8 +106,6 @@ struct Engine : EngineBase {
   int nsm = 148;
   int nfib_sets = 0;             // sets applied per fiber (k_fiber)
   int g_fib = 0, g_fibw = 0, nfib_sort = 0, nfib_warp = 0;
-  bool mich = false;   // l1 thresholds by k_mich before the radix rounds
-  int g_mich = 0;
   int g_fw[MAXP] = {0};
   size_t smem_fib = 0, smem_fw[MAXP] = {0};
   const std::vector<HostSet>* sets;
@@ -138,15 +133,8 @@ struct Engine : EngineBase {
     memset(&none, 0, sizeof(none));
     CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, l2_window ? &l2av : &none));
   }
-  int g_cgf = 1, g_cgf3 = 1, g_cg2f = 1, g_rhsf = 1;   // lean CG / rhs grids (CTAs per SM: 5 / 3 / 6 / 4)
-  bool u2 = false;               // lean CG unrolled by 2 (SIP_CG_U2)
-  int g_cgt1 = 0, g_cgt2 = 0;    // grids of the tile-staged CG kernels (0: unused)
-  size_t smem_t1 = 0, smem_t2 = 0;
+  int g_cgf = 1, g_cg2f = 1, g_rhsf = 1;   // lean CG / rhs grids (4 CTAs per SM)
   bool vec = false;
-  ZGeo zg{};                     // z-marching CG geometry (sip_zmarch.cuh)
-  SGeo sg{};                     // staged z-marching CG geometry (sip_cgs.cuh)
-  size_t smem_s1 = 0, smem_s2 = 0;
-  size_t smem_z = 0;
   size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0, smem_p1v = 0, smem_p1a = 0;
   // graph
   cudaGraphExec_t gexec = nullptr;
@@ -340,88 +328,6 @@ struct Engine : EngineBase {
     g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
     g_cg2f = g_cgf;   // 5-6 CTAs / SM measured no faster (latency per chunk, not occupancy)
     g_rhsf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
-    g_cgf3 = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 3));
-    u2 = getenv("SIP_CG_U2") != nullptr;
-    // z-marching CG: 3D grids whose rows split into whole warps of W-chunks
-    zg.on = 0;
-    if (vec && ndim == 3 && g.nx % (32 * W) == 0 && !getenv("SIP_NO_ZMARCH")) {
-      const int nxw = g.nx / (32 * W);
-      if (nxw >= 8 && nxw % 8 == 0) { zg.txw = 8; zg.tyw = 1; }
-      else if (nxw < 8 && 8 % nxw == 0) { zg.txw = nxw; zg.tyw = 8 / nxw; }
-      else zg.txw = 0;
-      if (zg.txw && g.ny % zg.tyw == 0) {
-        zg.row_pts = zg.txw * 32 * W;
-        zg.tiles_x = g.nx / zg.row_pts;
-        zg.tiles_y = g.ny / zg.tyw;
-        const int tiles = zg.tiles_x * zg.tiles_y;
-        int nzc = std::max(1, std::min(g.nz, (nsm * 4 + tiles - 1) / tiles));
-        zg.zc = (g.nz + nzc - 1) / nzc;
-        zg.nzc = (g.nz + zg.zc - 1) / zg.zc;
-        zg.on = 1;
-        smem_z = (size_t)2 * (zg.tyw + 2) * zg.row_pts * sizeof(T);
-      }
-    }
-    // staged z-marching CG (sip_cgs.cuh): tile = ty rows x tx chunks = BLOCK
-    // threads; whole-row tiles when they are at least 8 rows deep
-    sg.on = 0;
-    if (vec && getenv("SIP_CGS")) {   // measured slower than the register kernels on C4 (profiles/): opt-in
-      const int nxc = g.nx / W;
-      int tx = 0, ty = 0, full = 0;
-      if (ndim == 3) {
-        if (BLOCK % nxc == 0 && BLOCK / nxc >= 8 && g.ny % (BLOCK / nxc) == 0) { tx = nxc; ty = BLOCK / nxc; full = 1; }
-        else if (nxc % 32 == 0 && g.ny % 8 == 0) { tx = 32; ty = 8; }
-      } else if (nxc % BLOCK == 0) {
-        tx = BLOCK; ty = 1; full = (nxc == BLOCK);
-      }
-      if (tx) {
-        sg.tx = tx; sg.ty = ty; sg.full = full;
-        sg.hrow = ndim == 3 ? 1 : 0;
-        sg.rows = ty + 2 * sg.hrow;
-        sg.tiles_x = nxc / tx;
-        sg.tiles_y = g.ny / ty;
-        const int tiles = sg.tiles_x * sg.tiles_y;
-        smem_s1 = cgs_smem<T>(sg, g.nx, true);
-        smem_s2 = cgs_smem<T>(sg, g.nx, false);
-        if (smem_s1 <= 200 * 1024 && smem_s2 <= 200 * 1024 && sg.rows * (tx + 2) <= 3 * BLOCK) {
-          // one wave: tiles x z-chunks <= resident CTAs (a second partial wave
-          // would double the kernel time)
-          CU(cudaFuncSetAttribute(k_cg1s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          CU(cudaFuncSetAttribute(k_cg2s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          int o1 = 0, o2 = 0;
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cg1s<T>, BLOCK, smem_s1));
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cg2s<T>, BLOCK, smem_s2));
-          const int slots = nsm * std::max(1, std::min(o1, o2));
-          const int nzc = std::max(1, std::min(g.nz, slots / tiles));
-          sg.zc = (g.nz + nzc - 1) / nzc;
-          sg.nzc = (g.nz + sg.zc - 1) / sg.zc;
-          sg.on = 1;
-        }
-      }
-    }
-    // tile-staged flat CG (sip_cgt.cuh): one wave of resident CTAs
-    g_cgt1 = g_cgt2 = 0;
-    if (vec) {
-      const bool hy = ndim == 3;
-      smem_t1 = cgt_smem<T>(g.nx, hy, true);
-      smem_t2 = cgt_smem<T>(g.nx, hy, false);
-      if (smem_t1 <= 200 * 1024 && (!hy || g.plane >= g.nx + W)) {
-        int o1 = 0, o2 = 0;
-        if (hy) {
-          CU(cudaFuncSetAttribute(k_cg1t<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          CU(cudaFuncSetAttribute(k_cg2t<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cg1t<T, true>, BLOCK, smem_t1));
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cg2t<T, true>, BLOCK, smem_t2));
-        } else {
-          CU(cudaFuncSetAttribute(k_cg1t<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          CU(cudaFuncSetAttribute(k_cg2t<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_cg1t<T, false>, BLOCK, smem_t1));
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_cg2t<T, false>, BLOCK, smem_t2));
-        }
-        const int tiles = (g.N / W + BLOCK - 1) / BLOCK;
-        g_cgt1 = std::max(1, std::min(tiles, nsm * std::max(1, o1)));
-        g_cgt2 = std::max(1, std::min(tiles, nsm * std::max(1, o2)));
-      }
-    }
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
     smem_p1v = pass1_smem(P, false);                   // k_pass1t: slots + bulk-copy stages
@@ -449,8 +355,6 @@ struct Engine : EngineBase {
     Pr.ccnt = dalloc<unsigned>((size_t)MAXJOBS * std::max(g_sel, 1));
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
-    const int gz_ = std::max(zg.on ? zg.tiles_x * zg.tiles_y * zg.nzc : 1,
-                             sg.on ? sg.tiles_x * sg.tiles_y * sg.nzc : 1);
     // per-fiber sets (sip_fiber.cuh): one CTA per fiber, a single wave
     if (nfib_sets) {
       int nf = 1;
@@ -479,26 +383,12 @@ struct Engine : EngineBase {
         g_fibw = std::max(g_fibw, g_fw[i]);
       }
     }
-    // k_mich (l1 thresholds by Michelot's fixed point): one resident wave
-    mich = nranks == 1 && getenv("SIP_MICH");   // opt-in: measured slower than the radix rounds on C4
-    if (mich) {
-      bool any_l1 = false;
-      for (int i = 0; i < p; ++i) any_l1 |= (Pr.set[i].kind == K_L1 && Pr.set[i].job >= 0);
-      mich = any_l1;
-    }
-    if (mich) {
-      int per = 0;
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_mich<T>, BLOCK, 0));
-      g_mich = nsm * std::max(1, std::min(per, getenv("SIP_MICH_CTAS") ? atoi(getenv("SIP_MICH_CTAS")) : 3));   // few CTAs: cheap barriers, 8 loads in flight each
-    }
-    Pr.dbg = getenv("SIP_DEBUG_MICH") ? 1 : 0;
     Pr.poison = getenv("SIP_POISON") ? 1 : 0;
     Pr.init_zero = vec ? 0 : 1;
     Pr.fibv = (nfib_sets && nranks > 1) ? dalloc<double>(4 * MAXP) : nullptr;
     Pr.gbar = dalloc<unsigned>(2);
     CU(cudaMemsetAsync(Pr.gbar, 0, 2 * sizeof(unsigned), stream));
-    const int gmax = std::max(2 * g_mich, std::max(std::max(std::max(std::max(std::max(std::max(std::max(g_pts, g_sel), g_p2), g_vec), gz_), g_p1), g_cgf),
-                              std::max(std::max(std::max(g_cgt1, g_cgt2), g_cg2f), std::max(g_fib, g_fibw))));
+    const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cgf, g_cg2f, g_rhsf, g_fib, g_fibw});
     Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -525,10 +415,6 @@ struct Engine : EngineBase {
     CU(cudaEventCreate(&ev0));
     CU(cudaEventCreate(&ev1));
     CU(cudaFuncSetAttribute(k_pass1<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    if (sg.on) {   // the attribute is per function: use the largest any engine may launch with
-      CU(cudaFuncSetAttribute(k_cg1s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      CU(cudaFuncSetAttribute(k_cg2s<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    }
     CU(cudaFuncSetAttribute(k_pass1t<T, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CU(cudaFuncSetAttribute(k_pass1t<T, 0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CU(cudaFuncSetAttribute(k_pass1t<T, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -679,61 +565,30 @@ struct Engine : EngineBase {
   // ---- phase launchers (one rank's part of each step) -------------------
   void launch_blur(int mode, int j) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, mode, j); ++launches; }
   void launch_rhs() {
-    if (lean_cg()) {
+    if (vec) {
       if (ndim == 3) lk(k_rhsf<T, true>, g_rhsf, BLOCK, 0, Pr);
       else lk(k_rhsf<T, false>, g_rhsf, BLOCK, 0, Pr);
-    } else if (vec) k_rhsv<T><<<g_vec, BLOCK, 0, stream>>>(Pr);
-    else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
+    } else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
-  // lean flat CG kernels (sip_vec.cuh k_cg1f / k_cg2f); SIP_OLD_CG=1 keeps the
-  // z-marching / shuffle kernels for A/B measurements
-  // A/B switches read once per engine (launchers run per kernel when graphs are off)
-  const bool env_old_cg = getenv("SIP_OLD_CG") != nullptr;
-  const bool env_cgt = getenv("SIP_CGT") != nullptr;
-  bool lean_cg() const { return vec && !env_old_cg; }
-  bool tiled_cg() const { return lean_cg() && !sg.on && g_cgt1 > 0 && env_cgt; }   // opt-in: measured equal to the flat kernels
+  // flat CG kernels (sip_vec.cuh k_cg1f / k_cg2f) with the deferred x update;
+  // the scalar kernels (sip_kernels.cuh) for general shapes, the blur
+  // operator and n_cg > MAXCG (no ring slot per step)
+  bool lean_cg() const { return vec && Pr.defer_x; }
   void launch_cg1(int j) {
-    if (tiled_cg()) {
-      const bool hy = ndim == 3;
-      if (hy) k_cg1t<T, true><<<g_cgt1, BLOCK, smem_t1, stream>>>(Pr, j);
-      else k_cg1t<T, false><<<g_cgt1, BLOCK, smem_t1, stream>>>(Pr, j);
-    } else if (lean_cg() && !sg.on) {
-      if (u2) {
-        if (ndim == 3) lk(k_cg1f<T, true, true>, g_cgf3, BLOCK, 0, Pr, j);
-        else lk(k_cg1f<T, false, true>, g_cgf3, BLOCK, 0, Pr, j);
-      } else {
-        if (ndim == 3) lk(k_cg1f<T, true, false>, g_cgf, BLOCK, 0, Pr, j);
-        else lk(k_cg1f<T, false, false>, g_cgf, BLOCK, 0, Pr, j);
-      }
-    } else if (sg.on) {
-      k_cg1s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s1, stream>>>(Pr, sg, j);
-    } else if (zg.on) {
-      // measured on C4: z-marching wins for k_cg1 (operand recomputed from
-      // two arrays at 5 positions), the flat sweep for k_cg2 (profiles/)
-      k_cg1z<T, true><<<zg.tiles_x * zg.tiles_y * zg.nzc, BLOCK, smem_z, stream>>>(Pr, zg, j);
-    } else if (vec) {
-      k_cg1v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
+    if (lean_cg()) {
+      if (ndim == 3) lk(k_cg1f<T, true>, g_cgf, BLOCK, 0, Pr, j);
+      else lk(k_cg1f<T, false>, g_cgf, BLOCK, 0, Pr, j);
     } else {
       k_cg1<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
     }
     ++launches;
   }
   void launch_cg2(int j) {
-    if (tiled_cg() && Pr.defer_x) {
-      if (ndim == 3) k_cg2t<T, true><<<g_cgt2, BLOCK, smem_t2, stream>>>(Pr, j);
-      else k_cg2t<T, false><<<g_cgt2, BLOCK, smem_t2, stream>>>(Pr, j);
-    } else if (lean_cg() && !sg.on && Pr.defer_x) {
-      if (u2) {
-        if (ndim == 3) lk(k_cg2f<T, true, true>, g_cgf3, BLOCK, 0, Pr, j);
-        else lk(k_cg2f<T, false, true>, g_cgf3, BLOCK, 0, Pr, j);
-      } else {
-        if (ndim == 3) lk(k_cg2f<T, true, false>, g_cg2f, BLOCK, 0, Pr, j);
-        else lk(k_cg2f<T, false, false>, g_cg2f, BLOCK, 0, Pr, j);
-      }
-    } else if (sg.on && Pr.defer_x) k_cg2s<T><<<sg.tiles_x * sg.tiles_y * sg.nzc, BLOCK, smem_s2, stream>>>(Pr, sg, j);
-    else if (vec) k_cg2v<T><<<g_vec, BLOCK, 0, stream>>>(Pr, j);
-    else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
+    if (lean_cg()) {
+      if (ndim == 3) lk(k_cg2f<T, true>, g_cg2f, BLOCK, 0, Pr, j);
+      else lk(k_cg2f<T, false>, g_cg2f, BLOCK, 0, Pr, j);
+    } else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
     ++launches;
   }
   // deferred x update: one ring slot per CG step (vectorised path, n_cg <= MAXCG)
@@ -785,7 +640,6 @@ struct Engine : EngineBase {
     launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
-      if (mich) { lk(k_mich<T>, g_mich, BLOCK, 0, Pr); ++launches; mark(KB_SELECT); }
       for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
       if (has_card()) { launch_tie(); mark(KB_TIE); }
     }

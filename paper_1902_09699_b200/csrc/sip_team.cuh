@@ -12,7 +12,6 @@
 // rounding.
 #pragma once
 #include "sip_pass.cuh"
-#include "sip_zmarch.cuh"
 
 namespace sip {
 

@@ -66,319 +66,11 @@ template <> struct VT<double> {
   __device__ static void st(double* p, const double* o) { stT(p, o); }
 };
 
-// the 7-point neighbourhood of a chunk in the storage precision
-template <class T>
-struct Nbr {
-  static constexpr int W = VT<T>::W;
-  T c[W], zm[W], zp[W], ym[W], yp[W];
-  T xl, xr;
-};
-
-// fetch a vector's neighbourhood; USE_P: the fetched value is p_new = r + beta p_old
-template <class T, bool USE_P>
-__device__ __forceinline__ void fetch5(const Geo& g, const T* r, const T* p, T beta, int pt0, bool has_y,
-                                       Nbr<T>& n) {
-  constexpr int W = VT<T>::W;
-  T a[5][W], b[5][W];
-  const int off[5] = {0, -g.plane, g.plane, -g.nx, g.nx};
-  const int np = has_y ? 5 : 3;
-#pragma unroll
-  for (int q = 0; q < 5; ++q)
-    if (q < np) VT<T>::ldT(r + pt0 + off[q], a[q]);
-  if (USE_P) {
-#pragma unroll
-    for (int q = 0; q < 5; ++q)
-      if (q < np) VT<T>::ldT(p + pt0 + off[q], b[q]);
-  }
-#pragma unroll
-  for (int e = 0; e < W; ++e) {
-    auto f = [&](int q) { return USE_P ? a[q][e] + beta * b[q][e] : a[q][e]; };
-    n.c[e] = f(0);
-    n.zm[e] = f(1);
-    n.zp[e] = f(2);
-    n.ym[e] = has_y ? f(3) : (T)0;
-    n.yp[e] = has_y ? f(4) : (T)0;
-  }
-}
-
-// x neighbours by shuffle; warp-edge lanes load theirs
-template <class T, bool USE_P>
-__device__ __forceinline__ void fetch_x(const T* r, const T* p, T beta, int pt0, int lane, Nbr<T>& n) {
-  constexpr int W = VT<T>::W;
-  n.xl = __shfl_up_sync(0xffffffffu, n.c[W - 1], 1);
-  n.xr = __shfl_down_sync(0xffffffffu, n.c[0], 1);
-  if (lane == 0) n.xl = USE_P ? r[pt0 - 1] + beta * p[pt0 - 1] : r[pt0 - 1];
-  if (lane == 31) n.xr = USE_P ? r[pt0 + W] + beta * p[pt0 + W] : r[pt0 + W];
-}
-
 template <class T>
 struct CoefT {
   T cI, cz, cy, cx;
   __device__ explicit CoefT(const Ctrl& C) : cI((T)C.cI), cz((T)C.cz), cy((T)C.cy), cx((T)C.cx) {}
 };
-
-// (C p) at the W points of a chunk: C = cI I + cz Dz'Dz + cy Dy'Dy + cx Dx'Dx (Eq. 23)
-template <class T>
-__device__ __forceinline__ void apply_C_vec(const CoefT<T>& c, const Geo& g, bool has_z, bool has_y,
-                                            bool has_x, const Nbr<T>& n, const Loc& L, T* q) {
-  constexpr int W = VT<T>::W;
-  const bool zlo = L.gz >= 1, zhi = L.gz < g.nz_g - 1;
-  const bool ylo = L.iy >= 1, yhi = L.iy < g.ny - 1;
-#pragma unroll
-  for (int e = 0; e < W; ++e) {
-    const T p0 = n.c[e];
-    T v = c.cI * p0;
-    if (has_z) {
-      T a = 0;
-      if (zlo) a += p0 - n.zm[e];
-      if (zhi) a -= n.zp[e] - p0;
-      v += c.cz * a;
-    }
-    if (has_y) {
-      T a = 0;
-      if (ylo) a += p0 - n.ym[e];
-      if (yhi) a -= n.yp[e] - p0;
-      v += c.cy * a;
-    }
-    if (has_x) {
-      const int ix = L.ix + e;
-      const T left = e > 0 ? n.c[e - 1] : n.xl;
-      const T right = e < W - 1 ? n.c[e + 1] : n.xr;
-      T a = 0;
-      if (ix >= 1) a += p0 - left;
-      if (ix < g.nx - 1) a -= right - p0;
-      v += c.cx * a;
-    }
-    q[e] = v;
-  }
-}
-
-__device__ __forceinline__ bool pad_vec(const Geo& g, int prim, const Loc& L, int e) {
-  switch (prim) {
-    case PRIM_Z: return L.gz >= g.nz_g - 1;
-    case PRIM_Y: return L.iy >= g.ny - 1;
-    case PRIM_X: return L.ix + e >= g.nx - 1;
-    default: return false;
-  }
-}
-
-// ------------------------------------------------------------ k_rhsv
-// b = sum_i A_i^T (rho_i y_i + v_i) (Eq. 21 line 1), r = b - C x^k;
-// ||b||^2, ||r||^2; last CTA sets the Eq. 25 target and the CG flags.
-template <class T>
-__global__ void __launch_bounds__(BLOCK) k_rhsv(const __grid_constant__ Prob<T> P) {
-  constexpr int W = VT<T>::W;
-  Ctrl& C = *P.ctrl;
-  if (C.stopped) return;
-  __shared__ double sh[NWARP + 1];
-  __shared__ double out[2];
-  const Geo& g = P.g;
-  const int par = C.k & 1;
-  const CoefT<T> cf(C);
-  const bool hz = P.has[PRIM_Z], hy = P.has[PRIM_Y], hx = P.has[PRIM_X];
-  const int nch = g.N / W;
-  const int lane = threadIdx.x & 31;
-  double bb = 0.0, rr = 0.0;
-  for (int c0 = blockIdx.x * BLOCK + (threadIdx.x & ~31); c0 < nch; c0 += gridDim.x * BLOCK) {
-    const int c = c0 + lane;
-    const bool valid = c < nch;
-    const int pt0 = (valid ? c : nch - 1) * W;
-    const Loc L = locate(g, pt0);
-    T b[W];
-#pragma unroll
-    for (int e = 0; e < W; ++e) b[e] = 0;
-    for (int i = 0; i < P.P; ++i) {
-      const SetD<T>& S = P.set[i];
-      const T rho = (T)C.rho[i];
-      for (int bl = 0; bl < S.nblk; ++bl) {
-        const int prim = S.prim[bl];
-        const T* y = S.y[par] + (int64_t)bl * g.ld;
-        const T* v = S.v[par] + (int64_t)bl * g.ld;
-        T yy[W], vv[W], u[W];
-        VT<T>::ldT(y + pt0, yy);
-        VT<T>::ldT(v + pt0, vv);
-#pragma unroll
-        for (int e = 0; e < W; ++e) u[e] = rho * yy[e] + vv[e];
-        if (prim == PRIM_I) {
-#pragma unroll
-          for (int e = 0; e < W; ++e) b[e] += u[e];
-        } else if (prim == PRIM_X) {        // D_x^T: +u[x-1] - u[x] (pads hold 0)
-          T ul = __shfl_up_sync(0xffffffffu, u[W - 1], 1);
-          if (lane == 0) ul = rho * y[pt0 - 1] + v[pt0 - 1];
-          const T ih = (T)g.ihx;
-#pragma unroll
-          for (int e = 0; e < W; ++e) {
-            const T um = e > 0 ? u[e - 1] : ul;
-            T a = 0;
-            if (L.ix + e >= 1) a += um;
-            if (L.ix + e < g.nx - 1) a -= u[e];
-            b[e] += a * ih;
-          }
-        } else {                            // D_z^T / D_y^T
-          const bool z = prim == PRIM_Z;
-          const int d = z ? g.plane : g.nx;
-          T ym[W], vm[W];
-          VT<T>::ldT(y + pt0 - d, ym);
-          VT<T>::ldT(v + pt0 - d, vm);
-          const bool lo = z ? (L.gz >= 1) : (L.iy >= 1);
-          const bool hi = z ? (L.gz < g.nz_g - 1) : (L.iy < g.ny - 1);
-          const T ih = (T)(z ? g.ihz : g.ihy);
-#pragma unroll
-          for (int e = 0; e < W; ++e) {
-            T a = 0;
-            if (lo) a += rho * ym[e] + vm[e];
-            if (hi) a -= u[e];
-            b[e] += a * ih;
-          }
-        }
-      }
-    }
-    Nbr<T> n;
-    fetch5<T, false>(g, P.x, nullptr, (T)0, pt0, hy, n);
-    fetch_x<T, false>(P.x, nullptr, (T)0, pt0, lane, n);
-    T q[W], r[W];
-    apply_C_vec<T>(cf, g, hz, hy, hx, n, L, q);
-    T sb = 0, sr = 0;
-#pragma unroll
-    for (int e = 0; e < W; ++e) {
-      r[e] = b[e] - q[e];
-      sb += b[e] * b[e];
-      sr += r[e] * r[e];
-    }
-    if (valid) {
-      VT<T>::stT(P.r + pt0, r);
-      bb += (double)sb;
-      rr += (double)sr;
-    }
-  }
-  bb = block_sum(bb, sh);
-  rr = block_sum(rr, sh);
-  if (threadIdx.x == 0) { P.partials[blockIdx.x * 2] = bb; P.partials[blockIdx.x * 2 + 1] = rr; }
-  if (last_block(P.counter)) {
-    reduce_partials(P.partials, 2, out, sh);
-    if (threadIdx.x == 0) {
-      *P.counter = 0u;
-      if (P.nranks > 1) publish(P, out, 2, 0, 1);
-      else fin_rhs(C, out);
-    }
-  }
-}
-
-// ------------------------------------------------------------ CG
-// k_cg1v(j): p_j = r + beta p_{j-1} (p_0 = r); <p_j, C p_j>; alpha
-template <class T>
-__global__ void __launch_bounds__(BLOCK) k_cg1v(const __grid_constant__ Prob<T> P, int j) {
-  constexpr int W = VT<T>::W;
-  Ctrl& C = *P.ctrl;
-  if (C.stopped) return;
-  const Geo& g = P.g;
-  const int nch = g.N / W;
-  if (j == 0 && C.zero_x) {   // b = 0 gives x = 0
-    for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
-      T z[W] = {};
-      VT<T>::stT(P.x + c * W, z);
-    }
-    return;
-  }
-  if (!C.cg_active) return;
-  __shared__ double sh[NWARP + 1];
-  __shared__ double out[1];
-  const T beta = (T)C.beta;
-  const CoefT<T> cf(C);
-  const T* pold = j > 0 ? p_slot(P, j - 1) : nullptr;
-  T* pw = p_slot(P, j);
-  const bool hz = P.has[PRIM_Z], hy = P.has[PRIM_Y], hx = P.has[PRIM_X];
-  const int lane = threadIdx.x & 31;
-  double pq = 0.0;
-  for (int c0 = blockIdx.x * BLOCK + (threadIdx.x & ~31); c0 < nch; c0 += gridDim.x * BLOCK) {
-    const int c = c0 + lane;
-    const bool valid = c < nch;
-    const int pt0 = (valid ? c : nch - 1) * W;
-    const Loc L = locate(g, pt0);
-    Nbr<T> n;
-    if (j > 0) {
-      fetch5<T, true>(g, P.r, pold, beta, pt0, hy, n);
-      fetch_x<T, true>(P.r, pold, beta, pt0, lane, n);
-    } else {
-      fetch5<T, false>(g, P.r, pold, beta, pt0, hy, n);
-      fetch_x<T, false>(P.r, pold, beta, pt0, lane, n);
-    }
-    T q[W];
-    apply_C_vec<T>(cf, g, hz, hy, hx, n, L, q);
-    if (valid) {
-      VT<T>::stT(pw + pt0, n.c);
-      T s = 0;
-#pragma unroll
-      for (int e = 0; e < W; ++e) s += n.c[e] * q[e];
-      pq += (double)s;
-    }
-  }
-  pq = block_sum(pq, sh);
-  if (threadIdx.x == 0) P.partials[blockIdx.x] = pq;
-  if (last_block(P.counter)) {
-    reduce_partials(P.partials, 1, out, sh);
-    if (threadIdx.x == 0) {
-      *P.counter = 0u;
-      if (P.nranks > 1) publish(P, out, 1, 0, 1);
-      else fin_cg1(C, out, j);
-    }
-  }
-}
-
-// k_cg2v(j): x += alpha p, r -= alpha C p; <r, r>; beta, Eq. 25 test
-template <class T>
-__global__ void __launch_bounds__(BLOCK) k_cg2v(const __grid_constant__ Prob<T> P, int j) {
-  constexpr int W = VT<T>::W;
-  Ctrl& C = *P.ctrl;
-  if (C.stopped || !C.cg_active) return;
-  __shared__ double sh[NWARP + 1];
-  __shared__ double out[1];
-  const Geo& g = P.g;
-  const int nch = g.N / W;
-  const T* pv = p_slot(P, j);
-  const T alpha = (T)C.alpha;
-  const bool upx = !P.defer_x;
-  const CoefT<T> cf(C);
-  const bool hz = P.has[PRIM_Z], hy = P.has[PRIM_Y], hx = P.has[PRIM_X];
-  const int lane = threadIdx.x & 31;
-  double rr = 0.0;
-  for (int c0 = blockIdx.x * BLOCK + (threadIdx.x & ~31); c0 < nch; c0 += gridDim.x * BLOCK) {
-    const int c = c0 + lane;
-    const bool valid = c < nch;
-    const int pt0 = (valid ? c : nch - 1) * W;
-    const Loc L = locate(g, pt0);
-    T xv[W], rv[W];
-    if (upx) VT<T>::ldcs(P.x + pt0, xv);
-    VT<T>::ldcs(P.r + pt0, rv);
-    Nbr<T> n;
-    fetch5<T, false>(g, pv, nullptr, (T)0, pt0, hy, n);
-    fetch_x<T, false>(pv, nullptr, (T)0, pt0, lane, n);
-    T q[W];
-    apply_C_vec<T>(cf, g, hz, hy, hx, n, L, q);
-    T s = 0;
-#pragma unroll
-    for (int e = 0; e < W; ++e) {
-      xv[e] = xv[e] + alpha * n.c[e];
-      rv[e] = rv[e] - alpha * q[e];
-      s += rv[e] * rv[e];
-    }
-    if (valid) {
-      if (upx) VT<T>::stT(P.x + pt0, xv);
-      VT<T>::stT(P.r + pt0, rv);
-      rr += (double)s;
-    }
-  }
-  rr = block_sum(rr, sh);
-  if (threadIdx.x == 0) P.partials[blockIdx.x] = rr;
-  if (last_block(P.counter)) {
-    reduce_partials(P.partials, 1, out, sh);
-    if (threadIdx.x == 0) {
-      *P.counter = 0u;
-      if (P.nranks > 1) publish(P, out, 1, 0, 1);
-      else fin_cg2(C, out, j);
-    }
-  }
-}
 
 // k_cgx: the deferred x update after the CG loop, x += sum_j alpha_j p_j
 // over the cg_count completed steps, in step order (Eq. 21 line 1's CG)
@@ -458,8 +150,8 @@ __device__ __forceinline__ CoefT<T> coefs_present(const Prob<T>& P, const Ctrl& 
 }
 
 // k_cg1f(j): p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j>; p_j -> slot j
-template <class T, bool HY, bool U2>
-__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
+template <class T, bool HY>
+__global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
   pdl_begin();
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
@@ -487,7 +179,7 @@ __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg1f(const __grid_constan
   dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
   const int pl = g.plane, nx = g.nx;
   double pq = 0.0;
-#pragma unroll (U2 ? 2 : 1)
+#pragma unroll 1
   for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
     const int pt0 = c * W;
     const CGLoc<T> L(g, k, c, ncr, dncr);
@@ -534,8 +226,8 @@ __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg1f(const __grid_constan
 }
 
 // k_cg2f(j): r -= alpha C p_j and <r, r> (the x update is deferred to k_cgx)
-template <class T, bool HY, bool U2>
-__global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
+template <class T, bool HY>
+__global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
   pdl_begin();
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
@@ -552,7 +244,7 @@ __global__ void __launch_bounds__(BLOCK, U2 ? 3 : 4) k_cg2f(const __grid_constan
   dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
   const int pl = g.plane, nx = g.nx;
   double rr = 0.0;
-#pragma unroll (U2 ? 2 : 1)
+#pragma unroll 1
   for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
     const int pt0 = c * W;
     const CGLoc<T> L(g, k, c, ncr, dncr);

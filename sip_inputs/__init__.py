@@ -52,6 +52,18 @@ class Problem:
     n_levels: int = 1
     extra: dict = field(default_factory=dict)
 
+    def __post_init__(self):
+        # fp32 configurations: the model and per-entry bounds are the values
+        # an fp32 run holds, so both sides of a parity test start from the
+        # same bits (the oracle widens them exactly to fp64)
+        if self.dtype == "f32":
+            self.m = np.asarray(self.m, dtype=np.float64).astype(np.float32).astype(np.float64)
+            for s in self.sets:
+                for a in ("lo_vec", "hi_vec"):
+                    v = getattr(s, a)
+                    if v is not None:
+                        setattr(s, a, np.asarray(v, dtype=np.float64).astype(np.float32).astype(np.float64))
+
     @property
     def N(self) -> int:
         return int(np.prod(self.shape))

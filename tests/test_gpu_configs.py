@@ -31,7 +31,6 @@ def oracle_opts(prob, **kw):
     o = dict(prob.options)
     if prob.dtype == "f32":
         o["cg_tol_floor"] = 10 * F32_EPS
-        o["decide_f32"] = 1
     o.update(kw)
     return o
 

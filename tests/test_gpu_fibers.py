@@ -193,7 +193,6 @@ def test_fiber_fp32_medium_run():
     res, st = g.project(md, x, max_iter=150, tol=1e-3)
     o = dict(opts)
     o["cg_tol_floor"] = 10 * float(np.finfo(np.float32).eps)
-    o["decide_f32"] = 1
     ref = O.parsdmm(shape, sets, host(md), max_iter=150, **{k: v for k, v in o.items() if k != "max_iter"})
     assert O.relres(host(x), ref.x) < 1e-3
     g.close()

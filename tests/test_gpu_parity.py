@@ -220,7 +220,6 @@ def oracle_opts(prob, **kw):
     o = dict(prob.options)
     if prob.dtype == "f32":
         o["cg_tol_floor"] = 10 * float(np.finfo(np.float32).eps)   # reading L18
-        o["decide_f32"] = 1                                         # reading L27
     o.update(kw)
     return o
 

@@ -119,7 +119,7 @@ def test_slab_fp32_natural_mode_vs_oracle():
     prob = mid_problem()
     prob.sets.append(SetDef("DZ", "card", k_frac=0.05, relative=True))
     x, res, _, _ = run(prob, 4)
-    o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps), decide_f32=1)
+    o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps))
     ref = O.parsdmm(prob.shape, prob.sets, prob.m, **o)
     assert O.relres(x, ref.x) < 1e-3, (res["iterations"], ref.iterations)
 
@@ -181,7 +181,7 @@ def test_slab_multilevel_matches_oracle(shape, levels, kinds, ranks):
 
 def test_slab_multilevel_fp32_c5_like():
     prob = G.c5(seed=4, shape=(32, 32, 16))
-    o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps), decide_f32=1)
+    o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps))
     x_ref, _, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3, **o)
     g = grid_for(prob)
     g.set_option("virtual_ranks", 4)
