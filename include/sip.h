@@ -251,6 +251,16 @@ sip_status sip_get_state(sip_grid g, int set_id, int which, void *out);
 sip_status sip_get_log(sip_grid g, int max_iter, int *cg, int *branch, double *rho_trace,
                        double *gamma_trace, double *r_feas, double *r_evol);
 
+/* Cardinality support fingerprints of the last sip_project run (a test
+   instrument for SURVEY 8(c)'s "cardinality support at every iteration"):
+   out[(k-1) * p + i] = sum mod 2^64 of splitmix64(b * N_global + global grid
+   index of the owning point) over the non-zero entries of y_i after
+   iteration k, b the operator block; 0 for sets that are not whole-vector
+   cardinality sets.  Virtual ranks: summed over the slabs; NCCL ranks: this
+   rank's slab only (sum over ranks to compare).  out holds max_iter * p
+   uint64 (host).  Errors: SIP_ERR_ARG (null), SIP_ERR_STATE (no run). */
+sip_status sip_get_support_log(sip_grid g, int max_iter, uint64_t *out);
+
 /* Number of sets p, grid points N (this rank) and compact length of set i. */
 sip_status sip_get_sizes(sip_grid g, int *p, int64_t *n_local, int set_id, int64_t *m_compact);
 

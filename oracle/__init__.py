@@ -397,6 +397,28 @@ def restrict(shape, f):
     return c.reshape(cshape)
 
 
+def prolong_field(cshape, fshape, op, c):
+    """sipref_prolong_field: the coarse field of operator op (compact) on the
+    fine grid (compact)"""
+    cg, fg = make_grid(cshape), make_grid(fshape)
+    c = _f64(c).ravel()
+    from sip_inputs import SetDef  # plain data holder
+    M = op_len(fshape, SetDef(op, "bounds"))
+    f = np.zeros(M)
+    lib().sipref_prolong_field(C.byref(cg), C.byref(fg), OPS[op], _dp(c), _dp(f))
+    return f
+
+
+def resolve_set(shape, sd, m, h=None):
+    """sipref_resolve_set: (sigma, sigma_lo, sigma_hi, k) of a relative set"""
+    g = make_grid(shape, h)
+    hold = _SetHolder(sd)
+    out = Set()
+    m = _f64(m).ravel()
+    lib().sipref_resolve_set(C.byref(g), C.byref(hold.s), _dp(m), C.byref(out))
+    return float(out.sigma), float(out.sigma_lo), float(out.sigma_hi), int(out.k)
+
+
 def interp(c, fshape):
     c = _f64(c)
     cs = c.shape if c.ndim == 3 else (c.shape[0], 1, c.shape[1])

@@ -514,7 +514,7 @@ int sipref_adapt_rho_gamma(int64_t M, const double *v_hat, const double *v_hat0,
 /* ------------------------------------------------------------------ */
 /* set resolution: relative parameters (readings L4, L23)               */
 /* ------------------------------------------------------------------ */
-static void resolve_set(const sipref_grid *g, const sipref_set *in, const double *m,
+void sipref_resolve_set(const sipref_grid *g, const sipref_set *in, const double *m,
                         sipref_set *out) {
   *out = *in;
   out->fib_len = sipref_fiber_len(g, in);
@@ -587,7 +587,7 @@ static int parsdmm_run(const sipref_grid *g, int p, const sipref_set *in_sets,
   sipref_set *sets = (sipref_set *)calloc((size_t)P, sizeof(sipref_set));
   int64_t *M = (int64_t *)calloc((size_t)P, sizeof(int64_t));
   for (int i = 0; i < p; ++i) {
-    resolve_set(g, &in_sets[i], m, &sets[i]);
+    sipref_resolve_set(g, &in_sets[i], m, &sets[i]);
     M[i] = sipref_op_len(g, &sets[i]);
   }
   sets[p].op = SIPREF_OP_I;
@@ -857,9 +857,11 @@ void sipref_interp(int64_t cz, int64_t cy, int64_t cx, const double *c,
   }
 }
 
-/* interpolate the field of one operator (block by block for TV) */
-static void interp_field(const sipref_grid *cgd, const sipref_grid *fgd, int op,
-                         const double *c, double *f) {
+/* interpolate the field of one operator (block by block for TV): each block
+   is an image of its own shape ("as images"; reading L23), e.g.
+   D_z's (nz-1) x ny x nx */
+void sipref_prolong_field(const sipref_grid *cgd, const sipref_grid *fgd, int op,
+                          const double *c, double *f) {
   int64_t cz = cgd->n[0], cy = cgd->n[1], cx = cgd->n[2];
   int64_t fz = fgd->n[0], fy = fgd->n[1], fx = fgd->n[2];
   switch (op) {
@@ -918,11 +920,11 @@ int sipref_parsdmm_multilevel(const sipref_grid *g, int p, const sipref_set *set
       for (int i = 0; i < P; ++i) { rho[i] = o->rho0; gam[i] = o->gamma0; }
     } else {
       const sipref_grid *gc = &gr[l + 1];
-      interp_field(gc, gl, SIPREF_OP_I, xc, init_x);
+      sipref_prolong_field(gc, gl, SIPREF_OP_I, xc, init_x);
       for (int i = 0; i < P; ++i) {
         int op = (i < p) ? sets[i].op : SIPREF_OP_I;
-        interp_field(gc, gl, op, yc[i], yl[i]);
-        interp_field(gc, gl, op, vc[i], vl[i]);
+        sipref_prolong_field(gc, gl, op, yc[i], yl[i]);
+        sipref_prolong_field(gc, gl, op, vc[i], vl[i]);
       }
     }
     sipref_log *lg = logs ? &logs[l] : NULL;

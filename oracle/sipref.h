@@ -155,6 +155,15 @@ int sipref_parsdmm_multilevel(const sipref_grid *g, int p, const sipref_set *set
 
 /* multilevel transfers (exposed for pins) */
 void sipref_restrict(const sipref_grid *fine, const double *f, double *c);
+/* prolongation of one operator's field from the coarse to the fine grid:
+   every block interpolated on its own shape (reading L23) */
+void sipref_prolong_field(const sipref_grid *coarse, const sipref_grid *fine, int op,
+                          const double *c, double *f);
+/* relative parameters resolved from m (readings L4, L23): L1 sigma =
+   frac ||A m||_1, L2 sigma = frac ||A m||_2, ANNULUS bounds x ||A m||_2,
+   CARD k = floor(k_frac M) (the fiber length for per-fiber sets) */
+void sipref_resolve_set(const sipref_grid *g, const sipref_set *in, const double *m,
+                        sipref_set *out);
 void sipref_interp(int64_t cz, int64_t cy, int64_t cx, const double *c,
                    int64_t fz, int64_t fy, int64_t fx, double *f);
 

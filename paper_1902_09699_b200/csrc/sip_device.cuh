@@ -127,8 +127,6 @@ struct Job {
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
   unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
-  unsigned mich_passes;          // l1: Michelot passes of this iteration (k_mich)
-  double theta_w;                // l1: last threshold of this job, the next warm start (k_mich)
 };
 
 struct Ctrl {
@@ -162,8 +160,29 @@ struct Ctrl {
   // log
   int* log_cg; int* log_branch; double* log_rho; double* log_gamma;
   double* log_feas; double* log_evol;
+  unsigned long long* log_supp;  // [log_len * p] cardinality support fingerprints (atomic sums)
   int log_len;
 };
+
+// ---------------------------------------------------------------- support fingerprint
+// A test instrument, not part of the method: the support of a cardinality
+// set after iteration k is logged as the wrapping sum of splitmix64(b N_g +
+// global point index) over its non-zero entries (b the block, N_g the global
+// point count), so per-iteration supports can be compared with the oracle.
+__device__ __forceinline__ unsigned long long supp_mix(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// warp-uniform call: one atomic per warp
+__device__ __forceinline__ void supp_add_warp(const Ctrl& C, int i, unsigned long long h) {
+  const int k = C.k;
+  if (!C.log_supp || k - 1 >= C.log_len) return;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  if ((threadIdx.x & 31) == 0 && h) atomicAdd(C.log_supp + (size_t)(k - 1) * C.p + i, h);
+}
 
 // ---------------------------------------------------------------- keys
 // |v| as an order-preserving unsigned key and its significand / exponent

@@ -77,6 +77,9 @@ __global__ void __launch_bounds__(BLOCK) k_selectf(const __grid_constant__ Prob<
   using U = typename K::U;
   using LB = Limbs<T>;
   constexpr int W = VT<T>::W;
+  // the per-CTA candidate regions (cand_per) and the ccnt stride are sized
+  // for this grid: any other launch geometry would overrun them
+  if (gridDim.x != (unsigned)P.sel_grid) __trap();
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
   __shared__ unsigned h_cnt[NBUCK];

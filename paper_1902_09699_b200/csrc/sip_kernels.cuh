@@ -57,6 +57,7 @@ struct Prob {
   unsigned* cand[MAXJOBS];
   unsigned* ccnt;                 // [MAXJOBS][select grid]: candidates per CTA region
   long long cand_per;             // candidate region per select CTA (entries)
+  int sel_grid;                   // the grid k_selectf is sized for (regions, ccnt stride)
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
   int poison;                     // SIP_POISON: k_init writes NaN into fields that are written before read
   int init_zero;                  // k_init zeroes every state field (scalar kernels)
@@ -881,6 +882,7 @@ __global__ void __launch_bounds__(BLOCK) k_pass2(const __grid_constant__ Prob<T>
     T* yw = S.y[par ^ 1];
     T* vw = S.v[par ^ 1];
     double a_gv = 0, a_gg = 0, a_vv = 0;
+    unsigned long long hsum = 0;   // support fingerprint (cardinality)
     const int nt = S.nblk * P.ntiles_pb;
     for (int t = blockIdx.x; t < nt; t += gridDim.x) {
       const int bl = t / P.ntiles_pb, lt = t - bl * P.ntiles_pb;
@@ -919,6 +921,9 @@ __global__ void __launch_bounds__(BLOCK) k_pass2(const __grid_constant__ Prob<T>
           }
         }
         y = keep ? w : 0.0;
+        if (valid && y != 0.0)
+          hsum += supp_mix((unsigned long long)bl * ((unsigned long long)g.nz_g * g.plane) +
+                           (unsigned long long)g.z0 * g.plane + (unsigned long long)pt);
       } else {   // l2 ball / annulus: radial scaling (L7 at 0)
         y = azero ? ((bl == 0 && pt == S.first_real) ? C.sig_lo[i] : 0.0) : w * scale;
       }
@@ -939,6 +944,7 @@ __global__ void __launch_bounds__(BLOCK) k_pass2(const __grid_constant__ Prob<T>
       warp_acc(acc, nv, i * 4 + 1, a_gg);
       warp_acc(acc, nv, i * 4 + 2, a_vv);
     }
+    if (S.kind == K_CARD) supp_add_warp(C, i, hsum);
     // Eq. 26 numerator for l1 / cardinality from s (check iterations)
     if (check && S.sjob >= 0) {
       const Job& Js = C.job[S.sjob];

@@ -591,6 +591,13 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
     }
 #pragma unroll
     for (int e = 0; e < W; ++e) y[e] = keep[e] ? wv[e] : (T)0;
+    unsigned long long hsum = 0;   // support fingerprint (test instrument)
+    const unsigned long long gbase = (unsigned long long)bl * ((unsigned long long)g.nz_g * g.plane) +
+                                     (unsigned long long)g.z0 * g.plane + (unsigned long long)pt0;
+#pragma unroll
+    for (int e = 0; e < W; ++e)
+      if (!pad[e] && y[e] != (T)0) hsum += supp_mix(gbase + e);
+    supp_add_warp(C, i, hsum);
   } else {
     const T sc = (T)C.ann_scale[i];
     const int az = C.ann_zero[i];

@@ -119,6 +119,7 @@ struct Engine : EngineBase {
   int* d_log_cg = nullptr; int* d_log_br = nullptr;
   double* d_log_rho = nullptr; double* d_log_gam = nullptr; double* d_log_feas = nullptr;
   double* d_log_evol = nullptr;
+  unsigned long long* d_log_supp = nullptr;
   int log_cap = 0;
   int* h_flag = nullptr;       // pinned: stopped flags of the last launches
   cudaEvent_t ev_flag[2];
@@ -353,6 +354,7 @@ struct Engine : EngineBase {
       }
     }
     Pr.ccnt = dalloc<unsigned>((size_t)MAXJOBS * std::max(g_sel, 1));
+    Pr.sel_grid = g_sel;
     smem_p2 = (size_t)NWARP * P * 4 * sizeof(double);
     smem_init = (size_t)NWARP * P * 2 * sizeof(double);
     // per-fiber sets (sip_fiber.cuh): one CTA per fiber, a single wave
@@ -697,6 +699,7 @@ struct Engine : EngineBase {
     d_log_gam = dalloc<double>((size_t)max_iter * P);
     d_log_feas = dalloc<double>((size_t)max_iter * std::max(p, 1));
     d_log_evol = dalloc<double>(max_iter);
+    d_log_supp = dalloc<unsigned long long>((size_t)max_iter * std::max(p, 1));
   }
 
   // ---- control block -----------------------------------------------------
@@ -729,7 +732,7 @@ struct Engine : EngineBase {
     c.mreal[p] = (long long)nz_g * Pr.g.plane;
     make_coeffs(Pr, c.rho, &c.cI, &c.cz, &c.cy, &c.cx, &c.cF);
     c.log_cg = d_log_cg; c.log_branch = d_log_br; c.log_rho = d_log_rho; c.log_gamma = d_log_gam;
-    c.log_feas = d_log_feas; c.log_evol = d_log_evol; c.log_len = log_cap;
+    c.log_feas = d_log_feas; c.log_evol = d_log_evol; c.log_supp = d_log_supp; c.log_len = log_cap;
     hc = c;
     CU(cudaMemcpyAsync(d_ctrl, &hc, sizeof(Ctrl), cudaMemcpyHostToDevice, stream));
   }
@@ -739,6 +742,7 @@ struct Engine : EngineBase {
     k_fill<double><<<g_small_(), BLOCK, 0, stream>>>(d_log_feas, (long long)max_iter * std::max(p, 1), NAN);
     k_fill<double><<<g_small_(), BLOCK, 0, stream>>>(d_log_evol, (long long)max_iter, NAN);
     k_fill<int><<<g_small_(), BLOCK, 0, stream>>>(d_log_cg, (long long)max_iter, 0);
+    CU(cudaMemsetAsync(d_log_supp, 0, (size_t)max_iter * std::max(p, 1) * sizeof(unsigned long long), stream));
   }
 
   // init_yv: 1 = y_i = A_i m, v_i = 0; 0 = keep Y[1]/V[1] (prolonged / warm)
@@ -2134,10 +2138,41 @@ sip_status sip_get_log(sip_grid g, int max_iter, int* cg, int* branch, double* r
   });
 }
 
+sip_status sip_get_support_log(sip_grid g, int max_iter, uint64_t* out) {
+  if (!g || !out || max_iter < 0) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    auto run = [&](auto tag) -> sip_status {
+      using T = decltype(tag);
+      std::vector<Engine<T>*> es;
+      if (is_team(g) && g->last_team) {
+        for (auto& e : static_cast<Team<T>*>(g->last_team)->eng) es.push_back(e.get());
+      } else {
+        es.push_back(last_engine<T>(g));
+      }
+      const int p = es[0]->p;
+      memset(out, 0, (size_t)max_iter * std::max(p, 0) * sizeof(uint64_t));
+      std::vector<uint64_t> tmp;
+      for (Engine<T>* e : es) {
+        if (!e->ran) throw SipError{SIP_ERR_STATE, "no projection log"};
+        const int n = std::min(max_iter, e->log_cap);
+        tmp.assign((size_t)n * std::max(p, 1), 0);
+        if (p) CU(cudaMemcpy(tmp.data(), e->d_log_supp, (size_t)n * p * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        for (size_t q = 0; q < (size_t)n * p; ++q) out[q] += tmp[q];
+      }
+      return SIP_OK;
+    };
+    return g->dtype == SIP_F32 ? run(float()) : run(double());
+  });
+}
+
 sip_status sip_get_sizes(sip_grid g, int* p, int64_t* n_local, int set_id, int64_t* m_compact) {
   if (!g) return SIP_ERR_ARG;
   if (p) *p = (int)g->sets.size();
-  if (n_local) *n_local = g->n[0] * g->n[1] * g->n[2];
+  if (n_local) {
+    int z0 = 0, nzl = (int)g->n[0];
+    if (g->nranks > 1) slab_of((int)g->n[0], g->nranks, g->rank, &z0, &nzl);
+    *n_local = (int64_t)nzl * g->n[1] * g->n[2];
+  }
   if (m_compact) {
     if (set_id < 0 || set_id > (int)g->sets.size()) return SIP_ERR_ARG;
     *m_compact = set_id == (int)g->sets.size() ? g->n[0] * g->n[1] * g->n[2] : g->sets[set_id].M;

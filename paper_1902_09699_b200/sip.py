@@ -62,7 +62,7 @@ EXPORTS = [
     "sip_comm_unique_id", "sip_create_grid", "sip_add_set", "sip_set_option", "sip_project",
     "sip_project_multilevel", "sip_destroy", "sip_status_string", "sip_last_error",
     "sip_apply_op", "sip_apply_system", "sip_cg", "sip_project_set", "sip_get_state",
-    "sip_get_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
+    "sip_get_log", "sip_get_support_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
 ]
 KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm", "cgx", "fiber"]
 
@@ -143,6 +143,9 @@ def _current_stream():
     return C.c_void_p(0)
 
 
+_NP_DT = {"f32": "float32", "f64": "float64"}
+
+
 class Grid:
     """A PARSDMM problem on a 2D/3D grid (compgrid + set definitions)."""
 
@@ -187,6 +190,35 @@ class Grid:
     def N(self):
         return int(np.prod(self.shape))
 
+    def n_local(self):
+        """grid points of this rank's slab (the whole grid on one rank)"""
+        n = C.c_int64(0)
+        self._check(lib().sip_get_sizes(self.h, None, C.byref(n), -1, None))
+        return n.value
+
+    def _buf(self, a, n, what):
+        """validate a buffer handed to the C ABI: element count, dtype, layout
+        (the library copies n * sizeof(dtype) bytes through the pointer)"""
+        if a is None:
+            raise ValueError(f"{what}: buffer is None")
+        want = _NP_DT[self.dtype]
+        if hasattr(a, "data_ptr"):
+            dt = str(a.dtype).replace("torch.", "")
+            numel = a.numel()
+            if a.is_cuda:
+                import torch
+                if a.device.index != torch.cuda.current_device():
+                    raise ValueError(f"{what}: tensor on {a.device}, grid on cuda:{torch.cuda.current_device()}")
+        elif isinstance(a, np.ndarray):
+            dt, numel = a.dtype.name, a.size
+        else:
+            raise TypeError(f"{what}: unsupported array type {type(a)}")
+        if dt != want:
+            raise ValueError(f"{what}: dtype {dt}, the grid is {want}")
+        if numel != n:
+            raise ValueError(f"{what}: {numel} elements, expected {n}")
+        return _ptr(a)
+
     def set_option(self, key, value):
         self._check(lib().sip_set_option(self.h, key.encode(), float(value)))
 
@@ -221,13 +253,13 @@ class Grid:
 
     def project(self, m, x, max_iter=200, tol=1e-3):
         r = Result()
-        s = self._check(lib().sip_project(self.h, _ptr(m), _ptr(x), int(max_iter), float(tol),
+        s = self._check(lib().sip_project(self.h, self._buf(m, self.n_local(), "m"), self._buf(x, self.n_local(), "x"), int(max_iter), float(tol),
                                           C.byref(r)), (SIP_OK, SIP_NOT_CONVERGED))
         return _res(r, len(self.sets)), s
 
     def project_multilevel(self, m, x, n_levels, max_iter=200, tol=1e-3):
         rs = (Result * n_levels)()
-        s = self._check(lib().sip_project_multilevel(self.h, _ptr(m), _ptr(x), int(n_levels), 2,
+        s = self._check(lib().sip_project_multilevel(self.h, self._buf(m, self.n_local(), "m"), self._buf(x, self.n_local(), "x"), int(n_levels), 2,
                                                      int(max_iter), float(tol), rs),
                         (SIP_OK, SIP_NOT_CONVERGED))
         return [_res(rs[l], len(self.sets)) for l in range(n_levels)], s
@@ -238,23 +270,26 @@ class Grid:
         return mm.value
 
     def apply_op(self, set_id, x, y):
-        self._check(lib().sip_apply_op(self.h, int(set_id), _ptr(x), _ptr(y)))
+        self._check(lib().sip_apply_op(self.h, int(set_id), self._buf(x, self.N, "x"),
+                                         self._buf(y, self.m_len(set_id), "y")))
 
     def apply_system(self, rho, p, q):
         r = (C.c_double * len(rho))(*[float(v) for v in rho])
-        self._check(lib().sip_apply_system(self.h, r, _ptr(p), _ptr(q)))
+        self._check(lib().sip_apply_system(self.h, r, self._buf(p, self.N, "p"), self._buf(q, self.N, "q")))
 
     def cg(self, rho, b, x, n_cg, eq25=True):
         r = (C.c_double * len(rho))(*[float(v) for v in rho])
         it = C.c_int(0)
-        self._check(lib().sip_cg(self.h, r, _ptr(b), _ptr(x), int(n_cg), int(bool(eq25)), C.byref(it)))
+        self._check(lib().sip_cg(self.h, r, self._buf(b, self.N, "b"), self._buf(x, self.N, "x"), int(n_cg), int(bool(eq25)), C.byref(it)))
         return it.value
 
     def project_set(self, set_id, w, y):
-        self._check(lib().sip_project_set(self.h, int(set_id), _ptr(w), _ptr(y)))
+        self._check(lib().sip_project_set(self.h, int(set_id), self._buf(w, self.m_len(set_id), "w"),
+                                              self._buf(y, self.m_len(set_id), "y")))
 
     def get_state(self, set_id, which, out):
-        self._check(lib().sip_get_state(self.h, int(set_id), int(which), _ptr(out)))
+        self._check(lib().sip_get_state(self.h, int(set_id), int(which),
+                                           self._buf(out, self.m_len(set_id), "out")))
 
     def get_log(self, max_iter):
         P = len(self.sets) + 1
@@ -270,6 +305,13 @@ class Grid:
         return dict(cg=cg, branch=br.reshape(max_iter, P), rho=rt.reshape(max_iter, P),
                     gamma=gt.reshape(max_iter, P), r_feas=ft[: max_iter * p].reshape(max_iter, p),
                     r_evol=et)
+
+    def get_support_log(self, max_iter):
+        """per-iteration cardinality support fingerprints, (max_iter, p) uint64"""
+        p = len(self.sets)
+        out = np.zeros(max(1, max_iter * p), dtype=np.uint64)
+        self._check(lib().sip_get_support_log(self.h, int(max_iter), _ptr(out)))
+        return out[: max_iter * p].reshape(max_iter, p)
 
     def profile(self):
         """per-kernel-kind device ms and launch counts of the last project()"""

@@ -113,7 +113,7 @@ def test_project_set_per_fiber(shape, op, mode, kind, dtype, path, monkeypatch):
         np.testing.assert_array_equal(yh != 0, ref != 0)
         np.testing.assert_array_equal(yh, ref)
     else:
-        assert O.relres(yh, ref) <= TOL[dtype] * 10, O.relres(yh, ref)
+        assert O.relres(yh, ref) <= TOL[dtype], O.relres(yh, ref)
 
 
 def test_card_k_at_least_fiber_length_keeps_all():

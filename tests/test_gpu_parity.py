@@ -178,7 +178,7 @@ def test_project_set(dtype, kind, shape):
         np.testing.assert_array_equal(yh != 0, ref != 0)
         np.testing.assert_array_equal(yh, ref)
     else:
-        assert rel(yh, ref) <= TOL[dtype] * 10, rel(yh, ref)
+        assert rel(yh, ref) <= TOL[dtype], rel(yh, ref)
 
 
 # ------------------------------------------------------------ end to end
@@ -242,18 +242,23 @@ def test_tiny_bitexact_control_flow(seed, shape, kinds, path, monkeypatch):
         monkeypatch.setenv("SIP_NO_VEC", "1")
     prob = G.tiny(seed, shape, kinds)
     x, res, log, g = run_gpu(prob, want_log=True)
-    ref = O.parsdmm(prob.shape, prob.sets, prob.m, **prob.options)
+    ref = refy = O.parsdmm(prob.shape, prob.sets, prob.m, want_yv=True, **prob.options)
     it = ref.iterations
     assert res["iterations"] == it
     np.testing.assert_array_equal(log["cg"][:it], ref.cg_per_iter)
     np.testing.assert_array_equal(log["branch"][:it], ref.branch)
     assert res["converged"] == ref.converged
     assert rel(x, ref.x) < 1e-6
-    # cardinality supports of the final y (exact)
+    # cardinality supports at EVERY iteration (fingerprints, exact) and the
+    # final y of every set
+    sup = g.get_support_log(it)
     for i, sd in enumerate(prob.sets):
-        if sd.kind == "card":
+        if sd.kind == "card" and not sd.app_mode:
+            assert ref.supp_hash[:, i].any()
+            np.testing.assert_array_equal(sup[:it, i], ref.supp_hash[:, i])
             y = np.zeros(O.op_len(prob.shape, sd))
             g.get_state(i, 0, y)
+            np.testing.assert_array_equal(y != 0, refy.y[i] != 0)
     g.close()
 
 

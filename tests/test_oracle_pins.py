@@ -526,6 +526,13 @@ def test_multilevel_converges_and_is_cheaper():
     assert logs[0].converged
     assert O.relres(x, _box_mono_exact(m, 1500.0, 4500.0)) < 1e-2
     assert logs[0].cg_total < single.cg_total
+    # reading L23: rho and gamma carry over to the next finer level; iteration
+    # 1 of a level never adapts (snapshot only), so its logged rho / gamma
+    # are the coarser level's final values
+    for lf, lc in ((logs[0], logs[1]), (logs[1], logs[2])):
+        np.testing.assert_array_equal(lf.rho_trace[0], lc.rho)
+        np.testing.assert_array_equal(lf.gamma_trace[0], lc.gamma)
+    assert not np.allclose(logs[1].rho, 1e-2)    # the carried values are not the defaults
 
 
 # ------------------------------------------------------------ per-fiber sets (NEXT-1)
@@ -601,3 +608,89 @@ def test_parsdmm_fiber_l1_vs_dykstra():
     t = O.parsdmm(shape, sets, m - c0, eps_evol=1e-10, eps_feas=1e-10, n_cg=200, max_iter=50000)
     assert O.relres(t.x, ref.ravel()) < 1e-6
     assert all(np.abs(t.x.reshape(shape)).sum(axis=1) <= sig * (1 + 1e-6))
+
+
+# ------------------------------------------------------------ hand-derived traces (tests/golden/hand_traces.json)
+HT = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "hand_traces.json")))
+
+
+def _fr(s):
+    from fractions import Fraction
+    return float(Fraction(s))
+
+
+def _alg2_trace(max_iter, **opts):
+    sets = [SetDef("I", "bounds", lo=0.0, hi=1.0), SetDef("I", "bounds")]
+    m = np.full((2, 2), 3.0)
+    return O.parsdmm((2, 2), sets, m, want_yv=True, init=dict(rho=[3.0, 0.5, 1.0]),
+                     max_iter=max_iter, **opts)
+
+
+def test_alg2_callsite_hand_trace():
+    """Algorithm 2 at its call site: v_hat from the OLD y and v,
+    adapt at odd k with a snapshot-only first call, Delta h
+    against the k0 snapshot; pinned by a hand-derived 3-iteration trace."""
+    e = HT["alg2_callsite_trace"]
+    for k in (1, 2, 3):
+        r = _alg2_trace(k)
+        assert r.iterations == k
+        np.testing.assert_allclose(r.x, _fr(e["x"][k - 1]), rtol=0, atol=1e-14)
+        np.testing.assert_array_equal(r.cg_per_iter, e["cg"][:k])
+    r = _alg2_trace(3)
+    np.testing.assert_array_equal(r.branch[0], [-1, -1, -1])   # first call: snapshot only
+    np.testing.assert_array_equal(r.branch[1], [-1, -1, -1])   # even k: no adapt
+    np.testing.assert_array_equal(r.branch[2], e["branch_k3"])
+    np.testing.assert_allclose(r.rho_trace[2], [_fr(s) for s in e["rho_k3"]], rtol=1e-14)
+    np.testing.assert_allclose(r.gamma_trace[2], e["gamma_k3"], rtol=1e-14)
+    for i in range(3):
+        np.testing.assert_allclose(r.y[i], _fr(e["y_k3"][i]), atol=1e-14)
+        np.testing.assert_allclose(r.v[i], _fr(e["v_k3"][i]), atol=1e-14)
+    # L16: rho_i / rho_{p+1} clamped after the new rho_{p+1}
+    r = _alg2_trace(3, rho_ratio_cap=10.0)
+    np.testing.assert_allclose(r.rho_trace[2], [_fr(s) for s in e["rho_k3_cap10"]], rtol=1e-14)
+    # L15: gamma clamped to gamma_max at the call site
+    r = _alg2_trace(3, gamma_max=1.5)
+    np.testing.assert_allclose(r.gamma_trace[2], e["gamma_k3_gmax15"], rtol=1e-14)
+
+
+def test_eq27_history_window_hand_trace():
+    """Eq. 27's window of the last s = 5 iterates and the check every 5
+    (P:236-246), pinned by a hand-derived trace whose x^k is 5, 3, 1, 1, ..."""
+    e = HT["eq27_history_trace"]
+    sets = [SetDef("I", "bounds", lo=0.0, hi=1.0)]
+    r = O.parsdmm((2, 2), sets, np.full((2, 2), 3.0), max_iter=30, rho0=1.0,
+                  init=dict(x=np.full((2, 2), 5.0)))
+    assert r.iterations == e["iterations"] and r.converged
+    np.testing.assert_array_equal(r.cg_per_iter[:3], e["cg"])
+    assert r.r_evol_trace[4] == pytest.approx(e["r_evol_k5"], abs=1e-12)
+    assert abs(r.r_evol_trace[9] - e["r_evol_k10"]) < 1e-12
+    assert np.isnan(r.r_evol_trace[[0, 1, 2, 3, 5, 6, 7, 8]]).all()   # checked only at k = 5, 10
+    np.testing.assert_allclose(r.x, 1.0, atol=1e-12)
+
+
+def test_prolong_field_shapes():
+    """Algorithm 3's transfer of y_i, v_i: each operator field on its own
+    shape (reading L23)."""
+    e = HT["prolong_fields"]
+    cs, fs = tuple(e["coarse"]), tuple(e["fine"])
+    for op, key in (("DZ", "dz"), ("DX", "dx"), ("TV", "tv")):
+        f = O.prolong_field(cs, fs, op, e[key]["c"])
+        np.testing.assert_allclose(f, e[key]["f"], atol=1e-14)
+    # I field: constants are preserved on any shape
+    np.testing.assert_allclose(O.prolong_field(cs, fs, "I", np.full(4, 7.5)), 7.5, atol=1e-14)
+
+
+def test_relative_parameter_resolution():
+    """relative radii and k resolved from the input m (readings L4, L23)"""
+    e = HT["relative_params"]
+    shape, m = tuple(e["shape"]), np.array(e["m"], dtype=float)
+    s, _, _, _ = O.resolve_set(shape, SetDef("TV", "l1", sigma=0.5, relative=True), m)
+    assert s == pytest.approx(e["tv_l1_sigma"], rel=1e-15)
+    _, lo, hi, _ = O.resolve_set(shape, SetDef("I", "annulus", sigma_lo=0.9, sigma_hi=1.1, relative=True), m)
+    assert lo == pytest.approx(0.9 * np.sqrt(e["annulus_norm_sq"]), rel=1e-15)
+    assert hi == pytest.approx(1.1 * np.sqrt(e["annulus_norm_sq"]), rel=1e-15)
+    s, _, _, _ = O.resolve_set(shape, SetDef("DZ", "l2", sigma=0.5, relative=True), m)
+    assert s * s == pytest.approx(0.25 * e["l2_dz_sigma_sq_over_frac_sq"], rel=1e-14)
+    for frac, k in e["card_dx_k"].items():
+        _, _, _, kk = O.resolve_set(shape, SetDef("DX", "card", k_frac=float(frac), relative=True), m)
+        assert kk == k
