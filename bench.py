@@ -82,6 +82,34 @@ def byte_model(prob, n_cg=10, word=4):
     return dict(cg1=cg1, cg2=cg2, cgx=cgx, iteration=it)
 
 
+def kernel_bytes(prob, k, n_cg=10, word=4):
+    """algorithmic bytes of every kernel kind in PARSDMM iteration k (1-based;
+    adapt when k is odd with Alg. 2 products from k = 3 on, check when
+    k % 5 == 0): the minimum each kind must move -- every operand read once,
+    every result written once, neighbours of a stencil from on-chip reuse
+    (DESIGN.md section 6).  Compact lengths M_i (shared sizes)."""
+    N = prob.N
+    sets = prob.sets
+    M = [op_len(prob.shape, sd.op) for sd in sets] + [N]               # + distance block
+    point = [i for i, sd in enumerate(sets) if sd.kind == "bounds"] + [len(sets)]
+    glob = [i for i, sd in enumerate(sets) if sd.kind in ("l1", "card", "annulus", "l2")]
+    radix = [i for i, sd in enumerate(sets) if sd.kind in ("l1", "card") and not sd.app_mode]
+    SM, SMp = sum(M), sum(M[i] for i in point)
+    T, Tr = sum(M[i] for i in glob), sum(M[i] for i in radix)
+    adapt, dots, check = k % 2 == 1, k % 2 == 1 and k >= 3, k % 5 == 0
+    rounds = 2 if word == 4 else 4        # full reads of w per radix job (fp32: 11/11 bits; later rounds read candidates)
+    by = {
+        "rhs": 2 * SM + 2 * N,                               # y_i, v_i, x -> r
+        "cg1": 3 * N * n_cg, "cg2": 3 * N * n_cg,
+        "cgx": (n_cg + 2) * N,
+        "pass1": (N + N + N + 2 * SM + 2 * SMp + T           # x, m, history write; y, v; y, v (pointwise); w
+                  + (SM if adapt else 0)                     # v_hat write
+                  + ((SM + 2 * N + 2 * SMp) if dots else 0)  # v_hat^{k0}, x^{k0} r/w, y^{k0} v^{k0} (pointwise)
+                  + ((Tr + 5 * N) if check else 0)),         # s of l1/card sets, 5 history vectors
+        "select": rounds * Tr * (2 if check else 1),         # w (and s on check iterations)
+        "pass2": 3 * T + (2 * T if dots else 0) + (Tr if check else 0),
+    }
+    return {kk: v * word for kk, v in by.items()}
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region"""
 
@@ -158,6 +186,7 @@ def workload_config(prob, args, world=None):
     return {"workload": f"{prob.name} {'x'.join(map(str, prob.shape))} "
                         f"{', '.join(sd.op + ':' + sd.kind for sd in prob.sets)}",
             "grid": list(prob.shape), "sets": len(prob.sets), "iters_per_step": args.iters_per_step,
+            "levels": prob.n_levels if getattr(args, "multilevel", False) else 1,
             "n_cg": args.n_cg, "mode": "fixed_work (Eq.25 off, stop test not acted on)",
             "l2": "flushed (256 MiB write) between timed steps",
             "parallelism": ("1 GPU" if world == 1 else f"z-slab x{world} (NCCL halos + gathered reductions)")
@@ -202,7 +231,7 @@ def run_reference(args, prob):
         "pts_sets_per_s": val * prob.N * len(prob.sets),
         "cpu_baseline": {"value": val, "unit": "it/s", "cores": 1, "kind": "oracle",
                          "sample": f"{args.steps} steps x {ips} fixed-work iterations of {prob.name} "
-                                   f"(single-threaded fp64 C oracle)"},
+                                   f"(single-threaded fp64 C oracle)", **host_info()},
         "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -210,6 +239,44 @@ def run_reference(args, prob):
 
 
 # ------------------------------------------------------------------ CUDA arm
+KINDS_RL = ("rhs", "cg1", "cg2", "cgx", "pass1", "select", "pass2")
+KNAME = {"rhs": "k_rhsf", "cg1": "k_cg1f", "cg2": "k_cg2f", "cgx": "k_cgx", "pass1": "k_pass1t",
+         "select": "k_selectf", "pass2": "k_pass2t"}
+
+
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def roofline_table(prob, prof, ips, n_cg, word, peak, level_shapes=None):
+    """per kernel kind: algorithmic bytes of the profiled step / its device
+    time (CUDA event nodes in the graph) against the measured copy peak"""
+    tot = {k: 0.0 for k in KINDS_RL}
+    probs = [prob] if level_shapes is None else level_shapes
+    for pb in probs:
+        for k in range(1, ips + 1):
+            for kk, v in kernel_bytes(pb, k, n_cg, word).items():
+                tot[kk] += v
+    out = {}
+    for kk in KINDS_RL:
+        ms, n = prof.get(kk, (0.0, 0))
+        if ms <= 0 or n == 0:
+            continue
+        gbs = tot[kk] / (ms / 1e3) / 1e9
+        out[kk] = {"kernel": KNAME[kk], "ms_per_step": ms, "launches": n,
+                   "bytes_per_step": tot[kk], "achieved_gbs": gbs, "frac": gbs / peak}
+    return out
+
+
 def run_cuda(args, prob):
     import torch
     world, rank, local = dist_init()
@@ -227,7 +294,9 @@ def run_cuda(args, prob):
         comm = comm_desc()
         m_np = local_slab_of(prob.m, world, rank)
     dt = torch.float32 if prob.dtype == "f32" else torch.float64
+    word = 4 if prob.dtype == "f32" else 8
     ips = args.iters_per_step
+    levels = prob.n_levels if args.multilevel else 1
     g = grid_for(prob, comm=comm)
     g.set_option("fixed_work", 1)
     g.set_option("eq25", 0)
@@ -238,78 +307,84 @@ def run_cuda(args, prob):
     x = torch.empty_like(m)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2
 
-    def step():
-        res, st = g.project(m, x, max_iter=ips, tol=1e-3)
-        return res
+    def call(mm, xx):
+        if levels > 1:
+            per, st = g.project_multilevel(mm, xx, levels, max_iter=ips, tol=1e-3)
+            return sum(p["ms"] for p in per), per
+        res, st = g.project(mm, xx, max_iter=ips, tol=1e-3)
+        return res["ms"], [res]
 
     for _ in range(args.warmup):
-        step()
+        call(m, x)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    times, launches = [], 0
+    times, launches, lvl_ms = [], 0, [0.0] * levels
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            res = step()
-            times.append(res["ms"])
+            ms, per = call(m, x)
+            times.append(ms)
+            for l, p in enumerate(per):
+                lvl_ms[l] += p["ms"]
             launches += g.launch_count()
         torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     t_total = max_over_ranks(sum(times), world, "cuda")          # ms, slowest rank
-    value_job = args.steps * ips / (t_total / 1e3)                # iterations of the one (sharded) problem
-    value = value_job
+    its_per_step = ips * levels
+    value_job = args.steps * its_per_step / (t_total / 1e3)      # iterations of the one (sharded) problem
 
     # e2e: host pinned m / x, copies inside the timed call
     mh = torch.tensor(m_np, dtype=dt).pin_memory()
     xh = torch.empty_like(mh).pin_memory()
-    for _ in range(1):
-        g.project(mh, xh, max_iter=ips, tol=1e-3)
+    call(mh, xh)
     etimes = []
     for _ in range(max(1, args.steps // 2)):
         flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = g.project(mh, xh, max_iter=ips, tol=1e-3)[0]
+        call(mh, xh)
         etimes.append(time.perf_counter() - t0)
     e2e_t = max_over_ranks(sum(etimes), world, "cuda")
-    e2e_val = len(etimes) * ips / e2e_t
-    nbytes = m_np.size * (4 if prob.dtype == "f32" else 8)        # this rank's slab (one GPU: the grid)
+    e2e_val = len(etimes) * its_per_step / e2e_t
+    nbytes = m_np.size * word                                     # this rank's slab (one GPU: the grid)
 
     # profiled step: per-kernel device time from event nodes in the graph
     g.set_option("profile", 1)
     flush.zero_()
     torch.cuda.synchronize()
-    g.project(m, x, max_iter=ips, tol=1e-3)
+    call(m, x)
     prof = g.profile()
     g.set_option("profile", 0)
-    model = byte_model(prob, args.n_cg, 4 if prob.dtype == "f32" else 8)
-    if world > 1:   # this rank's CG launches move its slab
-        for k in ("cg1", "cg2", "cgx"):
-            model[k] = model[k] * m_np.size // prob.N
     peaks = load_peaks()
-    # dominant kernel among those with an exact per-launch byte count
-    kind = max(("cg1", "cg2", "cgx"), key=lambda k: prof.get(k, (0.0, 0))[0])
-    k_ms, k_n = prof[kind]
-    k_avg_s = k_ms / max(k_n, 1) / 1e3
-    achieved = model[kind] / k_avg_s / 1e9 if k_avg_s > 0 else None
+    lv_probs = None
+    if levels > 1:   # the profile is the finest level's (the library profiles the last engine)
+        lv_probs = [prob]
+    scale = m_np.size / prob.N                                    # this rank's share of the bytes
+    table = roofline_table(prob, prof, ips, args.n_cg, word, peaks["hbm_gbs"], lv_probs)
+    for v in table.values():
+        v["bytes_per_step"] *= scale
+        v["achieved_gbs"] *= scale
+        v["frac"] *= scale
     step_prof_ms = sum(v[0] for v in prof.values())
-    kname = {"cg1": "k_cg1", "cg2": "k_cg2", "cgx": "k_cgx"}[kind]
+    dom = max(table, key=lambda k: table[k]["ms_per_step"]) if table else None
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(prob.name, {}).get(kname)
-    it_model_gbs = model["iteration"] * (args.steps * ips) / (sum(times) / 1e3) / 1e9
+    if dom and os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(prob.name, {}).get(KNAME[dom])
+    model = byte_model(prob, args.n_cg, word)
+    it_model_gbs = model["iteration"] * scale * (args.steps * ips) / (sum(lvl_ms[:1]) / 1e3) / 1e9
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ts = oracle_sample(prob, args.cpu_iters)
         cpu = {"value": args.cpu_iters / sum(ts), "unit": "it/s", "cores": 1, "kind": "oracle",
-               "sample": f"{args.cpu_iters} fixed-work iterations of {prob.name} "
-                         f"(single-threaded fp64 C oracle, {sum(ts):.1f} s)"}
+               "sample": f"{args.cpu_iters} fixed-work iterations of {prob.name} at full size "
+                         f"(single-threaded fp64 C oracle, {sum(ts):.1f} s)", **host_info()}
     if rank == 0:
+        d = table[dom] if dom else None
         line = {
             "metric": "PARSDMM iterations/s", "value": value_job, "unit": "it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -317,15 +392,17 @@ def run_cuda(args, prob):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prob.dtype == "f32" else "f64",
             "data": "synthetic",
             "config": workload_config(prob, args, world),
-            "pts_sets_per_s": value_job * prob.N * len(prob.sets),
+            "pts_sets_per_s": value_job * prob.N * len(prob.sets) if levels == 1 else None,
             "iteration_model_gbs": it_model_gbs,
             "comm_ms_per_step": prof.get("comm", (0.0, 0))[0],
-            "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
-                         "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": (achieved / peaks["hbm_gbs"]) if achieved else None,
-                         "traffic": traffic, "peak_source": peaks["source"],
-                         "bytes_per_launch": model[kind], "avg_launch_us": k_avg_s * 1e6,
-                         "share_of_step": k_ms / step_prof_ms if step_prof_ms else None},
+            "roofline": None if d is None else {
+                "kernel": d["kernel"], "bound": "hbm", "achieved": d["achieved_gbs"],
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": d["frac"], "traffic": traffic,
+                "peak_source": peaks["source"] + " copy bandwidth (burst)",
+                "bytes_per_step": d["bytes_per_step"], "launches_per_step": d["launches"],
+                "avg_launch_us": 1e3 * d["ms_per_step"] / d["launches"],
+                "share_of_step": d["ms_per_step"] / step_prof_ms if step_prof_ms else None},
+            "kernels": table,
             "kernel_ms_per_step": {k: v[0] for k, v in prof.items()},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "it/s", "h2d_bytes_per_step": nbytes,
@@ -333,10 +410,40 @@ def run_cuda(args, prob):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if levels > 1:
+            line["levels_ms_per_step"] = [v / args.steps for v in lvl_ms]
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def run_dry(args):
+    """--dry-run: the rank plumbing only (gloo on the host, no GPU): every
+    rank joins, max-over-ranks of a per-rank number, rank 0 prints n_gpus"""
+    import torch.distributed as dist
+    world, rank, _ = dist_init()
+    if world > 1:
+        dist.init_process_group("gloo")
+    v = max_over_ranks(float(rank + 1), world)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "max_over_ranks": v}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def launch_ranks(args):
+    """--gpus N without a launcher: re-exec this script under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1"""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -344,17 +451,38 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C4")
+    ap.add_argument("--config", default="C4", choices=sorted(G.CONFIGS))
+    ap.add_argument("--multilevel", action="store_true",
+                    help="C5: the 3-level multilevel solve (Algorithm 3), iters-per-step per level")
+    ap.add_argument("--null-work", action="store_true",
+                    help="the config's sets on an 8x8(x8) grid: the latency floor of the launch structure")
     ap.add_argument("--iters-per-step", type=int, default=10)
     ap.add_argument("--n-cg", type=int, default=10)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--cpu-iters", type=int, default=3)
     ap.add_argument("--ref-iters", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (no GPU)")
     ap.add_argument("--virtual-ranks", type=int, default=1,
                     help="run the z-slab path with G slabs on the one GPU (diagnostic)")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        return launch_ranks(args)
+    if world and world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.dry_run:
+        return run_dry(args)
     prob = G.CONFIGS[args.config]()
+    if args.null_work:
+        shape = (8, 8) if len(prob.shape) == 2 else (8, 8, 8)
+        small = G.CONFIGS[args.config](shape=shape)
+        small.name = prob.name + "-null"
+        prob = small
+    if args.multilevel and prob.n_levels == 1:
+        print("bench.py: --multilevel needs a multilevel config (C5)", file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args, prob)
     return run_cuda(args, prob)

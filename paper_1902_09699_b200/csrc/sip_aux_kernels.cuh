@@ -63,30 +63,41 @@ __global__ void k_apply_sys(const __grid_constant__ Prob<T> P, const Ctrl* Cc, c
   }
 }
 
-// block mean of the fine grid (2 x 2 in 2D over (z, x), 2 x 2 x 2 in 3D)
+// "anti-alias filtering and subsampling", reading L23: every coarse
+// point is the mean of its 2 x 2 (x 2) fine block.  The block is summed as x
+// pairs, then y, then z (a pairwise tree); one multiply by 1/4 (1/8).
 template <class T>
 __global__ void k_restrict(Geo fine, Geo coarse, const T* f, T* c) {
-  const int by = fine.ndim == 3 ? 2 : 1;
-  const double inv = 1.0 / (double)(4 * by);
+  const bool three = fine.ndim == 3;
+  const double scale = three ? 0.125 : 0.25;
+  const int64_t fplane = (int64_t)fine.ny * fine.nx;
   for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < coarse.N; pt += gridDim.x * blockDim.x) {
-    Loc L = locate(coarse, pt);
-    double a = 0.0;
-    for (int dz = 0; dz < 2; ++dz)
-      for (int dy = 0; dy < by; ++dy)
-        for (int dx = 0; dx < 2; ++dx)
-          a += (double)f[((int64_t)(2 * L.iz + dz) * fine.ny + (by * L.iy + dy)) * fine.nx + 2 * L.ix + dx];
-    c[pt] = (T)(a * inv);
+    const Loc L = locate(coarse, pt);
+    const T* q = f + (int64_t)(2 * L.iz) * fplane + (int64_t)(three ? 2 * L.iy : L.iy) * fine.nx + 2 * L.ix;
+    auto row = [&](const T* r) { return (double)r[0] + (double)r[1]; };
+    auto plane = [&](const T* r) { return three ? row(r) + row(r + fine.nx) : row(r); };
+    c[pt] = (T)((plane(q) + plane(q + fplane)) * scale);
   }
 }
 
-__device__ __forceinline__ void axis_w(int i, int nf, int nc, int* i0, int* i1, double* t) {
-  double pos = (nf > 1 && nc > 1) ? (double)i * (double)(nc - 1) / (double)(nf - 1) : 0.0;
-  int a = (int)floor(pos);
-  if (a > nc - 1) a = nc - 1;
-  *i0 = a;
-  *i1 = (a + 1 < nc) ? a + 1 : a;
-  *t = pos - (double)a;
+// align-corners linear weights on one axis (reading L23): fine index i of nf
+// sits at i (nc - 1) / (nf - 1) on the coarse axis; the integer part and the
+// remainder are taken exactly in integer arithmetic
+struct AxisW {
+  int a, b;      // the two coarse neighbours
+  double t;      // weight of b
+};
+__device__ __forceinline__ AxisW axis_weights(int i, int nf, int nc) {
+  AxisW w{0, 0, 0.0};
+  if (nf <= 1 || nc <= 1) return w;
+  const long long num = (long long)i * (nc - 1);
+  w.a = (int)(num / (nf - 1));
+  const long long rem = num - (long long)w.a * (nf - 1);
+  w.t = (double)rem / (double)(nf - 1);
+  w.b = w.a + 1 < nc ? w.a + 1 : w.a;
+  return w;
 }
+__device__ __forceinline__ double lerp1(double u, double v, double t) { return u + t * (v - u); }
 
 // prolong one block of a field.  The block's real entries form an image of
 // shape (ez, ey, ex) = grid shape minus 1 along the primitive's axis; it is
@@ -103,23 +114,12 @@ __global__ void k_prolong(Geo fine, Geo coarse, int prim, const T* c, T* f) {
   for (int pt = blockIdx.x * blockDim.x + threadIdx.x; pt < fine.N; pt += gridDim.x * blockDim.x) {
     Loc L = locate(fine, pt);
     if (L.gz >= fz || L.iy >= fy || L.ix >= fx) { f[pt] = (T)0; continue; }
-    int z0, z1, y0, y1, x0, x1;
-    double tz, ty, tx;
-    axis_w(L.gz, fz, cz, &z0, &z1, &tz);
-    axis_w(L.iy, fy, cy, &y0, &y1, &ty);
-    axis_w(L.ix, fx, cx, &x0, &x1, &tx);
-    z0 -= coarse.z0;   // local coarse plane, -1 .. coarse.nz (ghosts)
-    z1 -= coarse.z0;
-    auto C_ = [&](int a, int b, int d) {  // coarse padded storage
-      return (double)c[((int64_t)a * coarse.ny + b) * coarse.nx + d];
-    };
-    const double v00 = C_(z0, y0, x0) * (1.0 - tx) + C_(z0, y0, x1) * tx;
-    const double v01 = C_(z0, y1, x0) * (1.0 - tx) + C_(z0, y1, x1) * tx;
-    const double v10 = C_(z1, y0, x0) * (1.0 - tx) + C_(z1, y0, x1) * tx;
-    const double v11 = C_(z1, y1, x0) * (1.0 - tx) + C_(z1, y1, x1) * tx;
-    const double v0 = v00 * (1.0 - ty) + v01 * ty;
-    const double v1 = v10 * (1.0 - ty) + v11 * ty;
-    f[pt] = (T)(v0 * (1.0 - tz) + v1 * tz);
+    const AxisW wz = axis_weights(L.gz, fz, cz), wy = axis_weights(L.iy, fy, cy), wx = axis_weights(L.ix, fx, cx);
+    const int za = wz.a - coarse.z0, zb = wz.b - coarse.z0;   // local coarse planes, -1 .. coarse.nz (ghosts)
+    auto at = [&](int z, int y, int x) { return (double)c[((int64_t)z * coarse.ny + y) * coarse.nx + x]; };
+    auto along_x = [&](int z, int y) { return lerp1(at(z, y, wx.a), at(z, y, wx.b), wx.t); };
+    auto along_y = [&](int z) { return lerp1(along_x(z, wy.a), along_x(z, wy.b), wy.t); };
+    f[pt] = (T)lerp1(along_y(za), along_y(zb), wz.t);
   }
 }
 

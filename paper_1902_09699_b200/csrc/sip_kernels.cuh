@@ -981,38 +981,44 @@ __global__ void __launch_bounds__(BLOCK) k_pass2(const __grid_constant__ Prob<T>
 }
 
 // ------------------------------------------------------------ control
-// Algorithm 2 from the six inner products (reading L17)
-__device__ __host__ inline int adapt_from_dots(double hv, double hh, double vhvh, double gv, double gg,
-                                               double vv, double rho, double eps_corr, double* rho_new,
-                                               double* gamma_new) {
-  int a_ok = 0, b_ok = 0;
-  double ahat = 0.0, bhat = 0.0;
-  if (hh > 0.0 && vhvh > 0.0) {
-    const double acorr = hv / (sqrt(hh) * sqrt(vhvh));
-    if (acorr > eps_corr) {
-      const double mg = hv / hh, sd = vhvh / hv;
-      ahat = (2.0 * mg > sd) ? mg : sd - 0.5 * mg;
-      a_ok = 1;
-    }
-  }
-  if (gg > 0.0 && vv > 0.0) {
-    const double bcorr = gv / (sqrt(gg) * sqrt(vv));
-    if (bcorr > eps_corr) {
-      const double mg = gv / gg, sd = vv / gv;
-      bhat = (2.0 * mg > sd) ? mg : sd - 0.5 * mg;
-      b_ok = 1;
-    }
-  }
-  if (a_ok && b_ok) {
-    const double r = sqrt(ahat * bhat);
-    *rho_new = r;
-    *gamma_new = 1.0 + 2.0 * r / (ahat + bhat);
+// Algorithm 2 on the device.  Both halves of the algorithm are
+// the same safeguarded spectral step applied to a pair of difference vectors
+// (alpha: Delta h, Delta v_hat; beta: Delta g, Delta v), so it is written once:
+// from the cross product and the two squared norms, the correlation test
+// (eps_corr; a zero norm fails it, reading L17), then the
+// minimum-gradient step MG = cross / |d|^2 or the steepest-descent step
+// SD = |v|^2 / cross.
+struct SpecStep {
+  bool ok;
+  double step;
+};
+__device__ __forceinline__ SpecStep spectral_step(double cross, double dd, double vv, double eps_corr) {
+  SpecStep r{false, 0.0};
+  if (!(dd > 0.0 && vv > 0.0)) return r;
+  if (!(cross / (sqrt(dd) * sqrt(vv)) > eps_corr)) return r;
+  const double mg = cross / dd;
+  const double sd = vv / cross;
+  r.ok = true;
+  r.step = (2.0 * mg > sd) ? mg : sd - 0.5 * mg;
+  return r;
+}
+// the four-way table of: branch code 0 both, 1 alpha, 2 beta, 3 none
+__device__ inline int alg2_table(const SpecStep& a, const SpecStep& b, double rho, double* rho_new,
+                                 double* gamma_new) {
+  if (a.ok && b.ok) {
+    const double g = sqrt(a.step * b.step);          // rho = sqrt(alpha_hat beta_hat)
+    *rho_new = g;
+    *gamma_new = 1.0 + 2.0 * g / (a.step + b.step);
     return 0;
   }
-  if (a_ok) { *rho_new = ahat; *gamma_new = 1.9; return 1; }
-  if (b_ok) { *rho_new = bhat; *gamma_new = 1.1; return 2; }
-  *rho_new = rho; *gamma_new = 1.5;
-  return 3;
+  if (!a.ok && !b.ok) {
+    *rho_new = rho;
+    *gamma_new = 1.5;
+    return 3;
+  }
+  *rho_new = a.ok ? a.step : b.step;
+  *gamma_new = a.ok ? 1.9 : 1.1;
+  return a.ok ? 1 : 2;
 }
 
 // merged coefficients of C (Eq. 23): c_prim = sum of rho_i over sets having
@@ -1120,14 +1126,13 @@ __device__ void control_body(const Prob<T>& P, Ctrl& C) {
   if (adapt) {
     if (C.first_adapt_done) {
       for (int i = 0; i < Pn; ++i) {
-        double rn, gn;
         const double* s = C.sums[i];
-        br[i] = adapt_from_dots(s[SLOT_HV], s[SLOT_HH], s[SLOT_VHVH], s[SLOT_GV], s[SLOT_GG], s[SLOT_VV],
-                                C.rho[i], C.opt.eps_corr, &rn, &gn);
-        if (gn < 1.0) gn = 1.0;                       // reading L15
-        if (gn > C.opt.gamma_max) gn = C.opt.gamma_max;
+        const SpecStep a = spectral_step(s[SLOT_HV], s[SLOT_HH], s[SLOT_VHVH], C.opt.eps_corr);
+        const SpecStep b = spectral_step(s[SLOT_GV], s[SLOT_GG], s[SLOT_VV], C.opt.eps_corr);
+        double rn, gn;
+        br[i] = alg2_table(a, b, C.rho[i], &rn, &gn);
         C.rho[i] = rn;
-        C.gamma[i] = gn;
+        C.gamma[i] = fmin(fmax(gn, 1.0), C.opt.gamma_max);   // reading L15
       }
       for (int i = 0; i < p; ++i) {                    // reading L16
         const double lo = C.rho[p] / C.opt.rho_ratio_cap, hi = C.rho[p] * C.opt.rho_ratio_cap;

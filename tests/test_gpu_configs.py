@@ -10,6 +10,8 @@ on fp32 keys (L27).  Configs too large for the oracle to finish in minutes
 end to end at a reduced size of the same generator.
 """
 import copy
+import json
+import os
 
 import numpy as np
 import pytest
@@ -105,21 +107,47 @@ def test_c2_full_fp64_path():
 
 
 def test_c2_full_fp32():
-    """C2 in its configured fp32: C2 does not converge within 200 iterations
-    (the oracle's own r_feas stay above 1e-3) and its cardinality set makes
-    the trajectory sensitive to the fp32 state: the measured deviation grows
-    from 1e-4 (20 iterations) to 2.1e-3 (200), all of it from top-k support
-    flips (2e-7 with the cardinality set removed, test below).  The bar here
-    is the measured deviation with margin, documented in DESIGN.md 7."""
+    """C2 in its configured fp32, trajectory parity (reading L24): C2 does
+    not converge within 200 iterations (the oracle's own r_feas stay near
+    0.035 / 0.098), so its iterate at 200 is a point of a trajectory, not a
+    solution, and its cardinality set makes the trajectory sensitive to the
+    fp32 state (w in fp32 swaps near-equal |w| around the k-th key).  Bars:
+    the control flow (CG count per iteration, Alg. 2 branch per set) equal
+    to the oracle's at EVERY iteration; the top-k support equal up to the
+    first divergence iteration (measured 12) and overlapping >= 99% at the
+    end; x within 1e-3 of the oracle at 20 iterations (measured 1.2e-4).
+    The measured drift at 60 / 200 iterations (8.7e-4 / 2.0e-3) is recorded
+    in BASELINE.md section 6; with the cardinality set removed the two agree
+    to 1e-5 (next test)."""
     prob = G.c2()
-    x, res, log = run_gpu(prob, 200)
-    ref = O.parsdmm(prob.shape, prob.sets, prob.m, **oracle_opts(prob))
-    assert res["iterations"] == ref.iterations
+    x, res, log = run_gpu(prob, 20)
+    ref = O.parsdmm(prob.shape, prob.sets, prob.m, **oracle_opts(prob, max_iter=20))
+    assert O.relres(x, ref.x) < 1e-3
+    g, xs, res, log, sup = run_gpu_keep(prob, 200)
+    ref = O.parsdmm(prob.shape, prob.sets, prob.m, want_yv=True, **oracle_opts(prob))
+    assert res["iterations"] == ref.iterations == 200
     np.testing.assert_array_equal(log["cg"][: ref.iterations], ref.cg_per_iter)
-    assert O.relres(x, ref.x) < 5e-3
-    fg, fo = feas_of(prob, x), feas_of(prob, ref.x)
-    for a, b in zip(fg, fo):
-        assert a <= 1.5 * b + 1e-4   # fp32 top-k support flips move the trajectory (DESIGN.md 7)
+    np.testing.assert_array_equal(log["branch"][: ref.iterations], ref.branch)
+    ic = [i for i, sd in enumerate(prob.sets) if sd.kind == "card"][0]
+    same = sup[:, ic] == ref.supp_hash[:, ic]
+    first = int(np.argmin(same)) + 1 if not same.all() else None
+    assert first is None or first >= 10, first
+    y = np.zeros(O.op_len(prob.shape, prob.sets[ic]), dtype=np.float32)
+    g.get_state(ic, 0, y)
+    a, b = y != 0, ref.y[ic] != 0
+    assert (a & b).sum() / (a | b).sum() >= 0.99
+    g.close()
+
+
+def run_gpu_keep(prob, max_iter, **opts):
+    """run_gpu, keeping the grid open (state queries) and the support log"""
+    g = grid_for(prob)
+    for k, v in opts.items():
+        g.set_option(k, v)
+    m = torch.tensor(prob.m, dtype=torch.float32 if prob.dtype == "f32" else torch.float64, device="cuda")
+    x = torch.empty_like(m)
+    res, st = g.project(m, x, max_iter=max_iter, tol=1e-3)
+    return g, x.double().cpu().numpy().ravel(), res, g.get_log(max_iter), g.get_support_log(max_iter)
 
 
 def test_c2_without_cardinality_fp32():
@@ -149,6 +177,58 @@ def test_c4_full_size_bounded():
     assert O.relres(x, ref.x) < 1e-4
 
 
+def _golden(name):
+    p = os.path.join(os.path.dirname(__file__), "golden", f"fullsize_{name}.json")
+    if not os.path.exists(p):
+        pytest.skip(f"{p} not generated (tools/oracle_fullsize.py)")
+    return json.load(open(p))
+
+
+def test_c4_full_size_natural_vs_oracle_reference():
+    """C4 end to end at full size in natural mode against the oracle's own
+    full run (tests/golden/fullsize_C4.json, tools/oracle_fullsize.py): all
+    of C4's sets are convex, so the solution is unique; the GPU stops
+    at the oracle's iteration (or within one check period), its x is within
+    1e-3 of the oracle's on the stored strided subsample (every 512th point),
+    and every constraint of the GPU's x, re-verified by the oracle's own
+    projectors (Eq. 26), is violated by < 1e-3."""
+    ref = _golden("C4")
+    prob = G.c4()
+    x, res, log = run_gpu(prob, 200)
+    lv = ref["levels"][0]
+    assert res["converged"] and lv["converged"]
+    assert abs(res["iterations"] - lv["iterations"]) <= 5, (res["iterations"], lv["iterations"])
+    xs = x[:: ref["stride"]]
+    assert O.relres(xs, np.array(ref["x_sub"])) < 1e-3
+    assert max(feas_of(prob, x)) < 1e-3
+    n = min(res["iterations"], lv["iterations"]) - 1
+    same = np.asarray(log["cg"][:n]) == np.asarray(lv["cg_per_iter"][:n])
+    assert same.mean() >= 0.9, same
+
+
+def test_c5_full_size_multilevel_vs_oracle_reference():
+    """C5 (67M points, 5 sets, 3 levels) end to end against the oracle's own
+    full multilevel run (tests/golden/fullsize_C5.json): per-level stop
+    iterations within one check period, the finest x within the stop test's
+    resolution of the oracle's on the stored subsample, and the GPU's
+    finest-level Eq. 26 values (re-verified by the oracle's projectors) no
+    worse than the oracle's own by more than 1e-3."""
+    ref = _golden("C5")
+    prob = G.c5()
+    g = grid_for(prob)
+    m = torch.tensor(prob.m, dtype=torch.float32, device="cuda")
+    x = torch.empty_like(m)
+    per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
+    xh = x.double().cpu().numpy().ravel()
+    for l in range(3):
+        assert abs(per[l]["iterations"] - ref["levels"][l]["iterations"]) <= 5, (l, per[l]["iterations"])
+    rl = O.relres(xh[:: ref["stride"]], np.array(ref["x_sub"]))
+    assert rl < 1e-2, rl
+    fg = feas_of(prob, xh)
+    for a, b in zip(fg, ref["levels"][0]["r_feas"]):
+        assert a <= max(b, 0.0) + 1e-3, (a, b)
+
+
 def test_c5_small_multilevel():
     prob = G.c5(seed=4, shape=(64, 64, 32))
     g = grid_for(prob)
@@ -158,22 +238,3 @@ def test_c5_small_multilevel():
     xo, sto, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3, **oracle_opts(prob))
     assert [p["iterations"] for p in per] == [lg.iterations for lg in logs]
     assert O.relres(x.double().cpu().numpy(), xo) < 1e-3
-
-
-def test_c5_full_size_gpu_properties():
-    """C5 at full size (67M points, 3 levels): the oracle cannot run it in
-    a test; check what holds at any size: the run completes, the finest level
-    result is finite, and the oracle's projectors re-verify Eq. 26 on the
-    sets that converged."""
-    prob = G.c5()
-    g = grid_for(prob)
-    m = torch.tensor(prob.m, dtype=torch.float32, device="cuda")
-    x = torch.empty_like(m)
-    per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
-    xh = x.double().cpu().numpy().ravel()
-    assert np.isfinite(xh).all()
-    assert len(per) == 3 and all(p["iterations"] >= 1 for p in per)
-    fg = feas_of(prob, xh)
-    for r_gpu, r_dev in zip(fg, per[0]["r_feas"]):
-        assert abs(r_gpu - r_dev) <= 1e-3 + 1e-2 * abs(r_gpu)
-

@@ -309,25 +309,50 @@ def test_multilevel_one_level_equals_zero_init_single_level():
     assert rel(host(x1), xo) < 1e-9
 
 
-def test_multilevel_fp32_small_c5_like():
+def test_multilevel_small_c5_like_fp64_exact():
+    """C5's sets and 3-level schedule at 32x32x16 through the fp64 kernels:
+    the implementation reproduces the oracle (exact per-level iteration and
+    CG counts, x within 1e-9)."""
     prob = G.c5(seed=4, shape=(32, 32, 16))
-    x_ref, _, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3,
-                                          **oracle_opts(prob))
+    prob.dtype = "f64"
+    x_ref, _, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3, **prob.options)
+    g = grid_for(prob)
+    m = dev(prob.m, "f64")
+    x = torch.empty_like(m)
+    per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
+    assert [p["iterations"] for p in per] == [lg.iterations for lg in logs]
+    assert [p["cg_iterations"] for p in per] == [lg.cg_total for lg in logs]
+    assert rel(host(x), x_ref) < 1e-9
+
+
+def test_multilevel_fp32_small_c5_like():
+    """The same in the configured fp32, trajectory parity (reading L24; C5
+    carries the non-convex cardinality and annulus sets).  Measured: the two
+    coarse levels take exactly the oracle's iterations and CG steps; at the
+    finest level the Eq. 28 test at k = 150 passes for the oracle and fails
+    for fp32 state (a borderline Eq. 26/27 value), so the GPU stops at the
+    next check, k = 155 -- with identical CG counts for every iteration
+    before.  Bars: coarse levels exact; finest level CG counts equal up to
+    the first stop check that differs; the stop iteration within one check
+    period (5); x within 1e-3 of the oracle when both stop at the same
+    check, else within eps_evol = 1e-2, the resolution of the stop test
+    itself (Eq. 27: x may still move by up to eps_evol ||x|| in 5
+    iterations).  Measured 5.4e-3."""
+    prob = G.c5(seed=4, shape=(32, 32, 16))
+    x_ref, _, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3, **oracle_opts(prob))
     g = grid_for(prob)
     m = dev(prob.m, "f32")
     x = torch.empty_like(m)
     per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
-    # C5 carries non-convex sets (cardinality, annulus): the fp32 trajectory
-    # may settle on another point of the same quality (reading L24; measured
-    # 5.4e-3 after a rounding-order change in the rhs sums).  The bar is the
-    # oracle's own quality: every Eq. 26 value of the GPU's x, recomputed by
-    # the oracle's projectors, within 1.5x of the oracle's plus 1e-4.
-    assert rel(host(x), x_ref) < 1e-2
-    sets = [absolute_set(sd, prob) for sd in prob.sets]
-    for sd, sda in zip(prob.sets, sets):
-        fg = O.feas(sda, O.apply_A(prob.shape, sd, host(x).ravel()))
-        fo = O.feas(sda, O.apply_A(prob.shape, sd, x_ref.ravel()))
-        assert fg <= 1.5 * fo + 1e-4, (sd.op, sd.kind, fg, fo)
+    for l in (2, 1):
+        assert per[l]["iterations"] == logs[l].iterations
+        assert per[l]["cg_iterations"] == logs[l].cg_total
+    ig, io = per[0]["iterations"], logs[0].iterations
+    assert abs(ig - io) <= 5
+    lg = g.get_log(200)
+    n = min(ig, io) - 1
+    np.testing.assert_array_equal(lg["cg"][:n], logs[0].cg_per_iter[:n])
+    assert rel(host(x), x_ref) < (1e-3 if ig == io else 1e-2)
 
 
 # ------------------------------------------------------------ no read before write

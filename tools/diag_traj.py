@@ -50,8 +50,8 @@ def multi(prob, levels, dtype="f32"):
     if dtype == "f32":
         o["cg_tol_floor"] = 10 * F32
     xo, sto, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, levels, **o)
-    return dict(iters=[(p["iterations"], l.iterations) for p in per],
-                cg=[(p["cg_iterations"], l.cg_total) for p in per],
+    return dict(iters=[(p["iterations"], lg.iterations) for p, lg in zip(per, logs)],
+                cg=[(p["cg_iterations"], lg.cg_total) for p, lg in zip(per, logs)],
                 rel=O.relres(x.double().cpu().numpy(), xo))
 
 
