@@ -23,7 +23,7 @@ _SRC = os.path.join(_HERE, "sipref.c")
 _LIB = os.path.join(_HERE, "libsipref.so")
 
 OPS = {"I": 0, "DZ": 1, "DY": 2, "DX": 3, "TV": 4, "BLUR_MASK": 5}
-KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4}
+KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6}
 BRANCH = {0: "both", 1: "alpha", 2: "beta", 3: "none", -1: "-"}
 
 
@@ -55,6 +55,7 @@ class Set(C.Structure):
         ("kernel", C.POINTER(C.c_double)), ("kh", C.c_int), ("kw", C.c_int),
         ("mask", C.POINTER(C.c_ubyte)),
         ("app_mode", C.c_int), ("fib_len", C.c_int64),
+        ("mrows", C.c_int64), ("mcols", C.c_int64),
     ]
 
 
@@ -217,11 +218,30 @@ def fiber_len(shape, sd, h=None) -> int:
     return int(lib().sipref_fiber_len(C.byref(g), C.byref(hold.s)))
 
 
+def matrix_shape(shape, op):
+    """(rows, cols) of one matrix of the view of op's output (reading L29)"""
+    g = make_grid(shape)
+    r, c = C.c_int64(0), C.c_int64(0)
+    lib().sipref_matrix_shape(C.byref(g), OPS[op], C.byref(r), C.byref(c))
+    return r.value, c.value
+
+
+def svd_values(a):
+    """singular values of a 2D array (one-sided Jacobi, descending)"""
+    a = _f64(a)
+    r, c = a.shape
+    sv = np.zeros(min(r, c))
+    lib().sipref_svd_values(C.c_int64(r), C.c_int64(c), _dp(a.ravel()), _dp(sv))
+    return sv
+
+
 def project(sd, w, shape=None):
-    """Table 1 projector; shape is needed for per-fiber sets (app_mode)"""
+    """Table 1 projector; shape is needed for per-fiber sets (app_mode) and
+    the matrix view of rank / nuclear-norm sets"""
     hold = _SetHolder(sd)
     if shape is not None:
         hold.s.fib_len = fiber_len(shape, sd)
+        hold.s.mrows, hold.s.mcols = matrix_shape(shape, sd.op)
     w = _f64(w).ravel()
     y = np.zeros_like(w)
     lib().sipref_project(C.byref(hold.s), C.c_int64(w.size), _dp(w), _dp(y))
@@ -239,6 +259,7 @@ def feas(sd, s_vec, shape=None):
     hold = _SetHolder(sd)
     if shape is not None:
         hold.s.fib_len = fiber_len(shape, sd)
+        hold.s.mrows, hold.s.mcols = matrix_shape(shape, sd.op)
     s_vec = _f64(s_vec).ravel()
     return float(lib().sipref_feas(C.byref(hold.s), C.c_int64(s_vec.size), _dp(s_vec)))
 

@@ -309,6 +309,126 @@ static void proj_card(int64_t M, const double *w, int64_t k, double *y) {
   free(t);
 }
 
+/* ------------------------------------------------------------------ */
+/* rank and nuclear-norm sets (Table 1): singular values of the */
+/* operator's output viewed as a matrix                                   */
+/* ------------------------------------------------------------------ */
+/* reading L29: 2D grids: the field of A x is one (z, x) matrix; 3D grids:
+   one (y, x) matrix per z-plane */
+void sipref_matrix_shape(const sipref_grid *g, int op, int64_t *rows, int64_t *cols) {
+  int64_t nz = g->n[0], ny = g->n[1], nx = g->n[2];
+  int64_t fz = nz - (op == SIPREF_OP_DZ), fy = ny - (op == SIPREF_OP_DY), fx = nx - (op == SIPREF_OP_DX);
+  if (g->ndim == 2) { *rows = fz; *cols = fx; }
+  else { *rows = fy; *cols = fx; }
+}
+
+/* One-sided Jacobi SVD (Hestenes): rotate pairs of columns of X (m x n,
+   n <= m, column j at X + j m) until every pair is orthogonal; V (n x n,
+   column-major) accumulates the rotations, so X_in V = X_out and the
+   singular values are the column norms of X_out. */
+static void jacobi_onesided(int64_t m, int64_t n, double *X, double *V) {
+  for (int64_t i = 0; i < n * n; ++i) V[i] = 0.0;
+  for (int64_t j = 0; j < n; ++j) V[j * n + j] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int rotated = 0;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = i + 1; j < n; ++j) {
+        double *xi = X + i * m, *xj = X + j * m;
+        double a = dot(m, xi, xi), b = dot(m, xj, xj), c = dot(m, xi, xj);
+        if (c == 0.0 || fabs(c) <= 1e-15 * sqrt(a * b)) continue;
+        double zeta = (b - a) / (2.0 * c);
+        double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        for (int64_t r = 0; r < m; ++r) {
+          double u = xi[r], v = xj[r];
+          xi[r] = cs * u - sn * v;
+          xj[r] = sn * u + cs * v;
+        }
+        double *vi = V + i * n, *vj = V + j * n;
+        for (int64_t r = 0; r < n; ++r) {
+          double u = vi[r], v = vj[r];
+          vi[r] = cs * u - sn * v;
+          vj[r] = sn * u + cs * v;
+        }
+        rotated = 1;
+      }
+    if (!rotated) break;
+  }
+}
+
+/* the matrix a (rows x cols, row-major) as X (m x n column-major, n <= m):
+   X = a^T's columns when cols <= rows (X column j = column j of a), else
+   the columns of a^T */
+static int load_cols(int64_t rows, int64_t cols, const double *a, double *X, int64_t *m, int64_t *n) {
+  int tr = cols > rows;              /* wide: work on a^T */
+  *m = tr ? cols : rows;
+  *n = tr ? rows : cols;
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < cols; ++j) {
+      if (!tr) X[j * rows + i] = a[i * cols + j];     /* column j of a */
+      else X[i * cols + j] = a[i * cols + j];         /* column i of a^T = row i of a */
+    }
+  return tr;
+}
+
+static int cmp_sv(const void *pa, const void *pb) {
+  const keyidx *a = (const keyidx *)pa, *b = (const keyidx *)pb;
+  if (a->a > b->a) return -1;
+  if (a->a < b->a) return 1;
+  return (a->i > b->i) - (a->i < b->i);
+}
+
+void sipref_svd_values(int64_t rows, int64_t cols, const double *a, double *sv) {
+  int64_t m, n;
+  double *X = dalloc(rows * cols), *V = NULL;
+  load_cols(rows, cols, a, X, &m, &n);
+  V = dalloc(n * n);
+  jacobi_onesided(m, n, X, V);
+  keyidx *t = (keyidx *)malloc((size_t)n * sizeof(keyidx));
+  for (int64_t j = 0; j < n; ++j) { t[j].a = nrm2(m, X + j * m); t[j].i = j; }
+  qsort(t, (size_t)n, sizeof(keyidx), cmp_sv);
+  for (int64_t j = 0; j < n; ++j) sv[j] = t[j].a;
+  free(t); free(X); free(V);
+}
+
+/* projection of one matrix: a = sum_j lambda_j u_j v_j^T (SVD);
+   RANK r: keep the r largest lambda_j (ties: lowest index; Eckart-Young,
+   the nearest matrix of rank <= r); NUCLEAR sigma: lambda projected onto
+   {sum lambda <= sigma} (lambda >= 0: the l1 ball of Duchi et al.).
+   y = sum_j f_j u_j v_j^T = sum_j (f_j / lambda_j) x_j v_j^T with x_j the
+   rotated columns (x_j = lambda_j u_j). */
+static void proj_matrix(const sipref_set *s, int64_t rows, int64_t cols, const double *a, double *y) {
+  int64_t m, n;
+  double *X = dalloc(rows * cols);
+  int tr = load_cols(rows, cols, a, X, &m, &n);
+  double *V = dalloc(n * n);
+  jacobi_onesided(m, n, X, V);
+  double *lam = dalloc(n), *f = dalloc(n);
+  for (int64_t j = 0; j < n; ++j) lam[j] = nrm2(m, X + j * m);
+  if (s->type == SIPREF_RANK) {
+    keyidx *t = (keyidx *)malloc((size_t)n * sizeof(keyidx));
+    for (int64_t j = 0; j < n; ++j) { t[j].a = lam[j]; t[j].i = j; }
+    qsort(t, (size_t)n, sizeof(keyidx), cmp_sv);
+    for (int64_t q = 0; q < n; ++q) f[t[q].i] = (q < s->k) ? lam[t[q].i] : 0.0;
+    free(t);
+  } else {
+    proj_l1(n, lam, s->sigma, f);    /* lam >= 0, so the l1 ball is the capped simplex */
+  }
+  double *B = dalloc(m * n);          /* B = X diag(f / lambda) V^T (column-major m x n) */
+  for (int64_t j = 0; j < n; ++j) {
+    if (lam[j] == 0.0 || f[j] == 0.0) continue;
+    double sc = f[j] / lam[j];
+    for (int64_t c = 0; c < n; ++c) {
+      double w = sc * V[j * n + c];   /* (V^T)[j][c] = V[c][j] = column j entry c */
+      for (int64_t r = 0; r < m; ++r) B[c * m + r] += X[j * m + r] * w;
+    }
+  }
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < cols; ++j)
+      y[i * cols + j] = tr ? B[i * cols + j] : B[j * rows + i];
+  free(X); free(V); free(lam); free(f); free(B);
+}
+
 static void project_whole(const sipref_set *s, int64_t M, const double *w, double *y);
 
 /* fiber length (reading L28): nx (nx - 1 for D_x) for x-fibers, nz
@@ -371,6 +491,12 @@ static void project_whole(const sipref_set *s, int64_t M, const double *w, doubl
       break;
     }
     case SIPREF_CARD: proj_card(M, w, s->k, y); break;
+    case SIPREF_RANK:
+    case SIPREF_NUCLEAR: {   /* every matrix of the view on its own (L29) */
+      int64_t mn = s->mrows * s->mcols;
+      for (int64_t o = 0; mn > 0 && o + mn <= M; o += mn) proj_matrix(s, s->mrows, s->mcols, w + o, y + o);
+      break;
+    }
   }
 }
 
@@ -518,6 +644,7 @@ void sipref_resolve_set(const sipref_grid *g, const sipref_set *in, const double
                         sipref_set *out) {
   *out = *in;
   out->fib_len = sipref_fiber_len(g, in);
+  sipref_matrix_shape(g, in->op, &out->mrows, &out->mcols);
   if (!in->relative) return;
   int64_t M = sipref_op_len(g, in);
   double *a = dalloc(M);
@@ -531,6 +658,20 @@ void sipref_resolve_set(const sipref_grid *g, const sipref_set *in, const double
   if (in->type == SIPREF_ANNULUS) {
     out->sigma_lo = in->sigma_lo * n2;
     out->sigma_hi = in->sigma_hi * n2;
+  }
+  if (in->type == SIPREF_NUCLEAR) {   /* sigma = frac x sum of the nuclear norms of A m's matrices */
+    int64_t r, cc;
+    sipref_matrix_shape(g, in->op, &r, &cc);
+    int64_t mn = r * cc, q = r < cc ? r : cc;
+    double *sv = dalloc(q), nuc = 0.0;
+    double *am = dalloc(M);
+    sipref_apply_A(g, in, m, am);
+    for (int64_t o = 0; o + mn <= M; o += mn) {
+      sipref_svd_values(r, cc, am + o, sv);
+      for (int64_t j = 0; j < q; ++j) nuc += sv[j];
+    }
+    out->sigma = in->sigma * nuc;
+    free(sv); free(am);
   }
   if (in->type == SIPREF_CARD)   /* per fiber: a fraction of the fiber length */
     out->k = (int64_t)floor(in->k_frac * (double)(in->app_mode ? out->fib_len : M));

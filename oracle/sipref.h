@@ -28,7 +28,7 @@ extern "C" {
 enum { SIPREF_OP_I = 0, SIPREF_OP_DZ = 1, SIPREF_OP_DY = 2, SIPREF_OP_DX = 3,
        SIPREF_OP_TV = 4, SIPREF_OP_BLUR_MASK = 5 };
 enum { SIPREF_BOUNDS = 0, SIPREF_L1 = 1, SIPREF_L2 = 2, SIPREF_ANNULUS = 3,
-       SIPREF_CARD = 4 };
+       SIPREF_CARD = 4, SIPREF_RANK = 5, SIPREF_NUCLEAR = 6 };
 
 typedef struct {
   int ndim;          /* 2 or 3 */
@@ -55,6 +55,11 @@ typedef struct {
                         independently ("each row/column
                         independently"; NEXT-1).  Single-block operators.   */
   int64_t fib_len;   /* fiber length (set by sipref_fiber_len)               */
+  int64_t mrows, mcols;  /* RANK / NUCLEAR: the operator's output viewed as
+                        matrices of mrows x mcols (row-major runs of the
+                        compact layout): 2D grids one matrix (z, x), 3D grids
+                        one per z-plane (y, x) -- reading L29; set by
+                        sipref_matrix_shape                                */
 } sipref_set;
 
 typedef struct {
@@ -86,6 +91,13 @@ typedef struct {
 } sipref_log;
 
 void sipref_default_options(sipref_options *o);
+
+/* matrix view of an operator's output for RANK / NUCLEAR sets (reading
+   L29): rows x cols of one matrix; the number of matrices is M / (rows cols) */
+void sipref_matrix_shape(const sipref_grid *g, int op, int64_t *rows, int64_t *cols);
+/* singular values of a rows x cols row-major matrix (one-sided Jacobi,
+   descending); sv holds min(rows, cols) values */
+void sipref_svd_values(int64_t rows, int64_t cols, const double *a, double *sv);
 
 /* support fingerprint key of entry j (compact layout) of operator op's
    output: splitmix64(b N + grid index of the owning point), b the block of

@@ -169,10 +169,40 @@ struct Engine : EngineBase {
   }
 
   // field of nblk blocks; returns pointer to block 0's first interior element
+  // guard bands (SIP_CANARY=1, a bounds check of our own): every field gets
+  // CANARY_N words before and after its storage filled with a canary pattern,
+  // checked after each solve -- any kernel writing outside a field's
+  // allocation (ghost planes included) is reported as SIP_ERR_CUDA
+  static constexpr size_t CANARY_N = 4096;
+  const bool canary = getenv("SIP_CANARY") != nullptr;
+  std::vector<std::pair<T*, size_t>> guards;
   T* field(int nblk) {
-    T* base = dalloc<T>((size_t)nblk * Pr.g.ld);
-    CU(cudaMemsetAsync(base, 0, (size_t)nblk * Pr.g.ld * sizeof(T), stream));
+    const size_t n = (size_t)nblk * Pr.g.ld;
+    if (canary) {
+      T* raw = dalloc<T>(n + 2 * CANARY_N);
+      CU(cudaMemsetAsync(raw, 0xA5, CANARY_N * sizeof(T), stream));
+      CU(cudaMemsetAsync(raw + CANARY_N, 0, n * sizeof(T), stream));
+      CU(cudaMemsetAsync(raw + CANARY_N + n, 0xA5, CANARY_N * sizeof(T), stream));
+      guards.push_back({raw, n});
+      return raw + CANARY_N + (size_t)GHOST * Pr.g.plane;
+    }
+    T* base = dalloc<T>(n);
+    CU(cudaMemsetAsync(base, 0, n * sizeof(T), stream));
     return base + (size_t)GHOST * Pr.g.plane;
+  }
+  void check_canaries() {
+    if (!canary) return;
+    std::vector<unsigned char> h(CANARY_N * sizeof(T));
+    for (size_t f = 0; f < guards.size(); ++f) {
+      for (int side = 0; side < 2; ++side) {
+        const T* p = guards[f].first + (side ? CANARY_N + guards[f].second : 0);
+        CU(cudaMemcpy(h.data(), p, h.size(), cudaMemcpyDeviceToHost));
+        for (size_t b = 0; b < h.size(); ++b)
+          if (h[b] != 0xA5)
+            throw SipError{SIP_ERR_CUDA, "SIP_CANARY: write outside field " + std::to_string(f) +
+                                             (side ? " (after its end)" : " (before its start)")};
+      }
+    }
   }
 
   // slab: this engine owns global planes [z0_, z0_ + nz_) of nz_g_ (rank of nranks_)
@@ -802,6 +832,7 @@ struct Engine : EngineBase {
     run_init(init_x, init_yv);
     run_iterations(max_iter, o.graph_iters, o.n_cg);
     read_ctrl();
+    check_canaries();
     ran = true;
     scratch_used = false;
   }
@@ -1195,7 +1226,7 @@ struct Team : EngineBase {
     each([&](Engine<T>& e) { e.run_init(init_x, init_yv); });
     site(ST_INIT, 0, 0, {{FS_X, 0, H_BOTH}, {FS_Y1, SS_ALL, H_LO}, {FS_V1, SS_ALL, H_LO}});
     run_iterations(max_iter, o.graph_iters, o.n_cg);
-    each([&](Engine<T>& e) { e.read_ctrl(); e.ran = true; e.scratch_used = false; });
+    each([&](Engine<T>& e) { e.read_ctrl(); e.check_canaries(); e.ran = true; e.scratch_used = false; });
     ran = true;
   }
 };

@@ -1,8 +1,8 @@
-"""Tiny PARSDMM runs for compute-sanitizer (memcheck / racecheck / synccheck /
-initcheck): every kernel family of the path runs once on small inputs --
+"""Tiny PARSDMM runs for the guard-band check (SIP_CANARY=1,
+tests/test_gpu_canary.py; compute-sanitizer is closed on this pool): every kernel family of the path runs once on small inputs --
 vectorised and scalar paths, fp32 and fp64, l1 / cardinality (ties) /
 annulus / blur sets, multilevel, virtual z slabs, per-fiber sets.
-Test infrastructure (tests/test_gpu_sanitizer.py)."""
+Test infrastructure."""
 import os
 import sys
 
