@@ -97,7 +97,10 @@ def kernel_bytes(prob, k, n_cg=10, word=4):
     SM, SMp = sum(M), sum(M[i] for i in point)
     T, Tr = sum(M[i] for i in glob), sum(M[i] for i in radix)
     adapt, dots, check = k % 2 == 1, k % 2 == 1 and k >= 3, k % 5 == 0
-    rounds = 2 if word == 4 else 4        # full reads of w per radix job (fp32: 11/11 bits; later rounds read candidates)
+    # full reads of w per radix job: fp32 (select v2, sip_select2.cuh) one
+    # streaming pass -- round A runs inside pass 1, the candidate rounds read
+    # only the candidates; fp64 radix rounds read w in each of their 6 rounds
+    rounds = 1 if word == 4 else 6
     by = {
         "rhs": 2 * SM + 2 * N,                               # y_i, v_i, x -> r
         "cg1": 3 * N * n_cg, "cg2": 3 * N * n_cg,

@@ -82,7 +82,19 @@ typedef enum {
   SIP_SET_L1_BALL = 1,     /* ||Ax||_1 <= sigma                              */
   SIP_SET_L2_BALL = 2,     /* ||Ax||_2 <= sigma                              */
   SIP_SET_ANNULUS = 3,     /* sigma_lo <= ||Ax||_2 <= sigma_hi (non-convex)  */
-  SIP_SET_CARDINALITY = 4  /* card(Ax) <= k (non-convex); ties: lowest index */
+  SIP_SET_CARDINALITY = 4, /* card(Ax) <= k (non-convex); ties: lowest index */
+  SIP_SET_RANK = 5,        /* rank(A x as matrices) <= k (non-convex):
+                              the truncated SVD of every matrix of the view
+                              (reading L29: 2D grids one (z, x) matrix, 3D
+                              grids one (y, x) matrix per z-plane); ties of
+                              singular values: lowest index                   */
+  SIP_SET_NUCLEAR = 6      /* sum of singular values <= sigma per matrix of
+                              the view; relative = 1: sigma is a
+                              fraction of the summed nuclear norms of A m
+                              (single-level projections only).  Both: single-
+                              block operators, min(rows, cols) <= 2048, the
+                              vectorised path (nx a multiple of 16 / sizeof),
+                              one rank; else SIP_ERR_CONFIG                   */
 } sip_set_type;
 
 typedef struct {
@@ -91,7 +103,7 @@ typedef struct {
   const double *hi_vec;   /*   M of the operator, compact layout; copied at add */
   double sigma;           /* L1_BALL / L2_BALL radius >= 0                      */
   double sigma_lo, sigma_hi; /* ANNULUS, 0 <= lo <= hi                         */
-  int64_t k;              /* CARDINALITY, 0 <= k <= M                           */
+  int64_t k;              /* CARDINALITY, 0 <= k <= M; RANK: the rank r >= 0   */
   double k_frac;          /* CARDINALITY with relative = 1: k = floor(k_frac*M) */
   int relative;           /* 1: sigma, sigma_lo, sigma_hi are fractions of the
                              norm of A m (l1 norm for L1_BALL, l2 otherwise),
@@ -269,8 +281,8 @@ sip_status sip_get_sizes(sip_grid g, int *p, int64_t *n_local, int set_id, int64
    the graph).  Kinds, in order: 0 blur (S G p), 1 rhs, 2 cg1, 3 cg2,
    4 pass1, 5 select, 6 tiecount, 7 pass2, 8 control, 9 comm (z-slab
    exchanges), 10 cgx (deferred CG x update), 11 fiber (per-fiber
-   projections).  ms[q] is the summed milliseconds, count[q] the number of
-   launches (arrays of n <= 12). */
+   projections), 12 svd (rank / nuclear-norm sets).  ms[q] is the summed
+   milliseconds, count[q] the number of launches (arrays of n <= 13). */
 sip_status sip_get_profile(sip_grid g, int n, double *ms, int64_t *count);
 
 /* Number of kernel launches enqueued by the last sip_project (bench evidence). */

@@ -22,7 +22,7 @@ constexpr int MAXCG = 16;       // p-vector ring of the deferred x update (n_cg 
 // primitive operators: every set's operator is a stack of 1..3 primitive blocks
 enum Prim { PRIM_I = 0, PRIM_Z = 1, PRIM_Y = 2, PRIM_X = 3, PRIM_F = 4, NPRIM = 5 };
 // set kinds (Table 1) + the distance block A_{p+1} = I (Eq. 17, 22)
-enum Kind { K_BOUNDS = 0, K_L1 = 1, K_L2 = 2, K_ANN = 3, K_CARD = 4, K_DIST = 5 };
+enum Kind { K_BOUNDS = 0, K_L1 = 1, K_L2 = 2, K_ANN = 3, K_CARD = 4, K_DIST = 5, K_RANK = 6, K_NUC = 7 };
 
 // reduction slots per set (fp64)
 enum Slot {
@@ -98,6 +98,7 @@ struct SetD {
   int first_real;         // point index of the first entry (annulus at 0, L7)
   int fib, flen;          // per-fiber application (0 whole; 1 x-, 2 z-fibers) and fiber length
   int fpath;              // 1: warp kernel k_fiberw; 0: CTA-per-fiber sort kernel k_fiber
+  int svd;                // rank / nuclear-norm set (sip_svd.cuh)
   T* y[2];                // ping-pong y_i (parity k & 1), nblk blocks of ld
   T* v[2];
   T* vh0;                 // Alg. 2 snapshot v-hat^{k0}
@@ -127,6 +128,7 @@ struct Job {
   int ties;                      // index-ordered tie break needed
   double tau_val2;               // tau value squared (feasibility of card)
   unsigned cand_n;               // candidates compacted by round 2 (rounds >= 3 read them)
+  unsigned long long width;      // select v2: the key window [prefix, prefix + width) of the next round
 };
 
 struct Ctrl {

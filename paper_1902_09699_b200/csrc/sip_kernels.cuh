@@ -58,6 +58,9 @@ struct Prob {
   unsigned* ccnt;                 // [MAXJOBS][select grid]: candidates per CTA region
   long long cand_per;             // candidate region per select CTA (entries)
   int sel_grid;                   // the grid k_selectf is sized for (regions, ccnt stride)
+  int selv2;                      // single-rank fp32: round A in pass 1, k_selB / k_selC (sip_select2.cuh)
+  double* svdX;                   // rank / nuclear sets: fp64 Jacobi scratch, X (m x n) per matrix
+  double* svdV;                   //   and V (n x n) per matrix
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
   int poison;                     // SIP_POISON: k_init writes NaN into fields that are written before read
   int init_zero;                  // k_init zeroes every state field (scalar kernels)
@@ -868,7 +871,7 @@ __global__ void __launch_bounds__(BLOCK) k_pass2(const __grid_constant__ Prob<T>
   __syncthreads();
   for (int i = 0; i < P.P; ++i) {
     const SetD<T>& S = P.set[i];
-    if (!S.global) continue;
+    if (!S.global || S.svd) continue;
     const double rho = C.rho[i];
     const Job* J = (S.kind == K_L1 || S.kind == K_CARD) ? &C.job[S.job] : nullptr;
     const int mode = J ? J->mode : JM_DONE;
@@ -1041,7 +1044,7 @@ __device__ inline void reset_jobs(const Prob<T>& P, Ctrl& C) {
   for (int jb = 0; jb < C.njobs; ++jb) {
     Job& J = C.job[jb];
     const int i = J.set;
-    J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u;
+    J.round = 0; J.prefix = 0ull; J.cnt_above = 0; J.sum_above = 0.0; J.cand_n = 0u; J.width = 0ull;
     J.theta = 0.0; J.tau = 0ull; J.keep_eq = 0; J.cnt_eq = 0; J.ties = 0; J.tau_val2 = 0.0;
     J.sigma = C.sigma[i];
     J.k = C.kcard[i];
@@ -1074,8 +1077,9 @@ __device__ void control_body(const Prob<T>& P, Ctrl& C) {
       const int kd = P.set[i].kind;
       const double s2 = C.sums[i][SLOT_S2];
       double fn = C.sums[i][SLOT_FN];
-      if (P.set[i].fib) {
-        // per-fiber sets: the fiber kernels' sum of per-fiber ||s - P(s)||^2
+      if (P.set[i].fib || P.set[i].svd) {
+        // per-fiber sets: the fiber kernels' sum of per-fiber ||s - P(s)||^2;
+        // rank / nuclear sets: k_svdproj's ||s - P(s)||^2
       } else if ((kd == K_L1 || kd == K_CARD) && P.set[i].sjob >= 0) {
         const Job& J = C.job[P.set[i].sjob];
         if (J.mode == JM_INSIDE || J.mode == JM_ALL) fn = 0.0;
@@ -1235,7 +1239,7 @@ __global__ void __launch_bounds__(BLOCK) k_init(const __grid_constant__ Prob<T> 
         n1 += fabs(am);
         n2 += am * am;
         if (init_yv) { S.y[1][off] = (T)am; S.v[1][off] = (T)0; }
-        if (P.init_zero || S.fib) {
+        if (P.init_zero || S.fib || S.svd) {
           S.y[0][off] = (T)0; S.v[0][off] = (T)0; S.vh0[off] = (T)0;
           if (S.w) S.w[off] = (T)0;
           if (S.s) S.s[off] = (T)0;

@@ -12,6 +12,7 @@
 // accumulated in fp64 (reading L20).
 #pragma once
 #include "sip_flat.cuh"
+#include "sip_select2.cuh"
 #include "sip_stage.cuh"
 
 namespace sip {
@@ -176,7 +177,7 @@ __device__ __forceinline__ void ld_s(const char* base, int idx, T* o) {   // chu
 template <class T, int KIND, int PRIM, int AD, int CK, int NA>
 __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, int bl, const IterFlags& f,
                                        int par, int c0, int c1, const T* xs_rd, double* acc, int nv,
-                                       Stage2<NA>& st) {
+                                       Stage2<NA>& st, unsigned* ha) {
   constexpr int W = VT<T>::W;
   const Geo& g = P.g;
   const SetD<T>& S = P.set[i];
@@ -331,6 +332,10 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
       } else {
         VT<T>::stT(wp + pt0, wv);
         if (sp) VT<T>::stT(sp + pt0, sv_);
+        if (KIND == 2 && ha) {   // select v2 round A: key counts of w (and s on checks)
+          hist_a<T>(ha, wv);
+          if (sp) hist_a<T>(ha + NBUCK, sv_);   // s is 0 on pads
+        }
       }
       if (adapt) VT<T>::stT(vhp + pt0, vh);
       d_w2 += (double)a_w2; d_hv += (double)a_hv; d_hh += (double)a_hh; d_vh += (double)a_vh;
@@ -338,6 +343,10 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
       d_s2 += (double)a_s2;
     }
     __syncthreads();   // stage s is refilled by the issue of tile t + 2
+  }
+  if (KIND == 2 && ha) {   // this CTA's counts of the segment into the job's histogram
+    hist_a_flush(ha, P.gh_cnt + (size_t)S.job * NBUCK);
+    if (sp) hist_a_flush(ha + NBUCK, P.gh_cnt + (size_t)S.sjob * NBUCK);
   }
   const int base = i * NSLOT;
   if (w2) warp_acc(acc, nv, base + SLOT_W2, d_w2);
@@ -482,7 +491,14 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
   T* xs_wr = P.xs[a & 1];
   for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
   Stage2<NA> st;
-  st.init(bars, reinterpret_cast<char*>(acc) + (((size_t)NWARP * nv * sizeof(double) + 127) / 128) * 128, BLOCK);
+  const size_t accb = (((size_t)NWARP * nv * sizeof(double) + 127) / 128) * 128;
+  st.init(bars, reinterpret_cast<char*>(acc) + accb, BLOCK);
+  // select v2 round A: two count histograms (w, s) after the stages
+  unsigned* ha = P.selv2 ? reinterpret_cast<unsigned*>(reinterpret_cast<char*>(acc) + accb +
+                                                       (size_t)2 * NA * (BLOCK + 1) * 16)
+                         : nullptr;
+  if (ha)
+    for (int d = threadIdx.x; d < 2 * NBUCK; d += BLOCK) ha[d] = 0u;
   const int nch = g.N / W;
   const int per = (nch + (int)gridDim.x - 1) / (int)gridDim.x;
   const int c0 = min(nch, (int)blockIdx.x * per), c1 = min(nch, c0 + per);
@@ -493,7 +509,8 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
     const int K = kd == K_BOUNDS ? 0 : (kd == K_DIST ? 1 : 2);
     switch (K * 4 + P.set[i].prim[bl]) {
 #define P1CASE(KK, PP) \
-      case KK * 4 + PP: p1_run<T, KK, PP, AD, CK, NA>(P, C, i, bl, f, par, c0, c1, xs_rd, acc, nv, st); break;
+      case KK * 4 + PP: p1_run<T, KK, PP, AD, CK, NA>(P, C, i, bl, f, par, c0, c1, xs_rd, acc, nv, st, \
+          (P.set[i].job >= 0 && C.job[P.set[i].job].mode == JM_SEARCH) ? ha : nullptr); break;
       P1CASE(0, PRIM_I) P1CASE(0, PRIM_Z) P1CASE(0, PRIM_Y) P1CASE(0, PRIM_X)
       P1CASE(1, PRIM_I)
       P1CASE(2, PRIM_I) P1CASE(2, PRIM_Z) P1CASE(2, PRIM_Y) P1CASE(2, PRIM_X)
@@ -512,9 +529,10 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
 }
 
 // dynamic shared memory of k_pass1t<T, AD, .>: per-warp slots + two stages
-__host__ inline size_t pass1_smem(int P, bool adapt) {
+__host__ inline size_t pass1_smem(int P, bool adapt, bool selv2 = false) {
   const size_t accb = ((size_t)NWARP * (P * NSLOT + NEVOL) * sizeof(double) + 127) / 128 * 128;
-  return accb + (size_t)2 * (adapt ? P1_NA_ADAPT : P1_NA_PLAIN) * (BLOCK + 1) * 16;
+  return accb + (size_t)2 * (adapt ? P1_NA_ADAPT : P1_NA_PLAIN) * (BLOCK + 1) * 16 +
+         (selv2 ? (size_t)2 * NBUCK * sizeof(unsigned) : 0);
 }
 
 // ------------------------------------------------------------ pass 2

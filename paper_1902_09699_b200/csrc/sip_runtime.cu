@@ -20,6 +20,7 @@
 #include "sip_aux_kernels.cuh"
 #include "sip_team.cuh"
 #include "sip_fiber.cuh"
+#include "sip_svd.cuh"
 
 using namespace sip;
 
@@ -81,6 +82,8 @@ inline int kind_of(sip_set_type t) {
     case SIP_SET_L1_BALL: return K_L1;
     case SIP_SET_L2_BALL: return K_L2;
     case SIP_SET_ANNULUS: return K_ANN;
+    case SIP_SET_RANK: return K_RANK;
+    case SIP_SET_NUCLEAR: return K_NUC;
     default: return K_CARD;
   }
 }
@@ -105,6 +108,7 @@ struct Engine : EngineBase {
   cudaStream_t stream;
   int nsm = 148;
   int nfib_sets = 0;             // sets applied per fiber (k_fiber)
+  int nsvd_sets = 0, g_svd = 0;  // rank / nuclear-norm sets (sip_svd.cuh): one CTA per matrix
   int g_fib = 0, g_fibw = 0, nfib_sort = 0, nfib_warp = 0;
   int g_fw[MAXP] = {0};
   size_t smem_fib = 0, smem_fw[MAXP] = {0};
@@ -253,7 +257,10 @@ struct Engine : EngineBase {
           for (int t = 0; t < hs.kh * hs.kw; ++t) Pr.taps[t] = hs.kernel[t];
         }
       }
-      S.global = (S.kind == K_L1 || S.kind == K_L2 || S.kind == K_ANN || S.kind == K_CARD);
+      S.global = (S.kind == K_L1 || S.kind == K_L2 || S.kind == K_ANN || S.kind == K_CARD ||
+                  S.kind == K_RANK || S.kind == K_NUC);
+      S.svd = (S.kind == K_RANK || S.kind == K_NUC);
+      if (S.svd) nsvd_sets++;
       S.job = S.sjob = -1;
       S.fib = (i < p) ? s[i].fib : 0;
       // fiber length on this engine's own grid (multilevel levels differ)
@@ -269,7 +276,7 @@ struct Engine : EngineBase {
       if (S.global) Pr.nglob++;
       for (int b = 0; b < S.nblk; ++b) {
         Pr.seg_set[1 + Pr.nseg1] = (short)i; Pr.seg_blk[1 + Pr.nseg1] = (short)b; Pr.nseg1++;
-        if (S.global && !S.fib) { Pr.seg2_set[Pr.nseg2] = (short)i; Pr.seg2_blk[Pr.nseg2] = (short)b; Pr.nseg2++; }
+        if (S.global && !S.fib && !S.svd) { Pr.seg2_set[Pr.nseg2] = (short)i; Pr.seg2_blk[Pr.nseg2] = (short)b; Pr.nseg2++; }
       }
     }
     Pr.nseg1 += 1;   // segment 0: the per-point x work
@@ -297,7 +304,7 @@ struct Engine : EngineBase {
       S.v[0] = field(S.nblk); S.v[1] = field(S.nblk);
       S.vh0 = field(S.nblk);
       S.w = S.global ? field(S.nblk) : nullptr;
-      S.s = (S.kind == K_L1 || S.kind == K_CARD) ? field(S.nblk) : nullptr;
+      S.s = (S.kind == K_L1 || S.kind == K_CARD || S.svd) ? field(S.nblk) : nullptr;
       if (i < p && (!s[i].lo_vec.empty() || !s[i].hi_vec.empty())) {
         if (!s[i].lo_vec.empty()) S.lo_vec = upload_compact(i, s[i].lo_vec);
         if (!s[i].hi_vec.empty()) S.hi_vec = upload_compact(i, s[i].hi_vec);
@@ -354,6 +361,20 @@ struct Engine : EngineBase {
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
     if (nfib_sets && !vec)
       throw SipError{SIP_ERR_CONFIG, "per-fiber sets need nx % (16 / sizeof(dtype)) == 0 and no blur/mask operator"};
+    if (nsvd_sets && (!vec || nranks > 1))
+      throw SipError{SIP_ERR_CONFIG, "rank / nuclear sets need nx % (16 / sizeof(dtype)) == 0, no blur/mask operator, one rank"};
+    if (nsvd_sets) {   // fp64 scratch of the batched Jacobi kernel: X (m x n) and V (n x n) per matrix
+      size_t nx_ = 0, nv_ = 0;
+      for (int i = 0; i < p; ++i) {
+        if (!Pr.set[i].svd) continue;
+        const MatView mv = mat_view(ndim, nz_g, ny, nx, Pr.set[i].prim[0]);
+        nx_ = std::max(nx_, (size_t)mv.nmat * mv.m * mv.n);
+        nv_ = std::max(nv_, (size_t)mv.nmat * mv.n * mv.n);
+        g_svd = std::max(g_svd, mv.nmat);
+      }
+      Pr.svdX = dalloc<double>(nx_);
+      Pr.svdV = dalloc<double>(nv_);
+    }
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
     // lean CG / rhs: one wave of resident CTAs (4 per SM)
     g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
@@ -361,8 +382,10 @@ struct Engine : EngineBase {
     g_rhsf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
-    smem_p1v = pass1_smem(P, false);                   // k_pass1t: slots + bulk-copy stages
-    smem_p1a = pass1_smem(P, true);
+    // select v2 (sip_select2.cuh): single-rank fp32 runs with a radix job
+    Pr.selv2 = (vec && sizeof(T) == 4 && nranks == 1 && njobs > 0 && !getenv("SIP_SEL_V1")) ? 1 : 0;
+    smem_p1v = pass1_smem(P, false, Pr.selv2);        // k_pass1t: slots + bulk-copy stages (+ round-A counts)
+    smem_p1a = pass1_smem(P, true, Pr.selv2);
     // pass 1: segment-major over one contiguous chunk range per CTA
     // (3 CTAs / SM plain, 2 on adapt iterations: registers + stage buffers)
     g_p1 = std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * 3));
@@ -376,6 +399,9 @@ struct Engine : EngineBase {
       const long long per_it = (long long)BLOCK * SEL_U;
       const long long its = (chunks + (long long)g_sel * per_it - 1) / ((long long)g_sel * per_it);
       Pr.cand_per = its * per_it * VT<T>::W;
+      const long long per2 = (long long)BLOCK * SEL2_U;   // k_selB's tiles
+      const long long its2 = (chunks + (long long)g_sel * per2 - 1) / ((long long)g_sel * per2);
+      Pr.cand_per = std::max(Pr.cand_per, its2 * per2 * VT<T>::W);
       for (int i = 0; i < P; ++i) {
         const SetD<T>& S = Pr.set[i];
         if (S.job < 0) continue;
@@ -420,8 +446,8 @@ struct Engine : EngineBase {
     Pr.fibv = (nfib_sets && nranks > 1) ? dalloc<double>(4 * MAXP) : nullptr;
     Pr.gbar = dalloc<unsigned>(2);
     CU(cudaMemsetAsync(Pr.gbar, 0, 2 * sizeof(unsigned), stream));
-    const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cgf, g_cg2f, g_rhsf, g_fib, g_fibw});
-    Pr.partials = dalloc<double>((size_t)(gmax + 2) * (nv1 + 8));
+    const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cgf, g_cg2f, g_rhsf, g_fib, g_fibw, g_svd});
+    Pr.partials = dalloc<double>(std::max((size_t)(gmax + 2) * (nv1 + 8), (size_t)(g_sel + 2) * MAXJOBS * 3));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
       for (int st = ST_INIT; st <= ST_PASS2; ++st) xs_ = std::max(xs_, site_payload(st, P, njobs));
@@ -525,7 +551,7 @@ struct Engine : EngineBase {
   // profiling: an event is recorded before the first kernel and after every
   // kernel; consecutive pairs give each kernel's device time (kind list)
   // KB_COMM: a z-slab site's exchange + finalisers (multi-rank only)
-  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, KB_CGX, KB_FIBER, NKIND };
+  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, KB_CGX, KB_FIBER, KB_SVD, NKIND };
   bool prof = false;
   std::vector<cudaEvent_t> pev;      // events of one graph (capture order)
   std::vector<int> pkind;            // kind of the kernel ending at pev[i+1]
@@ -607,6 +633,7 @@ struct Engine : EngineBase {
   // the scalar kernels (sip_kernels.cuh) for general shapes, the blur
   // operator and n_cg > MAXCG (no ring slot per step)
   bool lean_cg() const { return vec && Pr.defer_x; }
+  const bool sel_debug = getenv("SIP_SEL_DEBUG") != nullptr;
   void launch_cg1(int j) {
     if (lean_cg()) {
       if (ndim == 3) lk(k_cg1f<T, true>, g_cgf, BLOCK, 0, Pr, j);
@@ -654,6 +681,16 @@ struct Engine : EngineBase {
     if (nfib_sort) { lk(k_fiber<T>, g_fib, BLOCK, smem_fib, Pr); ++launches; }
   }
   void launch_control() { lk(k_control<T>, 1, BLOCK, 0, Pr); ++launches; }
+  // rank / nuclear-norm sets: y, v of every matrix (which 0), the Eq. 26
+  // numerator of s on check iterations (which 1; the kernel returns on others)
+  void launch_svd() {
+    for (int i = 0; i < p; ++i) {
+      if (!Pr.set[i].svd) continue;
+      const MatView mv = mat_view(ndim, nz_g, ny, nx, Pr.set[i].prim[0]);
+      lk(k_svdproj<T>, mv.nmat, SVD_BLOCK, 0, Pr, i, 0); ++launches;
+      lk(k_svdproj<T>, mv.nmat, SVD_BLOCK, 0, Pr, i, 1); ++launches;
+    }
+  }
   void launch_fin(int site, int j, int round) {
     k_fin<T><<<1, BLOCK, 0, stream>>>(Pr, site, j, round);
     ++launches;
@@ -672,7 +709,13 @@ struct Engine : EngineBase {
     launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
-      for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
+      if (Pr.selv2) {   // one streaming pass + candidate rounds (round A ran in pass 1)
+        lk(k_selB<T>, g_sel, BLOCK, 0, Pr); ++launches; mark(KB_SELECT);
+        for (int r = 1; r <= 3; ++r) { lk(k_selC<T>, g_sel, BLOCK, 0, Pr, r); ++launches; mark(KB_SELECT); }
+      } else {
+        for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
+      }
+      if (sel_debug) k_seldbg<T><<<1, 32, 0, stream>>>(Pr);
       if (has_card()) { launch_tie(); mark(KB_TIE); }
     }
     if (Pr.nseg2 > 0) {
@@ -680,6 +723,7 @@ struct Engine : EngineBase {
       ++launches; mark(KB_PASS2);
     }
     if (nfib_sets) { launch_fiber(); mark(KB_FIBER); }   // per-fiber projections, after pass 2's sums
+    if (nsvd_sets) { launch_svd(); mark(KB_SVD); }       // rank / nuclear-norm sets
     launch_control(); mark(KB_CTRL);
   }
 
@@ -830,6 +874,13 @@ struct Engine : EngineBase {
     fill_ctrl(o, max_iter, eps_feas, eps_evol, floor_, rho_in, gamma_in);
     fill_logs_nan(max_iter);
     run_init(init_x, init_yv);
+    for (int i = 0; i < p; ++i) {   // relative nuclear-norm radius: sigma = frac ||A m||_* (y = A m after init)
+      if (!(Pr.set[i].kind == K_NUC && (*sets)[i].prm.relative)) continue;
+      if (!init_yv) throw SipError{SIP_ERR_CONFIG, "relative nuclear-norm radius needs y = A m at the start (no warm start / multilevel)"};
+      const MatView mv = mat_view(ndim, nz_g, ny, nx, Pr.set[i].prim[0]);
+      k_svdproj<T><<<mv.nmat, SVD_BLOCK, 0, stream>>>(Pr, i, 2);
+      ++launches;
+    }
     run_iterations(max_iter, o.graph_iters, o.n_cg);
     read_ctrl();
     check_canaries();
@@ -1369,7 +1420,7 @@ sip_status project_T(sip_grid g, const void* m, void* x, int max_iter, double to
   g->have_m = true;
   g->last_launches = e->launches;
   g->last = e;
-  if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, e->hc.numeric_err == 3 ? "internal: kernel variant does not match the iteration" : "NaN/Inf in the PARSDMM state"};
+  if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, e->hc.numeric_err == 3 ? "internal: kernel variant does not match the iteration" : e->hc.numeric_err == 4 ? "internal: threshold search window inconsistent" : "NaN/Inf in the PARSDMM state"};
   return e->hc.converged ? SIP_OK : SIP_NOT_CONVERGED;
 }
 
@@ -1408,6 +1459,8 @@ sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int ma
     CU(cudaEventCreate(&a)); CU(cudaEventCreate(&b));
     CU(cudaEventRecord(a, g->stream));
     e->launches = 0;
+    e->prof = g->opt.profile != 0;   // per-kernel profile of every level (sip_get_profile: the finest)
+    for (int q = 0; q < Engine<T>::NKIND; ++q) { e->prof_ms[q] = 0; e->prof_cnt[q] = 0; }
     if (l == n_levels - 1) {
       // coarsest: x = m_L, y_i = v_i = 0 (reading L13)
       for (int i = 0; i < e->P; ++i) {
@@ -1448,7 +1501,7 @@ sip_status multilevel_T(sip_grid g, const void* m, void* x, int n_levels, int ma
     cudaEventDestroy(a); cudaEventDestroy(b);
     if (per_level) e->fill_result(&per_level[l], ms);
     launches += e->launches;
-    if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, e->hc.numeric_err == 3 ? "internal: kernel variant does not match the iteration" : "NaN/Inf in the PARSDMM state"};
+    if (e->hc.numeric_err) throw SipError{SIP_ERR_NUMERIC, e->hc.numeric_err == 3 ? "internal: kernel variant does not match the iteration" : e->hc.numeric_err == 4 ? "internal: threshold search window inconsistent" : "NaN/Inf in the PARSDMM state"};
   }
   copy_out(fine, fine->Pr.x, x, N);
   CU(cudaStreamSynchronize(g->stream));
@@ -1684,6 +1737,13 @@ template <class T>
 sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
   Engine<T>* e = engine_of<T>(g);
   if (!e->ran) throw SipError{SIP_ERR_STATE, "sip_project_set needs a previous sip_project"};
+  // the step-level projection runs pass 1 / the radix rounds directly (no
+  // select v2: its round-A counts would be left behind for the next solve)
+  struct V2Off {
+    int* f; int v;
+    ~V2Off() { *f = v; }
+  } v2off{&e->Pr.selv2, e->Pr.selv2};
+  e->Pr.selv2 = 0;
   const Geo& G = e->Pr.g;
   SetD<T>& S = e->Pr.set[set_id];
   const long long M = e->set_len(set_id);
@@ -1734,7 +1794,10 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     }
     e->hc = c;
     CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
-    if (S.fib) {   // per-fiber projection: k_fiberw / k_fiber write y[1]
+    if (S.svd) {   // rank / nuclear-norm set: the batched Jacobi kernel writes y[1]
+      const MatView mv = mat_view(e->ndim, e->nz_g, e->ny, e->nx, S.prim[0]);
+      k_svdproj<T><<<mv.nmat, SVD_BLOCK, 0, e->stream>>>(e->Pr, set_id, 0);
+    } else if (S.fib) {   // per-fiber projection: k_fiberw / k_fiber write y[1]
       if (S.fpath) FiberW<T>::of(S.flen)<<<e->g_fw[set_id], BLOCK, e->smem_fw[set_id], e->stream>>>(e->Pr, set_id);
       else k_fiber<T><<<e->g_fib, BLOCK, e->smem_fib, e->stream>>>(e->Pr);
     } else if (S.job >= 0) {
@@ -1747,7 +1810,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
         else k_tiecount<T><<<e->g_p2, BLOCK, 0, e->stream>>>(e->Pr);
       }
     }
-    if (S.fib) {
+    if (S.fib || S.svd) {
     } else if (e->vec) k_pass2t<T, 2, 2><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
     else k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
   } else {
@@ -1961,7 +2024,7 @@ sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtyp
 sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type type,
                        const sip_set_params* prm, int* set_id) {
   if (!g || !prm) return SIP_ERR_ARG;
-  if (op < SIP_OP_IDENTITY || op > SIP_OP_BLUR_MASK || type < SIP_SET_BOUNDS || type > SIP_SET_CARDINALITY)
+  if (op < SIP_OP_IDENTITY || op > SIP_OP_BLUR_MASK || type < SIP_SET_BOUNDS || type > SIP_SET_NUCLEAR)
     return SIP_ERR_ARG;
   if ((int)g->sets.size() >= SIP_MAX_SETS) { g->err = "more than 16 sets"; return SIP_ERR_CONFIG; }
   if (op == SIP_OP_DY && g->ndim != 3) { g->err = "D_y needs a 3D grid"; return SIP_ERR_CONFIG; }
@@ -2020,6 +2083,16 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type 
     } else if (type == SIP_SET_CARDINALITY) {
       if (prm->relative) { if (!(prm->k_frac >= 0 && prm->k_frac <= 1)) return SIP_ERR_PARAM; }
       else if (prm->k < 0 || prm->k > hs.M) return SIP_ERR_PARAM;
+    } else if (type == SIP_SET_RANK || type == SIP_SET_NUCLEAR) {
+      // matrix view (reading L29); the batched Jacobi kernel's limits
+      if (op == SIP_OP_TV || op == SIP_OP_BLUR_MASK) { g->err = "rank / nuclear sets need a single-block operator"; return SIP_ERR_CONFIG; }
+      if (g->nranks > 1) { g->err = "rank / nuclear sets: one rank only"; return SIP_ERR_CONFIG; }
+      const int prim = op == SIP_OP_IDENTITY ? PRIM_I : op == SIP_OP_DZ ? PRIM_Z : op == SIP_OP_DY ? PRIM_Y : PRIM_X;
+      const MatView mv = mat_view(g->ndim, (int)nz, (int)ny, (int)nx, prim);
+      if (mv.n > SVD_NMAX || mv.n < 1) { g->err = "rank / nuclear sets: min(rows, cols) of the matrix view must be 1..2048"; return SIP_ERR_CONFIG; }
+      if (type == SIP_SET_RANK && (prm->relative || prm->k < 0)) return SIP_ERR_PARAM;
+      if (type == SIP_SET_NUCLEAR && !(prm->sigma >= 0)) return SIP_ERR_PARAM;
+      if (prm->app_mode != SIP_APPLY_WHOLE) { g->err = "rank / nuclear sets act on whole matrices"; return SIP_ERR_CONFIG; }
     }
     // per-fiber application (NEXT-1)
     if (prm->app_mode < SIP_APPLY_WHOLE || prm->app_mode > SIP_APPLY_Z_FIBERS) return SIP_ERR_ARG;

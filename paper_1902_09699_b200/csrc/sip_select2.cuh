@@ -1,0 +1,471 @@
+// sip_select2.cuh -- the exact l1-ball threshold and cardinality k-th key for
+// single-rank fp32 runs (sm_100a), in one streaming pass of w after pass 1.
+//
+// What is computed is unchanged (readings L5, L6): the l1 ball's
+// theta with sum_j max(|w_j| - theta, 0) = sigma (Duchi's active set), or the
+// key of the k-th largest |w| with the index-ordered tie count.  The keys are
+// the IEEE bit patterns of |w| (monotone for non-negative floats).
+//
+//   round A  (inside k_pass1t, while w is written): a COUNT histogram of the
+//            top 11 key bits of every radix job -- one shared atomic per
+//            entry, no second read of w.
+//   k_selB   every CTA turns the counts into a candidate key range [lo, hi)
+//            that must contain the answer (cardinality: the bucket of the
+//            k-th key; l1: bounds of sum max(|w| - e, 0) at every bucket
+//            edge e from the counts alone), then streams w once: entries
+//            >= hi are summed into (count, sum) in registers, entries in
+//            [lo, hi) are appended to the CTA's candidate region.
+//   k_selC   2-3 rounds over the candidates only (L2-resident): exact
+//            histograms (counts + 16-bit limb sums) of a window of keys that
+//            shrinks 2048-fold per round down to a single key.
+//
+// Replaces three full-read radix rounds with three shared atomics per entry
+// each (k_selectf): one full read and one atomic per entry.  Multi-rank and
+// fp64 runs keep k_selectf (its finalisers gather across ranks).
+#pragma once
+#include "sip_flat.cuh"
+
+namespace sip {
+
+constexpr int A_SHIFT = 20;                 // round-A digit: key bits 30..20 (11 bits)
+constexpr int SEL2_U = 8;                   // chunks in flight per thread in k_selB
+
+__device__ __forceinline__ unsigned key32(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+__device__ __forceinline__ double kval(unsigned key) { return (double)__uint_as_float(key); }
+
+// round A: one count per non-zero entry (zeros never decide: a zero never
+// displaces a non-zero of the top k and adds nothing to an l1 sum)
+template <class T>
+__device__ __forceinline__ void hist_a(unsigned* h, const T* v) {
+  if constexpr (sizeof(T) == 4) {
+    constexpr int W = VT<T>::W;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      const unsigned k = key32((float)v[e]);
+      if (k) atomicAdd(&h[k >> A_SHIFT], 1u);
+    }
+  }
+}
+__device__ __forceinline__ void hist_a_flush(unsigned* h, unsigned* g) {
+  __syncthreads();
+  for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+    const unsigned c = h[d];
+    if (c) { atomicAdd(g + d, c); h[d] = 0u; }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- ranges
+// The candidate range of a job from the round-A counts c_d (bucket d holds
+// the keys [d 2^20, (d+1) 2^20), values in [e_d, e_{d+1})).  Computed
+// identically by every CTA of k_selB (no serial tail), fixed reduction order.
+struct SelRange {
+  int mode;            // JM_SEARCH, or a final JM_ZERO / JM_INSIDE / JM_ALL
+  unsigned lo, hi;     // candidates lo <= key < hi (non-zero); key >= hi: above
+};
+
+// the exclusive suffix (over the threads after this one) of per-thread values,
+// fixed order: a warp-level inclusive suffix by shuffles, then the totals of
+// the later warps
+template <class V>
+__device__ __forceinline__ V suffix_excl(V v, V* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  V inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const V t = __shfl_down_sync(0xffffffffu, inc, o);
+    if (lane + o < 32) inc += t;
+  }
+  if (lane == 0) sh[w] = inc;
+  __syncthreads();
+  V later = (V)0;
+  for (int q = NWARP - 1; q > w; --q) later += sh[q];
+  __syncthreads();
+  return later + inc - v;
+}
+
+// the lower edge value of round-A bucket d; the buckets of the inf / NaN
+// keys (d >= 0x7f8: exponent 255) never hold entries and get FLT_MAX, so no
+// inf (or 0 x inf) enters the sums
+__device__ __forceinline__ double edge_a(int d) {
+  return d < 0x7f8 ? kval((unsigned)d << A_SHIFT) : 3.4028234663852886e38;
+}
+
+__device__ inline SelRange range_of_job(const Job& J, const unsigned* gcnt) {
+  __shared__ unsigned long long s_u[NWARP];
+  __shared__ double s_d[NWARP];
+  __shared__ int s_best[2];
+  SelRange R{JM_SEARCH, 0u, 0u};
+  constexpr int PER = NBUCK / BLOCK;        // 8 buckets per thread
+  const int d0 = threadIdx.x * PER;
+  unsigned c[PER];
+  unsigned long long ct = 0;
+  double et = 0.0, e1t = 0.0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    c[q] = __ldcg(gcnt + d0 + q);
+    ct += c[q];
+    et += (double)c[q] * edge_a(d0 + q);
+    e1t += (double)c[q] * edge_a(d0 + q + 1);
+  }
+  const unsigned long long c_after = suffix_excl<unsigned long long>(ct, s_u);
+  const double e_after = suffix_excl<double>(et, s_d);
+  const double e1_after = suffix_excl<double>(e1t, s_d);
+  if (threadIdx.x == 0) { s_best[0] = -1; s_best[1] = -1; }
+  __syncthreads();
+  int best_lo = -1, best_hi = -1;
+  unsigned long long C = c_after;
+  double E = e_after, E1 = e1_after;
+#pragma unroll
+  for (int q = PER - 1; q >= 0; --q) {       // C, E, E1 over the buckets >= d
+    const int d = d0 + q;
+    C += c[q];
+    const double e = edge_a(d);
+    E += (double)c[q] * e;
+    E1 += (double)c[q] * edge_a(d + 1);
+    if (J.kind == K_CARD) {
+      if (C >= (unsigned long long)J.k && best_hi < d) best_hi = d;
+    } else {
+      // f(e_d) = sum_{|w| >= e_d} (|w| - e_d) lies in [E - e_d C, E1 - e_d C];
+      // an absolute margin keeps the bounds safe under fp64 rounding
+      const double L = E - e * (double)C - 1e-12 * E;
+      const double U = E1 - e * (double)C + 1e-12 * E1;
+      if (L > J.sigma && best_lo < d) best_lo = d;
+      if (U > J.sigma && best_hi < d) best_hi = d;
+    }
+  }
+  if (best_lo >= 0) atomicMax(&s_best[0], best_lo);
+  if (best_hi >= 0) atomicMax(&s_best[1], best_hi);
+  __syncthreads();
+  const int blo = s_best[0], bhi = s_best[1];
+  __syncthreads();
+  if (J.kind == K_CARD) {
+    if (bhi < 0) { R.mode = JM_ALL; return R; }              // fewer than k non-zeros: keep all
+    R.lo = (unsigned)bhi << A_SHIFT;
+    R.hi = (unsigned)(bhi + 1) << A_SHIFT;
+    return R;
+  }
+  if (J.sigma <= 0.0) { R.mode = JM_ZERO; return R; }        // the ball is {0} (L5)
+  if (bhi < 0) { R.mode = JM_INSIDE; return R; }             // ||w||_1 <= U(0) <= sigma
+  R.lo = blo < 0 ? 0u : (unsigned)blo << A_SHIFT;
+  R.hi = (unsigned)(bhi + 1) << A_SHIFT;
+  return R;
+}
+
+__device__ __forceinline__ bool job_live(const Job& J, bool check) {
+  return J.mode == JM_SEARCH && J.round == 0 && (!J.on_s || check);
+}
+
+// ---------------------------------------------------------------- k_selB
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
+  if constexpr (sizeof(T) != 4) return;
+  else {
+    constexpr int W = VT<T>::W;
+    if (gridDim.x != (unsigned)P.sel_grid) __trap();   // regions are sized for this grid
+    Ctrl& C = *P.ctrl;
+    if (C.stopped) return;
+    __shared__ SelRange s_rng[MAXJOBS];
+    __shared__ unsigned s_cn;
+    __shared__ double sh[NWARP + 1];
+    const bool check = (C.k % C.opt.check_every) == 0;
+    const Geo& g = P.g;
+    const int nch = g.N / W;
+    const int nj = C.njobs;
+    bool any = false;
+    for (int jb = 0; jb < nj; ++jb) {
+      const Job& J = C.job[jb];
+      if (!job_live(J, check)) continue;
+      any = true;
+      const SelRange R = range_of_job(J, P.gh_cnt + (size_t)jb * NBUCK);
+      if (threadIdx.x == 0) s_rng[jb] = R;
+      __syncthreads();
+      double* part = P.partials + ((size_t)blockIdx.x * MAXJOBS + jb) * 3;
+      unsigned* cand = P.cand[jb] + (size_t)blockIdx.x * P.cand_per;
+      if (R.mode != JM_SEARCH) {
+        if (threadIdx.x == 0) { part[0] = 0.0; part[1] = 0.0; part[2] = 0.0; P.ccnt[(size_t)jb * gridDim.x + blockIdx.x] = 0u; }
+        continue;
+      }
+      const SetD<T>& S = P.set[J.set];
+      const T* buf = J.on_s ? S.s : S.w;
+      const int tot = S.nblk * nch;
+      const unsigned lo = R.lo, hi = R.hi;
+      const bool l1 = J.kind == K_L1;
+      if (threadIdx.x == 0) s_cn = 0u;
+      __syncthreads();
+      unsigned long long n_ab = 0;
+      double s_ab = 0.0, s_tot = 0.0;
+      const int stride = gridDim.x * BLOCK * SEL2_U;
+      const int lane = threadIdx.x & 31;
+      for (int b0 = blockIdx.x * BLOCK * SEL2_U; b0 < tot; b0 += stride) {
+        T v[SEL2_U][W];
+        bool ok[SEL2_U];
+#pragma unroll
+        for (int u = 0; u < SEL2_U; ++u) {     // every load of the tile first
+          const int q = b0 + u * BLOCK + threadIdx.x;
+          ok[u] = q < tot;
+          const int qq = ok[u] ? q : tot - 1;
+          const int bl = (qq >= nch) + (qq >= 2 * nch);   // nblk <= 3
+          VT<T>::ldcs(buf + (int64_t)bl * g.ld + (int64_t)(qq - bl * nch) * W, v[u]);
+        }
+        unsigned mine = 0;   // candidates of this thread (bit u*W+e)
+#pragma unroll
+        for (int u = 0; u < SEL2_U; ++u) {
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            const unsigned k = ok[u] ? key32((float)v[u][e]) : 0u;
+            const double a = kval(k);
+            if (k >= hi) { ++n_ab; s_ab += a; }
+            else if (k >= lo && k != 0u) mine |= 1u << (u * W + e);
+            if (l1) s_tot += a;
+          }
+        }
+        // warp-aggregated append to this CTA's region (one shared atomic per warp)
+        const int cnt = __popc(mine);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t_ = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t_;
+        }
+        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+        if (wtot) {
+          unsigned base = 0u;
+          if (lane == 31) base = atomicAdd(&s_cn, (unsigned)wtot);
+          unsigned pos = __shfl_sync(0xffffffffu, base, 31) + (unsigned)(incl - cnt);
+#pragma unroll
+          for (int u = 0; u < SEL2_U; ++u)
+#pragma unroll
+            for (int e = 0; e < W; ++e)
+              if (mine & (1u << (u * W + e))) cand[pos++] = key32((float)v[u][e]);
+        }
+      }
+      // per-CTA (count, sum above, total): fixed-order block sums
+      const double d_ab = block_sum((double)n_ab, sh);
+      const double d_sab = block_sum(s_ab, sh);
+      const double d_tot = block_sum(s_tot, sh);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        part[0] = d_ab; part[1] = d_sab; part[2] = d_tot;
+        P.ccnt[(size_t)jb * gridDim.x + blockIdx.x] = s_cn;
+      }
+      __syncthreads();
+    }
+    if (!any) return;
+    if (last_block(P.counter)) {
+      for (int jb = 0; jb < nj; ++jb) {
+        Job& J = C.job[jb];
+        if (!job_live(J, check)) continue;
+        const SelRange R = s_rng[jb];
+        double tot3[3];
+        for (int q = 0; q < 3; ++q) {            // fixed order over the CTAs
+          double a = 0.0;
+          for (int b = threadIdx.x; b < (int)gridDim.x; b += BLOCK)
+            a += __ldcg(P.partials + ((size_t)b * MAXJOBS + jb) * 3 + q);
+          tot3[q] = block_sum(a, sh);
+        }
+        if (threadIdx.x == 0) {
+          if (R.mode != JM_SEARCH) {
+            J.mode = R.mode;
+          } else if (J.kind == K_L1 && tot3[2] <= J.sigma) {
+            J.mode = JM_INSIDE;                  // ||w||_1 <= sigma: w is in the ball (L5)
+          } else {
+            J.cnt_above = (long long)tot3[0];
+            J.sum_above = tot3[1];
+            J.prefix = R.lo;                     // the window of the candidate rounds
+            J.width = (unsigned long long)(R.hi - R.lo);
+            J.round = 1;
+          }
+        }
+        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;   // next round A
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) *P.counter = 0u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- k_selC
+// window [lo, lo + width) split into <= 2048 buckets of 2^shift keys; every
+// bucket lies inside one exponent (lo is a multiple of 2^20, shift <= 20),
+// so its limb sums are exact multiples of one power of two
+__device__ __forceinline__ int sel_shift(unsigned long long width) {
+  int b = 0;
+  while ((1ull << b) < width) ++b;        // ceil(log2(width))
+  return b > 11 ? b - 11 : 0;
+}
+
+// last CTA of k_selC: the bucket d* of the window holding the answer (the
+// walk of resolve_round over linear sub-buckets), then either the next,
+// 2048x narrower window or -- single-key buckets -- the final theta / tau
+__device__ void resolve_window(Ctrl& C, Job& J, const unsigned* hc, const unsigned long long* h0) {
+  __shared__ long long s_cnt[BLOCK];
+  __shared__ double s_sum[BLOCK];
+  __shared__ int s_dstar;
+  __shared__ long long s_cab;
+  __shared__ double s_sab;
+  const unsigned lo = (unsigned)J.prefix;
+  const int sh = sel_shift(J.width);
+  const int nbk = (int)((J.width + (1ull << sh) - 1) >> sh);
+  const int per = (nbk + BLOCK - 1) / BLOCK;
+  const int d0 = threadIdx.x * per;
+  auto bsum = [&](int d) {     // exact sum of the bucket's values: limbs x 2^(e - 150)
+    const unsigned kb = lo + ((unsigned)d << sh);
+    return (double)__ldcg(h0 + d) * SigT<float>::scale(kb);
+  };
+  long long c_loc = 0;
+  double s_loc = 0.0;
+  for (int d = d0; d < d0 + per && d < nbk; ++d) { c_loc += __ldcg(hc + d); s_loc += bsum(d); }
+  s_cnt[threadIdx.x] = c_loc;
+  s_sum[threadIdx.x] = s_loc;
+  __syncthreads();
+  if (threadIdx.x == 0) {      // suffix totals of the threads above, fixed order
+    long long c = 0; double sm = 0.0;
+    for (int t = BLOCK - 1; t >= 0; --t) {
+      const long long ct = s_cnt[t]; const double st = s_sum[t];
+      s_cnt[t] = c; s_sum[t] = sm;
+      c += ct; sm += st;
+    }
+    s_dstar = -1;
+  }
+  __syncthreads();
+  long long c_ge = J.cnt_above + s_cnt[threadIdx.x];
+  double s_ge = J.sum_above + s_sum[threadIdx.x];
+  int best = -1;
+  for (int d = min(d0 + per, nbk) - 1; d >= d0; --d) {
+    const unsigned kb = lo + ((unsigned)d << sh);
+    c_ge += __ldcg(hc + d);
+    s_ge += bsum(d);
+    const bool ok = (J.kind == K_L1) ? (s_ge - kval(kb) * (double)c_ge) > J.sigma   // f(e_d) > sigma
+                                     : c_ge >= J.k;                                 // C(>= d) >= k
+    if (ok && d > best) best = d;
+  }
+  if (best >= 0) atomicMax(&s_dstar, best);
+  __syncthreads();
+  const int dstar = s_dstar;
+  if (dstar >= d0 && dstar < d0 + per) {   // totals strictly above d*
+    long long c = J.cnt_above + s_cnt[threadIdx.x];
+    double sm = J.sum_above + s_sum[threadIdx.x];
+    for (int d = min(d0 + per, nbk) - 1; d > dstar; --d) { c += __ldcg(hc + d); sm += bsum(d); }
+    s_cab = c;
+    s_sab = sm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (dstar < 0) {
+      // k_selB's range guarantees the answer inside the window
+      C.numeric_err = 4;
+      J.mode = JM_ALL;
+    } else {
+      const unsigned kb = lo + ((unsigned)dstar << sh);
+      J.cnt_above = s_cab;
+      J.sum_above = s_sab;
+      if (sh == 0) {                         // single-key buckets: the answer
+        if (J.kind == K_L1) {                // entries == kb are inactive
+          J.theta = (J.sum_above - J.sigma) / (double)J.cnt_above;
+          J.mode = JM_DONE;
+        } else {
+          J.tau = kb;
+          const long long ceq = __ldcg(hc + dstar);
+          J.cnt_eq = ceq;
+          J.keep_eq = J.k - J.cnt_above;
+          J.ties = (J.keep_eq < ceq) ? 1 : 0;
+          const double tv = kval(kb);
+          J.tau_val2 = tv * tv;
+          J.mode = JM_DONE;
+        }
+      } else {
+        const unsigned long long top = (unsigned long long)lo + J.width;
+        J.prefix = kb;
+        J.width = min(1ull << sh, top - (unsigned long long)kb);
+        J.round += 1;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_selC(const __grid_constant__ Prob<T> P, int round) {
+  pdl_begin();
+  if constexpr (sizeof(T) != 4) return;
+  else {
+    if (gridDim.x != (unsigned)P.sel_grid) __trap();
+    Ctrl& C = *P.ctrl;
+    if (C.stopped) return;
+    using LB = Limbs<float>;
+    __shared__ unsigned h_cnt[NBUCK];
+    __shared__ unsigned h_l[LB::N][NBUCK];
+    const bool check = (C.k % C.opt.check_every) == 0;
+    const int nj = C.njobs;
+    bool any = false;
+    for (int jb = 0; jb < nj; ++jb) {
+      const Job& J = C.job[jb];
+      if (J.mode != JM_SEARCH || J.round != round || (J.on_s && !check)) continue;
+      any = true;
+      const bool sums = J.kind == K_L1;
+      const unsigned lo = (unsigned)J.prefix;
+      const unsigned long long width = J.width;
+      const int sh = sel_shift(width);
+      for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+        h_cnt[d] = 0u;
+#pragma unroll
+        for (int q = 0; q < LB::N; ++q) h_l[q][d] = 0u;
+      }
+      __syncthreads();
+      const unsigned* cand = P.cand[jb] + (size_t)blockIdx.x * P.cand_per;
+      const int n = (int)__ldcg(P.ccnt + (size_t)jb * gridDim.x + blockIdx.x);
+      for (int q = threadIdx.x; q < n; q += BLOCK) {
+        const unsigned k = __ldcg(cand + q);
+        if (k < lo || (unsigned long long)(k - lo) >= width) continue;
+        const int d = (int)((k - lo) >> sh);
+        atomicAdd(&h_cnt[d], 1u);
+        if (sums) {
+          unsigned l[LB::N];
+          LB::split(k, l);
+#pragma unroll
+          for (int t = 0; t < LB::N; ++t) atomicAdd(&h_l[t][d], l[t]);
+        }
+      }
+      __syncthreads();
+      unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
+      unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
+      for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+        if (!h_cnt[d]) continue;
+        atomicAdd(gc + d, h_cnt[d]);
+        if (sums) atomicAdd(g0 + d, (unsigned long long)h_l[0][d] + ((unsigned long long)h_l[1][d] << 16));
+      }
+      __syncthreads();
+    }
+    if (!any) return;
+    if (last_block(P.counter)) {
+      for (int jb = 0; jb < nj; ++jb) {
+        Job& J = C.job[jb];
+        if (J.mode != JM_SEARCH || J.round != round || (J.on_s && !check)) continue;
+        resolve_window(C, J, P.gh_cnt + (size_t)jb * NBUCK, P.gh_s0 + (size_t)jb * NBUCK);
+        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+          P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;
+          P.gh_s0[(size_t)jb * NBUCK + d] = 0ull;
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) *P.counter = 0u;
+    }
+  }
+}
+
+// SIP_SEL_DEBUG=1: the jobs after the threshold search (diagnostics)
+template <class T>
+__global__ void k_seldbg(const __grid_constant__ Prob<T> P) {
+  const Ctrl& C = *P.ctrl;
+  if (threadIdx.x || blockIdx.x || C.stopped) return;
+  for (int jb = 0; jb < C.njobs; ++jb) {
+    const Job& J = C.job[jb];
+    printf("k=%d job=%d on_s=%d kind=%d mode=%d round=%d theta=%.17g tau=%llu cnt_above=%lld sum_above=%.17g prefix=%llu width=%llu keep_eq=%lld ties=%d\n",
+           C.k, jb, J.on_s, J.kind, J.mode, J.round, J.theta, J.tau, J.cnt_above, J.sum_above, J.prefix, J.width,
+           J.keep_eq, J.ties);
+  }
+}
+
+}  // namespace sip

@@ -21,7 +21,7 @@ SIP_OK = 0
 SIP_NOT_CONVERGED = 1
 SIP_MAX_SETS = 16
 OPS = {"I": 0, "IDENTITY": 0, "DZ": 1, "DY": 2, "DX": 3, "TV": 4, "BLUR_MASK": 5}
-KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4}
+KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6}
 DTYPES = {"f32": 0, "f64": 1}
 
 
@@ -64,7 +64,8 @@ EXPORTS = [
     "sip_apply_op", "sip_apply_system", "sip_cg", "sip_project_set", "sip_get_state",
     "sip_get_log", "sip_get_support_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
 ]
-KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm", "cgx", "fiber"]
+KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm", "cgx", "fiber",
+                "svd"]
 
 _lib = None
 

@@ -1,0 +1,101 @@
+"""Rank and nuclear-norm sets (Table 1) on the
+GPU against the oracle: the batched one-sided Jacobi projection per matrix of
+the view (reading L29) through sip_project_set (per-kernel bar: 1e-5 fp32,
+1e-10 fp64), and PARSDMM end to end with box + rank / nuclear sets (tiny
+fp64: exact iteration and CG counts; fp32 within 1e-3).  Marked gpu."""
+import numpy as np
+import pytest
+
+import oracle as O
+import sip_inputs as G
+from sip_inputs import SetDef
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1902_09699_b200 import Grid  # noqa: E402
+
+TD = {"f32": torch.float32, "f64": torch.float64}
+TOL = {"f32": 1e-5, "f64": 1e-10}
+
+
+def mk(shape, sets, dtype):
+    g = Grid(shape, None, dtype)
+    for sd in sets:
+        g.add_set(sd)
+    return g
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("shape,op,kind", [((48, 40), "I", "rank"), ((40, 48), "DZ", "rank"),
+                                           ((36, 64), "DX", "nuclear"), ((64, 36), "I", "nuclear"),
+                                           ((6, 20, 16), "I", "rank"), ((5, 12, 24), "DY", "nuclear")])
+def test_project_set_svd(dtype, shape, op, kind):
+    r = np.random.default_rng(len(shape) * 7 + shape[0])
+    sd = SetDef(op, kind, k=3, sigma=0.0)
+    M = O.op_len(shape, sd)
+    w = r.normal(size=M) * 10.0
+    if kind == "nuclear":
+        rows, cols = O.matrix_shape(shape, op)
+        nuc = sum(O.svd_values(w[o:o + rows * cols].reshape(rows, cols)).sum() for o in range(0, M, rows * cols))
+        sd.sigma = 0.3 * nuc / (M // (rows * cols))
+    g = mk(shape, [sd], dtype)
+    m = torch.zeros(shape, dtype=TD[dtype], device="cuda")
+    x = torch.empty_like(m)
+    g.project(m, x, max_iter=1)
+    wd = torch.tensor(w, dtype=TD[dtype], device="cuda")
+    y = torch.empty_like(wd)
+    g.project_set(0, wd, y)
+    ref = O.project(sd, wd.double().cpu().numpy(), shape=shape)
+    assert O.relres(y.double().cpu().numpy(), ref) <= TOL[dtype], O.relres(y.double().cpu().numpy(), ref)
+    g.close()
+
+
+def _prob(kind, shape, dtype):
+    m = G.tiny_model(140 + len(shape), shape)
+    sets = [SetDef("I", "bounds", lo=float(m.min()) + 100.0, hi=float(m.max()) - 100.0)]
+    if kind == "rank":
+        sets.append(SetDef("I", "rank", k=2))
+    else:
+        sets.append(SetDef("I", "nuclear", sigma=0.6, relative=True))
+    return G.Problem("svd", shape, dtype, m, sets, options=dict(G.DEFAULT_OPTIONS))
+
+
+@pytest.mark.parametrize("kind", ["rank", "nuclear"])
+@pytest.mark.parametrize("shape", [(16, 12), (4, 8, 6)])
+def test_parsdmm_svd_sets_fp64_exact(kind, shape):
+    prob = _prob(kind, shape, "f64")
+    g = mk(shape, prob.sets, "f64")
+    m = torch.tensor(prob.m, dtype=torch.float64, device="cuda")
+    x = torch.empty_like(m)
+    res, st = g.project(m, x, max_iter=200, tol=1e-3)
+    lg = g.get_log(200)
+    ref = O.parsdmm(shape, prob.sets, prob.m, **prob.options)
+    assert res["iterations"] == ref.iterations
+    np.testing.assert_array_equal(lg["cg"][: ref.iterations], ref.cg_per_iter)
+    np.testing.assert_array_equal(lg["branch"][: ref.iterations], ref.branch)
+    assert O.relres(x.cpu().numpy(), ref.x) < 1e-8
+    g.close()
+
+
+@pytest.mark.parametrize("kind", ["rank", "nuclear"])
+def test_parsdmm_svd_sets_fp32(kind):
+    shape = (64, 48)
+    prob = _prob(kind, shape, "f32")
+    g = mk(shape, prob.sets, "f32")
+    m = torch.tensor(prob.m, dtype=torch.float32, device="cuda")
+    x = torch.empty_like(m)
+    res, st = g.project(m, x, max_iter=200, tol=1e-3)
+    o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps))
+    ref = O.parsdmm(shape, prob.sets, prob.m, **o)
+    assert O.relres(x.double().cpu().numpy(), ref.x) < 1e-3
+    g.close()
+
+
+def test_svd_set_refusals():
+    g = Grid((16, 16), None, "f32")
+    with pytest.raises(Exception):
+        g.add_set(SetDef("TV", "rank", k=2))
+    g.close()

@@ -694,3 +694,112 @@ def test_relative_parameter_resolution():
     for frac, k in e["card_dx_k"].items():
         _, _, _, kk = O.resolve_set(shape, SetDef("DX", "card", k_frac=float(frac), relative=True), m)
         assert kk == k
+
+
+# ------------------------------------------------------------ rank / nuclear-norm sets (NEXT-2, Table 1)
+def _np_rank(a, r):
+    U, s, Vt = np.linalg.svd(a, full_matrices=False)
+    return (U[:, :r] * s[:r]) @ Vt[:r]
+
+
+def _np_nuclear(a, sigma):
+    U, s, Vt = np.linalg.svd(a, full_matrices=False)
+    if s.sum() <= sigma:
+        return a.copy()
+    lam = _l1_ball_sorted(s, sigma)
+    return (U * lam) @ Vt
+
+
+def _l1_ball_sorted(s, sigma):
+    """projection of a non-negative vector onto {sum <= sigma} by its KKT
+    conditions: lam = max(s - theta, 0) with theta the root of sum = sigma
+    (bisection, independent of the oracle's sort-based Duchi)"""
+    lo, hi = 0.0, float(s.max())
+    for _ in range(200):
+        th = 0.5 * (lo + hi)
+        if np.maximum(s - th, 0).sum() > sigma:
+            lo = th
+        else:
+            hi = th
+    return np.maximum(s - 0.5 * (lo + hi), 0)
+
+
+@pytest.mark.parametrize("shape", [(7, 5), (5, 7), (6, 6), (12, 3)])
+def test_svd_values_vs_numpy(shape):
+    r = np.random.default_rng(sum(shape))
+    a = r.normal(size=shape)
+    np.testing.assert_allclose(O.svd_values(a), np.linalg.svd(a, compute_uv=False), rtol=0, atol=1e-13)
+    b = np.outer(r.normal(size=shape[0]), r.normal(size=shape[1]))       # rank 1
+    sv = O.svd_values(b)
+    assert sv[0] == pytest.approx(np.linalg.norm(b), rel=1e-14) and np.all(sv[1:] < 1e-13 * sv[0])
+
+
+def test_matrix_view_shapes():
+    """reading L29: 2D grids one (z, x) matrix, 3D grids one (y, x) matrix per z-plane"""
+    assert O.matrix_shape((5, 7), "I") == (5, 7)
+    assert O.matrix_shape((5, 7), "DZ") == (4, 7)
+    assert O.matrix_shape((5, 7), "DX") == (5, 6)
+    assert O.matrix_shape((4, 5, 6), "I") == (5, 6)
+    assert O.matrix_shape((4, 5, 6), "DY") == (4, 6)
+    assert O.matrix_shape((4, 5, 6), "DZ") == (5, 6)
+
+
+@pytest.mark.parametrize("shape,op", [((9, 7), "I"), ((7, 9), "DZ"), ((6, 8), "DX"), ((4, 5, 6), "I"),
+                                      ((4, 6, 5), "DY")])
+def test_rank_projection_is_eckart_young(shape, op):
+    """P(A) for {rank <= r} = the truncated SVD (Eckart-Young), per matrix of the view"""
+    r = np.random.default_rng(len(shape) + shape[0])
+    sd = SetDef(op, "rank", k=2)
+    M = O.op_len(shape, sd)
+    w = r.normal(size=M)
+    y = O.project(sd, w, shape=shape)
+    rows, cols = O.matrix_shape(shape, op)
+    for o in range(0, M, rows * cols):
+        a = w[o:o + rows * cols].reshape(rows, cols)
+        np.testing.assert_allclose(y[o:o + rows * cols].reshape(rows, cols), _np_rank(a, 2), atol=1e-12)
+        assert np.linalg.matrix_rank(y[o:o + rows * cols].reshape(rows, cols), tol=1e-9) == 2
+    np.testing.assert_allclose(O.project(sd, y, shape=shape), y, atol=1e-12)        # idempotent
+
+
+def test_nuclear_projection_worked_example_and_numpy():
+    """diag(3, 2, 1) onto {||A||_* <= 3}: theta = 1, singular values (2, 1, 0)
+    (the simplex projection of Table 1's nuclear-norm row); random matrices
+    against numpy's SVD with an independent bisection for theta"""
+    a = np.diag([3.0, 2.0, 1.0])
+    sd = SetDef("I", "nuclear", sigma=3.0)
+    y = O.project(sd, a.ravel(), shape=(3, 3)).reshape(3, 3)
+    np.testing.assert_allclose(y, np.diag([2.0, 1.0, 0.0]), atol=1e-14)
+    r = np.random.default_rng(5)
+    for shape in [(8, 5), (5, 8)]:
+        b = r.normal(size=shape)
+        nuc = np.linalg.svd(b, compute_uv=False).sum()
+        sd = SetDef("I", "nuclear", sigma=0.4 * nuc)
+        y = O.project(sd, b.ravel(), shape=shape).reshape(shape)
+        np.testing.assert_allclose(y, _np_nuclear(b, 0.4 * nuc), atol=1e-10)
+        assert np.linalg.svd(y, compute_uv=False).sum() <= 0.4 * nuc * (1 + 1e-12)
+        inside = SetDef("I", "nuclear", sigma=2 * nuc)
+        np.testing.assert_allclose(O.project(inside, b.ravel(), shape=shape), b.ravel(), atol=1e-15)
+
+
+def test_nuclear_relative_radius():
+    """relative sigma of a nuclear-norm set = frac x the nuclear norm of A m
+    (summed over the matrices of the view), reading L23/L29"""
+    r = np.random.default_rng(9)
+    m = r.normal(size=(6, 5))
+    sig, _, _, _ = O.resolve_set((6, 5), SetDef("I", "nuclear", sigma=0.5, relative=True), m)
+    assert sig == pytest.approx(0.5 * np.linalg.svd(m, compute_uv=False).sum(), rel=1e-13)
+
+
+def test_parsdmm_nuclear_box_vs_dykstra():
+    """box ∩ nuclear-norm ball (both convex, exact projectors): PARSDMM's
+    tightly converged point equals parallel Dykstra's (Algorithm 4)"""
+    shape = (8, 6)
+    r = np.random.default_rng(13)
+    m = r.normal(size=shape) * 2.0
+    nuc = np.linalg.svd(m, compute_uv=False).sum()
+    sig = 0.5 * nuc
+    projs = [lambda z: np.clip(z, -1.5, 1.5), lambda z: _np_nuclear(z, sig)]
+    ref = _dykstra(m, projs)
+    sets = [SetDef("I", "bounds", lo=-1.5, hi=1.5), SetDef("I", "nuclear", sigma=sig)]
+    t = O.parsdmm(shape, sets, m, eps_evol=1e-10, eps_feas=1e-10, n_cg=50, max_iter=50000)
+    assert O.relres(t.x, ref) < 1e-6
