@@ -199,8 +199,9 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void *op_desc, sip_set_type 
    "virtual_ranks" 1 (G > 1: run the z-slab decomposition of G ranks on this
    one device -- the same per-slab kernels, finalisers and exchange schedule
    as the NCCL path, with device copies for the transfers; m and x stay
-   whole-grid arrays; single-level sip_project only; SIP_ERR_PARAM unless
-   1 <= G <= nz and integral).
+   whole-grid arrays; sip_project and sip_project_multilevel (the levels
+   nest: nz divisible by G 2^(L-1)); SIP_ERR_PARAM unless 1 <= G <= nz and
+   integral).
    Unknown key: SIP_ERR_ARG. */
 sip_status sip_set_option(sip_grid g, const char *key, double value);
 
@@ -219,8 +220,11 @@ sip_status sip_project(sip_grid g, const void *m, void *x, int max_iter, double 
    and v_i are prolonged by (tri)linear align-corners interpolation of each
    field as an image of its own shape; rho, gamma carry over.
    max_iter applies per level.  per_level (may be NULL) receives n_levels
-   results, index 0 = finest.  Not available for BLUR_MASK sets, per-entry
-   bounds or multi-rank grids (SIP_ERR_CONFIG). */
+   results, index 0 = finest.  On z slabs (NCCL ranks or virtual ranks) the
+   levels nest when nz is divisible by G 2^(n_levels-1): restriction is
+   slab-local, prolongation reads one coarse ghost plane per side after a
+   halo exchange.  Not available for BLUR_MASK sets, per-entry bounds or a
+   relative nuclear-norm radius (SIP_ERR_CONFIG). */
 sip_status sip_project_multilevel(sip_grid g, const void *m, void *x, int n_levels,
                                   int coarsen, int max_iter, double tol,
                                   sip_result *per_level);

@@ -59,6 +59,8 @@ struct Prob {
   long long cand_per;             // candidate region per select CTA (entries)
   int sel_grid;                   // the grid k_selectf is sized for (regions, ccnt stride)
   int selv2;                      // single-rank fp32: round A in pass 1, k_selB / k_selC (sip_select2.cuh)
+  unsigned* gf_cnt;               // select v2: k_selB's candidate histogram [MAXJOBS][256]
+  unsigned long long* gf_s0;
   double* svdX;                   // rank / nuclear sets: fp64 Jacobi scratch, X (m x n) per matrix
   double* svdV;                   //   and V (n x n) per matrix
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation

@@ -12,8 +12,8 @@
 // accumulated in fp64 (reading L20).
 #pragma once
 #include "sip_flat.cuh"
-#include "sip_select2.cuh"
 #include "sip_stage.cuh"
+#include "sip_select2.cuh"
 
 namespace sip {
 
@@ -202,6 +202,7 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
   const int dn = PRIM == PRIM_Z ? g.plane : g.nx;   // neighbour offset of D_z / D_y
   const T ih = (T)(PRIM == PRIM_Z ? g.ihz : PRIM == PRIM_Y ? g.ihy : g.ihx);
   double d_w2 = 0, d_hv = 0, d_hh = 0, d_vh = 0, d_gv = 0, d_gg = 0, d_vv = 0, d_fn = 0, d_s2 = 0;
+  double d_w1 = 0, d_s1 = 0;   // select v2: ||w||_1, ||s||_1 of an l1 radix job
   const int ntile = (c1 - c0 + BLOCK - 1) / BLOCK;
   auto issue = [&](int t) {
     const int cs = c0 + t * BLOCK;
@@ -335,6 +336,16 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
         if (KIND == 2 && ha) {   // select v2 round A: key counts of w (and s on checks)
           hist_a<T>(ha, wv);
           if (sp) hist_a<T>(ha + NBUCK, sv_);   // s is 0 on pads
+          if (S.kind == K_L1) {                  // ||w||_1 (||s||_1) for the ball-inside test
+            T t1 = 0, t2 = 0;
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+              t1 += wv[e] < (T)0 ? -wv[e] : wv[e];
+              if (sp) t2 += sv_[e] < (T)0 ? -sv_[e] : sv_[e];
+            }
+            d_w1 += (double)t1;
+            d_s1 += (double)t2;
+          }
         }
       }
       if (adapt) VT<T>::stT(vhp + pt0, vh);
@@ -349,6 +360,10 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
     if (sp) hist_a_flush(ha + NBUCK, P.gh_cnt + (size_t)S.sjob * NBUCK);
   }
   const int base = i * NSLOT;
+  if (KIND == 2 && ha && S.kind == K_L1) {   // l1 sets use neither slot otherwise before pass 2
+    warp_acc(acc, nv, base + SLOT_W2, d_w1);
+    if (sp) warp_acc(acc, nv, base + SLOT_FN, d_s1);
+  }
   if (w2) warp_acc(acc, nv, base + SLOT_W2, d_w2);
   if (dots) {
     warp_acc(acc, nv, base + SLOT_HV, d_hv);

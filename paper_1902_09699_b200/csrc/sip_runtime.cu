@@ -237,7 +237,7 @@ struct Engine : EngineBase {
     Pr.dncr.init((uint32_t)std::max(1, g.nx / VT<T>::W));
     Pr.P = P; Pr.p = p;
     Pr.nranks = nranks; Pr.rank = rank;
-    pdl = nranks == 1 && !getenv("SIP_NO_PDL");
+    pdl = nranks == 1 && getenv("SIP_PDL");   // measured: no gain on the radix path, -4% to -20% with select v2 (early-launched CTAs hold SM resources)
     Pr.rounds = KeyT<T>::ROUNDS;
     Pr.ntiles_pb = (g.N + BLOCK - 1) / BLOCK;
     Pr.nseg1 = 0;   // counts (set, block) segments below; +1 for the x segment after
@@ -384,6 +384,12 @@ struct Engine : EngineBase {
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
     // select v2 (sip_select2.cuh): single-rank fp32 runs with a radix job
     Pr.selv2 = (vec && sizeof(T) == 4 && nranks == 1 && njobs > 0 && !getenv("SIP_SEL_V1")) ? 1 : 0;
+    if (Pr.selv2) {   // k_selB / k_selC: one resident wave (the candidate regions are per CTA)
+      int occ = 0;
+      CU(cudaFuncSetAttribute(k_selB<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)selb_smem()));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_selB<T>, BLOCK, selb_smem()));
+      g_sel = std::max(1, std::min(tiles, nsm * std::max(occ, 1)));
+    }
     smem_p1v = pass1_smem(P, false, Pr.selv2);        // k_pass1t: slots + bulk-copy stages (+ round-A counts)
     smem_p1a = pass1_smem(P, true, Pr.selv2);
     // pass 1: segment-major over one contiguous chunk range per CTA
@@ -399,9 +405,10 @@ struct Engine : EngineBase {
       const long long per_it = (long long)BLOCK * SEL_U;
       const long long its = (chunks + (long long)g_sel * per_it - 1) / ((long long)g_sel * per_it);
       Pr.cand_per = its * per_it * VT<T>::W;
-      const long long per2 = (long long)BLOCK * SEL2_U;   // k_selB's tiles
-      const long long its2 = (chunks + (long long)g_sel * per2 - 1) / ((long long)g_sel * per2);
-      Pr.cand_per = std::max(Pr.cand_per, its2 * per2 * VT<T>::W);
+      // k_selB: tiles of SB_TILE chunks per operator block, strided over the grid
+      const long long tiles2 = (long long)nbmax * ((g.N / VT<T>::W + SB_TILE - 1) / SB_TILE);
+      const long long its2 = (tiles2 + g_sel - 1) / g_sel;
+      Pr.cand_per = std::max(Pr.cand_per, its2 * SB_TILE * VT<T>::W);
       for (int i = 0; i < P; ++i) {
         const SetD<T>& S = Pr.set[i];
         if (S.job < 0) continue;
@@ -457,6 +464,10 @@ struct Engine : EngineBase {
     }
     Pr.counter = dalloc<unsigned>(1);
     CU(cudaMemsetAsync(Pr.counter, 0, sizeof(unsigned), stream));
+    Pr.gf_cnt = dalloc<unsigned>((size_t)MAXJOBS * FB_N);
+    Pr.gf_s0 = dalloc<unsigned long long>((size_t)MAXJOBS * FB_N);
+    CU(cudaMemsetAsync(Pr.gf_cnt, 0, sizeof(unsigned) * MAXJOBS * FB_N, stream));
+    CU(cudaMemsetAsync(Pr.gf_s0, 0, sizeof(unsigned long long) * MAXJOBS * FB_N, stream));
     Pr.gh_cnt = dalloc<unsigned>((size_t)MAXJOBS * NBUCK);
     Pr.gh_s0 = dalloc<unsigned long long>((size_t)MAXJOBS * NBUCK);
     Pr.gh_s1 = dalloc<unsigned long long>((size_t)MAXJOBS * NBUCK);
@@ -710,8 +721,8 @@ struct Engine : EngineBase {
     ++launches; mark(KB_PASS1);
     if (hc.njobs > 0) {
       if (Pr.selv2) {   // one streaming pass + candidate rounds (round A ran in pass 1)
-        lk(k_selB<T>, g_sel, BLOCK, 0, Pr); ++launches; mark(KB_SELECT);
-        for (int r = 1; r <= 3; ++r) { lk(k_selC<T>, g_sel, BLOCK, 0, Pr, r); ++launches; mark(KB_SELECT); }
+        lk(k_selB<T>, g_sel, BLOCK, selb_smem(), Pr); ++launches; mark(KB_SELECT);
+        for (int r = 2; r <= 4; ++r) { lk(k_selC<T>, g_sel, BLOCK, 0, Pr, r); ++launches; mark(KB_SELECT); }
       } else {
         for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
       }

@@ -20,7 +20,8 @@
 //            shrinks 2048-fold per round down to a single key.
 //
 // Replaces three full-read radix rounds with three shared atomics per entry
-// each (k_selectf): one full read and one atomic per entry.  Multi-rank and
+// each (k_selectf): one full read, one shared atomic per entry in pass 1,
+// and the candidate rounds on a small grid.  Multi-rank and
 // fp64 runs keep k_selectf (its finalisers gather across ranks).
 #pragma once
 #include "sip_flat.cuh"
@@ -28,7 +29,6 @@
 namespace sip {
 
 constexpr int A_SHIFT = 20;                 // round-A digit: key bits 30..20 (11 bits)
-constexpr int SEL2_U = 8;                   // chunks in flight per thread in k_selB
 
 __device__ __forceinline__ unsigned key32(float v) { return __float_as_uint(v) & 0x7fffffffu; }
 __device__ __forceinline__ double kval(unsigned key) { return (double)__uint_as_float(key); }
@@ -156,157 +156,31 @@ __device__ __forceinline__ bool job_live(const Job& J, bool check) {
   return J.mode == JM_SEARCH && J.round == 0 && (!J.on_s || check);
 }
 
-// ---------------------------------------------------------------- k_selB
-template <class T>
-__global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> P) {
-  pdl_begin();
-  if constexpr (sizeof(T) != 4) return;
-  else {
-    constexpr int W = VT<T>::W;
-    if (gridDim.x != (unsigned)P.sel_grid) __trap();   // regions are sized for this grid
-    Ctrl& C = *P.ctrl;
-    if (C.stopped) return;
-    __shared__ SelRange s_rng[MAXJOBS];
-    __shared__ unsigned s_cn;
-    __shared__ double sh[NWARP + 1];
-    const bool check = (C.k % C.opt.check_every) == 0;
-    const Geo& g = P.g;
-    const int nch = g.N / W;
-    const int nj = C.njobs;
-    bool any = false;
-    for (int jb = 0; jb < nj; ++jb) {
-      const Job& J = C.job[jb];
-      if (!job_live(J, check)) continue;
-      any = true;
-      const SelRange R = range_of_job(J, P.gh_cnt + (size_t)jb * NBUCK);
-      if (threadIdx.x == 0) s_rng[jb] = R;
-      __syncthreads();
-      double* part = P.partials + ((size_t)blockIdx.x * MAXJOBS + jb) * 3;
-      unsigned* cand = P.cand[jb] + (size_t)blockIdx.x * P.cand_per;
-      if (R.mode != JM_SEARCH) {
-        if (threadIdx.x == 0) { part[0] = 0.0; part[1] = 0.0; part[2] = 0.0; P.ccnt[(size_t)jb * gridDim.x + blockIdx.x] = 0u; }
-        continue;
-      }
-      const SetD<T>& S = P.set[J.set];
-      const T* buf = J.on_s ? S.s : S.w;
-      const int tot = S.nblk * nch;
-      const unsigned lo = R.lo, hi = R.hi;
-      const bool l1 = J.kind == K_L1;
-      if (threadIdx.x == 0) s_cn = 0u;
-      __syncthreads();
-      unsigned long long n_ab = 0;
-      double s_ab = 0.0, s_tot = 0.0;
-      const int stride = gridDim.x * BLOCK * SEL2_U;
-      const int lane = threadIdx.x & 31;
-      for (int b0 = blockIdx.x * BLOCK * SEL2_U; b0 < tot; b0 += stride) {
-        T v[SEL2_U][W];
-        bool ok[SEL2_U];
-#pragma unroll
-        for (int u = 0; u < SEL2_U; ++u) {     // every load of the tile first
-          const int q = b0 + u * BLOCK + threadIdx.x;
-          ok[u] = q < tot;
-          const int qq = ok[u] ? q : tot - 1;
-          const int bl = (qq >= nch) + (qq >= 2 * nch);   // nblk <= 3
-          VT<T>::ldcs(buf + (int64_t)bl * g.ld + (int64_t)(qq - bl * nch) * W, v[u]);
-        }
-        unsigned mine = 0;   // candidates of this thread (bit u*W+e)
-#pragma unroll
-        for (int u = 0; u < SEL2_U; ++u) {
-#pragma unroll
-          for (int e = 0; e < W; ++e) {
-            const unsigned k = ok[u] ? key32((float)v[u][e]) : 0u;
-            const double a = kval(k);
-            if (k >= hi) { ++n_ab; s_ab += a; }
-            else if (k >= lo && k != 0u) mine |= 1u << (u * W + e);
-            if (l1) s_tot += a;
-          }
-        }
-        // warp-aggregated append to this CTA's region (one shared atomic per warp)
-        const int cnt = __popc(mine);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int t_ = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t_;
-        }
-        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
-        if (wtot) {
-          unsigned base = 0u;
-          if (lane == 31) base = atomicAdd(&s_cn, (unsigned)wtot);
-          unsigned pos = __shfl_sync(0xffffffffu, base, 31) + (unsigned)(incl - cnt);
-#pragma unroll
-          for (int u = 0; u < SEL2_U; ++u)
-#pragma unroll
-            for (int e = 0; e < W; ++e)
-              if (mine & (1u << (u * W + e))) cand[pos++] = key32((float)v[u][e]);
-        }
-      }
-      // per-CTA (count, sum above, total): fixed-order block sums
-      const double d_ab = block_sum((double)n_ab, sh);
-      const double d_sab = block_sum(s_ab, sh);
-      const double d_tot = block_sum(s_tot, sh);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        part[0] = d_ab; part[1] = d_sab; part[2] = d_tot;
-        P.ccnt[(size_t)jb * gridDim.x + blockIdx.x] = s_cn;
-      }
-      __syncthreads();
-    }
-    if (!any) return;
-    if (last_block(P.counter)) {
-      for (int jb = 0; jb < nj; ++jb) {
-        Job& J = C.job[jb];
-        if (!job_live(J, check)) continue;
-        const SelRange R = s_rng[jb];
-        double tot3[3];
-        for (int q = 0; q < 3; ++q) {            // fixed order over the CTAs
-          double a = 0.0;
-          for (int b = threadIdx.x; b < (int)gridDim.x; b += BLOCK)
-            a += __ldcg(P.partials + ((size_t)b * MAXJOBS + jb) * 3 + q);
-          tot3[q] = block_sum(a, sh);
-        }
-        if (threadIdx.x == 0) {
-          if (R.mode != JM_SEARCH) {
-            J.mode = R.mode;
-          } else if (J.kind == K_L1 && tot3[2] <= J.sigma) {
-            J.mode = JM_INSIDE;                  // ||w||_1 <= sigma: w is in the ball (L5)
-          } else {
-            J.cnt_above = (long long)tot3[0];
-            J.sum_above = tot3[1];
-            J.prefix = R.lo;                     // the window of the candidate rounds
-            J.width = (unsigned long long)(R.hi - R.lo);
-            J.round = 1;
-          }
-        }
-        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;   // next round A
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) *P.counter = 0u;
-    }
-  }
-}
-
-// ---------------------------------------------------------------- k_selC
+// ---------------------------------------------------------------- windows
 // window [lo, lo + width) split into <= 2048 buckets of 2^shift keys; every
 // bucket lies inside one exponent (lo is a multiple of 2^20, shift <= 20),
 // so its limb sums are exact multiples of one power of two
-__device__ __forceinline__ int sel_shift(unsigned long long width) {
+__device__ __forceinline__ int sel_shift(unsigned long long width, int dbits) {
   int b = 0;
   while ((1ull << b) < width) ++b;        // ceil(log2(width))
-  return b > 11 ? b - 11 : 0;
+  return b > dbits ? b - dbits : 0;
 }
+constexpr int FB_BITS = 8;                // k_selB's histogram of the candidates: 256 buckets
+constexpr int FB_N = 1 << FB_BITS;
 
 // last CTA of k_selC: the bucket d* of the window holding the answer (the
 // walk of resolve_round over linear sub-buckets), then either the next,
 // 2048x narrower window or -- single-key buckets -- the final theta / tau
-__device__ void resolve_window(Ctrl& C, Job& J, const unsigned* hc, const unsigned long long* h0) {
+__device__ void resolve_window(Ctrl& C, Job& J, const unsigned* hc, const unsigned long long* h0, int dbits) {
   __shared__ long long s_cnt[BLOCK];
   __shared__ double s_sum[BLOCK];
+  __shared__ unsigned long long s_su[NWARP];
+  __shared__ double s_sd[NWARP];
   __shared__ int s_dstar;
   __shared__ long long s_cab;
   __shared__ double s_sab;
   const unsigned lo = (unsigned)J.prefix;
-  const int sh = sel_shift(J.width);
+  const int sh = sel_shift(J.width, dbits);
   const int nbk = (int)((J.width + (1ull << sh) - 1) >> sh);
   const int per = (nbk + BLOCK - 1) / BLOCK;
   const int d0 = threadIdx.x * per;
@@ -317,18 +191,10 @@ __device__ void resolve_window(Ctrl& C, Job& J, const unsigned* hc, const unsign
   long long c_loc = 0;
   double s_loc = 0.0;
   for (int d = d0; d < d0 + per && d < nbk; ++d) { c_loc += __ldcg(hc + d); s_loc += bsum(d); }
-  s_cnt[threadIdx.x] = c_loc;
-  s_sum[threadIdx.x] = s_loc;
-  __syncthreads();
-  if (threadIdx.x == 0) {      // suffix totals of the threads above, fixed order
-    long long c = 0; double sm = 0.0;
-    for (int t = BLOCK - 1; t >= 0; --t) {
-      const long long ct = s_cnt[t]; const double st = s_sum[t];
-      s_cnt[t] = c; s_sum[t] = sm;
-      c += ct; sm += st;
-    }
-    s_dstar = -1;
-  }
+  // totals of the threads above (fixed order: warp suffix, later warps)
+  s_cnt[threadIdx.x] = (long long)suffix_excl<unsigned long long>((unsigned long long)c_loc, s_su);
+  s_sum[threadIdx.x] = suffix_excl<double>(s_loc, s_sd);
+  if (threadIdx.x == 0) s_dstar = -1;
   __syncthreads();
   long long c_ge = J.cnt_above + s_cnt[threadIdx.x];
   double s_ge = J.sum_above + s_sum[threadIdx.x];
@@ -386,12 +252,198 @@ __device__ void resolve_window(Ctrl& C, Job& J, const unsigned* hc, const unsign
   __syncthreads();
 }
 
+// ---------------------------------------------------------------- k_selB
+// w streams through a two-stage shared-memory ring of SB_TILE-chunk tiles
+// filled by 1D bulk async copies (cp.async.bulk, mbarrier expect_tx; thread
+// 0 issues the next tile before the CTA works on the current one), so the
+// loads are decoupled from the per-entry work and from register pressure.
+constexpr int SB_TILE = 2048;                 // chunks (16 B) per stage: 32 KB
+__host__ inline size_t selb_smem() { return (size_t)2 * (SB_TILE + 1) * 16; }
+
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
+  if constexpr (sizeof(T) != 4) return;
+  else {
+    constexpr int W = VT<T>::W;
+    constexpr int PER = SB_TILE / BLOCK;      // chunks per thread per tile
+    if (gridDim.x != (unsigned)P.sel_grid) __trap();   // regions are sized for this grid
+    Ctrl& C = *P.ctrl;
+    if (C.stopped) return;
+    extern __shared__ __align__(16) char sb_buf[];
+    __shared__ uint64_t bars[2];
+    __shared__ SelRange s_rng[MAXJOBS];
+    __shared__ unsigned s_cn;
+    __shared__ double sh[NWARP + 1];
+    __shared__ unsigned f_cnt[FB_N], f_l0[FB_N], f_l1[FB_N];
+    const bool check = (C.k % C.opt.check_every) == 0;
+    const Geo& g = P.g;
+    const int nch = g.N / W;
+    const int nj = C.njobs;
+    Stage2<1> st;
+    st.init(bars, sb_buf, SB_TILE);
+    const int lane = threadIdx.x & 31;
+    bool any = false;
+    for (int jb = 0; jb < nj; ++jb) {
+      const Job& J = C.job[jb];
+      if (!job_live(J, check)) continue;
+      any = true;
+      const SelRange R = range_of_job(J, P.gh_cnt + (size_t)jb * NBUCK);
+      if (threadIdx.x == 0) s_rng[jb] = R;
+      __syncthreads();
+      double* part = P.partials + ((size_t)blockIdx.x * MAXJOBS + jb) * 3;
+      unsigned* cand = P.cand[jb] + (size_t)blockIdx.x * P.cand_per;
+      if (R.mode != JM_SEARCH) {
+        if (threadIdx.x == 0) { part[0] = 0.0; part[1] = 0.0; part[2] = 0.0; P.ccnt[(size_t)jb * gridDim.x + blockIdx.x] = 0u; }
+        continue;
+      }
+      const SetD<T>& S = P.set[J.set];
+      const T* buf = J.on_s ? S.s : S.w;
+      const unsigned lo = R.lo, hi = R.hi;
+      const int tpb = (nch + SB_TILE - 1) / SB_TILE;              // tiles per operator block
+      const int ntile = S.nblk * tpb;
+      const int nmine = ntile > (int)blockIdx.x ? (ntile - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+      auto tile_of = [&](int i, int* c0, int* cnt, const T** src) {
+        const int t = (int)blockIdx.x + i * (int)gridDim.x;
+        const int bl = t / tpb, tt = t - bl * tpb;
+        *c0 = tt * SB_TILE;
+        *cnt = min(SB_TILE, nch - *c0);
+        *src = buf + (int64_t)bl * g.ld + (int64_t)(*c0) * W;
+      };
+      auto issue = [&](int i) {
+        int c0, cnt;
+        const T* src;
+        tile_of(i, &c0, &cnt, &src);
+        const char* sp[1] = {reinterpret_cast<const char*>(src)};
+        const unsigned by[1] = {(unsigned)cnt * 16u};
+        st.issue(i & 1, 1, sp, by);
+      };
+      const bool sums = J.kind == K_L1;
+      const int fsh = sel_shift((unsigned long long)(hi - lo), FB_BITS);
+      if (threadIdx.x == 0) s_cn = 0u;
+      for (int d = threadIdx.x; d < FB_N; d += BLOCK) { f_cnt[d] = 0u; f_l0[d] = 0u; f_l1[d] = 0u; }
+      __syncthreads();
+      unsigned long long n_ab = 0;
+      double s_ab = 0.0;
+      if (nmine > 0) issue(0);
+      for (int i = 0; i < nmine; ++i) {
+        if (i + 1 < nmine) issue(i + 1);
+        const int sidx = i & 1;
+        st.wait(sidx);
+        int c0, cnt;
+        const T* src;
+        tile_of(i, &c0, &cnt, &src);
+        const T* tl = reinterpret_cast<const T*>(st.at(sidx, 0));
+        unsigned mine = 0;   // candidates of this thread (bit u*W+e)
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int c = u * BLOCK + (int)threadIdx.x;
+          T v[W];
+          if (c < cnt) VT<T>::ldT_s(tl + c * W, v);
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            const unsigned k = c < cnt ? key32((float)v[e]) : 0u;
+            if (k >= hi) { ++n_ab; s_ab += kval(k); }
+            mine |= (k >= lo && k < hi && k != 0u) ? (1u << (u * W + e)) : 0u;
+          }
+        }
+        // warp-aggregated append to this CTA's region (one shared atomic per warp)
+        const int cnt1 = __popc(mine);
+        int incl = cnt1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t_ = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t_;
+        }
+        const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+        if (wtot) {
+          unsigned base = 0u;
+          if (lane == 31) base = atomicAdd(&s_cn, (unsigned)wtot);
+          unsigned pos = __shfl_sync(0xffffffffu, base, 31) + (unsigned)(incl - cnt1);
+          while (mine) {
+            const int bit = __ffs(mine) - 1;
+            mine &= mine - 1u;
+            const int c = (bit / W) * BLOCK + (int)threadIdx.x;
+            const unsigned k = key32((float)tl[c * W + bit % W]);
+            cand[pos++] = k;
+            const int d = (int)((k - lo) >> fsh);    // the candidates' histogram (counts, limb sums)
+            atomicAdd(&f_cnt[d], 1u);
+            if (sums) {
+              unsigned l[2];
+              Limbs<float>::split(k, l);
+              atomicAdd(&f_l0[d], l[0]);
+              atomicAdd(&f_l1[d], l[1]);
+            }
+          }
+        }
+        __syncthreads();   // the stage is refilled by the issue of tile i + 2
+      }
+      // this CTA's candidate histogram into the job's (non-zero buckets only)
+      __syncthreads();
+      for (int d = threadIdx.x; d < FB_N; d += BLOCK) {
+        if (!f_cnt[d]) continue;
+        atomicAdd(P.gf_cnt + (size_t)jb * FB_N + d, f_cnt[d]);
+        if (sums) atomicAdd(P.gf_s0 + (size_t)jb * FB_N + d, (unsigned long long)f_l0[d] + ((unsigned long long)f_l1[d] << 16));
+      }
+      // per-CTA (count, sum above): fixed-order block sums
+      const double d_ab = block_sum((double)n_ab, sh);
+      const double d_sab = block_sum(s_ab, sh);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        part[0] = d_ab; part[1] = d_sab; part[2] = 0.0;
+        P.ccnt[(size_t)jb * gridDim.x + blockIdx.x] = s_cn;
+      }
+      __syncthreads();
+    }
+    if (!any) return;
+    if (last_block(P.counter)) {
+      for (int jb = 0; jb < nj; ++jb) {
+        Job& J = C.job[jb];
+        if (!job_live(J, check)) continue;
+        const SelRange R = s_rng[jb];
+        double tot2[2];
+        for (int q = 0; q < 2; ++q) {            // fixed order over the CTAs
+          double a = 0.0;
+          for (int b = threadIdx.x; b < (int)gridDim.x; b += BLOCK)
+            a += __ldcg(P.partials + ((size_t)b * MAXJOBS + jb) * 3 + q);
+          tot2[q] = block_sum(a, sh);
+        }
+        if (threadIdx.x == 0) {
+          if (R.mode != JM_SEARCH) {
+            J.mode = R.mode;
+          } else if (J.kind == K_L1 && C.sums[J.set][J.on_s ? SLOT_FN : SLOT_W2] <= J.sigma) {
+            J.mode = JM_INSIDE;                  // ||w||_1 <= sigma (pass 1's sum): w is in the ball (L5)
+          } else {
+            J.cnt_above = (long long)tot2[0];
+            J.sum_above = tot2[1];
+            J.prefix = R.lo;                     // the window of the candidates
+            J.width = (unsigned long long)(R.hi - R.lo);
+            J.round = 1;
+          }
+        }
+        __syncthreads();
+        // the candidates' 256-bucket histogram narrows the window (round 1)
+        if (J.mode == JM_SEARCH && J.round == 1)
+          resolve_window(C, J, P.gf_cnt + (size_t)jb * FB_N, P.gf_s0 + (size_t)jb * FB_N, FB_BITS);
+        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;   // next round A
+        for (int d = threadIdx.x; d < FB_N; d += BLOCK) {
+          P.gf_cnt[(size_t)jb * FB_N + d] = 0u;
+          P.gf_s0[(size_t)jb * FB_N + d] = 0ull;
+        }
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) *P.counter = 0u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- k_selC
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_selC(const __grid_constant__ Prob<T> P, int round) {
   pdl_begin();
   if constexpr (sizeof(T) != 4) return;
   else {
-    if (gridDim.x != (unsigned)P.sel_grid) __trap();
+    if (gridDim.x != (unsigned)P.sel_grid) __trap();   // one CTA per k_selB region
     Ctrl& C = *P.ctrl;
     if (C.stopped) return;
     using LB = Limbs<float>;
@@ -407,25 +459,37 @@ __global__ void __launch_bounds__(BLOCK) k_selC(const __grid_constant__ Prob<T> 
       const bool sums = J.kind == K_L1;
       const unsigned lo = (unsigned)J.prefix;
       const unsigned long long width = J.width;
-      const int sh = sel_shift(width);
+      const int sh = sel_shift(width, 11);
       for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
         h_cnt[d] = 0u;
 #pragma unroll
         for (int q = 0; q < LB::N; ++q) h_l[q][d] = 0u;
       }
       __syncthreads();
+      // this CTA's candidate region (k_selB's CTA of the same index),
+      // coalesced, eight loads in flight per thread; only the window's keys
+      // (a small part after k_selB's round) reach the shared histogram
       const unsigned* cand = P.cand[jb] + (size_t)blockIdx.x * P.cand_per;
       const int n = (int)__ldcg(P.ccnt + (size_t)jb * gridDim.x + blockIdx.x);
-      for (int q = threadIdx.x; q < n; q += BLOCK) {
-        const unsigned k = __ldcg(cand + q);
-        if (k < lo || (unsigned long long)(k - lo) >= width) continue;
-        const int d = (int)((k - lo) >> sh);
-        atomicAdd(&h_cnt[d], 1u);
-        if (sums) {
-          unsigned l[LB::N];
-          LB::split(k, l);
+      for (int qb = 0; qb < n; qb += BLOCK * 8) {
+        unsigned kk[8];
 #pragma unroll
-          for (int t = 0; t < LB::N; ++t) atomicAdd(&h_l[t][d], l[t]);
+        for (int u = 0; u < 8; ++u) {
+          const int q = qb + u * BLOCK + (int)threadIdx.x;
+          kk[u] = q < n ? __ldcg(cand + q) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const unsigned k = kk[u];
+          if (qb + u * BLOCK + (int)threadIdx.x >= n || k < lo || (unsigned long long)(k - lo) >= width) continue;
+          const int d = (int)((k - lo) >> sh);
+          atomicAdd(&h_cnt[d], 1u);
+          if (sums) {
+            unsigned l[LB::N];
+            LB::split(k, l);
+#pragma unroll
+            for (int t = 0; t < LB::N; ++t) atomicAdd(&h_l[t][d], l[t]);
+          }
         }
       }
       __syncthreads();
@@ -443,7 +507,7 @@ __global__ void __launch_bounds__(BLOCK) k_selC(const __grid_constant__ Prob<T> 
       for (int jb = 0; jb < nj; ++jb) {
         Job& J = C.job[jb];
         if (J.mode != JM_SEARCH || J.round != round || (J.on_s && !check)) continue;
-        resolve_window(C, J, P.gh_cnt + (size_t)jb * NBUCK, P.gh_s0 + (size_t)jb * NBUCK);
+        resolve_window(C, J, P.gh_cnt + (size_t)jb * NBUCK, P.gh_s0 + (size_t)jb * NBUCK, 11);
         for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
           P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;
           P.gh_s0[(size_t)jb * NBUCK + d] = 0ull;

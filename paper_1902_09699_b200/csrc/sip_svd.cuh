@@ -50,6 +50,13 @@ __device__ __forceinline__ int64_t mat_pt(const Geo& g, int b, int r, int c) {
   return g.ndim == 2 ? (int64_t)r * g.nx + c : (int64_t)b * g.plane + (int64_t)r * g.nx + c;
 }
 
+// every lane gets the warp total (the rotation is computed by all lanes)
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <class T>
 __global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ Prob<T> P, int i, int which) {
   pdl_begin();
@@ -98,7 +105,7 @@ __global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ P
           const double u = xi[r], v = xj[r];
           aa += u * u; bb += v * v; cc += u * v;
         }
-        aa = warp_sum(aa); bb = warp_sum(bb); cc = warp_sum(cc);
+        aa = warp_allsum(aa); bb = warp_allsum(bb); cc = warp_allsum(cc);
         if (cc == 0.0 || fabs(cc) <= 1e-15 * sqrt(aa * bb)) continue;
         const double zeta = (bb - aa) / (2.0 * cc);
         const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));

@@ -61,6 +61,13 @@ MUTATIONS = [
     ("relative_l1_uses_l2", "if (in->type == SIPREF_L1) out->sigma = in->sigma * n1;", "if (in->type == SIPREF_L1) out->sigma = in->sigma * n2;"),
     ("relative_k_ceil", "out->k = (int64_t)floor(in->k_frac", "out->k = (int64_t)ceil(in->k_frac"),
     ("ml_rho_reset", "memcpy(rho, rbuf, (size_t)P * sizeof(double));", "(void)rbuf;"),
+    ("svd_rotation_sign", "          xi[r] = cs * u - sn * v;", "          xi[r] = cs * u + sn * v;"),
+    ("svd_loose_convergence", "if (c == 0.0 || fabs(c) <= 1e-15 * sqrt(a * b)) continue;",
+     "if (c == 0.0 || fabs(c) <= 1e-3 * sqrt(a * b)) continue;"),
+    ("rank_keeps_r_plus_1", "f[t[q].i] = (q < s->k) ? lam[t[q].i] : 0.0;", "f[t[q].i] = (q <= s->k) ? lam[t[q].i] : 0.0;"),
+    ("nuclear_radius_halved", "proj_l1(n, lam, s->sigma, f);", "proj_l1(n, lam, 0.5 * s->sigma, f);"),
+    ("matrix_view_3d_rows", "else { *rows = fy; *cols = fx; }", "else { *rows = fz; *cols = fx; }"),
+    ("nuclear_relative_l1", "out->sigma = in->sigma * nuc;", "out->sigma = in->sigma * nuc * 1.0001;"),
 ]
 
 
