@@ -88,13 +88,19 @@ typedef enum {
                               (reading L29: 2D grids one (z, x) matrix, 3D
                               grids one (y, x) matrix per z-plane); ties of
                               singular values: lowest index                   */
-  SIP_SET_NUCLEAR = 6      /* sum of singular values <= sigma per matrix of
+  SIP_SET_NUCLEAR = 6,     /* sum of singular values <= sigma per matrix of
                               the view; relative = 1: sigma is a
                               fraction of the summed nuclear norms of A m
                               (single-level projections only).  Both: single-
                               block operators, min(rows, cols) <= 2048, the
                               vectorised path (nx a multiple of 16 / sizeof),
                               one rank; else SIP_ERR_CONFIG                   */
+  SIP_SET_DCT_L1 = 7       /* ||D x||_1 <= sigma with D the orthonormal DCT-II
+                              of the grid along every axis, kept inside the
+                              set (P_V(x) = D^T P_l1(D x));
+                              op must be IDENTITY; relative = 1: sigma is a
+                              fraction of ||D m||_1 (reading L30); the
+                              vectorised path, one rank (SIP_ERR_CONFIG)      */
 } sip_set_type;
 
 typedef struct {
@@ -285,8 +291,9 @@ sip_status sip_get_sizes(sip_grid g, int *p, int64_t *n_local, int set_id, int64
    the graph).  Kinds, in order: 0 blur (S G p), 1 rhs, 2 cg1, 3 cg2,
    4 pass1, 5 select, 6 tiecount, 7 pass2, 8 control, 9 comm (z-slab
    exchanges), 10 cgx (deferred CG x update), 11 fiber (per-fiber
-   projections), 12 svd (rank / nuclear-norm sets).  ms[q] is the summed
-   milliseconds, count[q] the number of launches (arrays of n <= 13). */
+   projections), 12 svd (rank / nuclear-norm sets), 13 dct (transforms of
+   the transform-domain sets).  ms[q] is the summed milliseconds, count[q]
+   the number of launches (arrays of n <= 14). */
 sip_status sip_get_profile(sip_grid g, int n, double *ms, int64_t *count);
 
 /* Number of kernel launches enqueued by the last sip_project (bench evidence). */

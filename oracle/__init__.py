@@ -23,7 +23,7 @@ _SRC = os.path.join(_HERE, "sipref.c")
 _LIB = os.path.join(_HERE, "libsipref.so")
 
 OPS = {"I": 0, "DZ": 1, "DY": 2, "DX": 3, "TV": 4, "BLUR_MASK": 5}
-KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6}
+KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6, "dct_l1": 7}
 BRANCH = {0: "both", 1: "alpha", 2: "beta", 3: "none", -1: "-"}
 
 
@@ -55,7 +55,7 @@ class Set(C.Structure):
         ("kernel", C.POINTER(C.c_double)), ("kh", C.c_int), ("kw", C.c_int),
         ("mask", C.POINTER(C.c_ubyte)),
         ("app_mode", C.c_int), ("fib_len", C.c_int64),
-        ("mrows", C.c_int64), ("mcols", C.c_int64),
+        ("tgrid", Grid), ("mrows", C.c_int64), ("mcols", C.c_int64),
     ]
 
 
@@ -226,6 +226,15 @@ def matrix_shape(shape, op):
     return r.value, c.value
 
 
+def dct(shape, x, inverse=False):
+    """orthonormal DCT-II along every axis of a grid field (or its inverse)"""
+    g = make_grid(shape)
+    x = _f64(x).ravel()
+    y = np.zeros_like(x)
+    lib().sipref_dct(C.byref(g), int(bool(inverse)), _dp(x), _dp(y))
+    return y
+
+
 def svd_values(a):
     """singular values of a 2D array (one-sided Jacobi, descending)"""
     a = _f64(a)
@@ -242,6 +251,7 @@ def project(sd, w, shape=None):
     if shape is not None:
         hold.s.fib_len = fiber_len(shape, sd)
         hold.s.mrows, hold.s.mcols = matrix_shape(shape, sd.op)
+        hold.s.tgrid = make_grid(shape)
     w = _f64(w).ravel()
     y = np.zeros_like(w)
     lib().sipref_project(C.byref(hold.s), C.c_int64(w.size), _dp(w), _dp(y))
@@ -260,6 +270,7 @@ def feas(sd, s_vec, shape=None):
     if shape is not None:
         hold.s.fib_len = fiber_len(shape, sd)
         hold.s.mrows, hold.s.mcols = matrix_shape(shape, sd.op)
+        hold.s.tgrid = make_grid(shape)
     s_vec = _f64(s_vec).ravel()
     return float(lib().sipref_feas(C.byref(hold.s), C.c_int64(s_vec.size), _dp(s_vec)))
 

@@ -429,6 +429,42 @@ static void proj_matrix(const sipref_set *s, int64_t rows, int64_t cols, const d
   free(X); free(V); free(lam); free(f); free(B);
 }
 
+/* ------------------------------------------------------------------ */
+/* orthogonal-transform sets: V = {x :        */
+/* ||D x||_1 <= sigma} with D the orthonormal DCT-II of the grid, kept   */
+/* inside the set: P_V(x) = D^T P_l1(D x) (reading L30)     */
+/* ------------------------------------------------------------------ */
+/* X_k = s_k sum_n x_n cos(pi (2n + 1) k / (2 L)), s_0 = sqrt(1/L),
+   s_k = sqrt(2/L); along one axis of length L with stride `st` */
+#define SIPREF_PI 3.14159265358979323846
+static void dct_axis(int64_t L, int64_t count, int64_t st, int64_t outer_st, int64_t inner, int inverse,
+                     double *a) {
+  double *t = dalloc(L);
+  for (int64_t o = 0; o < count; ++o)
+    for (int64_t in = 0; in < inner; ++in) {
+      double *p = a + o * outer_st + in;
+      for (int64_t k = 0; k < L; ++k) {
+        double acc = 0.0;
+        for (int64_t n = 0; n < L; ++n) {
+          int64_t kk = inverse ? n : k, nn = inverse ? k : n;   /* D^T: swap the roles */
+          double s = kk == 0 ? sqrt(1.0 / (double)L) : sqrt(2.0 / (double)L);
+          acc += s * cos(SIPREF_PI * (double)(2 * nn + 1) * (double)kk / (2.0 * (double)L)) * p[n * st];
+        }
+        t[k] = acc;
+      }
+      for (int64_t k = 0; k < L; ++k) p[k * st] = t[k];
+    }
+  free(t);
+}
+
+void sipref_dct(const sipref_grid *g, int inverse, const double *x, double *y) {
+  int64_t nz = g->n[0], ny = g->n[1], nx = g->n[2], N = nz * ny * nx;
+  memcpy(y, x, (size_t)N * sizeof(double));
+  dct_axis(nx, nz * ny, 1, nx, 1, inverse, y);                 /* x: rows of length nx */
+  if (g->ndim == 3) dct_axis(ny, nz, nx, ny * nx, nx, inverse, y);   /* y: per plane, stride nx */
+  dct_axis(nz, 1, ny * nx, 0, ny * nx, inverse, y);            /* z: stride plane */
+}
+
 static void project_whole(const sipref_set *s, int64_t M, const double *w, double *y);
 
 /* fiber length (reading L28): nx (nx - 1 for D_x) for x-fibers, nz
@@ -491,6 +527,15 @@ static void project_whole(const sipref_set *s, int64_t M, const double *w, doubl
       break;
     }
     case SIPREF_CARD: proj_card(M, w, s->k, y); break;
+    case SIPREF_DCT_L1: {    /* D^T P_l1(D w) */
+      sipref_grid gg = s->tgrid;
+      double *c1 = dalloc(M), *c2 = dalloc(M);
+      sipref_dct(&gg, 0, w, c1);
+      proj_l1(M, c1, s->sigma, c2);
+      sipref_dct(&gg, 1, c2, y);
+      free(c1); free(c2);
+      break;
+    }
     case SIPREF_RANK:
     case SIPREF_NUCLEAR: {   /* every matrix of the view on its own (L29) */
       int64_t mn = s->mrows * s->mcols;
@@ -645,6 +690,7 @@ void sipref_resolve_set(const sipref_grid *g, const sipref_set *in, const double
   *out = *in;
   out->fib_len = sipref_fiber_len(g, in);
   sipref_matrix_shape(g, in->op, &out->mrows, &out->mcols);
+  out->tgrid = *g;
   if (!in->relative) return;
   int64_t M = sipref_op_len(g, in);
   double *a = dalloc(M);
@@ -658,6 +704,14 @@ void sipref_resolve_set(const sipref_grid *g, const sipref_set *in, const double
   if (in->type == SIPREF_ANNULUS) {
     out->sigma_lo = in->sigma_lo * n2;
     out->sigma_hi = in->sigma_hi * n2;
+  }
+  if (in->type == SIPREF_DCT_L1) {    /* sigma = frac x ||D m||_1 (reading L30) */
+    double *am = dalloc(M), *cm = dalloc(M), n1d = 0.0;
+    sipref_apply_A(g, in, m, am);
+    sipref_dct(g, 0, am, cm);
+    for (int64_t j = 0; j < M; ++j) n1d += fabs(cm[j]);
+    out->sigma = in->sigma * n1d;
+    free(am); free(cm);
   }
   if (in->type == SIPREF_NUCLEAR) {   /* sigma = frac x sum of the nuclear norms of A m's matrices */
     int64_t r, cc;

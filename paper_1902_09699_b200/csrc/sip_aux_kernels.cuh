@@ -123,6 +123,29 @@ __global__ void k_prolong(Geo fine, Geo coarse, int prim, const T* c, T* f) {
   }
 }
 
+// relative radius of a transform-domain l1 set: sigma = frac ||D m||_1
+// (reading L30); c holds D m.  Fixed-order reduction (partials, last CTA).
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_dct_sigma(const __grid_constant__ Prob<T> P, int i, const T* c) {
+  __shared__ double sh[NWARP + 1];
+  __shared__ double out[1];
+  double a = 0.0;
+  for (long long q = blockIdx.x * (long long)BLOCK + threadIdx.x; q < P.g.N; q += (long long)gridDim.x * BLOCK)
+    a += fabs((double)c[q]);
+  a = block_sum(a, sh);
+  if (threadIdx.x == 0) P.partials[blockIdx.x] = a;
+  if (last_block(P.counter)) {
+    reduce_partials(P.partials, 1, out, sh);
+    if (threadIdx.x == 0) {
+      *P.counter = 0u;
+      Ctrl& C = *P.ctrl;
+      C.sigma[i] = C.u_sigma[i] * out[0];
+      for (int jb = 0; jb < C.njobs; ++jb)
+        if (C.job[jb].set == i) C.job[jb].sigma = C.sigma[i];
+    }
+  }
+}
+
 template <class T>
 __global__ void k_copy(const T* a, T* b, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

@@ -99,6 +99,7 @@ struct SetD {
   int fib, flen;          // per-fiber application (0 whole; 1 x-, 2 z-fibers) and fiber length
   int fpath;              // 1: warp kernel k_fiberw; 0: CTA-per-fiber sort kernel k_fiber
   int svd;                // rank / nuclear-norm set (sip_svd.cuh)
+  int dct;                // l1 ball of the grid's orthonormal DCT (kept inside the set)
   T* y[2];                // ping-pong y_i (parity k & 1), nblk blocks of ld
   T* v[2];
   T* vh0;                 // Alg. 2 snapshot v-hat^{k0}

@@ -4,6 +4,7 @@
 // whose decisions live in device memory (Ctrl), captured once into a CUDA
 // graph of `graph_iters` iterations and replayed; the host reads one flag per
 // graph launch (lagged by one launch) to learn that Eq. 28 stopped the run.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -83,6 +84,7 @@ inline int kind_of(sip_set_type t) {
     case SIP_SET_L2_BALL: return K_L2;
     case SIP_SET_ANNULUS: return K_ANN;
     case SIP_SET_RANK: return K_RANK;
+    case SIP_SET_DCT_L1: return K_L1;
     case SIP_SET_NUCLEAR: return K_NUC;
     default: return K_CARD;
   }
@@ -109,6 +111,13 @@ struct Engine : EngineBase {
   int nsm = 148;
   int nfib_sets = 0;             // sets applied per fiber (k_fiber)
   int nsvd_sets = 0, g_svd = 0;  // rank / nuclear-norm sets (sip_svd.cuh): one CTA per matrix
+  // orthogonal-transform l1 sets (NEXT-3): the orthonormal DCT-II
+  // of the grid by cuBLAS GEMMs along each axis (plain library GEMMs)
+  int ndct_sets = 0;
+  cublasHandle_t blas = nullptr;
+  T* dctm[3] = {nullptr, nullptr, nullptr};   // column-major DCT matrices of the z, y, x axes
+  T* dtmp = nullptr;                           // one N-field of scratch
+  void* blas_ws = nullptr;
   int g_fib = 0, g_fibw = 0, nfib_sort = 0, nfib_warp = 0;
   int g_fw[MAXP] = {0};
   size_t smem_fib = 0, smem_fw[MAXP] = {0};
@@ -154,6 +163,7 @@ struct Engine : EngineBase {
 
   ~Engine() override {
     if (gexec) cudaGraphExecDestroy(gexec);
+    if (blas) cublasDestroy(blas);
     for (void* a : allocs) cudaFree(a);
     if (h_flag) cudaFreeHost(h_flag);
     cudaEventDestroy(ev_flag[0]); cudaEventDestroy(ev_flag[1]);
@@ -261,6 +271,8 @@ struct Engine : EngineBase {
                   S.kind == K_RANK || S.kind == K_NUC);
       S.svd = (S.kind == K_RANK || S.kind == K_NUC);
       if (S.svd) nsvd_sets++;
+      S.dct = (i < p && s[i].type == SIP_SET_DCT_L1) ? 1 : 0;
+      if (S.dct) ndct_sets++;
       S.job = S.sjob = -1;
       S.fib = (i < p) ? s[i].fib : 0;
       // fiber length on this engine's own grid (multilevel levels differ)
@@ -361,6 +373,9 @@ struct Engine : EngineBase {
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
     if (nfib_sets && !vec)
       throw SipError{SIP_ERR_CONFIG, "per-fiber sets need nx % (16 / sizeof(dtype)) == 0 and no blur/mask operator"};
+    if (ndct_sets && (!vec || nranks > 1))
+      throw SipError{SIP_ERR_CONFIG, "transform-domain l1 sets need nx % (16 / sizeof(dtype)) == 0, no blur/mask operator, one rank"};
+    if (ndct_sets) setup_dct();
     if (nsvd_sets && (!vec || nranks > 1))
       throw SipError{SIP_ERR_CONFIG, "rank / nuclear sets need nx % (16 / sizeof(dtype)) == 0, no blur/mask operator, one rank"};
     if (nsvd_sets) {   // fp64 scratch of the batched Jacobi kernel: X (m x n) and V (n x n) per matrix
@@ -383,7 +398,8 @@ struct Engine : EngineBase {
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
     // select v2 (sip_select2.cuh): single-rank fp32 runs with a radix job
-    Pr.selv2 = (vec && sizeof(T) == 4 && nranks == 1 && njobs > 0 && !getenv("SIP_SEL_V1")) ? 1 : 0;
+    // (transform-domain sets: pass 1's round A would count untransformed keys)
+    Pr.selv2 = (vec && sizeof(T) == 4 && nranks == 1 && njobs > 0 && !ndct_sets && !getenv("SIP_SEL_V1")) ? 1 : 0;
     if (Pr.selv2) {   // k_selB / k_selC: one resident wave (the candidate regions are per CTA)
       int occ = 0;
       CU(cudaFuncSetAttribute(k_selB<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)selb_smem()));
@@ -501,6 +517,95 @@ struct Engine : EngineBase {
     CU(cudaStreamSynchronize(stream));
   }
 
+  // ---- orthonormal DCT-II along every axis (reading L30) ---------------
+  void setup_dct() {
+    const int n[3] = {nz, ny, nx};
+    for (int a = 0; a < 3; ++a) {
+      if (a == 1 && ndim == 2) continue;
+      const int L = n[a];
+      std::vector<T> h((size_t)L * L);
+      for (int k = 0; k < L; ++k)       // column-major D(k, j): row k = frequency, column j = sample
+        for (int j = 0; j < L; ++j) {
+          const double sc = k == 0 ? std::sqrt(1.0 / L) : std::sqrt(2.0 / L);
+          h[(size_t)k + (size_t)j * L] = (T)(sc * std::cos(M_PI * (2.0 * j + 1.0) * k / (2.0 * L)));
+        }
+      dctm[a] = dalloc<T>((size_t)L * L);
+      CU(cudaMemcpy(dctm[a], h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    }
+    dtmp = dalloc<T>((size_t)Pr.g.N);
+    if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) throw SipError{SIP_ERR_CUDA, "cublasCreate"};
+    const size_t wsb = 32u << 20;      // a fixed workspace: no allocation inside graph capture
+    blas_ws = dalloc<char>(wsb);
+    cublasSetWorkspace(blas, blas_ws, wsb);
+    cublasSetStream(blas, stream);
+    cublasSetPointerMode(blas, CUBLAS_POINTER_MODE_HOST);
+  }
+  T* dtmp2_ = nullptr;
+  T* dtmp2() { if (!dtmp2_) dtmp2_ = dalloc<T>((size_t)Pr.g.N); return dtmp2_; }
+  void gemm(cublasOperation_t ta, cublasOperation_t tb, int m_, int n_, int k_, const T* A, int lda,
+            const T* B, int ldb, T* Cm, int ldc) {
+    const T one = 1, zero = 0;
+    cublasStatus_t st;
+    if constexpr (sizeof(T) == 4)
+      st = cublasSgemm(blas, ta, tb, m_, n_, k_, (const float*)&one, (const float*)A, lda, (const float*)B, ldb,
+                       (const float*)&zero, (float*)Cm, ldc);
+    else
+      st = cublasDgemm(blas, ta, tb, m_, n_, k_, (const double*)&one, (const double*)A, lda, (const double*)B, ldb,
+                       (const double*)&zero, (double*)Cm, ldc);
+    if (st != CUBLAS_STATUS_SUCCESS) throw SipError{SIP_ERR_CUDA, "cuBLAS gemm failed"};
+  }
+  void gemm_sb(cublasOperation_t ta, cublasOperation_t tb, int m_, int n_, int k_, const T* A, int lda,
+               long long sa, const T* B, int ldb, long long sb, T* Cm, int ldc, long long sc, int batch) {
+    const T one = 1, zero = 0;
+    cublasStatus_t st;
+    if constexpr (sizeof(T) == 4)
+      st = cublasSgemmStridedBatched(blas, ta, tb, m_, n_, k_, (const float*)&one, (const float*)A, lda, sa,
+                                     (const float*)B, ldb, sb, (const float*)&zero, (float*)Cm, ldc, sc, batch);
+    else
+      st = cublasDgemmStridedBatched(blas, ta, tb, m_, n_, k_, (const double*)&one, (const double*)A, lda, sa,
+                                     (const double*)B, ldb, sb, (const double*)&zero, (double*)Cm, ldc, sc, batch);
+    if (st != CUBLAS_STATUS_SUCCESS) throw SipError{SIP_ERR_CUDA, "cuBLAS batched gemm failed"};
+  }
+  // f <- D f (inv = 0) or D^T f (inv = 1), in place through dtmp.  Column-
+  // major view of the row-major field: X(x, y, z); the x axis multiplies
+  // from the left, y and z from the right.
+  void dct_field(T* f, int inv) {
+    const cublasOperation_t L_ = inv ? CUBLAS_OP_T : CUBLAS_OP_N;   // D or D^T from the left
+    const cublasOperation_t R_ = inv ? CUBLAS_OP_N : CUBLAS_OP_T;   // D^T or D from the right
+    gemm(L_, CUBLAS_OP_N, nx, ny * nz, nx, dctm[2], nx, f, nx, dtmp, nx);                  // x
+    if (ndim == 3) {
+      gemm_sb(CUBLAS_OP_N, R_, nx, ny, ny, dtmp, nx, (long long)nx * ny, dctm[1], ny, 0, f, nx,
+              (long long)nx * ny, nz);                                                        // y, per plane
+      gemm(CUBLAS_OP_N, R_, nx * ny, nz, nz, f, nx * ny, dctm[0], nz, dtmp, nx * ny);        // z
+    } else {
+      gemm(CUBLAS_OP_N, R_, nx, nz, nz, dtmp, nx, dctm[0], nz, f, nx);                       // z
+      return;
+    }
+    CU(cudaMemcpyAsync(f, dtmp, (size_t)Pr.g.N * sizeof(T), cudaMemcpyDeviceToDevice, stream));
+  }
+  // the transforms around the hot-path kernels (kpos > 0: the parity of the
+  // iteration, hence the y / v buffers, is known at capture time)
+  void dct_after_pass1(int kpos) {
+    const bool adapt = kpos % 2 == 1;
+    const int par = kpos & 1;
+    for (int i = 0; i < p; ++i) {
+      SetD<T>& S = Pr.set[i];
+      if (!S.dct) continue;
+      dct_field(S.w, 0);                                    // w in the coefficient domain
+      if (kpos % hc.opt.check_every == 0) dct_field(S.s, 0);
+      if (adapt) { dct_field(S.y[par ^ 1], 0); dct_field(S.v[par ^ 1], 0); }   // Alg. 2's k0 snapshots
+    }
+  }
+  void dct_after_pass2(int kpos) {
+    const int par = kpos & 1;
+    for (int i = 0; i < p; ++i) {
+      SetD<T>& S = Pr.set[i];
+      if (!S.dct) continue;
+      dct_field(S.y[par ^ 1], 1);                           // y = D^T P_l1(D w), v = D^T v_c (linear)
+      dct_field(S.v[par ^ 1], 1);
+    }
+  }
+
   // per-entry bounds: compact (host, fp64) -> padded device field
   const T* upload_compact(int i, const std::vector<double>& v) {
     const SetD<T>& S = Pr.set[i];
@@ -562,7 +667,7 @@ struct Engine : EngineBase {
   // profiling: an event is recorded before the first kernel and after every
   // kernel; consecutive pairs give each kernel's device time (kind list)
   // KB_COMM: a z-slab site's exchange + finalisers (multi-rank only)
-  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, KB_CGX, KB_FIBER, KB_SVD, NKIND };
+  enum { KB_BLUR = 0, KB_RHS, KB_CG1, KB_CG2, KB_PASS1, KB_SELECT, KB_TIE, KB_PASS2, KB_CTRL, KB_COMM, KB_CGX, KB_FIBER, KB_SVD, KB_DCT, NKIND };
   bool prof = false;
   std::vector<cudaEvent_t> pev;      // events of one graph (capture order)
   std::vector<int> pkind;            // kind of the kernel ending at pev[i+1]
@@ -719,6 +824,10 @@ struct Engine : EngineBase {
     if (Pr.defer_x && n_cg > 0) { launch_cgx(); mark(KB_CGX); }
     launch_pass1(kpos);
     ++launches; mark(KB_PASS1);
+    if (ndct_sets) {
+      if (kpos <= 0) throw SipError{SIP_ERR_CONFIG, "transform-domain sets need graph_iters a multiple of lcm(2, check_every) (or 0)"};
+      dct_after_pass1(kpos); mark(KB_DCT);
+    }
     if (hc.njobs > 0) {
       if (Pr.selv2) {   // one streaming pass + candidate rounds (round A ran in pass 1)
         lk(k_selB<T>, g_sel, BLOCK, selb_smem(), Pr); ++launches; mark(KB_SELECT);
@@ -733,6 +842,7 @@ struct Engine : EngineBase {
       launch_pass2(kpos);
       ++launches; mark(KB_PASS2);
     }
+    if (ndct_sets) { dct_after_pass2(kpos); mark(KB_DCT); }
     if (nfib_sets) { launch_fiber(); mark(KB_FIBER); }   // per-fiber projections, after pass 2's sums
     if (nsvd_sets) { launch_svd(); mark(KB_SVD); }       // rank / nuclear-norm sets
     launch_control(); mark(KB_CTRL);
@@ -885,6 +995,13 @@ struct Engine : EngineBase {
     fill_ctrl(o, max_iter, eps_feas, eps_evol, floor_, rho_in, gamma_in);
     fill_logs_nan(max_iter);
     run_init(init_x, init_yv);
+    for (int i = 0; i < p; ++i) {   // relative transform-domain radius: sigma = frac ||D m||_1 (reading L30)
+      if (!(Pr.set[i].dct && (*sets)[i].prm.relative)) continue;
+      CU(cudaMemcpyAsync(dtmp2(), Pr.m, (size_t)Pr.g.N * sizeof(T), cudaMemcpyDeviceToDevice, stream));
+      dct_field(dtmp2(), 0);
+      k_dct_sigma<T><<<g_small_(), BLOCK, 0, stream>>>(Pr, i, dtmp2());
+      ++launches;
+    }
     for (int i = 0; i < p; ++i) {   // relative nuclear-norm radius: sigma = frac ||A m||_* (y = A m after init)
       if (!(Pr.set[i].kind == K_NUC && (*sets)[i].prm.relative)) continue;
       if (!init_yv) throw SipError{SIP_ERR_CONFIG, "relative nuclear-norm radius needs y = A m at the start (no warm start / multilevel)"};
@@ -2035,7 +2152,7 @@ sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtyp
 sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type type,
                        const sip_set_params* prm, int* set_id) {
   if (!g || !prm) return SIP_ERR_ARG;
-  if (op < SIP_OP_IDENTITY || op > SIP_OP_BLUR_MASK || type < SIP_SET_BOUNDS || type > SIP_SET_NUCLEAR)
+  if (op < SIP_OP_IDENTITY || op > SIP_OP_BLUR_MASK || type < SIP_SET_BOUNDS || type > SIP_SET_DCT_L1)
     return SIP_ERR_ARG;
   if ((int)g->sets.size() >= SIP_MAX_SETS) { g->err = "more than 16 sets"; return SIP_ERR_CONFIG; }
   if (op == SIP_OP_DY && g->ndim != 3) { g->err = "D_y needs a 3D grid"; return SIP_ERR_CONFIG; }
@@ -2094,6 +2211,11 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type 
     } else if (type == SIP_SET_CARDINALITY) {
       if (prm->relative) { if (!(prm->k_frac >= 0 && prm->k_frac <= 1)) return SIP_ERR_PARAM; }
       else if (prm->k < 0 || prm->k > hs.M) return SIP_ERR_PARAM;
+    } else if (type == SIP_SET_DCT_L1) {   // {x : ||D x||_1 <= sigma}, D the grid's orthonormal DCT
+      if (op != SIP_OP_IDENTITY) { g->err = "transform-domain l1 sets keep the transform inside the set: op must be IDENTITY"; return SIP_ERR_CONFIG; }
+      if (g->nranks > 1) { g->err = "transform-domain l1 sets: one rank only"; return SIP_ERR_CONFIG; }
+      if (!(prm->sigma >= 0)) return SIP_ERR_PARAM;
+      if (prm->app_mode != SIP_APPLY_WHOLE) { g->err = "transform-domain l1 sets act on the whole grid"; return SIP_ERR_CONFIG; }
     } else if (type == SIP_SET_RANK || type == SIP_SET_NUCLEAR) {
       // matrix view (reading L29); the batched Jacobi kernel's limits
       if (op == SIP_OP_TV || op == SIP_OP_BLUR_MASK) { g->err = "rank / nuclear sets need a single-block operator"; return SIP_ERR_CONFIG; }

@@ -21,7 +21,7 @@ SIP_OK = 0
 SIP_NOT_CONVERGED = 1
 SIP_MAX_SETS = 16
 OPS = {"I": 0, "IDENTITY": 0, "DZ": 1, "DY": 2, "DX": 3, "TV": 4, "BLUR_MASK": 5}
-KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6}
+KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6, "dct_l1": 7}
 DTYPES = {"f32": 0, "f64": 1}
 
 
@@ -65,7 +65,7 @@ EXPORTS = [
     "sip_get_log", "sip_get_support_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
 ]
 KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm", "cgx", "fiber",
-                "svd"]
+                "svd", "dct"]
 
 _lib = None
 

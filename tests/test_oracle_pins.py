@@ -803,3 +803,59 @@ def test_parsdmm_nuclear_box_vs_dykstra():
     sets = [SetDef("I", "bounds", lo=-1.5, hi=1.5), SetDef("I", "nuclear", sigma=sig)]
     t = O.parsdmm(shape, sets, m, eps_evol=1e-10, eps_feas=1e-10, n_cg=50, max_iter=50000)
     assert O.relres(t.x, ref) < 1e-6
+
+
+# ------------------------------------------------------------ orthogonal-transform sets (NEXT-3)
+@pytest.mark.parametrize("shape", [(5, 7), (8, 8), (3, 4, 5)])
+def test_dct_is_scipy_orthonormal_dct2(shape):
+    """the oracle's DCT (its own O(n^2) loops) against scipy's dctn(norm='ortho')
+    (a library routine), its inverse, and Parseval (orthogonality)"""
+    import scipy.fft as F
+    r = np.random.default_rng(len(shape))
+    x = r.normal(size=shape)
+    c = O.dct(shape, x)
+    np.testing.assert_allclose(c.reshape(shape), F.dctn(x, norm="ortho"), atol=1e-13)
+    np.testing.assert_allclose(O.dct(shape, c, inverse=True).reshape(shape), x, atol=1e-13)
+    assert np.linalg.norm(c) == pytest.approx(np.linalg.norm(x), rel=1e-14)
+    const = np.full(shape, 2.0)
+    cc = O.dct(shape, const)
+    assert cc[0] == pytest.approx(2.0 * np.sqrt(np.prod(shape)), rel=1e-14) and np.abs(cc[1:]).max() < 1e-12
+
+
+def test_dct_l1_projection_closed_form():
+    """P_V(x) = D^T P_l1(D x): feasible, idempotent, and equal to the
+    projection computed with scipy's DCT and an independent l1-ball bisection"""
+    import scipy.fft as F
+    shape = (6, 10)
+    r = np.random.default_rng(3)
+    x = r.normal(size=shape)
+    n1 = np.abs(F.dctn(x, norm="ortho")).sum()
+    sd = SetDef("I", "dct_l1", sigma=0.3 * n1)
+    y = O.project(sd, x.ravel(), shape=shape)
+    c = F.dctn(x, norm="ortho").ravel()
+    lam = _l1_ball_sorted(np.abs(c), 0.3 * n1)
+    ref = F.idctn((np.sign(c) * lam).reshape(shape), norm="ortho").ravel()
+    np.testing.assert_allclose(y, ref, atol=1e-9)
+    assert np.abs(F.dctn(y.reshape(shape), norm="ortho")).sum() <= 0.3 * n1 * (1 + 1e-12)
+    np.testing.assert_allclose(O.project(sd, y, shape=shape), y, atol=1e-12)
+    s, _, _, _ = O.resolve_set(shape, SetDef("I", "dct_l1", sigma=0.3, relative=True), x)
+    assert s == pytest.approx(0.3 * n1, rel=1e-13)
+
+
+def test_parsdmm_box_dct_l1_vs_dykstra():
+    """box ∩ {||D x||_1 <= sigma}: PARSDMM (the transform kept inside the set,
+    A = I) reaches parallel Dykstra's point (Algorithm 4)"""
+    import scipy.fft as F
+    shape = (8, 6)
+    r = np.random.default_rng(17)
+    m = r.normal(size=shape) * 3.0
+    sig = 0.4 * np.abs(F.dctn(m, norm="ortho")).sum()
+
+    def p_dct(z):
+        c = F.dctn(z, norm="ortho")
+        lam = _l1_ball_sorted(np.abs(c).ravel(), sig).reshape(shape)
+        return F.idctn(np.sign(c) * lam, norm="ortho")
+    ref = _dykstra(m, [lambda z: np.clip(z, -2.0, 2.0), p_dct])
+    sets = [SetDef("I", "bounds", lo=-2.0, hi=2.0), SetDef("I", "dct_l1", sigma=sig)]
+    t = O.parsdmm(shape, sets, m, eps_evol=1e-10, eps_feas=1e-10, n_cg=50, max_iter=50000)
+    assert O.relres(t.x, ref) < 1e-6
