@@ -1922,6 +1922,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     }
     e->hc = c;
     CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
+    if (S.dct) e->dct_field(S.w, 0);   // the search and pass 2 act on D w
     if (S.svd) {   // rank / nuclear-norm set: the batched Jacobi kernel writes y[1]
       const MatView mv = mat_view(e->ndim, e->nz_g, e->ny, e->nx, S.prim[0]);
       k_svdproj<T><<<mv.nmat, SVD_BLOCK, 0, e->stream>>>(e->Pr, set_id, 0);
@@ -1941,6 +1942,7 @@ sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
     if (S.fib || S.svd) {
     } else if (e->vec) k_pass2t<T, 2, 2><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
     else k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
+    if (S.dct) e->dct_field(S.y[1], 1);   // y = D^T P_l1(D w)
   } else {
     // pointwise: gamma = 0 and v = 0 make x-bar = y_old and w = y_old, so
     // pass1 evaluates y = P(w) on the given w placed in y[0]
