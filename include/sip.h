@@ -283,6 +283,29 @@ sip_status sip_get_log(sip_grid g, int max_iter, int *cg, int *branch, double *r
    uint64 (host).  Errors: SIP_ERR_ARG (null), SIP_ERR_STATE (no run). */
 sip_status sip_get_support_log(sip_grid g, int max_iter, uint64_t *out);
 
+/* Algorithm 4, parallel Dykstra: the comparator of the paper's
+   Fig. 1 experiment.  Projects m onto the
+   grid's sets with weights 1/p; P_{V_i} is the set's projector when its
+   operator is IDENTITY, otherwise PARSDMM with that one set (natural mode,
+   inner_max_iter iterations at most, tolerance inner_tol; the paper's
+   ARADMM role), started from v_i.  Relative parameters are resolved
+   once from m.  Stops when ||x^k - x^{k-1}|| / ||x^k|| < tol or after
+   max_outer iterations (SIP_NOT_CONVERGED).  m, x: N-vectors (host or
+   device).  log (host arrays, may be NULL): per outer iteration the largest
+   CG count of the sub-problems, the l1-ball projections (inner iterations
+   of the l1 sub-problems), inner iterations per set, Eq. 26 of x^k per set
+   and r_evol.  One rank only (SIP_ERR_CONFIG). */
+typedef struct {
+  int iterations;
+  int *cg_max;            /* [max_outer]     */
+  int *l1_proj;           /* [max_outer]     */
+  int *inner_iters;       /* [max_outer * p] */
+  double *r_feas;         /* [max_outer * p] */
+  double *r_evol;         /* [max_outer]     */
+} sip_dykstra_log;
+sip_status sip_dykstra(sip_grid g, const void *m, void *x, int max_outer, double tol, int inner_max_iter,
+                       double inner_tol, sip_dykstra_log *log);
+
 /* Number of sets p, grid points N (this rank) and compact length of set i. */
 sip_status sip_get_sizes(sip_grid g, int *p, int64_t *n_local, int set_id, int64_t *m_compact);
 

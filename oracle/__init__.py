@@ -420,6 +420,34 @@ def parsdmm_multilevel(shape, setdefs, m, n_levels, h=None, **opts):
     return x, st, [_result(None, st, logs[l], allbufs[l], p, o.max_iter) for l in range(n_levels)]
 
 
+class DykLog(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("cg_max", C.POINTER(C.c_int)), ("l1_proj", C.POINTER(C.c_int)),
+                ("inner_iters", C.POINTER(C.c_int)), ("r_feas", C.POINTER(C.c_double)),
+                ("r_evol", C.POINTER(C.c_double))]
+
+
+def dykstra(shape, setdefs, m, max_outer=100, tol=1e-6, h=None, **inner_opts):
+    """Algorithm 4 with PARSDMM sub-problems (the Fig. 1 comparator)"""
+    g = make_grid(shape, h)
+    arr, _hold = _sets_array(setdefs)
+    o = options(**inner_opts)
+    p = len(setdefs)
+    m = _f64(m).ravel()
+    x = np.zeros(m.size)
+    b = dict(cg_max=np.zeros(max_outer, dtype=np.int32), l1_proj=np.zeros(max_outer, dtype=np.int32),
+             inner_iters=np.zeros(max_outer * p, dtype=np.int32), r_feas=np.zeros(max_outer * p),
+             r_evol=np.zeros(max_outer))
+    lg = DykLog()
+    lg.cg_max = _ip(b["cg_max"]); lg.l1_proj = _ip(b["l1_proj"]); lg.inner_iters = _ip(b["inner_iters"])
+    lg.r_feas = _dp(b["r_feas"]); lg.r_evol = _dp(b["r_evol"])
+    st = lib().sipref_dykstra(C.byref(g), p, arr, C.byref(o), int(max_outer), C.c_double(tol), _dp(m),
+                              _dp(x), C.byref(lg))
+    it = lg.iterations
+    return dict(x=x, status=int(st), iterations=it, cg_max=b["cg_max"][:it].copy(),
+                l1_proj=b["l1_proj"][:it].copy(), inner_iters=b["inner_iters"].reshape(max_outer, p)[:it].copy(),
+                r_feas=b["r_feas"].reshape(max_outer, p)[:it].copy(), r_evol=b["r_evol"][:it].copy())
+
+
 def restrict(shape, f):
     g = make_grid(shape)
     f = _f64(f).ravel()

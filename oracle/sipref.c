@@ -1150,3 +1150,72 @@ int sipref_parsdmm_multilevel(const sipref_grid *g, int p, const sipref_set *set
   free(ml); free(gr); free(rho); free(gam);
   return status;
 }
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 4, parallel Dykstra, Fig. 1 comparator         */
+/* ------------------------------------------------------------------ */
+int sipref_dykstra(const sipref_grid *g, int p, const sipref_set *in_sets, const sipref_options *inner,
+                   int max_outer, double tol, const double *m, double *x, sipref_dykstra_log *log) {
+  int64_t N = sipref_npts(g);
+  sipref_set *sets = (sipref_set *)calloc((size_t)(p > 0 ? p : 1), sizeof(sipref_set));
+  for (int i = 0; i < p; ++i) sipref_resolve_set(g, &in_sets[i], m, &sets[i]);   /* from m, once */
+  double **v = (double **)calloc((size_t)p, sizeof(double *));
+  double **y = (double **)calloc((size_t)p, sizeof(double *));
+  double *xo = dalloc(N);
+  memcpy(x, m, (size_t)N * sizeof(double));                          /* 0a */
+  for (int i = 0; i < p; ++i) {                                      /* 0b */
+    v[i] = dalloc(N); y[i] = dalloc(N);
+    memcpy(v[i], x, (size_t)N * sizeof(double));
+  }
+  const double w = 1.0 / (double)p;                                  /* 0c */
+  int k;
+  for (k = 1; k <= max_outer; ++k) {
+    int cg_max = 0, l1p = 0;
+    for (int i = 0; i < p; ++i) {                                    /* 1 */
+      int it = 0, cg = 0;
+      if (sets[i].op == SIPREF_OP_I) {
+        sipref_project(&sets[i], N, v[i], y[i]);
+        it = 1;
+      } else {
+        sipref_log lg;
+        memset(&lg, 0, sizeof(lg));
+        sipref_parsdmm(g, 1, &sets[i], inner, v[i], y[i], NULL, NULL, NULL, NULL, NULL, NULL, NULL, &lg);
+        it = lg.iterations;
+        cg = lg.cg_total;
+      }
+      if (cg > cg_max) cg_max = cg;
+      if (sets[i].type == SIPREF_L1) l1p += it;
+      if (log && log->inner_iters) log->inner_iters[(size_t)(k - 1) * p + i] = it;
+    }
+    memcpy(xo, x, (size_t)N * sizeof(double));
+    for (int64_t j = 0; j < N; ++j) {                                /* 2 */
+      double a = 0.0;
+      for (int i = 0; i < p; ++i) a += w * y[i][j];
+      x[j] = a;
+    }
+    for (int i = 0; i < p; ++i)                                      /* 3 */
+      for (int64_t j = 0; j < N; ++j) v[i][j] = x[j] + v[i][j] - y[i][j];
+    double d = 0.0;
+    for (int64_t j = 0; j < N; ++j) d += (x[j] - xo[j]) * (x[j] - xo[j]);
+    double xn = nrm2(N, x);
+    double re = xn > 0.0 ? sqrt(d) / xn : 0.0;
+    if (log) {
+      if (log->cg_max) log->cg_max[k - 1] = cg_max;
+      if (log->l1_proj) log->l1_proj[k - 1] = l1p;
+      if (log->r_evol) log->r_evol[k - 1] = re;
+      if (log->r_feas)
+        for (int i = 0; i < p; ++i) {
+          int64_t M = sipref_op_len(g, &sets[i]);
+          double *a = dalloc(M);
+          sipref_apply_A(g, &sets[i], x, a);
+          log->r_feas[(size_t)(k - 1) * p + i] = sipref_feas(&sets[i], M, a);
+          free(a);
+        }
+    }
+    if (re < tol) break;
+  }
+  if (log) log->iterations = k > max_outer ? max_outer : k;
+  for (int i = 0; i < p; ++i) { free(v[i]); free(y[i]); }
+  free(v); free(y); free(xo); free(sets);
+  return k > max_outer ? 1 : 0;
+}

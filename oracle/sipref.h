@@ -163,6 +163,27 @@ int sipref_parsdmm(const sipref_grid *g, int p, const sipref_set *sets,
                    double *const *out_y, double *const *out_v,
                    sipref_log *log);
 
+/* Algorithm 4 (parallel Dykstra) -- the comparator of the
+   paper's Fig. 1 experiment.  Weights rho_i =
+   1/p; P_{V_i} for A_i = I is the set's projector, otherwise PARSDMM with
+   that one set (the role of ARADMM in the paper: "the same update
+   scheme"), options `inner`, started from v_i.  Relative parameters are
+   resolved once from m.  Stops when ||x^k - x^{k-1}|| / ||x^k|| < tol or at
+   max_outer.  Per outer iteration the log records the paper's counters
+   (P:497-501): the largest CG count among the sub-problems, the number of
+   l1-ball projections (the inner iterations of the l1 sub-problems), and
+   Eq. 26 of x^k for every set. */
+typedef struct {
+  int iterations;
+  int *cg_max;        /* [max_outer] */
+  int *l1_proj;       /* [max_outer] */
+  int *inner_iters;   /* [max_outer * p] */
+  double *r_feas;     /* [max_outer * p] */
+  double *r_evol;     /* [max_outer] */
+} sipref_dykstra_log;
+int sipref_dykstra(const sipref_grid *g, int p, const sipref_set *sets, const sipref_options *inner,
+                   int max_outer, double tol, const double *m, double *x, sipref_dykstra_log *log);
+
 /* Algorithm 3 (multilevel).  Level l grid is the fine grid coarsened
    (l-1) times by 2 (box mean + stride, reading L23); h doubles per level.
    logs: array of n_levels logs (index 0 = finest), may be NULL. */

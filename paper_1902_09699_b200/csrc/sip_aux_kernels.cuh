@@ -146,6 +146,61 @@ __global__ void __launch_bounds__(BLOCK) k_dct_sigma(const __grid_constant__ Pro
   }
 }
 
+// ---- Algorithm 4 (parallel Dykstra) vector steps
+template <class T>
+struct DykPtrs {
+  T* y[MAXP];
+  T* v[MAXP];
+};
+// x_old = x; x = sum_i y_i / p (step 2); v_i = x + v_i - y_i (step 3);
+// out = (||x - x_old||^2, ||x||^2), fixed-order reduction
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_dyk_update(T* x, T* xo, DykPtrs<T> P, int p, long long n,
+                                                      double* partials, unsigned* counter, double* out) {
+  __shared__ double sh[NWARP + 1];
+  __shared__ double o2[2];
+  double d2 = 0.0, x2 = 0.0;
+  const double w = 1.0 / (double)p;
+  for (long long q = blockIdx.x * (long long)BLOCK + threadIdx.x; q < n; q += (long long)gridDim.x * BLOCK) {
+    double a = 0.0;
+    for (int i = 0; i < p; ++i) a += w * (double)P.y[i][q];
+    const T xn = (T)a;
+    const double d = (double)xn - (double)x[q];
+    d2 += d * d;
+    x2 += (double)xn * (double)xn;
+    xo[q] = x[q];
+    x[q] = xn;
+    for (int i = 0; i < p; ++i) P.v[i][q] = xn + P.v[i][q] - P.y[i][q];
+  }
+  d2 = block_sum(d2, sh);
+  x2 = block_sum(x2, sh);
+  if (threadIdx.x == 0) { partials[blockIdx.x * 2] = d2; partials[blockIdx.x * 2 + 1] = x2; }
+  if (last_block(counter)) {
+    reduce_partials(partials, 2, o2, sh);
+    if (threadIdx.x == 0) { *counter = 0u; out[0] = o2[0]; out[1] = o2[1]; }
+  }
+}
+// (||a - pa||^2, ||a||^2) for Eq. 26
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_feas2(const T* a, const T* pa, long long n, double* partials,
+                                                 unsigned* counter, double* out) {
+  __shared__ double sh[NWARP + 1];
+  __shared__ double o2[2];
+  double d2 = 0.0, a2 = 0.0;
+  for (long long q = blockIdx.x * (long long)BLOCK + threadIdx.x; q < n; q += (long long)gridDim.x * BLOCK) {
+    const double d = (double)a[q] - (double)pa[q];
+    d2 += d * d;
+    a2 += (double)a[q] * (double)a[q];
+  }
+  d2 = block_sum(d2, sh);
+  a2 = block_sum(a2, sh);
+  if (threadIdx.x == 0) { partials[blockIdx.x * 2] = d2; partials[blockIdx.x * 2 + 1] = a2; }
+  if (last_block(counter)) {
+    reduce_partials(partials, 2, o2, sh);
+    if (threadIdx.x == 0) { *counter = 0u; out[0] = o2[0]; out[1] = o2[1]; }
+  }
+}
+
 template <class T>
 __global__ void k_copy(const T* a, T* b, long long n) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

@@ -1432,6 +1432,7 @@ struct sip_grid_s {
   EngineBase* last = nullptr;                      // engine of the last projection (finest level)
   EngineBase* last_team = nullptr;                 // z slabs: Team of the last projection (finest level)
   std::vector<std::unique_ptr<EngineBase>> levels; // multilevel (index 0 = finest)
+  std::unique_ptr<EngineBase> dyk;                 // sip_dykstra's sub-engines (kept alive until the next call)
   bool have_m = false;
   long long last_launches = 0;
 };
@@ -1749,8 +1750,13 @@ sip_status multilevel_team_T(sip_grid g, const void* m, void* x, int n_levels, i
 }
 
 template <class T>
+sip_status apply_op_E(Engine<T>* e, int set_id, const void* x, void* y);
+template <class T>
 sip_status apply_op_T(sip_grid g, int set_id, const void* x, void* y) {
-  Engine<T>* e = engine_of<T>(g);
+  return apply_op_E<T>(engine_of<T>(g), set_id, x, y);
+}
+template <class T>
+sip_status apply_op_E(Engine<T>* e, int set_id, const void* x, void* y) {
   const Geo& G = e->Pr.g;
   const SetD<T>& S = e->Pr.set[set_id];
   T* xin = e->Pr.pb[0];
@@ -1862,9 +1868,15 @@ sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg,
 }
 
 template <class T>
+sip_status project_set_E(Engine<T>* e, int set_id, const void* w, void* y);
+template <class T>
 sip_status project_set_T(sip_grid g, int set_id, const void* w, void* y) {
   Engine<T>* e = engine_of<T>(g);
   if (!e->ran) throw SipError{SIP_ERR_STATE, "sip_project_set needs a previous sip_project"};
+  return project_set_E<T>(e, set_id, w, y);
+}
+template <class T>
+sip_status project_set_E(Engine<T>* e, int set_id, const void* w, void* y) {
   // the step-level projection runs pass 1 / the radix rounds directly (no
   // select v2: its round-A counts would be left behind for the next solve)
   struct V2Off {
@@ -2040,6 +2052,116 @@ sip_status get_log_T(sip_grid g, int max_iter, int* cg, int* branch, double* rho
   if (feas && p) CU(cudaMemcpy(feas, e->d_log_feas, (size_t)n * p * sizeof(double), cudaMemcpyDeviceToHost));
   if (evol) CU(cudaMemcpy(evol, e->d_log_evol, n * sizeof(double), cudaMemcpyDeviceToHost));
   return SIP_OK;
+}
+
+// ---- Algorithm 4, parallel Dykstra: the Fig. 1 comparator --
+// Sub-problem i (P_{V_i}): the set's projector when A_i = I, else PARSDMM
+// with that one set (the paper's ARADMM role) on an engine of its own,
+// started from v_i; relative parameters resolved once from m by the main
+// engine; weights 1/p; counters of P:497-501 per outer iteration.
+struct DykState : EngineBase {
+  std::vector<std::vector<HostSet>> sets;       // one set per sub-engine (absolute parameters)
+  std::vector<std::unique_ptr<EngineBase>> eng;
+};
+
+template <class T>
+sip_status dykstra_T(sip_grid g, const void* m_in, void* x_out, int max_outer, double tol, int inner_max,
+                     double inner_tol, sip_dykstra_log* log) {
+  if (is_team(g)) throw SipError{SIP_ERR_CONFIG, "sip_dykstra: one rank only"};
+  Engine<T>* e = engine_of<T>(g);
+  const int p = e->p;
+  if (p < 1) throw SipError{SIP_ERR_CONFIG, "sip_dykstra needs at least one set"};
+  const size_t N = (size_t)e->Pr.g.N;
+  // resolve the relative parameters from m: one iteration of the main engine
+  copy_in(e, m_in, const_cast<T*>(e->Pr.m), N);
+  e->solve(g->opt, 1, 1e-3, 1e-2, 1, 1, nullptr, nullptr);
+  auto st = std::make_unique<DykState>();
+  for (int i = 0; i < p; ++i) {
+    HostSet hs = g->sets[i];
+    hs.prm.relative = 0;
+    hs.prm.sigma = e->hc.sigma[i];
+    hs.prm.sigma_lo = e->hc.sig_lo[i];
+    hs.prm.sigma_hi = e->hc.sig_hi[i];
+    hs.prm.k = e->hc.kcard[i];
+    if (hs.type == SIP_SET_L2_BALL) hs.prm.sigma = e->hc.sig_hi[i];
+    st->sets.push_back({hs});
+  }
+  for (int i = 0; i < p; ++i) {
+    auto se = std::make_unique<Engine<T>>();
+    se->setup(g->ndim, (int)g->n[0], (int)g->n[1], (int)g->n[2], g->h, g->stream, st->sets[i]);
+    st->eng.push_back(std::move(se));
+  }
+  auto E = [&](int i) { return static_cast<Engine<T>*>(st->eng[i].get()); };
+  struct Release {   // this call's work buffers: freed on return (e->allocs is append-only)
+    Engine<T>* e; size_t n0;
+    ~Release() { while (e->allocs.size() > n0) { cudaFree(e->allocs.back()); e->allocs.pop_back(); } }
+  } rel{e, e->allocs.size()};
+  T* x = e->template dalloc<T>(N);
+  T* xo = e->template dalloc<T>(N);
+  DykPtrs<T> ptr{};
+  for (int i = 0; i < p; ++i) { ptr.y[i] = e->template dalloc<T>(N); ptr.v[i] = e->template dalloc<T>(N); }
+  long long Mmax = (long long)N;
+  for (int i = 0; i < p; ++i) Mmax = std::max(Mmax, E(i)->set_len(0));
+  T* a = e->template dalloc<T>((size_t)Mmax);
+  T* pa = e->template dalloc<T>((size_t)Mmax);
+  double* red = e->template dalloc<double>(2);
+  copy_in(e, m_in, x, N);                                                   // 0a
+  for (int i = 0; i < p; ++i)                                               // 0b
+    CU(cudaMemcpyAsync(ptr.v[i], x, N * sizeof(T), cudaMemcpyDeviceToDevice, g->stream));
+  Options oin = g->opt;                                                     // the sub-problems: natural mode
+  oin.fixed_work = 0;
+  oin.eq25 = 1;
+  const double eps_evol = inner_tol > 0 ? 10.0 * inner_tol : 1e-2;
+  int k;
+  double h2[2];
+  for (k = 1; k <= max_outer; ++k) {
+    int cg_max = 0, l1p = 0;
+    for (int i = 0; i < p; ++i) {                                           // 1: y_i = P_{V_i}(v_i)
+      Engine<T>* s = E(i);
+      int it = 0, cg = 0;
+      if (st->sets[i][0].op == SIP_OP_IDENTITY) {
+        if (!s->ran) { copy_in(s, ptr.v[i], const_cast<T*>(s->Pr.m), N); s->solve(oin, 1, 1e-3, 1e-2, 1, 1, nullptr, nullptr); }
+        project_set_E<T>(s, 0, ptr.v[i], ptr.y[i]);
+        it = 1;
+      } else {
+        CU(cudaMemcpyAsync(const_cast<T*>(s->Pr.m), ptr.v[i], N * sizeof(T), cudaMemcpyDeviceToDevice, g->stream));
+        s->solve(oin, inner_max, inner_tol > 0 ? inner_tol : 1e-3, eps_evol, 1, 1, nullptr, nullptr);
+        CU(cudaMemcpyAsync(ptr.y[i], s->Pr.x, N * sizeof(T), cudaMemcpyDeviceToDevice, g->stream));
+        it = std::min(s->hc.k, s->hc.opt.max_iter);
+        cg = s->hc.cg_total;
+      }
+      cg_max = std::max(cg_max, cg);
+      if (st->sets[i][0].type == SIP_SET_L1_BALL) l1p += it;
+      if (log && log->inner_iters) log->inner_iters[(size_t)(k - 1) * p + i] = it;
+    }
+    k_dyk_update<T><<<e->g_small_(), BLOCK, 0, g->stream>>>(x, xo, ptr, p, (long long)N, e->Pr.partials,
+                                                             e->Pr.counter, red);          // 2, 3
+    CU(cudaMemcpyAsync(h2, red, 2 * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    const double re = h2[1] > 0.0 ? std::sqrt(h2[0]) / std::sqrt(h2[1]) : 0.0;
+    if (log) {
+      if (log->cg_max) log->cg_max[k - 1] = cg_max;
+      if (log->l1_proj) log->l1_proj[k - 1] = l1p;
+      if (log->r_evol) log->r_evol[k - 1] = re;
+      if (log->r_feas)
+        for (int i = 0; i < p; ++i) {                                       // Eq. 26 of x^k
+          Engine<T>* s = E(i);
+          const long long M = s->set_len(0);
+          apply_op_E<T>(s, 0, x, a);
+          project_set_E<T>(s, 0, a, pa);
+          k_feas2<T><<<e->g_small_(), BLOCK, 0, g->stream>>>(a, pa, M, e->Pr.partials, e->Pr.counter, red);
+          CU(cudaMemcpyAsync(h2, red, 2 * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+          CU(cudaStreamSynchronize(g->stream));
+          log->r_feas[(size_t)(k - 1) * p + i] = h2[1] > 0.0 ? std::sqrt(h2[0]) / std::sqrt(h2[1]) : 0.0;
+        }
+    }
+    if (re < tol) break;
+  }
+  if (log) log->iterations = k > max_outer ? max_outer : k;
+  copy_out(e, x, x_out, N);
+  CU(cudaStreamSynchronize(g->stream));
+  g->dyk = std::move(st);
+  return k > max_outer ? SIP_NOT_CONVERGED : SIP_OK;
 }
 
 template <class F>
@@ -2401,6 +2523,15 @@ sip_status sip_get_support_log(sip_grid g, int max_iter, uint64_t* out) {
       return SIP_OK;
     };
     return g->dtype == SIP_F32 ? run(float()) : run(double());
+  });
+}
+
+sip_status sip_dykstra(sip_grid g, const void* m, void* x, int max_outer, double tol, int inner_max_iter,
+                       double inner_tol, sip_dykstra_log* log) {
+  if (!g || !m || !x || max_outer < 1 || inner_max_iter < 1) return SIP_ERR_ARG;
+  return guarded(g, [&]() -> sip_status {
+    return g->dtype == SIP_F32 ? dykstra_T<float>(g, m, x, max_outer, tol, inner_max_iter, inner_tol, log)
+                               : dykstra_T<double>(g, m, x, max_outer, tol, inner_max_iter, inner_tol, log);
   });
 }
 

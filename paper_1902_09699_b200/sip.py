@@ -62,7 +62,7 @@ EXPORTS = [
     "sip_comm_unique_id", "sip_create_grid", "sip_add_set", "sip_set_option", "sip_project",
     "sip_project_multilevel", "sip_destroy", "sip_status_string", "sip_last_error",
     "sip_apply_op", "sip_apply_system", "sip_cg", "sip_project_set", "sip_get_state",
-    "sip_get_log", "sip_get_support_log", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
+    "sip_get_log", "sip_get_support_log", "sip_dykstra", "sip_get_sizes", "sip_get_launch_count", "sip_get_profile", "sip_slab",
 ]
 KERNEL_KINDS = ["blur", "rhs", "cg1", "cg2", "pass1", "select", "tiecount", "pass2", "control", "comm", "cgx", "fiber",
                 "svd", "dct"]
@@ -107,6 +107,8 @@ def lib():
         L.sip_get_profile.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         L.sip_slab.argtypes = [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.sip_comm_unique_id.argtypes = [C.c_void_p]
+        L.sip_dykstra.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_double,
+                                  C.c_void_p]
         _lib = L
     return _lib
 
@@ -145,6 +147,12 @@ def _current_stream():
 
 
 _NP_DT = {"f32": "float32", "f64": "float64"}
+
+
+class DykstraLog(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("cg_max", C.POINTER(C.c_int)), ("l1_proj", C.POINTER(C.c_int)),
+                ("inner_iters", C.POINTER(C.c_int)), ("r_feas", C.POINTER(C.c_double)),
+                ("r_evol", C.POINTER(C.c_double))]
 
 
 class Grid:
@@ -313,6 +321,27 @@ class Grid:
         out = np.zeros(max(1, max_iter * p), dtype=np.uint64)
         self._check(lib().sip_get_support_log(self.h, int(max_iter), _ptr(out)))
         return out[: max_iter * p].reshape(max_iter, p)
+
+    def dykstra(self, m, x, max_outer=100, tol=1e-6, inner_max_iter=200, inner_tol=1e-3):
+        """Algorithm 4 (parallel Dykstra, PARSDMM sub-problems): the Fig. 1
+        comparator; returns the per-outer-iteration counters"""
+        p = len(self.sets)
+        b = dict(cg_max=np.zeros(max_outer, dtype=np.int32), l1_proj=np.zeros(max_outer, dtype=np.int32),
+                 inner_iters=np.zeros(max_outer * p, dtype=np.int32), r_feas=np.zeros(max_outer * p),
+                 r_evol=np.zeros(max_outer))
+        lg = DykstraLog()
+        lg.cg_max = b["cg_max"].ctypes.data_as(C.POINTER(C.c_int))
+        lg.l1_proj = b["l1_proj"].ctypes.data_as(C.POINTER(C.c_int))
+        lg.inner_iters = b["inner_iters"].ctypes.data_as(C.POINTER(C.c_int))
+        lg.r_feas = b["r_feas"].ctypes.data_as(C.POINTER(C.c_double))
+        lg.r_evol = b["r_evol"].ctypes.data_as(C.POINTER(C.c_double))
+        s = self._check(lib().sip_dykstra(self.h, self._buf(m, self.N, "m"), self._buf(x, self.N, "x"),
+                                          int(max_outer), float(tol), int(inner_max_iter), float(inner_tol),
+                                          C.byref(lg)), (SIP_OK, SIP_NOT_CONVERGED))
+        it = lg.iterations
+        return dict(status=s, iterations=it, cg_max=b["cg_max"][:it].copy(), l1_proj=b["l1_proj"][:it].copy(),
+                    inner_iters=b["inner_iters"].reshape(max_outer, p)[:it].copy(),
+                    r_feas=b["r_feas"].reshape(max_outer, p)[:it].copy(), r_evol=b["r_evol"][:it].copy())
 
     def profile(self):
         """per-kernel-kind device ms and launch counts of the last project()"""

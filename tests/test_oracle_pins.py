@@ -859,3 +859,34 @@ def test_parsdmm_box_dct_l1_vs_dykstra():
     sets = [SetDef("I", "bounds", lo=-2.0, hi=2.0), SetDef("I", "dct_l1", sigma=sig)]
     t = O.parsdmm(shape, sets, m, eps_evol=1e-10, eps_feas=1e-10, n_cg=50, max_iter=50000)
     assert O.relres(t.x, ref) < 1e-6
+
+
+# ------------------------------------------------------------ Algorithm 4 comparator (NEXT-4, Fig. 1)
+def test_oracle_dykstra_matches_algorithm4_with_exact_projectors():
+    """the oracle's parallel Dykstra (PARSDMM sub-problems for A != I) against
+    Algorithm 4 with exact projectors (box, clip(PAVA) for D_z x >= 0):
+    same point; the counters are the paper's"""
+    shape = (8, 6)
+    m = tiny_model(33, shape)
+    lo, hi = float(np.percentile(m, 10)), float(np.percentile(m, 90))
+    sets = [SetDef("I", "bounds", lo=lo, hi=hi), SetDef("DZ", "bounds", lo=0.0, hi=INF)]
+    ref = _dykstra(m, [lambda z: np.clip(z, lo, hi),
+                       lambda z: np.column_stack([so.isotonic_regression(z[:, j]).x for j in range(shape[1])])])
+    d = O.dykstra(shape, sets, m, max_outer=3000, tol=1e-13, eps_evol=1e-12, eps_feas=1e-12, n_cg=100,
+                  max_iter=20000)
+    assert O.relres(d["x"], ref) < 1e-6
+    assert (d["cg_max"] > 0).all() and (d["l1_proj"] == 0).all()
+    assert (d["inner_iters"][:, 0] == 1).all()          # A = I: one projection, no CG
+
+
+def test_oracle_dykstra_counts_l1_projections():
+    """with a TV l1 set, every outer iteration projects onto the l1 ball as
+    often as the TV sub-problem iterates"""
+    shape = (8, 8)
+    m = tiny_model(34, shape)
+    sets = [SetDef("I", "bounds", lo=float(m.min()) + 50, hi=float(m.max()) - 50),
+            SetDef("TV", "l1", sigma=0.5, relative=True)]
+    d = O.dykstra(shape, sets, m, max_outer=5, tol=0.0)
+    assert d["iterations"] == 5
+    np.testing.assert_array_equal(d["l1_proj"], d["inner_iters"][:, 1])
+    assert (d["l1_proj"] >= 1).all()
