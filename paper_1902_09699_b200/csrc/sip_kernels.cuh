@@ -61,6 +61,8 @@ struct Prob {
   int selv2;                      // single-rank fp32: round A in pass 1, k_selB / k_selC (sip_select2.cuh)
   unsigned* gf_cnt;               // select v2: k_selB's candidate histogram [MAXJOBS][256]
   unsigned long long* gf_s0;
+  T* ub;                          // vectorised CG with a separable blur: c_F G^T S G p_j (sip_blur.cuh)
+  double gz_[MAXTAPS / 9], gx[MAXTAPS / 9];   // the blur's separable factors, K[r][c] = gz_[r] gx[c]
   double* svdX;                   // rank / nuclear sets: fp64 Jacobi scratch, X (m x n) per matrix
   double* svdV;                   //   and V (n x n) per matrix
   unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation

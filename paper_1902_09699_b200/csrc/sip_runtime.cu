@@ -22,6 +22,7 @@
 #include "sip_team.cuh"
 #include "sip_fiber.cuh"
 #include "sip_svd.cuh"
+#include "sip_blur.cuh"
 
 using namespace sip;
 
@@ -113,6 +114,9 @@ struct Engine : EngineBase {
   int nsvd_sets = 0, g_svd = 0;  // rank / nuclear-norm sets (sip_svd.cuh): one CTA per matrix
   // orthogonal-transform l1 sets (NEXT-3): the orthonormal DCT-II
   // of the grid by cuBLAS GEMMs along each axis (plain library GEMMs)
+  bool cgv = false;              // vectorised CG kernels (vec, or vec except a separable blur set)
+  size_t smem_bf = 0;
+  int g_bf = 1;
   int ndct_sets = 0;
   cublasHandle_t blas = nullptr;
   T* dctm[3] = {nullptr, nullptr, nullptr};   // column-major DCT matrices of the z, y, x axes
@@ -371,6 +375,34 @@ struct Engine : EngineBase {
     // vectorised CG kernels: W = 16/sizeof(T) points per thread along x
     constexpr int W = VT<T>::W;
     vec = (g.nx % W == 0) && !Pr.has[PRIM_F] && !getenv("SIP_NO_VEC");
+    // the vectorised CG kernels also serve a grid with the blur / mask
+    // operator when its kernel is separable (K = g_z g_x^T): the operator's
+    // term of C p comes from k_blurF (sip_blur.cuh); the set passes stay scalar
+    cgv = vec;
+    if (Pr.has[PRIM_F] && (g.nx % W == 0) && !getenv("SIP_NO_VEC") && !getenv("SIP_BLUR_SCALAR") && nranks == 1) {
+      for (int i = 0; i < p; ++i) {
+        if (s[i].op != SIP_OP_BLUR_MASK) continue;
+        const int kh = s[i].kh, kw = s[i].kw;
+        const std::vector<double>& K = s[i].kernel;
+        int r0 = 0, c0 = 0;
+        for (int a = 0; a < kh * kw; ++a) if (std::fabs(K[a]) > std::fabs(K[r0 * kw + c0])) { r0 = a / kw; c0 = a % kw; }
+        const double piv = K[r0 * kw + c0];
+        double kmax = std::fabs(piv), err = 0.0;
+        for (int rr = 0; rr < kh; ++rr) Pr.gz_[rr] = K[rr * kw + c0];
+        for (int cc = 0; cc < kw; ++cc) Pr.gx[cc] = piv != 0.0 ? K[r0 * kw + cc] / piv : 0.0;
+        for (int rr = 0; rr < kh; ++rr)
+          for (int cc = 0; cc < kw; ++cc) err = std::max(err, std::fabs(K[rr * kw + cc] - Pr.gz_[rr] * Pr.gx[cc]));
+        if (piv != 0.0 && err <= 1e-12 * kmax) {
+          cgv = true;
+          smem_bf = blurf_smem(kh, kw, sizeof(T));
+          CU(cudaFuncSetAttribute(k_blurF<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bf));
+          int occ = 0;
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_blurF<T>, BLOCK, smem_bf));
+          const int tiles = ((g.nx + BF_TX - 1) / BF_TX) * ((g.nz + BF_TZ - 1) / BF_TZ);
+          g_bf = std::max(1, std::min(tiles, nsm * std::max(occ, 1)));
+        }
+      }
+    }
     if (nfib_sets && !vec)
       throw SipError{SIP_ERR_CONFIG, "per-fiber sets need nx % (16 / sizeof(dtype)) == 0 and no blur/mask operator"};
     if (ndct_sets && (!vec || nranks > 1))
@@ -748,7 +780,7 @@ struct Engine : EngineBase {
   // flat CG kernels (sip_vec.cuh k_cg1f / k_cg2f) with the deferred x update;
   // the scalar kernels (sip_kernels.cuh) for general shapes, the blur
   // operator and n_cg > MAXCG (no ring slot per step)
-  bool lean_cg() const { return vec && Pr.defer_x; }
+  bool lean_cg() const { return cgv && Pr.defer_x; }
   const bool sel_debug = getenv("SIP_SEL_DEBUG") != nullptr;
   void launch_cg1(int j) {
     if (lean_cg()) {
@@ -768,7 +800,8 @@ struct Engine : EngineBase {
   }
   // deferred x update: one ring slot per CG step (vectorised path, n_cg <= MAXCG)
   void ensure_ring(int n_cg) {
-    if (!vec || n_cg < 1 || n_cg > MAXCG || getenv("SIP_NO_DEFER_X")) { Pr.defer_x = 0; return; }
+    if (!cgv || n_cg < 1 || n_cg > MAXCG || getenv("SIP_NO_DEFER_X")) { Pr.defer_x = 0; return; }
+    if (Pr.has[PRIM_F] && !Pr.ub) Pr.ub = field(1);
     while (npr < n_cg) Pr.pr[npr++] = field(1);
     Pr.defer_x = 1;
   }
@@ -817,7 +850,11 @@ struct Engine : EngineBase {
     if (Pr.has[PRIM_F]) { launch_blur(0, 0); mark(KB_BLUR); }
     launch_rhs(); mark(KB_RHS);
     for (int j = 0; j < n_cg; ++j) {
-      if (Pr.has[PRIM_F]) { launch_blur(1, j); mark(KB_BLUR); }
+      if (Pr.has[PRIM_F]) {
+        if (lean_cg()) { lk(k_blurF<T>, g_bf, BLOCK, smem_bf, Pr, j); ++launches; }
+        else launch_blur(1, j);
+        mark(KB_BLUR);
+      }
       launch_cg1(j); mark(KB_CG1);
       launch_cg2(j); mark(KB_CG2);
     }
@@ -1849,11 +1886,12 @@ sip_status cg_T(sip_grid g, const double* rho, const void* b, void* x, int n_cg,
   if (e->Pr.has[PRIM_F]) { k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2, 0, 0); }
   k_rhs<T><<<e->g_pts, BLOCK, 0, e->stream>>>(P2);
   for (int j = 0; j < n_cg; ++j) {
-    if (e->Pr.has[PRIM_F]) k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, 1, j);
-    if (e->vec) {   // the same kernels as the hot path
+    if (e->lean_cg()) {   // the same kernels as the hot path
+      if (e->Pr.has[PRIM_F]) k_blurF<T><<<e->g_bf, BLOCK, e->smem_bf, e->stream>>>(e->Pr, j);
       e->launch_cg1(j);
       e->launch_cg2(j);
     } else {
+      if (e->Pr.has[PRIM_F]) k_blur_t<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, 1, j);
       k_cg1<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
       k_cg2<T><<<e->g_pts, BLOCK, 0, e->stream>>>(e->Pr, j);
     }

@@ -207,6 +207,12 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
     }
     T q[W];
     L.template apply<W>(a0, a1, a2, a3, a4, rl, rr_, HY, q);
+    if (P.ub) {   // the data operator's term, c_F G^T S G p_j (k_blurF)
+      T u[W];
+      VT<T>::ldT(P.ub + pt0, u);
+#pragma unroll
+      for (int e = 0; e < W; ++e) q[e] += u[e];
+    }
     VT<T>::stT(pw + pt0, a0);
     T s = 0;
 #pragma unroll
@@ -257,6 +263,12 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<
     VT<T>::ldcs(P.r + pt0, rv);
     T q[W];
     L.template apply<W>(a0, a1, a2, a3, a4, xl, xr, HY, q);
+    if (P.ub) {
+      T u[W];
+      VT<T>::ldT(P.ub + pt0, u);
+#pragma unroll
+      for (int e = 0; e < W; ++e) q[e] += u[e];
+    }
     T s = 0;
 #pragma unroll
     for (int e = 0; e < W; ++e) {
