@@ -373,3 +373,36 @@ def test_state_written_before_read(seed, shape, kinds, path, monkeypatch):
     np.testing.assert_array_equal(log["cg"][:ref.iterations], ref.cg_per_iter)
     assert rel(x, ref.x) < 1e-6
     g.close()
+
+
+# ------------------------------------------------------------ per-kernel parity at C5-L1 size
+@pytest.mark.parametrize("kind", ["card", "l1"])
+def test_project_set_c5_l1_size(kind):
+    """sip_project_set at C5's finest size (512x512x256, D_z: 66,977,792
+    entries) in fp32: the cardinality support (k = 1,339,555 = floor(0.02 M))
+    exact, the l1 ball at 1e-5 -- the launch geometry of the full-size run"""
+    shape = (512, 512, 256)
+    sd = SetDef("DZ", "card", k=1339555) if kind == "card" else SetDef("DZ", "l1", sigma=0.0)
+    g = mk_grid(shape, [sd], "f32")
+    M = g.m_len(0)
+    assert M == 66977792
+    r = np.random.default_rng(7)
+    w = (r.standard_normal(M) * 30.0).astype(np.float32)
+    if kind == "l1":
+        sd.sigma = 0.3 * float(np.abs(w.astype(np.float64)).sum())
+        g.close()
+        g = mk_grid(shape, [sd], "f32")
+    m = torch.zeros(shape, dtype=torch.float32, device="cuda")
+    x = torch.empty_like(m)
+    g.project(m, x, max_iter=1)
+    wd = torch.from_numpy(w).cuda()
+    y = torch.empty_like(wd)
+    g.project_set(0, wd, y)
+    yh = y.cpu().numpy()
+    g.close()
+    ref = O.project(sd, w.astype(np.float64))
+    if kind == "card":
+        np.testing.assert_array_equal(yh != 0, ref != 0)
+        assert int((yh != 0).sum()) == 1339555
+    else:
+        assert rel(yh, ref) <= 1e-5
