@@ -323,8 +323,10 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
       if (threadIdx.x == 0) s_cn = 0u;
       for (int d = threadIdx.x; d < FB_N; d += BLOCK) { f_cnt[d] = 0u; f_l0[d] = 0u; f_l1[d] = 0u; }
       __syncthreads();
-      unsigned long long n_ab = 0;
+      unsigned n_ab = 0;                        // per thread: <= the entries it visits
       double s_ab = 0.0;
+      const unsigned lo1 = lo > 1u ? lo : 1u;   // zeros are never candidates
+      const unsigned wid1 = hi > lo1 ? hi - lo1 : 0u;
       if (nmine > 0) issue(0);
       for (int i = 0; i < nmine; ++i) {
         if (i + 1 < nmine) issue(i + 1);
@@ -338,13 +340,15 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
           const int c = u * BLOCK + (int)threadIdx.x;
-          T v[W];
-          if (c < cnt) VT<T>::ldT_s(tl + c * W, v);
+          T v[W] = {};
+          if (c < cnt) VT<T>::ldT_s(tl + c * W, v);     // the tile's tail reads as zeros
 #pragma unroll
           for (int e = 0; e < W; ++e) {
-            const unsigned k = c < cnt ? key32((float)v[e]) : 0u;
-            if (k >= hi) { ++n_ab; s_ab += kval(k); }
-            mine |= (k >= lo && k < hi && k != 0u) ? (1u << (u * W + e)) : 0u;
+            const unsigned k = key32((float)v[e]);
+            const bool ab = k >= hi;
+            n_ab += ab ? 1u : 0u;
+            s_ab += ab ? kval(k) : 0.0;
+            mine |= (unsigned)(k - lo1 < wid1) << (u * W + e);
           }
         }
         // warp-aggregated append to this CTA's region (one shared atomic per warp)
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
         if (sums) atomicAdd(P.gf_s0 + (size_t)jb * FB_N + d, (unsigned long long)f_l0[d] + ((unsigned long long)f_l1[d] << 16));
       }
       // per-CTA (count, sum above): fixed-order block sums
-      const double d_ab = block_sum((double)n_ab, sh);
+      const double d_ab = block_sum((double)n_ab, sh);   // exact: counts < 2^53
       const double d_sab = block_sum(s_ab, sh);
       __syncthreads();
       if (threadIdx.x == 0) {
