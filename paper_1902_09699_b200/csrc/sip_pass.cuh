@@ -237,6 +237,7 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
     const int s = t & 1;
     st.wait(s);
     const int c = c0 + t * BLOCK + (int)threadIdx.x;
+    T hw_[W] = {}, hs_[W] = {};   // round-A keys of this chunk (zeros: not counted)
     if (c < c1) {
       const int pt0 = c * W;
       const int tid = threadIdx.x;
@@ -334,8 +335,8 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
         VT<T>::stT(wp + pt0, wv);
         if (sp) VT<T>::stT(sp + pt0, sv_);
         if (KIND == 2 && ha) {   // select v2 round A: key counts of w (and s on checks)
-          hist_a<T>(ha, wv);
-          if (sp) hist_a<T>(ha + NBUCK, sv_);   // s is 0 on pads
+#pragma unroll
+          for (int e = 0; e < W; ++e) { hw_[e] = wv[e]; hs_[e] = sp ? sv_[e] : (T)0; }   // s is 0 on pads
           if (S.kind == K_L1) {                  // ||w||_1 (||s||_1) for the ball-inside test
             T t1 = 0, t2 = 0;
 #pragma unroll
@@ -352,6 +353,10 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
       d_w2 += (double)a_w2; d_hv += (double)a_hv; d_hh += (double)a_hh; d_vh += (double)a_vh;
       d_gv += (double)a_gv; d_gg += (double)a_gg; d_vv += (double)a_vv; d_fn += (double)a_fn;
       d_s2 += (double)a_s2;
+    }
+    if (KIND == 2 && ha) {   // every lane of the warp (warp-grouped counts)
+      hist_a<T>(ha, hw_);
+      if (sp) hist_a<T>(ha + NBUCK, hs_);
     }
     __syncthreads();   // stage s is refilled by the issue of tile t + 2
   }

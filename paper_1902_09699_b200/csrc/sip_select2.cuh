@@ -35,6 +35,9 @@ __device__ __forceinline__ double kval(unsigned key) { return (double)__uint_as_
 
 // round A: one count per non-zero entry (zeros never decide: a zero never
 // displaces a non-zero of the top k and adds nothing to an l1 sum)
+// one shared atomic per non-zero entry (grouping the lanes of a warp by
+// bucket with __match_any_sync first was measured slower: pass 1 3.24 vs
+// 2.65 ms per C4 step)
 template <class T>
 __device__ __forceinline__ void hist_a(unsigned* h, const T* v) {
   if constexpr (sizeof(T) == 4) {
