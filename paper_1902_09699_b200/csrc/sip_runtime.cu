@@ -23,6 +23,7 @@
 #include "sip_fiber.cuh"
 #include "sip_svd.cuh"
 #include "sip_blur.cuh"
+#include "sip_select_small.cuh"
 
 using namespace sip;
 
@@ -115,6 +116,7 @@ struct Engine : EngineBase {
   // orthogonal-transform l1 sets (NEXT-3): the orthonormal DCT-II
   // of the grid by cuBLAS GEMMs along each axis (plain library GEMMs)
   bool cgv = false;              // vectorised CG kernels (vec, or vec except a separable blur set)
+  bool sel_small = false;        // every radix job small: k_selsmall (one CTA per job)
   size_t smem_bf = 0;
   int g_bf = 1;
   int ndct_sets = 0;
@@ -431,7 +433,13 @@ struct Engine : EngineBase {
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
     // select v2 (sip_select2.cuh): single-rank fp32 runs with a radix job
     // (transform-domain sets: pass 1's round A would count untransformed keys)
-    Pr.selv2 = (vec && sizeof(T) == 4 && nranks == 1 && njobs > 0 && !ndct_sets && !getenv("SIP_SEL_V1")) ? 1 : 0;
+    // small jobs (every radix job <= SEL_SMALL_MAX entries, one rank): one
+    // sorting CTA per job (sip_select_small.cuh)
+    sel_small = nranks == 1 && njobs > 0 && !getenv("SIP_SEL_V1");
+    for (int i = 0; i < P && sel_small; ++i)
+      if (Pr.set[i].job >= 0 && (long long)Pr.set[i].nblk * g.N > SEL_SMALL_MAX) sel_small = false;
+    if (sel_small) CU(cudaFuncSetAttribute(k_selsmall<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)selsmall_smem()));
+    Pr.selv2 = (vec && sizeof(T) == 4 && nranks == 1 && njobs > 0 && !ndct_sets && !sel_small && !getenv("SIP_SEL_V1")) ? 1 : 0;
     if (Pr.selv2) {   // k_selB / k_selC: one resident wave (the candidate regions are per CTA)
       int occ = 0;
       CU(cudaFuncSetAttribute(k_selB<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)selb_smem()));
@@ -866,7 +874,9 @@ struct Engine : EngineBase {
       dct_after_pass1(kpos); mark(KB_DCT);
     }
     if (hc.njobs > 0) {
-      if (Pr.selv2) {   // one streaming pass + candidate rounds (round A ran in pass 1)
+      if (sel_small) {
+        lk(k_selsmall<T>, hc.njobs, BLOCK, selsmall_smem(), Pr); ++launches; mark(KB_SELECT);
+      } else if (Pr.selv2) {   // one streaming pass + candidate rounds (round A ran in pass 1)
         lk(k_selB<T>, g_sel, BLOCK, selb_smem(), Pr); ++launches; mark(KB_SELECT);
         for (int r = 2; r <= 4; ++r) { lk(k_selC<T>, g_sel, BLOCK, 0, Pr, r); ++launches; mark(KB_SELECT); }
       } else {
