@@ -789,6 +789,12 @@ struct Engine : EngineBase {
   // the scalar kernels (sip_kernels.cuh) for general shapes, the blur
   // operator and n_cg > MAXCG (no ring slot per step)
   bool lean_cg() const { return cgv && Pr.defer_x; }
+  // small grids: one CTA runs the CG loop (at most SMALL_CG_CHUNKS 16-byte chunks)
+  static constexpr int SMALL_CG_CHUNKS = 4096;
+  bool small_cg() const {
+    return lean_cg() && nranks == 1 && !Pr.has[PRIM_F] && Pr.g.N / VT<T>::W <= SMALL_CG_CHUNKS &&
+           !getenv("SIP_NO_SMALL_CG");
+  }
   const bool sel_debug = getenv("SIP_SEL_DEBUG") != nullptr;
   void launch_cg1(int j) {
     if (lean_cg()) {
@@ -857,6 +863,11 @@ struct Engine : EngineBase {
     if (prof && pev_used == 0) mark(-1);
     if (Pr.has[PRIM_F]) { launch_blur(0, 0); mark(KB_BLUR); }
     launch_rhs(); mark(KB_RHS);
+    if (small_cg()) {   // the whole CG loop in one CTA (small grids)
+      if (ndim == 3) lk(k_cgsmall<T, true>, 1, BLOCK, 0, Pr, n_cg);
+      else lk(k_cgsmall<T, false>, 1, BLOCK, 0, Pr, n_cg);
+      ++launches; mark(KB_CG1);
+    } else
     for (int j = 0; j < n_cg; ++j) {
       if (Pr.has[PRIM_F]) {
         if (lean_cg()) { lk(k_blurF<T>, g_bf, BLOCK, smem_bf, Pr, j); ++launches; }

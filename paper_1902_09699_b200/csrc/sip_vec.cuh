@@ -149,6 +149,121 @@ __device__ __forceinline__ CoefT<T> coefs_present(const Prob<T>& P, const Ctrl& 
   return k;
 }
 
+// plain (coherent) or read-only-path loads: the single-CTA CG re-reads in
+// the same kernel what other threads wrote
+template <class T, bool NC>
+__device__ __forceinline__ void ldv(const T* p, T* o) {
+  if (NC) VT<T>::ldT(p, o);
+  else VT<T>::ldT_s(p, o);
+}
+
+// p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j> over chunks c_first,
+// c_first + c_step, ...; p_j -> ring slot j
+template <class T, bool HY, bool NC>
+__device__ __forceinline__ double cg1_chunks(const Prob<T>& P, const Ctrl& C, int j, int c_first, int c_step) {
+  constexpr int W = VT<T>::W;
+  const Geo& g = P.g;
+  const int nch = g.N / W;
+  const CoefT<T> k = coefs_present(P, C);
+  const T beta = (T)C.beta;
+  const bool usep = j > 0;
+  const T* r = P.r;
+  const T* po = usep ? p_slot(P, j - 1) : P.r;
+  T* pw = p_slot(P, j);
+  const int ncr = g.nx / W;
+  FastDiv dncr;
+  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
+  const int pl = g.plane, nx = g.nx;
+  double pq = 0.0;
+#pragma unroll 1
+  for (int c = c_first; c < nch; c += c_step) {
+    const int pt0 = c * W;
+    const CGLoc<T> L(g, k, c, ncr, dncr);
+    T a0[W], a1[W], a2[W], a3[W], a4[W], b0[W], b1[W], b2[W], b3[W], b4[W];
+    ldv<T, NC>(r + pt0, a0);
+    ldv<T, NC>(r + pt0 - pl, a1);
+    ldv<T, NC>(r + pt0 + pl, a2);
+    if (HY) { ldv<T, NC>(r + pt0 - nx, a3); ldv<T, NC>(r + pt0 + nx, a4); }
+    T rl = r[pt0 - 1], rr_ = r[pt0 + W];
+    if (usep) {
+      ldv<T, NC>(po + pt0, b0);
+      ldv<T, NC>(po + pt0 - pl, b1);
+      ldv<T, NC>(po + pt0 + pl, b2);
+      if (HY) { ldv<T, NC>(po + pt0 - nx, b3); ldv<T, NC>(po + pt0 + nx, b4); }
+      const T bl = po[pt0 - 1], br = po[pt0 + W];
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        a0[e] = a0[e] + beta * b0[e];
+        a1[e] = a1[e] + beta * b1[e];
+        a2[e] = a2[e] + beta * b2[e];
+        if (HY) { a3[e] = a3[e] + beta * b3[e]; a4[e] = a4[e] + beta * b4[e]; }
+      }
+      rl = rl + beta * bl;
+      rr_ = rr_ + beta * br;
+    }
+    T q[W];
+    L.template apply<W>(a0, a1, a2, a3, a4, rl, rr_, HY, q);
+    if (P.ub) {   // the data operator's term, c_F G^T S G p_j (k_blurF)
+      T u[W];
+      ldv<T, NC>(P.ub + pt0, u);
+#pragma unroll
+      for (int e = 0; e < W; ++e) q[e] += u[e];
+    }
+    VT<T>::stT(pw + pt0, a0);
+    T s = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) s += a0[e] * q[e];
+    pq += (double)s;
+  }
+  return pq;
+}
+
+// r -= alpha C p_j and <r, r> over chunks c_first, c_first + c_step, ...
+template <class T, bool HY, bool NC>
+__device__ __forceinline__ double cg2_chunks(const Prob<T>& P, const Ctrl& C, int j, int c_first, int c_step) {
+  constexpr int W = VT<T>::W;
+  const Geo& g = P.g;
+  const int nch = g.N / W;
+  const CoefT<T> k = coefs_present(P, C);
+  const T alpha = (T)C.alpha;
+  const T* p = p_slot(P, j);
+  const int ncr = g.nx / W;
+  FastDiv dncr;
+  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
+  const int pl = g.plane, nx = g.nx;
+  double rr = 0.0;
+#pragma unroll 1
+  for (int c = c_first; c < nch; c += c_step) {
+    const int pt0 = c * W;
+    const CGLoc<T> L(g, k, c, ncr, dncr);
+    T a0[W], a1[W], a2[W], a3[W], a4[W], rv[W];
+    ldv<T, NC>(p + pt0, a0);
+    ldv<T, NC>(p + pt0 - pl, a1);
+    ldv<T, NC>(p + pt0 + pl, a2);
+    if (HY) { ldv<T, NC>(p + pt0 - nx, a3); ldv<T, NC>(p + pt0 + nx, a4); }
+    const T xl = p[pt0 - 1], xr = p[pt0 + W];
+    if (NC) VT<T>::ldcs(P.r + pt0, rv);
+    else VT<T>::ldT_s(P.r + pt0, rv);
+    T q[W];
+    L.template apply<W>(a0, a1, a2, a3, a4, xl, xr, HY, q);
+    if (P.ub) {
+      T u[W];
+      ldv<T, NC>(P.ub + pt0, u);
+#pragma unroll
+      for (int e = 0; e < W; ++e) q[e] += u[e];
+    }
+    T s = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      rv[e] = rv[e] - alpha * q[e];
+      s += rv[e] * rv[e];
+    }
+    VT<T>::stT(P.r + pt0, rv);
+    rr += (double)s;
+  }
+  return rr;
+}
+
 // k_cg1f(j): p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j>; p_j -> slot j
 template <class T, bool HY>
 __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
@@ -168,57 +283,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
   if (!C.cg_active) return;
   __shared__ double sh[NWARP + 1];
   __shared__ double out[1];
-  const CoefT<T> k = coefs_present(P, C);
-  const T beta = (T)C.beta;
-  const bool usep = j > 0;
-  const T* r = P.r;
-  const T* po = usep ? p_slot(P, j - 1) : P.r;
-  T* pw = p_slot(P, j);
-  const int ncr = g.nx / W;
-  FastDiv dncr;
-  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
-  const int pl = g.plane, nx = g.nx;
-  double pq = 0.0;
-#pragma unroll 1
-  for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
-    const int pt0 = c * W;
-    const CGLoc<T> L(g, k, c, ncr, dncr);
-    T a0[W], a1[W], a2[W], a3[W], a4[W], b0[W], b1[W], b2[W], b3[W], b4[W];
-    VT<T>::ldT(r + pt0, a0);
-    VT<T>::ldT(r + pt0 - pl, a1);
-    VT<T>::ldT(r + pt0 + pl, a2);
-    if (HY) { VT<T>::ldT(r + pt0 - nx, a3); VT<T>::ldT(r + pt0 + nx, a4); }
-    T rl = r[pt0 - 1], rr_ = r[pt0 + W];
-    if (usep) {
-      VT<T>::ldT(po + pt0, b0);
-      VT<T>::ldT(po + pt0 - pl, b1);
-      VT<T>::ldT(po + pt0 + pl, b2);
-      if (HY) { VT<T>::ldT(po + pt0 - nx, b3); VT<T>::ldT(po + pt0 + nx, b4); }
-      const T bl = po[pt0 - 1], br = po[pt0 + W];
-#pragma unroll
-      for (int e = 0; e < W; ++e) {
-        a0[e] = a0[e] + beta * b0[e];
-        a1[e] = a1[e] + beta * b1[e];
-        a2[e] = a2[e] + beta * b2[e];
-        if (HY) { a3[e] = a3[e] + beta * b3[e]; a4[e] = a4[e] + beta * b4[e]; }
-      }
-      rl = rl + beta * bl;
-      rr_ = rr_ + beta * br;
-    }
-    T q[W];
-    L.template apply<W>(a0, a1, a2, a3, a4, rl, rr_, HY, q);
-    if (P.ub) {   // the data operator's term, c_F G^T S G p_j (k_blurF)
-      T u[W];
-      VT<T>::ldT(P.ub + pt0, u);
-#pragma unroll
-      for (int e = 0; e < W; ++e) q[e] += u[e];
-    }
-    VT<T>::stT(pw + pt0, a0);
-    T s = 0;
-#pragma unroll
-    for (int e = 0; e < W; ++e) s += a0[e] * q[e];
-    pq += (double)s;
-  }
+  double pq = cg1_chunks<T, HY, true>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
   pq = block_sum(pq, sh);
   if (threadIdx.x == 0) P.partials[blockIdx.x] = pq;
   if (last_block(P.counter)) {
@@ -235,49 +300,11 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
 template <class T, bool HY>
 __global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
   pdl_begin();
-  constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
   if (C.stopped || !C.cg_active) return;
   __shared__ double sh[NWARP + 1];
   __shared__ double out[1];
-  const Geo& g = P.g;
-  const int nch = g.N / W;
-  const CoefT<T> k = coefs_present(P, C);
-  const T alpha = (T)C.alpha;
-  const T* p = p_slot(P, j);
-  const int ncr = g.nx / W;
-  FastDiv dncr;
-  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
-  const int pl = g.plane, nx = g.nx;
-  double rr = 0.0;
-#pragma unroll 1
-  for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
-    const int pt0 = c * W;
-    const CGLoc<T> L(g, k, c, ncr, dncr);
-    T a0[W], a1[W], a2[W], a3[W], a4[W], rv[W];
-    VT<T>::ldT(p + pt0, a0);
-    VT<T>::ldT(p + pt0 - pl, a1);
-    VT<T>::ldT(p + pt0 + pl, a2);
-    if (HY) { VT<T>::ldT(p + pt0 - nx, a3); VT<T>::ldT(p + pt0 + nx, a4); }
-    const T xl = p[pt0 - 1], xr = p[pt0 + W];
-    VT<T>::ldcs(P.r + pt0, rv);
-    T q[W];
-    L.template apply<W>(a0, a1, a2, a3, a4, xl, xr, HY, q);
-    if (P.ub) {
-      T u[W];
-      VT<T>::ldT(P.ub + pt0, u);
-#pragma unroll
-      for (int e = 0; e < W; ++e) q[e] += u[e];
-    }
-    T s = 0;
-#pragma unroll
-    for (int e = 0; e < W; ++e) {
-      rv[e] = rv[e] - alpha * q[e];
-      s += rv[e] * rv[e];
-    }
-    VT<T>::stT(P.r + pt0, rv);
-    rr += (double)s;
-  }
+  double rr = cg2_chunks<T, HY, true>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
   rr = block_sum(rr, sh);
   if (threadIdx.x == 0) P.partials[blockIdx.x] = rr;
   if (last_block(P.counter)) {
@@ -287,6 +314,38 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<
       if (P.nranks > 1) publish(P, out, 1, 0, 1);
       else fin_cg2(C, out, j);
     }
+  }
+}
+
+// k_cgsmall: the whole CG loop of a small grid (one rank) in ONE CTA, the
+// block barrier in place of the kernel boundaries: the same chunk bodies,
+// block sums and finalisers (fin_cg1 / fin_cg2, Eq. 25) as k_cg1f / k_cg2f,
+// 2 n_cg launches -> 1 (C1 and the tiny cases are latency-bound)
+template <class T, bool HY>
+__global__ void __launch_bounds__(BLOCK) k_cgsmall(const __grid_constant__ Prob<T> P, int n_cg) {
+  constexpr int W = VT<T>::W;
+  Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  __shared__ double sh[NWARP + 1];
+  const int nch = P.g.N / W;
+  if (C.zero_x) {   // b = 0 gives x = 0
+    for (int c = threadIdx.x; c < nch; c += BLOCK) {
+      T z[W] = {};
+      VT<T>::stT(P.x + c * W, z);
+    }
+    return;
+  }
+  for (int j = 0; j < n_cg; ++j) {
+    if (!C.cg_active) break;
+    double pq = cg1_chunks<T, HY, false>(P, C, j, threadIdx.x, BLOCK);
+    pq = block_sum(pq, sh);
+    if (threadIdx.x == 0) fin_cg1(C, &pq, j);
+    __syncthreads();
+    if (!C.cg_active) break;
+    double rr = cg2_chunks<T, HY, false>(P, C, j, threadIdx.x, BLOCK);
+    rr = block_sum(rr, sh);
+    if (threadIdx.x == 0) fin_cg2(C, &rr, j);
+    __syncthreads();
   }
 }
 
