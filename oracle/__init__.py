@@ -23,7 +23,7 @@ _SRC = os.path.join(_HERE, "sipref.c")
 _LIB = os.path.join(_HERE, "libsipref.so")
 
 OPS = {"I": 0, "DZ": 1, "DY": 2, "DX": 3, "TV": 4, "BLUR_MASK": 5}
-KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6, "dct_l1": 7}
+KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6, "dct_l1": 7, "haar_l1": 8}
 BRANCH = {0: "both", 1: "alpha", 2: "beta", 3: "none", -1: "-"}
 
 
@@ -232,6 +232,15 @@ def dct(shape, x, inverse=False):
     x = _f64(x).ravel()
     y = np.zeros_like(x)
     lib().sipref_dct(C.byref(g), int(bool(inverse)), _dp(x), _dp(y))
+    return y
+
+
+def haar(shape, x, inverse=False):
+    """orthonormal full-depth Haar transform along every axis (or its inverse)"""
+    g = make_grid(shape)
+    x = _f64(x).ravel()
+    y = np.zeros_like(x)
+    lib().sipref_haar(C.byref(g), int(bool(inverse)), _dp(x), _dp(y))
     return y
 
 

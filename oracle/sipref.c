@@ -465,6 +465,57 @@ void sipref_dct(const sipref_grid *g, int inverse, const double *x, double *y) {
   dct_axis(nz, 1, ny * nx, 0, ny * nx, inverse, y);            /* z: stride plane */
 }
 
+/* Orthonormal Haar wavelet transform (the paper's "wavelet" example of an
+   orthogonal transform; reading L30), full depth, along one axis
+   of length L = 2^J: the pyramid step on the leading n entries
+       a_i = (u_{2i} + u_{2i+1}) / sqrt(2),  d_i = (u_{2i} - u_{2i+1}) / sqrt(2)
+   stores [a, d] and repeats on a with n/2 until n = 1; the output is
+   [a_J, d_J, d_{J-1}, ..., d_1].  The inverse undoes the steps in reverse
+   order: u_{2i} = (a_i + d_i) / sqrt(2), u_{2i+1} = (a_i - d_i) / sqrt(2). */
+static void haar_axis(int64_t L, int64_t count, int64_t st, int64_t outer_st, int64_t inner, int inverse,
+                      double *a) {
+  double *u = dalloc(L), *t = dalloc(L);
+  const double r2 = sqrt(0.5);
+  for (int64_t o = 0; o < count; ++o)
+    for (int64_t in = 0; in < inner; ++in) {
+      double *p = a + o * outer_st + in;
+      for (int64_t k = 0; k < L; ++k) u[k] = p[k * st];
+      if (!inverse) {
+        for (int64_t n = L; n > 1; n /= 2) {
+          for (int64_t i = 0; i < n / 2; ++i) {
+            t[i] = (u[2 * i] + u[2 * i + 1]) * r2;
+            t[n / 2 + i] = (u[2 * i] - u[2 * i + 1]) * r2;
+          }
+          for (int64_t i = 0; i < n; ++i) u[i] = t[i];
+        }
+      } else {
+        for (int64_t n = 2; n <= L; n *= 2) {
+          for (int64_t i = 0; i < n / 2; ++i) {
+            t[2 * i] = (u[i] + u[n / 2 + i]) * r2;
+            t[2 * i + 1] = (u[i] - u[n / 2 + i]) * r2;
+          }
+          for (int64_t i = 0; i < n; ++i) u[i] = t[i];
+        }
+      }
+      for (int64_t k = 0; k < L; ++k) p[k * st] = u[k];
+    }
+  free(u); free(t);
+}
+
+void sipref_haar(const sipref_grid *g, int inverse, const double *x, double *y) {
+  int64_t nz = g->n[0], ny = g->n[1], nx = g->n[2], N = nz * ny * nx;
+  memcpy(y, x, (size_t)N * sizeof(double));
+  haar_axis(nx, nz * ny, 1, nx, 1, inverse, y);
+  if (g->ndim == 3) haar_axis(ny, nz, nx, ny * nx, nx, inverse, y);
+  haar_axis(nz, 1, ny * nx, 0, ny * nx, inverse, y);
+}
+
+/* the set's transform: DCT-II (DCT_L1) or Haar (HAAR_L1) */
+static void transform(const sipref_grid *g, int type, int inverse, const double *x, double *y) {
+  if (type == SIPREF_HAAR_L1) sipref_haar(g, inverse, x, y);
+  else sipref_dct(g, inverse, x, y);
+}
+
 static void project_whole(const sipref_set *s, int64_t M, const double *w, double *y);
 
 /* fiber length (reading L28): nx (nx - 1 for D_x) for x-fibers, nz
@@ -527,12 +578,13 @@ static void project_whole(const sipref_set *s, int64_t M, const double *w, doubl
       break;
     }
     case SIPREF_CARD: proj_card(M, w, s->k, y); break;
-    case SIPREF_DCT_L1: {    /* D^T P_l1(D w) */
+    case SIPREF_DCT_L1:
+    case SIPREF_HAAR_L1: {   /* D^T P_l1(D w) */
       sipref_grid gg = s->tgrid;
       double *c1 = dalloc(M), *c2 = dalloc(M);
-      sipref_dct(&gg, 0, w, c1);
+      transform(&gg, s->type, 0, w, c1);
       proj_l1(M, c1, s->sigma, c2);
-      sipref_dct(&gg, 1, c2, y);
+      transform(&gg, s->type, 1, c2, y);
       free(c1); free(c2);
       break;
     }
@@ -705,10 +757,10 @@ void sipref_resolve_set(const sipref_grid *g, const sipref_set *in, const double
     out->sigma_lo = in->sigma_lo * n2;
     out->sigma_hi = in->sigma_hi * n2;
   }
-  if (in->type == SIPREF_DCT_L1) {    /* sigma = frac x ||D m||_1 (reading L30) */
+  if (in->type == SIPREF_DCT_L1 || in->type == SIPREF_HAAR_L1) {   /* sigma = frac x ||D m||_1 (reading L30) */
     double *am = dalloc(M), *cm = dalloc(M), n1d = 0.0;
     sipref_apply_A(g, in, m, am);
-    sipref_dct(g, 0, am, cm);
+    transform(g, in->type, 0, am, cm);
     for (int64_t j = 0; j < M; ++j) n1d += fabs(cm[j]);
     out->sigma = in->sigma * n1d;
     free(am); free(cm);

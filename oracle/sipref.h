@@ -28,7 +28,8 @@ extern "C" {
 enum { SIPREF_OP_I = 0, SIPREF_OP_DZ = 1, SIPREF_OP_DY = 2, SIPREF_OP_DX = 3,
        SIPREF_OP_TV = 4, SIPREF_OP_BLUR_MASK = 5 };
 enum { SIPREF_BOUNDS = 0, SIPREF_L1 = 1, SIPREF_L2 = 2, SIPREF_ANNULUS = 3,
-       SIPREF_CARD = 4, SIPREF_RANK = 5, SIPREF_NUCLEAR = 6, SIPREF_DCT_L1 = 7 };
+       SIPREF_CARD = 4, SIPREF_RANK = 5, SIPREF_NUCLEAR = 6, SIPREF_DCT_L1 = 7,
+       SIPREF_HAAR_L1 = 8 };
 
 typedef struct {
   int ndim;          /* 2 or 3 */
@@ -55,7 +56,7 @@ typedef struct {
                         independently ("each row/column
                         independently"; NEXT-1).  Single-block operators.   */
   int64_t fib_len;   /* fiber length (set by sipref_fiber_len)               */
-  sipref_grid tgrid; /* DCT_L1: the grid of the transform (set by resolve)   */
+  sipref_grid tgrid; /* DCT_L1 / HAAR_L1: the grid of the transform (resolve) */
   int64_t mrows, mcols;  /* RANK / NUCLEAR: the operator's output viewed as
                         matrices of mrows x mcols (row-major runs of the
                         compact layout): 2D grids one matrix (z, x), 3D grids
@@ -96,6 +97,9 @@ void sipref_default_options(sipref_options *o);
 /* orthonormal DCT-II of a grid field along every axis (y = D x) or its
    inverse (x = D^T y); NEXT-3's transform-domain l1 set, reading L30 */
 void sipref_dct(const sipref_grid *g, int inverse, const double *x, double *y);
+/* orthonormal full-depth Haar wavelet transform along every axis (every
+   length a power of two), y = H x, or its inverse; the HAAR_L1 set */
+void sipref_haar(const sipref_grid *g, int inverse, const double *x, double *y);
 
 /* matrix view of an operator's output for RANK / NUCLEAR sets (reading
    L29): rows x cols of one matrix; the number of matrices is M / (rows cols) */

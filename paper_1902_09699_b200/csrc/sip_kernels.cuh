@@ -65,7 +65,6 @@ struct Prob {
   double gz_[MAXTAPS / 9], gx[MAXTAPS / 9];   // the blur's separable factors, K[r][c] = gz_[r] gx[c]
   double* svdX;                   // rank / nuclear sets: fp64 Jacobi scratch, X (m x n) per matrix
   double* svdV;                   //   and V (n x n) per matrix
-  unsigned* gbar;                 // grid barrier of k_mich: arrivals, generation
   int poison;                     // SIP_POISON: k_init writes NaN into fields that are written before read
   int init_zero;                  // k_init zeroes every state field (scalar kernels)
   double* fibv;                   // z slabs: this rank's fiber-set sums (4 per set), added to pass 2's

@@ -507,8 +507,6 @@ struct Engine : EngineBase {
     Pr.poison = getenv("SIP_POISON") ? 1 : 0;
     Pr.init_zero = vec ? 0 : 1;
     Pr.fibv = (nfib_sets && nranks > 1) ? dalloc<double>(4 * MAXP) : nullptr;
-    Pr.gbar = dalloc<unsigned>(2);
-    CU(cudaMemsetAsync(Pr.gbar, 0, 2 * sizeof(unsigned), stream));
     const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cgf, g_cg2f, g_rhsf, g_fib, g_fibw, g_svd});
     Pr.partials = dalloc<double>(std::max((size_t)(gmax + 2) * (nv1 + 8), (size_t)(g_sel + 2) * MAXJOBS * 3));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)

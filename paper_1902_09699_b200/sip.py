@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libsip.so")
+# SIP_LIBPATH: another in-tree build of the same library (A/B timing tools)
+_LIBPATH = os.environ.get("SIP_LIBPATH") or os.path.join(_HERE, "libsip.so")
 
 SIP_OK = 0
 SIP_NOT_CONVERGED = 1

@@ -53,6 +53,26 @@ def test_project_set_svd(dtype, shape, op, kind):
     g.close()
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_rank_ties_to_lowest_index(dtype):
+    """equal singular values are ranked by column index (reading L29), the
+    oracle's pin test_rank_ties_to_lowest_index on an 8 x 8 diagonal"""
+    d = np.array([5.0, 5.0, 3.0, 3.0, 3.0, 1.0, 1.0, 1.0])
+    for k in (1, 3, 4):
+        sd = SetDef("I", "rank", k=k)
+        g = mk((8, 8), [sd], dtype)
+        m = torch.zeros((8, 8), dtype=TD[dtype], device="cuda")
+        x = torch.empty_like(m)
+        g.project(m, x, max_iter=1)
+        wd = torch.tensor(np.diag(d).ravel(), dtype=TD[dtype], device="cuda")
+        y = torch.empty_like(wd)
+        g.project_set(0, wd, y)
+        ref = O.project(sd, np.diag(d).ravel(), shape=(8, 8))
+        np.testing.assert_array_equal(ref, np.diag(np.where(np.arange(8) < k, d, 0.0)).ravel())
+        np.testing.assert_array_equal(y.double().cpu().numpy(), ref)
+        g.close()
+
+
 def _prob(kind, shape, dtype):
     m = G.tiny_model(140 + len(shape), shape)
     sets = [SetDef("I", "bounds", lo=float(m.min()) + 100.0, hi=float(m.max()) - 100.0)]

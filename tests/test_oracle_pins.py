@@ -761,6 +761,18 @@ def test_rank_projection_is_eckart_young(shape, op):
     np.testing.assert_allclose(O.project(sd, y, shape=shape), y, atol=1e-12)        # idempotent
 
 
+def test_rank_ties_to_lowest_index():
+    """reading L29: equal singular values are ranked by index, so rank 1 of
+    diag(2, 2, 1) keeps the first column's direction: diag(2, 0, 0) (a
+    diagonal matrix needs no Jacobi rotation, the column order is the
+    matrix's own)"""
+    a = np.diag([2.0, 2.0, 1.0])
+    y = O.project(SetDef("I", "rank", k=1), a.ravel(), shape=(3, 3)).reshape(3, 3)
+    np.testing.assert_array_equal(y, np.diag([2.0, 0.0, 0.0]))
+    y2 = O.project(SetDef("I", "rank", k=2), a.ravel(), shape=(3, 3)).reshape(3, 3)
+    np.testing.assert_array_equal(y2, np.diag([2.0, 2.0, 0.0]))
+
+
 def test_nuclear_projection_worked_example_and_numpy():
     """diag(3, 2, 1) onto {||A||_* <= 3}: theta = 1, singular values (2, 1, 0)
     (the simplex projection of Table 1's nuclear-norm row); random matrices
@@ -890,3 +902,81 @@ def test_oracle_dykstra_counts_l1_projections():
     assert d["iterations"] == 5
     np.testing.assert_array_equal(d["l1_proj"], d["inner_iters"][:, 1])
     assert (d["l1_proj"] >= 1).all()
+
+
+def _haar_matrix(L):
+    """the orthonormal Haar matrix by its Kronecker recursion (a closed form,
+    not the oracle's pyramid): H_1 = [1], H_2n = [H_n (x) [1, 1]; I_n (x) [1, -1]] / sqrt(2)"""
+    H = np.ones((1, 1))
+    while H.shape[0] < L:
+        n = H.shape[0]
+        H = np.vstack([np.kron(H, [1.0, 1.0]), np.kron(np.eye(n), [1.0, -1.0])]) / np.sqrt(2.0)
+    return H
+
+
+def _haar_sep(x):
+    """the separable transform: the Haar matrix applied along every axis"""
+    y = np.asarray(x, dtype=np.float64)
+    for ax in range(y.ndim):
+        y = np.moveaxis(np.tensordot(_haar_matrix(y.shape[ax]), np.moveaxis(y, ax, 0), axes=1), 0, ax)
+    return y
+
+
+@pytest.mark.parametrize("shape", [(4, 4), (8, 16), (2, 4, 8)])
+def test_haar_against_kronecker_matrix(shape):
+    """the oracle's Haar pyramid ("wavelet", reading L30) against the
+    Kronecker-recursion Haar matrix along every axis, the inverse, Parseval"""
+    r = np.random.default_rng(sum(shape))
+    x = r.normal(size=shape)
+    c = O.haar(shape, x)
+    np.testing.assert_allclose(c.reshape(shape), _haar_sep(x), atol=1e-13)
+    np.testing.assert_allclose(O.haar(shape, c, inverse=True).reshape(shape), x, atol=1e-13)
+    assert np.linalg.norm(c) == pytest.approx(np.linalg.norm(x), rel=1e-14)
+
+
+def test_haar_worked_examples():
+    """4 x 4 by hand: a constant 1 gives the single coefficient sqrt(16) = 4;
+    x = e_(0,0) - e_(0,1): the row step gives d_1[0] = (1 - (-1)) / sqrt(2) =
+    sqrt(2) at x-position 2, then column 2 = (sqrt(2), 0, 0, 0) -> a = (1, 0),
+    d = (1, 0) -> [1/sqrt(2), 1/sqrt(2), 1, 0]"""
+    c = O.haar((4, 4), np.ones(16)).reshape(4, 4)
+    ref = np.zeros((4, 4))
+    ref[0, 0] = 4.0
+    np.testing.assert_allclose(c, ref, atol=1e-15)
+    x = np.zeros((4, 4))
+    x[0, 0], x[0, 1] = 1.0, -1.0
+    c = O.haar((4, 4), x).reshape(4, 4)
+    ref = np.zeros((4, 4))
+    ref[:, 2] = [np.sqrt(0.5), np.sqrt(0.5), 1.0, 0.0]
+    np.testing.assert_allclose(c, ref, atol=1e-15)
+
+
+def test_haar_l1_projection_closed_form_and_dykstra():
+    """P_V(x) = H^T P_l1(H x) with the Kronecker Haar matrix and an
+    independent l1-ball projection; relative sigma from ||H m||_1; PARSDMM
+    box + Haar-l1 reaches parallel Dykstra's point (Algorithm 4)"""
+    shape = (8, 16)
+    r = np.random.default_rng(23)
+    x = r.normal(size=shape)
+    n1 = np.abs(_haar_sep(x)).sum()
+    sd = SetDef("I", "haar_l1", sigma=0.3 * n1)
+    y = O.project(sd, x.ravel(), shape=shape)
+    c = _haar_sep(x).ravel()
+    lam = _l1_ball_sorted(np.abs(c), 0.3 * n1)
+    Hz, Hx = _haar_matrix(shape[0]), _haar_matrix(shape[1])
+    ref = (Hz.T @ (np.sign(c) * lam).reshape(shape) @ Hx).ravel()
+    np.testing.assert_allclose(y, ref, atol=1e-9)
+    np.testing.assert_allclose(O.project(sd, y, shape=shape), y, atol=1e-12)
+    s, _, _, _ = O.resolve_set(shape, SetDef("I", "haar_l1", sigma=0.3, relative=True), x)
+    assert s == pytest.approx(0.3 * n1, rel=1e-13)
+    m = r.normal(size=shape) * 3.0
+    sig = 0.4 * np.abs(_haar_sep(m)).sum()
+
+    def p_haar(z):
+        cz = _haar_sep(z)
+        lz = _l1_ball_sorted(np.abs(cz).ravel(), sig).reshape(shape)
+        return Hz.T @ (np.sign(cz) * lz) @ Hx
+    dref = _dykstra(m, [lambda z: np.clip(z, -2.0, 2.0), p_haar])
+    sets = [SetDef("I", "bounds", lo=-2.0, hi=2.0), SetDef("I", "haar_l1", sigma=sig)]
+    t = O.parsdmm(shape, sets, m, eps_evol=1e-10, eps_feas=1e-10, n_cg=50, max_iter=50000)
+    assert O.relres(t.x, dref) < 1e-6

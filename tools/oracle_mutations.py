@@ -47,7 +47,10 @@ MUTATIONS = [
     ("cg_no_eq25", "if (eq25 && sqrt(rr) / bn < tol) break;", "(void)tol;"),
     ("eq25_factor", "double tol = 0.1 * sqrt(rr) / bn;", "double tol = 0.5 * sqrt(rr) / bn;"),
     ("l1_theta_index", "double t = (cs - sigma) / (double)(j + 1);", "double t = (cs - sigma) / (double)(j + 2);"),
-    ("card_ties_high_index", "return (a->i > b->i) - (a->i < b->i);", "return (a->i < b->i) - (a->i > b->i);"),
+    ("card_ties_high_index", "static int cmp_keyidx(const void *pa, const void *pb) {\n  const keyidx *a = (const keyidx *)pa, *b = (const keyidx *)pb;\n  if (a->a > b->a) return -1;\n  if (a->a < b->a) return 1;\n  return (a->i > b->i) - (a->i < b->i);",
+     "static int cmp_keyidx(const void *pa, const void *pb) {\n  const keyidx *a = (const keyidx *)pa, *b = (const keyidx *)pb;\n  if (a->a > b->a) return -1;\n  if (a->a < b->a) return 1;\n  return (a->i < b->i) - (a->i > b->i);"),
+    ("rank_ties_high_index", "static int cmp_sv(const void *pa, const void *pb) {\n  const keyidx *a = (const keyidx *)pa, *b = (const keyidx *)pb;\n  if (a->a > b->a) return -1;\n  if (a->a < b->a) return 1;\n  return (a->i > b->i) - (a->i < b->i);",
+     "static int cmp_sv(const void *pa, const void *pb) {\n  const keyidx *a = (const keyidx *)pa, *b = (const keyidx *)pb;\n  if (a->a > b->a) return -1;\n  if (a->a < b->a) return 1;\n  return (a->i < b->i) - (a->i > b->i);"),
     ("dz_adj_sign", "if (iz >= 1) a += y[((iz - 1) * g->n[1] + iy) * g->n[2] + ix];",
      "if (iz >= 1) a -= y[((iz - 1) * g->n[1] + iy) * g->n[2] + ix];"),
     ("dx_fwd_h", "(x[IDX(g, iz, iy, ix + 1)] - x[IDX(g, iz, iy, ix)]) / g->h[2];",
@@ -68,6 +71,18 @@ MUTATIONS = [
     ("nuclear_radius_halved", "proj_l1(n, lam, s->sigma, f);", "proj_l1(n, lam, 0.5 * s->sigma, f);"),
     ("matrix_view_3d_rows", "else { *rows = fy; *cols = fx; }", "else { *rows = fz; *cols = fx; }"),
     ("nuclear_relative_l1", "out->sigma = in->sigma * nuc;", "out->sigma = in->sigma * nuc * 1.0001;"),
+    ("dct_dc_unscaled", "double s = kk == 0 ? sqrt(1.0 / (double)L) : sqrt(2.0 / (double)L);",
+     "double s = sqrt(2.0 / (double)L);"),
+    ("dct_inverse_is_forward", "int64_t kk = inverse ? n : k, nn = inverse ? k : n;", "int64_t kk = k, nn = n;"),
+    ("dct_relative_untransformed", "    sipref_dct(g, 0, am, cm);\n    for (int64_t j = 0; j < M; ++j) n1d",
+     "    memcpy(cm, am, (size_t)M * sizeof(double));\n    for (int64_t j = 0; j < M; ++j) n1d"),
+    ("haar_unnormalised", "const double r2 = sqrt(0.5);", "const double r2 = 0.5;"),
+    ("haar_one_level", "for (int64_t n = L; n > 1; n /= 2) {", "for (int64_t n = L; n > L / 2 && n > 1; n /= 2) {"),
+    ("haar_inverse_swapped", "t[2 * i + 1] = (u[i] - u[n / 2 + i]) * r2;", "t[2 * i + 1] = (u[n / 2 + i] - u[i]) * r2;"),
+    ("haar_z_axis_skipped", "  haar_axis(nz, 1, ny * nx, 0, ny * nx, inverse, y);\n", ""),
+    ("dykstra_weight", "const double w = 1.0 / (double)p;", "const double w = 1.0 / (double)(p + 1);"),
+    ("dykstra_v_sign", "v[i][j] = x[j] + v[i][j] - y[i][j];", "v[i][j] = x[j] - v[i][j] + y[i][j];"),
+    ("dykstra_l1_count_all", "if (sets[i].type == SIPREF_L1) l1p += it;", "l1p += it;"),
 ]
 
 
