@@ -95,12 +95,17 @@ typedef enum {
                               block operators, min(rows, cols) <= 2048, the
                               vectorised path (nx a multiple of 16 / sizeof),
                               one rank; else SIP_ERR_CONFIG                   */
-  SIP_SET_DCT_L1 = 7       /* ||D x||_1 <= sigma with D the orthonormal DCT-II
+  SIP_SET_DCT_L1 = 7,      /* ||D x||_1 <= sigma with D the orthonormal DCT-II
                               of the grid along every axis, kept inside the
                               set (P_V(x) = D^T P_l1(D x));
                               op must be IDENTITY; relative = 1: sigma is a
                               fraction of ||D m||_1 (reading L30); the
                               vectorised path, one rank (SIP_ERR_CONFIG)      */
+  SIP_SET_HAAR_L1 = 8      /* ||H x||_1 <= sigma with H the orthonormal full-
+                              depth Haar wavelet transform along every axis
+                              (the paper's wavelet example, P:400-402;
+                              reading L30); as DCT_L1, and every axis length
+                              a power of two (else SIP_ERR_CONFIG)            */
 } sip_set_type;
 
 typedef struct {

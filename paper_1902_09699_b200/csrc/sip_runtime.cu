@@ -87,6 +87,7 @@ inline int kind_of(sip_set_type t) {
     case SIP_SET_ANNULUS: return K_ANN;
     case SIP_SET_RANK: return K_RANK;
     case SIP_SET_DCT_L1: return K_L1;
+    case SIP_SET_HAAR_L1: return K_L1;
     case SIP_SET_NUCLEAR: return K_NUC;
     default: return K_CARD;
   }
@@ -121,7 +122,7 @@ struct Engine : EngineBase {
   int g_bf = 1;
   int ndct_sets = 0;
   cublasHandle_t blas = nullptr;
-  T* dctm[3] = {nullptr, nullptr, nullptr};   // column-major DCT matrices of the z, y, x axes
+  T* dctm[2][3] = {};   // column-major transform matrices (DCT-II, Haar) of the z, y, x axes
   T* dtmp = nullptr;                           // one N-field of scratch
   void* blas_ws = nullptr;
   int g_fib = 0, g_fibw = 0, nfib_sort = 0, nfib_warp = 0;
@@ -277,7 +278,7 @@ struct Engine : EngineBase {
                   S.kind == K_RANK || S.kind == K_NUC);
       S.svd = (S.kind == K_RANK || S.kind == K_NUC);
       if (S.svd) nsvd_sets++;
-      S.dct = (i < p && s[i].type == SIP_SET_DCT_L1) ? 1 : 0;
+      S.dct = i >= p ? 0 : s[i].type == SIP_SET_DCT_L1 ? 1 : s[i].type == SIP_SET_HAAR_L1 ? 2 : 0;
       if (S.dct) ndct_sets++;
       S.job = S.sjob = -1;
       S.fib = (i < p) ? s[i].fib : 0;
@@ -558,17 +559,40 @@ struct Engine : EngineBase {
   // ---- orthonormal DCT-II along every axis (reading L30) ---------------
   void setup_dct() {
     const int n[3] = {nz, ny, nx};
-    for (int a = 0; a < 3; ++a) {
-      if (a == 1 && ndim == 2) continue;
-      const int L = n[a];
-      std::vector<T> h((size_t)L * L);
-      for (int k = 0; k < L; ++k)       // column-major D(k, j): row k = frequency, column j = sample
-        for (int j = 0; j < L; ++j) {
-          const double sc = k == 0 ? std::sqrt(1.0 / L) : std::sqrt(2.0 / L);
-          h[(size_t)k + (size_t)j * L] = (T)(sc * std::cos(M_PI * (2.0 * j + 1.0) * k / (2.0 * L)));
+    bool want[2] = {false, false};
+    for (int i = 0; i < p; ++i)
+      if (Pr.set[i].dct) want[Pr.set[i].dct - 1] = true;
+    for (int tk = 0; tk < 2; ++tk) {
+      if (!want[tk]) continue;
+      for (int a = 0; a < 3; ++a) {
+        if (a == 1 && ndim == 2) continue;
+        const int L = n[a];
+        std::vector<double> h((size_t)L * L, 0.0);   // column-major D(k, j): row k = coefficient, column j = sample
+        if (tk == 0) {
+          for (int k = 0; k < L; ++k)
+            for (int j = 0; j < L; ++j) {
+              const double sc = k == 0 ? std::sqrt(1.0 / L) : std::sqrt(2.0 / L);
+              h[(size_t)k + (size_t)j * L] = sc * std::cos(M_PI * (2.0 * j + 1.0) * k / (2.0 * L));
+            }
+        } else {
+          // Haar basis, coefficient order [a_J, d_J, ..., d_1]: row 0 is the
+          // constant 1/sqrt(L); the detail function at scale 2^s (support
+          // 2^s samples starting at q 2^s) is +2^(-s/2) on the first half,
+          // -2^(-s/2) on the second; its row is L / 2^s + q
+          for (int j = 0; j < L; ++j) h[(size_t)j * L] = 1.0 / std::sqrt((double)L);
+          for (int w = 2; w <= L; w *= 2) {
+            const double amp = 1.0 / std::sqrt((double)w);
+            for (int q = 0; q < L / w; ++q) {
+              const int k = L / w + q;
+              for (int t = 0; t < w; ++t) h[(size_t)k + (size_t)(q * w + t) * L] = t < w / 2 ? amp : -amp;
+            }
+          }
         }
-      dctm[a] = dalloc<T>((size_t)L * L);
-      CU(cudaMemcpy(dctm[a], h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+        std::vector<T> ht(h.size());
+        for (size_t e = 0; e < h.size(); ++e) ht[e] = (T)h[e];
+        dctm[tk][a] = dalloc<T>((size_t)L * L);
+        CU(cudaMemcpy(dctm[tk][a], ht.data(), ht.size() * sizeof(T), cudaMemcpyHostToDevice));
+      }
     }
     dtmp = dalloc<T>((size_t)Pr.g.N);
     if (cublasCreate(&blas) != CUBLAS_STATUS_SUCCESS) throw SipError{SIP_ERR_CUDA, "cublasCreate"};
@@ -607,16 +631,17 @@ struct Engine : EngineBase {
   // f <- D f (inv = 0) or D^T f (inv = 1), in place through dtmp.  Column-
   // major view of the row-major field: X(x, y, z); the x axis multiplies
   // from the left, y and z from the right.
-  void dct_field(T* f, int inv) {
+  void dct_field(T* f, int inv, int kind) {
+    T* const* dm = dctm[kind - 1];
     const cublasOperation_t L_ = inv ? CUBLAS_OP_T : CUBLAS_OP_N;   // D or D^T from the left
     const cublasOperation_t R_ = inv ? CUBLAS_OP_N : CUBLAS_OP_T;   // D^T or D from the right
-    gemm(L_, CUBLAS_OP_N, nx, ny * nz, nx, dctm[2], nx, f, nx, dtmp, nx);                  // x
+    gemm(L_, CUBLAS_OP_N, nx, ny * nz, nx, dm[2], nx, f, nx, dtmp, nx);                  // x
     if (ndim == 3) {
-      gemm_sb(CUBLAS_OP_N, R_, nx, ny, ny, dtmp, nx, (long long)nx * ny, dctm[1], ny, 0, f, nx,
+      gemm_sb(CUBLAS_OP_N, R_, nx, ny, ny, dtmp, nx, (long long)nx * ny, dm[1], ny, 0, f, nx,
               (long long)nx * ny, nz);                                                        // y, per plane
-      gemm(CUBLAS_OP_N, R_, nx * ny, nz, nz, f, nx * ny, dctm[0], nz, dtmp, nx * ny);        // z
+      gemm(CUBLAS_OP_N, R_, nx * ny, nz, nz, f, nx * ny, dm[0], nz, dtmp, nx * ny);        // z
     } else {
-      gemm(CUBLAS_OP_N, R_, nx, nz, nz, dtmp, nx, dctm[0], nz, f, nx);                       // z
+      gemm(CUBLAS_OP_N, R_, nx, nz, nz, dtmp, nx, dm[0], nz, f, nx);                       // z
       return;
     }
     CU(cudaMemcpyAsync(f, dtmp, (size_t)Pr.g.N * sizeof(T), cudaMemcpyDeviceToDevice, stream));
@@ -629,9 +654,9 @@ struct Engine : EngineBase {
     for (int i = 0; i < p; ++i) {
       SetD<T>& S = Pr.set[i];
       if (!S.dct) continue;
-      dct_field(S.w, 0);                                    // w in the coefficient domain
-      if (kpos % hc.opt.check_every == 0) dct_field(S.s, 0);
-      if (adapt) { dct_field(S.y[par ^ 1], 0); dct_field(S.v[par ^ 1], 0); }   // Alg. 2's k0 snapshots
+      dct_field(S.w, 0, S.dct);                             // w in the coefficient domain
+      if (kpos % hc.opt.check_every == 0) dct_field(S.s, 0, S.dct);
+      if (adapt) { dct_field(S.y[par ^ 1], 0, S.dct); dct_field(S.v[par ^ 1], 0, S.dct); }   // Alg. 2's k0 snapshots
     }
   }
   void dct_after_pass2(int kpos) {
@@ -639,8 +664,8 @@ struct Engine : EngineBase {
     for (int i = 0; i < p; ++i) {
       SetD<T>& S = Pr.set[i];
       if (!S.dct) continue;
-      dct_field(S.y[par ^ 1], 1);                           // y = D^T P_l1(D w), v = D^T v_c (linear)
-      dct_field(S.v[par ^ 1], 1);
+      dct_field(S.y[par ^ 1], 1, S.dct);                    // y = D^T P_l1(D w), v = D^T v_c (linear)
+      dct_field(S.v[par ^ 1], 1, S.dct);
     }
   }
 
@@ -1054,7 +1079,7 @@ struct Engine : EngineBase {
     for (int i = 0; i < p; ++i) {   // relative transform-domain radius: sigma = frac ||D m||_1 (reading L30)
       if (!(Pr.set[i].dct && (*sets)[i].prm.relative)) continue;
       CU(cudaMemcpyAsync(dtmp2(), Pr.m, (size_t)Pr.g.N * sizeof(T), cudaMemcpyDeviceToDevice, stream));
-      dct_field(dtmp2(), 0);
+      dct_field(dtmp2(), 0, Pr.set[i].dct);
       k_dct_sigma<T><<<g_small_(), BLOCK, 0, stream>>>(Pr, i, dtmp2());
       ++launches;
     }
@@ -1991,7 +2016,7 @@ sip_status project_set_E(Engine<T>* e, int set_id, const void* w, void* y) {
     }
     e->hc = c;
     CU(cudaMemcpyAsync(e->d_ctrl, &e->hc, sizeof(Ctrl), cudaMemcpyHostToDevice, e->stream));
-    if (S.dct) e->dct_field(S.w, 0);   // the search and pass 2 act on D w
+    if (S.dct) e->dct_field(S.w, 0, S.dct);   // the search and pass 2 act on D w
     if (S.svd) {   // rank / nuclear-norm set: the batched Jacobi kernel writes y[1]
       const MatView mv = mat_view(e->ndim, e->nz_g, e->ny, e->nx, S.prim[0]);
       k_svdproj<T><<<mv.nmat, SVD_BLOCK, 0, e->stream>>>(e->Pr, set_id, 0);
@@ -2011,7 +2036,7 @@ sip_status project_set_E(Engine<T>* e, int set_id, const void* w, void* y) {
     if (S.fib || S.svd) {
     } else if (e->vec) k_pass2t<T, 2, 2><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
     else k_pass2<T><<<e->g_p2, BLOCK, e->smem_p2, e->stream>>>(e->Pr);
-    if (S.dct) e->dct_field(S.y[1], 1);   // y = D^T P_l1(D w)
+    if (S.dct) e->dct_field(S.y[1], 1, S.dct);   // y = D^T P_l1(D w)
   } else {
     // pointwise: gamma = 0 and v = 0 make x-bar = y_old and w = y_old, so
     // pass1 evaluates y = P(w) on the given w placed in y[0]
@@ -2333,7 +2358,7 @@ sip_status sip_create_grid(int ndim, const int64_t* n, const double* h, sip_dtyp
 sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type type,
                        const sip_set_params* prm, int* set_id) {
   if (!g || !prm) return SIP_ERR_ARG;
-  if (op < SIP_OP_IDENTITY || op > SIP_OP_BLUR_MASK || type < SIP_SET_BOUNDS || type > SIP_SET_DCT_L1)
+  if (op < SIP_OP_IDENTITY || op > SIP_OP_BLUR_MASK || type < SIP_SET_BOUNDS || type > SIP_SET_HAAR_L1)
     return SIP_ERR_ARG;
   if ((int)g->sets.size() >= SIP_MAX_SETS) { g->err = "more than 16 sets"; return SIP_ERR_CONFIG; }
   if (op == SIP_OP_DY && g->ndim != 3) { g->err = "D_y needs a 3D grid"; return SIP_ERR_CONFIG; }
@@ -2392,7 +2417,12 @@ sip_status sip_add_set(sip_grid g, sip_op op, const void* op_desc, sip_set_type 
     } else if (type == SIP_SET_CARDINALITY) {
       if (prm->relative) { if (!(prm->k_frac >= 0 && prm->k_frac <= 1)) return SIP_ERR_PARAM; }
       else if (prm->k < 0 || prm->k > hs.M) return SIP_ERR_PARAM;
-    } else if (type == SIP_SET_DCT_L1) {   // {x : ||D x||_1 <= sigma}, D the grid's orthonormal DCT
+    } else if (type == SIP_SET_DCT_L1 || type == SIP_SET_HAAR_L1) {   // {x : ||D x||_1 <= sigma}, D orthonormal
+      if (type == SIP_SET_HAAR_L1) {
+        const long long ax[3] = {nz, ny, nx};
+        for (int a = 0; a < 3; ++a)
+          if (ax[a] < 1 || (ax[a] & (ax[a] - 1))) { g->err = "Haar l1 sets need every grid axis a power of two"; return SIP_ERR_CONFIG; }
+      }
       if (op != SIP_OP_IDENTITY) { g->err = "transform-domain l1 sets keep the transform inside the set: op must be IDENTITY"; return SIP_ERR_CONFIG; }
       if (g->nranks > 1) { g->err = "transform-domain l1 sets: one rank only"; return SIP_ERR_CONFIG; }
       if (!(prm->sigma >= 0)) return SIP_ERR_PARAM;

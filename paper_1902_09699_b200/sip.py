@@ -22,7 +22,7 @@ SIP_OK = 0
 SIP_NOT_CONVERGED = 1
 SIP_MAX_SETS = 16
 OPS = {"I": 0, "IDENTITY": 0, "DZ": 1, "DY": 2, "DX": 3, "TV": 4, "BLUR_MASK": 5}
-KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6, "dct_l1": 7}
+KINDS = {"bounds": 0, "l1": 1, "l2": 2, "annulus": 3, "card": 4, "rank": 5, "nuclear": 6, "dct_l1": 7, "haar_l1": 8}
 DTYPES = {"f32": 0, "f64": 1}
 
 

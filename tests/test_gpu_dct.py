@@ -1,5 +1,6 @@
 """Orthogonal-transform l1 sets: {x :
-||D x||_1 <= sigma} with D the grid's orthonormal DCT-II, projected as
+||D x||_1 <= sigma} with D the grid's orthonormal DCT-II or full-depth Haar
+wavelet transform (reading L30), projected as
 D^T P_l1(D x) (the transform kept inside the set, A = I).  GPU against the
 oracle: sip_project_set (1e-5 fp32, 1e-10 fp64) and PARSDMM end to end
 (tiny fp64: exact iteration / CG counts; fp32 within 1e-3).  Marked gpu."""
@@ -28,13 +29,17 @@ def mk(shape, sets, dtype):
     return g
 
 
+TRANSFORM = {"dct_l1": O.dct, "haar_l1": O.haar}
+
+
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-@pytest.mark.parametrize("shape", [(48, 64), (96, 32), (6, 20, 16)])
-def test_project_set_dct(dtype, shape):
+@pytest.mark.parametrize("kind,shape", [("dct_l1", (48, 64)), ("dct_l1", (96, 32)), ("dct_l1", (6, 20, 16)),
+                                        ("haar_l1", (32, 64)), ("haar_l1", (128, 16)), ("haar_l1", (8, 16, 32))])
+def test_project_set_dct(dtype, kind, shape):
     r = np.random.default_rng(shape[0])
     w = r.normal(size=int(np.prod(shape))) * 5.0
-    n1 = np.abs(O.dct(shape, w)).sum()
-    sd = SetDef("I", "dct_l1", sigma=0.25 * n1)
+    n1 = np.abs(TRANSFORM[kind](shape, w)).sum()
+    sd = SetDef("I", kind, sigma=0.25 * n1)
     g = mk(shape, [sd], dtype)
     m = torch.zeros(shape, dtype=TD[dtype], device="cuda")
     x = torch.empty_like(m)
@@ -47,16 +52,17 @@ def test_project_set_dct(dtype, shape):
     g.close()
 
 
-def _prob(shape, dtype):
+def _prob(shape, dtype, kind="dct_l1"):
     m = G.tiny_model(160 + len(shape), shape)
     sets = [SetDef("I", "bounds", lo=float(m.min()) + 100.0, hi=float(m.max()) - 100.0),
-            SetDef("I", "dct_l1", sigma=0.6, relative=True)]
+            SetDef("I", kind, sigma=0.6, relative=True)]
     return G.Problem("dct", shape, dtype, m, sets, options=dict(G.DEFAULT_OPTIONS))
 
 
-@pytest.mark.parametrize("shape", [(16, 12), (4, 8, 6)])
-def test_parsdmm_dct_fp64_exact(shape):
-    prob = _prob(shape, "f64")
+@pytest.mark.parametrize("kind,shape", [("dct_l1", (16, 12)), ("dct_l1", (4, 8, 6)), ("haar_l1", (16, 8)),
+                                        ("haar_l1", (4, 8, 8))])
+def test_parsdmm_dct_fp64_exact(kind, shape):
+    prob = _prob(shape, "f64", kind)
     g = mk(shape, prob.sets, "f64")
     m = torch.tensor(prob.m, dtype=torch.float64, device="cuda")
     x = torch.empty_like(m)
@@ -70,9 +76,9 @@ def test_parsdmm_dct_fp64_exact(shape):
     g.close()
 
 
-def test_parsdmm_dct_fp32():
-    shape = (64, 96)
-    prob = _prob(shape, "f32")
+@pytest.mark.parametrize("kind,shape", [("dct_l1", (64, 96)), ("haar_l1", (64, 128))])
+def test_parsdmm_dct_fp32(kind, shape):
+    prob = _prob(shape, "f32", kind)
     g = mk(shape, prob.sets, "f32")
     m = torch.tensor(prob.m, dtype=torch.float32, device="cuda")
     x = torch.empty_like(m)
@@ -87,4 +93,8 @@ def test_dct_refusals():
     g = Grid((16, 16), None, "f32")
     with pytest.raises(Exception):
         g.add_set(SetDef("DZ", "dct_l1", sigma=1.0))
+    g.close()
+    g = Grid((16, 12), None, "f32")
+    with pytest.raises(Exception):
+        g.add_set(SetDef("I", "haar_l1", sigma=1.0))   # 12 is not a power of two
     g.close()
