@@ -113,7 +113,8 @@ struct Engine : EngineBase {
   cudaStream_t stream;
   int nsm = 148;
   int nfib_sets = 0;             // sets applied per fiber (k_fiber)
-  int nsvd_sets = 0, g_svd = 0;  // rank / nuclear-norm sets (sip_svd.cuh): one CTA per matrix
+  int nsvd_sets = 0, g_svd = 0;  // rank / nuclear-norm sets (sip_svd.cuh): a cluster of svd_cl CTAs per matrix
+  int svd_cl[SIP_MAX_SETS] = {};
   // orthogonal-transform l1 sets (NEXT-3): the orthonormal DCT-II
   // of the grid by cuBLAS GEMMs along each axis (plain library GEMMs)
   bool cgv = false;              // vectorised CG kernels (vec, or vec except a separable blur set)
@@ -420,7 +421,26 @@ struct Engine : EngineBase {
         const MatView mv = mat_view(ndim, nz_g, ny, nx, Pr.set[i].prim[0]);
         nx_ = std::max(nx_, (size_t)mv.nmat * mv.m * mv.n);
         nv_ = std::max(nv_, (size_t)mv.nmat * mv.n * mv.n);
-        g_svd = std::max(g_svd, mv.nmat);
+        // few large matrices: a cluster of CTAs per matrix (the column
+        // pairs of a round split over the cluster, sip_svd.cuh)
+        int cl = 1;
+        if (!getenv("SIP_SVD_CL1") && mv.n >= 64)
+          for (int c : {16, 8, 4}) {
+            if (mv.nmat * c > 2 * nsm) continue;
+            if (c > 8) CU(cudaFuncSetAttribute(k_svdproj<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)(mv.nmat * c));
+            cfg.blockDim = dim3((unsigned)SVD_BLOCK);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)c; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at; cfg.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, k_svdproj<T>, &cfg) == cudaSuccess && ncl > 0) { cl = c; break; }
+            cudaGetLastError();
+          }
+        svd_cl[i] = cl;
+        g_svd = std::max(g_svd, mv.nmat * cl);
       }
       Pr.svdX = dalloc<double>(nx_);
       Pr.svdV = dalloc<double>(nv_);
@@ -869,12 +889,25 @@ struct Engine : EngineBase {
   void launch_control() { lk(k_control<T>, 1, BLOCK, 0, Pr); ++launches; }
   // rank / nuclear-norm sets: y, v of every matrix (which 0), the Eq. 26
   // numerator of s on check iterations (which 1; the kernel returns on others)
+  void launch_svd_one(int i, int which, int nmat) {
+    const int cl = std::max(1, svd_cl[i]);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nmat * cl));
+    cfg.blockDim = dim3((unsigned)SVD_BLOCK);
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cl; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = cl > 1 ? 1 : 0;
+    CU(cudaLaunchKernelEx(&cfg, k_svdproj<T>, Pr, i, which, cl));
+  }
   void launch_svd() {
     for (int i = 0; i < p; ++i) {
       if (!Pr.set[i].svd) continue;
       const MatView mv = mat_view(ndim, nz_g, ny, nx, Pr.set[i].prim[0]);
-      lk(k_svdproj<T>, mv.nmat, SVD_BLOCK, 0, Pr, i, 0); ++launches;
-      lk(k_svdproj<T>, mv.nmat, SVD_BLOCK, 0, Pr, i, 1); ++launches;
+      launch_svd_one(i, 0, mv.nmat); ++launches;
+      launch_svd_one(i, 1, mv.nmat); ++launches;
     }
   }
   void launch_fin(int site, int j, int round) {
@@ -1087,7 +1120,7 @@ struct Engine : EngineBase {
       if (!(Pr.set[i].kind == K_NUC && (*sets)[i].prm.relative)) continue;
       if (!init_yv) throw SipError{SIP_ERR_CONFIG, "relative nuclear-norm radius needs y = A m at the start (no warm start / multilevel)"};
       const MatView mv = mat_view(ndim, nz_g, ny, nx, Pr.set[i].prim[0]);
-      k_svdproj<T><<<mv.nmat, SVD_BLOCK, 0, stream>>>(Pr, i, 2);
+      launch_svd_one(i, 2, mv.nmat);
       ++launches;
     }
     run_iterations(max_iter, o.graph_iters, o.n_cg);
@@ -2019,7 +2052,7 @@ sip_status project_set_E(Engine<T>* e, int set_id, const void* w, void* y) {
     if (S.dct) e->dct_field(S.w, 0, S.dct);   // the search and pass 2 act on D w
     if (S.svd) {   // rank / nuclear-norm set: the batched Jacobi kernel writes y[1]
       const MatView mv = mat_view(e->ndim, e->nz_g, e->ny, e->nx, S.prim[0]);
-      k_svdproj<T><<<mv.nmat, SVD_BLOCK, 0, e->stream>>>(e->Pr, set_id, 0);
+      e->launch_svd_one(set_id, 0, mv.nmat);
     } else if (S.fib) {   // per-fiber projection: k_fiberw / k_fiber write y[1]
       if (S.fpath) FiberW<T>::of(S.flen)<<<e->g_fw[set_id], BLOCK, e->smem_fw[set_id], e->stream>>>(e->Pr, set_id);
       else k_fiber<T><<<e->g_fib, BLOCK, e->smem_fib, e->stream>>>(e->Pr);

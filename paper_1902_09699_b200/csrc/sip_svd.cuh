@@ -57,8 +57,97 @@ __device__ __forceinline__ double warp_allsum(double v) {
   return v;
 }
 
+// ---- thread-block cluster helpers (one matrix per cluster of CL CTAs) ----
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// all threads of every CTA of the cluster; release / acquire at cluster scope
+__device__ __forceinline__ void cl_sync(int cl) {
+  if (cl == 1) { __syncthreads(); return; }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of `p` (this CTA's shared memory) in CTA `r` of the cluster
+__device__ __forceinline__ unsigned cl_map(const void* p, unsigned r) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(p), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(r));
+  return ra;
+}
+__device__ __forceinline__ void cl_st(unsigned ra, int v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+__device__ __forceinline__ int cl_ld(unsigned ra) {
+  int v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+  return v;
+}
+
+// One Jacobi step on the column pair (xi, xj) of length m (and the same
+// rotation on V's columns vi, vj of length n), by one warp.  Lane l holds
+// rows l, l + 32, ... (accumulated in that order, as a plain lane loop
+// would); columns of at most 32 R rows stay in registers between the inner
+// products and the rotation (one L2 round trip per column).  Returns whether
+// the pair was rotated.
+template <int R>
+__device__ __forceinline__ void rot_cols(double* a, double* b, int len, int lane, double cs, double sn) {
+  for (int r0 = 0; r0 < len; r0 += 32 * R) {
+    double u[R], v[R];
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int r = r0 + lane + 32 * e;
+      u[e] = r < len ? __ldcg(a + r) : 0.0;
+      v[e] = r < len ? __ldcg(b + r) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int r = r0 + lane + 32 * e;
+      if (r < len) { a[r] = cs * u[e] - sn * v[e]; b[r] = sn * u[e] + cs * v[e]; }
+    }
+  }
+}
+template <int R>
+__device__ __forceinline__ bool jacobi_pair(double* xi, double* xj, double* vi, double* vj, int m, int n, int lane) {
+  double aa = 0.0, bb = 0.0, cc = 0.0;
+  double u[R], v[R];
+  const bool inreg = m <= 32 * R;
+  for (int r0 = 0; r0 < m; r0 += 32 * R) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int r = r0 + lane + 32 * e;
+      u[e] = r < m ? __ldcg(xi + r) : 0.0;
+      v[e] = r < m ? __ldcg(xj + r) : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      if (r0 + lane + 32 * e < m) { aa += u[e] * u[e]; bb += v[e] * v[e]; cc += u[e] * v[e]; }
+    }
+  }
+  aa = warp_allsum(aa); bb = warp_allsum(bb); cc = warp_allsum(cc);
+  if (cc == 0.0 || fabs(cc) <= 1e-15 * sqrt(aa * bb)) return false;
+  const double zeta = (bb - aa) / (2.0 * cc);
+  const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+  const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
+  if (inreg) {
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      const int r = lane + 32 * e;
+      if (r < m) { xi[r] = cs * u[e] - sn * v[e]; xj[r] = sn * u[e] + cs * v[e]; }
+    }
+  } else {
+    rot_cols<R>(xi, xj, m, lane, cs, sn);
+  }
+  rot_cols<R>(vi, vj, n, lane, cs, sn);
+  return true;
+}
+
+// k_svdproj: one matrix of the view per cluster of `cl` CTAs (cl = 1: a
+// plain launch).  The CTAs of a cluster split the column pairs of every
+// round-robin round (cluster barrier between rounds), then each CTA forms
+// the singular values and f / lambda redundantly and writes its share of
+// the output entries.
 template <class T>
-__global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ Prob<T> P, int i, int which) {
+__global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ Prob<T> P, int i, int which, int cl) {
   pdl_begin();
   Ctrl& C = *P.ctrl;
   if (C.stopped) return;
@@ -68,72 +157,63 @@ __global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ P
   const SetD<T>& S = P.set[i];
   const MatView mv = mat_view(g.ndim, g.nz_g, g.ny, g.nx, S.prim[0]);
   const int m = mv.m, n = mv.n;
-  const int b = blockIdx.x;
+  const int crank = cl > 1 ? (int)cl_rank() : 0;
+  const int b = blockIdx.x / cl;
   double* X = P.svdX + (size_t)b * m * n;
   double* V = P.svdV + (size_t)b * n * n;
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   constexpr int NW = SVD_BLOCK / 32;
+  const int ct = crank * SVD_BLOCK + tid, cstep = cl * SVD_BLOCK;   // thread index within the cluster
   __shared__ double lam[SVD_NMAX];
   __shared__ double gsc[SVD_NMAX];
-  __shared__ int s_rot;
+  __shared__ int s_rot[2];
+  __shared__ int s_nz;
+  __shared__ short s_jl[SVD_NMAX];
   __shared__ double sh[NW + 1];
   const T* src = which == 0 ? S.w : (which == 1 ? S.s : S.y[1]);
   // load: column j of X = column j of a (tr = 0) or row j of a (tr = 1)
-  for (int64_t q = tid; q < (int64_t)m * n; q += SVD_BLOCK) {
+  for (int64_t q = ct; q < (int64_t)m * n; q += cstep) {
     const int j = (int)(q / m), r = (int)(q - (int64_t)j * m);
     const int ar = mv.tr ? j : r, ac = mv.tr ? r : j;
     X[q] = (double)src[mat_pt(g, b, ar, ac)];
   }
-  for (int64_t q = tid; q < (int64_t)n * n; q += SVD_BLOCK) V[q] = (q / n == q % n) ? 1.0 : 0.0;
-  __syncthreads();
+  for (int64_t q = ct; q < (int64_t)n * n; q += cstep) V[q] = (q / n == q % n) ? 1.0 : 0.0;
+  if (tid == 0) { s_rot[0] = 0; s_rot[1] = 0; }
+  cl_sync(cl);
   // one-sided Jacobi sweeps, round-robin pairing of n' = n (+1 if odd) players
   const int np = n + (n & 1);
+  const unsigned rot0 = cl > 1 ? cl_map(&s_rot[0], 0) : 0u;
   for (int sweep = 0; sweep < 60 && n > 1; ++sweep) {
-    if (tid == 0) s_rot = 0;
-    __syncthreads();
+    bool rotated = false;
     for (int t = 0; t < np - 1; ++t) {
-      for (int k = wp; k < np / 2; k += NW) {
+      for (int k = crank * NW + wp; k < np / 2; k += cl * NW) {
         int a = k == 0 ? np - 1 : (t + k) % (np - 1);
         int c = (t - k + (np - 1)) % (np - 1);
         if (k == 0) c = t % (np - 1);
         if (a >= n || c >= n) continue;            // the dummy player of odd n
         const int ci = min(a, c), cj = max(a, c);
-        double* xi = X + (size_t)ci * m;
-        double* xj = X + (size_t)cj * m;
-        double aa = 0.0, bb = 0.0, cc = 0.0;
-        for (int r = lane; r < m; r += 32) {
-          const double u = xi[r], v = xj[r];
-          aa += u * u; bb += v * v; cc += u * v;
-        }
-        aa = warp_allsum(aa); bb = warp_allsum(bb); cc = warp_allsum(cc);
-        if (cc == 0.0 || fabs(cc) <= 1e-15 * sqrt(aa * bb)) continue;
-        const double zeta = (bb - aa) / (2.0 * cc);
-        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + tt * tt), sn = cs * tt;
-        for (int r = lane; r < m; r += 32) {
-          const double u = xi[r], v = xj[r];
-          xi[r] = cs * u - sn * v;
-          xj[r] = sn * u + cs * v;
-        }
-        double* vi = V + (size_t)ci * n;
-        double* vj = V + (size_t)cj * n;
-        for (int r = lane; r < n; r += 32) {
-          const double u = vi[r], v = vj[r];
-          vi[r] = cs * u - sn * v;
-          vj[r] = sn * u + cs * v;
-        }
-        if (lane == 0) s_rot = 1;
+        rotated |= jacobi_pair<16>(X + (size_t)ci * m, X + (size_t)cj * m, V + (size_t)ci * n, V + (size_t)cj * n,
+                                   m, n, lane);
       }
-      __syncthreads();
+      cl_sync(cl);
     }
-    if (!s_rot) break;
-    __syncthreads();
+    // did any warp of the cluster rotate in this sweep (flag of this sweep's parity in CTA 0)
+    const int par = sweep & 1;
+    if (rotated && lane == 0) {
+      if (cl > 1) cl_st(rot0 + 4u * par, 1);
+      else s_rot[par] = 1;
+    }
+    cl_sync(cl);
+    const int any = cl > 1 ? cl_ld(rot0 + 4u * par) : s_rot[par];
+    if (crank == 0 && tid == 0) s_rot[par ^ 1] = 0;   // last read a sweep ago (all CTAs passed the barrier)
+    if (!any) break;
   }
-  // singular values
+  cl_sync(cl);   // every CTA has read CTA 0's flag before any CTA can exit
+  // singular values (every CTA of the cluster, the same values)
   for (int j = wp; j < n; j += NW) {
     const double* xj = X + (size_t)j * m;
     double a = 0.0;
-    for (int r = lane; r < m; r += 32) a += xj[r] * xj[r];
+    for (int r = lane; r < m; r += 32) { const double u = __ldcg(xj + r); a += u * u; }
     a = warp_sum(a);
     if (lane == 0) lam[j] = sqrt(a);
   }
@@ -142,7 +222,7 @@ __global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ P
     double a = 0.0;
     for (int j = tid; j < n; j += SVD_BLOCK) a += lam[j];
     a = block_sum(a, sh);
-    if (tid == 0) P.partials[(size_t)b * 4] = a;
+    if (tid == 0) P.partials[(size_t)blockIdx.x * 4] = crank == 0 ? a : 0.0;
   } else {
     // f_j / lambda_j
     const bool rank = S.kind == K_RANK;
@@ -195,6 +275,14 @@ __global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ P
       gsc[j] = (lam[j] > 0.0 && f > 0.0) ? f / lam[j] : 0.0;
     }
     __syncthreads();
+    if (tid == 0) {   // the columns that contribute, in index order
+      int c = 0;
+      for (int j = 0; j < n; ++j)
+        if (gsc[j] != 0.0) s_jl[c++] = (short)j;
+      s_nz = c;
+    }
+    __syncthreads();
+    const int nz = s_nz;
     // P(a) element by element: X diag(g) V^T, mapped back to the field
     const T rho = (T)C.rho[i];
     const int par = C.k & 1;
@@ -202,12 +290,12 @@ __global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ P
     T* yw = S.y[par ^ 1];
     T* vw = S.v[par ^ 1];
     double a_gv = 0.0, a_gg = 0.0, a_vv = 0.0, a_fn = 0.0;
-    for (int64_t q = tid; q < (int64_t)m * n; q += SVD_BLOCK) {
+    for (int64_t q = ct; q < (int64_t)m * n; q += cstep) {
       const int c = (int)(q / m), r = (int)(q - (int64_t)c * m);   // element (r, c) of X-space
       double y = 0.0;
-      for (int j = 0; j < n; ++j) {
-        const double gj = gsc[j];
-        if (gj != 0.0) y += X[(size_t)j * m + r] * gj * V[(size_t)j * n + c];
+      for (int e = 0; e < nz; ++e) {
+        const int j = s_jl[e];
+        y += __ldcg(X + (size_t)j * m + r) * gsc[j] * __ldcg(V + (size_t)j * n + c);
       }
       const int ar = mv.tr ? c : r, ac = mv.tr ? r : c;
       const int64_t pt = mat_pt(g, b, ar, ac);
@@ -230,7 +318,7 @@ __global__ void __launch_bounds__(SVD_BLOCK) k_svdproj(const __grid_constant__ P
     const double p0 = block_sum(a_gv, sh), p1 = block_sum(a_gg, sh), p2 = block_sum(a_vv, sh),
                  p3 = block_sum(a_fn, sh);
     if (tid == 0) {
-      double* pp = P.partials + (size_t)b * 4;
+      double* pp = P.partials + (size_t)blockIdx.x * 4;
       pp[0] = p0; pp[1] = p1; pp[2] = p2; pp[3] = p3;
     }
   }

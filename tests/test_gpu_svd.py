@@ -31,7 +31,9 @@ def mk(shape, sets, dtype):
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("shape,op,kind", [((48, 40), "I", "rank"), ((40, 48), "DZ", "rank"),
                                            ((36, 64), "DX", "nuclear"), ((64, 36), "I", "nuclear"),
-                                           ((6, 20, 16), "I", "rank"), ((5, 12, 24), "DY", "nuclear")])
+                                           ((6, 20, 16), "I", "rank"), ((5, 12, 24), "DY", "nuclear"),
+                                           ((96, 80), "I", "rank"), ((130, 72), "DZ", "nuclear"),
+                                           ((2, 80, 96), "I", "rank")])
 def test_project_set_svd(dtype, shape, op, kind):
     r = np.random.default_rng(len(shape) * 7 + shape[0])
     sd = SetDef(op, kind, k=3, sigma=0.0)
@@ -51,6 +53,33 @@ def test_project_set_svd(dtype, shape, op, kind):
     ref = O.project(sd, wd.double().cpu().numpy(), shape=shape)
     assert O.relres(y.double().cpu().numpy(), ref) <= TOL[dtype], O.relres(y.double().cpu().numpy(), ref)
     g.close()
+
+
+@pytest.mark.parametrize("kind", ["rank", "nuclear"])
+def test_svd_cluster_matches_single_cta(kind, monkeypatch):
+    """min(rows, cols) >= 64 and few matrices: a cluster of CTAs per matrix
+    splits every round's column pairs; the per-pair arithmetic is the one
+    CTA's, so the projection is bitwise identical to SIP_SVD_CL1=1's"""
+    shape = (160, 128)
+    r = np.random.default_rng(44)
+    w = r.normal(size=int(np.prod(shape))) * 3.0
+    sd = SetDef("I", kind, k=5, sigma=0.2 * np.linalg.svd(w.reshape(shape), compute_uv=False).sum())
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("SIP_SVD_CL1", env)
+        g = mk(shape, [sd], "f64")
+        m = torch.zeros(shape, dtype=torch.float64, device="cuda")
+        x = torch.empty_like(m)
+        g.project(m, x, max_iter=1)
+        wd = torch.tensor(w, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(wd)
+        g.project_set(0, wd, y)
+        out.append(y.cpu().numpy())
+        g.close()
+    np.testing.assert_array_equal(out[0], out[1])
+    ref = O.project(sd, w, shape=shape)
+    assert O.relres(out[0], ref) <= 1e-10
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
