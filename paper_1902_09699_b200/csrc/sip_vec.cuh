@@ -157,10 +157,14 @@ __device__ __forceinline__ void ldv(const T* p, T* o) {
   else VT<T>::ldT_s(p, o);
 }
 
-// p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j> over chunks c_first,
-// c_first + c_step, ...; p_j -> ring slot j
+// Energy form of k_cg1's dot: C = c_I I + sum_a c_a D_a^T D_a (+ c_F G^T S G,
+// the ub term), so <p, C p> = c_I ||p||^2 + sum_a c_a ||D_a p||^2 (+ <p, ub>).
+// Each chunk adds its points' forward differences (the pair (i, i+1) belongs
+// to i, absent when i is the last point of the axis), so only the z+1, y+1
+// and x+1 neighbours of p_j are rebuilt from r and p_{j-1} (3 instead of 7
+// positions; every term is >= 0, nothing cancels).  p_j -> ring slot j.
 template <class T, bool HY, bool NC>
-__device__ __forceinline__ double cg1_chunks(const Prob<T>& P, const Ctrl& C, int j, int c_first, int c_step) {
+__device__ __forceinline__ double cg1e_chunks(const Prob<T>& P, const Ctrl& C, int j, int c_first, int c_step) {
   constexpr int W = VT<T>::W;
   const Geo& g = P.g;
   const int nch = g.N / W;
@@ -179,40 +183,46 @@ __device__ __forceinline__ double cg1_chunks(const Prob<T>& P, const Ctrl& C, in
   for (int c = c_first; c < nch; c += c_step) {
     const int pt0 = c * W;
     const CGLoc<T> L(g, k, c, ncr, dncr);
-    T a0[W], a1[W], a2[W], a3[W], a4[W], b0[W], b1[W], b2[W], b3[W], b4[W];
+    T a0[W], az[W], ay[W], b0[W], bz[W], by[W];
     ldv<T, NC>(r + pt0, a0);
-    ldv<T, NC>(r + pt0 - pl, a1);
-    ldv<T, NC>(r + pt0 + pl, a2);
-    if (HY) { ldv<T, NC>(r + pt0 - nx, a3); ldv<T, NC>(r + pt0 + nx, a4); }
-    T rl = r[pt0 - 1], rr_ = r[pt0 + W];
+    ldv<T, NC>(r + pt0 + pl, az);
+    if (HY) ldv<T, NC>(r + pt0 + nx, ay);
+    T ar = r[pt0 + W];
     if (usep) {
       ldv<T, NC>(po + pt0, b0);
-      ldv<T, NC>(po + pt0 - pl, b1);
-      ldv<T, NC>(po + pt0 + pl, b2);
-      if (HY) { ldv<T, NC>(po + pt0 - nx, b3); ldv<T, NC>(po + pt0 + nx, b4); }
-      const T bl = po[pt0 - 1], br = po[pt0 + W];
+      ldv<T, NC>(po + pt0 + pl, bz);
+      if (HY) ldv<T, NC>(po + pt0 + nx, by);
+      const T br = po[pt0 + W];
 #pragma unroll
       for (int e = 0; e < W; ++e) {
         a0[e] = a0[e] + beta * b0[e];
-        a1[e] = a1[e] + beta * b1[e];
-        a2[e] = a2[e] + beta * b2[e];
-        if (HY) { a3[e] = a3[e] + beta * b3[e]; a4[e] = a4[e] + beta * b4[e]; }
+        az[e] = az[e] + beta * bz[e];
+        if (HY) ay[e] = ay[e] + beta * by[e];
       }
-      rl = rl + beta * bl;
-      rr_ = rr_ + beta * br;
+      ar = ar + beta * br;
     }
-    T q[W];
-    L.template apply<W>(a0, a1, a2, a3, a4, rl, rr_, HY, q);
+    VT<T>::stT(pw + pt0, a0);
+    T sI = 0, sz = 0, sy = 0, sx = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      sI += a0[e] * a0[e];
+      const T dz = az[e] - a0[e];
+      sz += dz * dz;
+      if (HY) { const T dy = ay[e] - a0[e]; sy += dy * dy; }
+      if (e < W - 1) { const T dx = a0[e + 1] - a0[e]; sx += dx * dx; }
+    }
+    {
+      const T dx = ar - a0[W - 1];
+      if (L.xhi) sx += dx * dx;
+    }
+    T s = L.cI * sI + (L.zhi ? L.cz * sz : (T)0) + L.cx * sx;
+    if (HY && L.yhi) s += L.cy * sy;
     if (P.ub) {   // the data operator's term, c_F G^T S G p_j (k_blurF)
       T u[W];
       ldv<T, NC>(P.ub + pt0, u);
 #pragma unroll
-      for (int e = 0; e < W; ++e) q[e] += u[e];
+      for (int e = 0; e < W; ++e) s += a0[e] * u[e];
     }
-    VT<T>::stT(pw + pt0, a0);
-    T s = 0;
-#pragma unroll
-    for (int e = 0; e < W; ++e) s += a0[e] * q[e];
     pq += (double)s;
   }
   return pq;
@@ -283,7 +293,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
   if (!C.cg_active) return;
   __shared__ double sh[NWARP + 1];
   __shared__ double out[1];
-  double pq = cg1_chunks<T, HY, true>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
+  double pq = cg1e_chunks<T, HY, true>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
   pq = block_sum(pq, sh);
   if (threadIdx.x == 0) P.partials[blockIdx.x] = pq;
   if (last_block(P.counter)) {
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(BLOCK) k_cgsmall(const __grid_constant__ Prob<
   }
   for (int j = 0; j < n_cg; ++j) {
     if (!C.cg_active) break;
-    double pq = cg1_chunks<T, HY, false>(P, C, j, threadIdx.x, BLOCK);
+    double pq = cg1e_chunks<T, HY, false>(P, C, j, threadIdx.x, BLOCK);
     pq = block_sum(pq, sh);
     if (threadIdx.x == 0) fin_cg1(C, &pq, j);
     __syncthreads();
