@@ -360,10 +360,6 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
     }
     __syncthreads();   // stage s is refilled by the issue of tile t + 2
   }
-  if (KIND == 2 && ha) {   // this CTA's counts of the segment into the job's histogram
-    hist_a_flush(ha, P.gh_cnt + (size_t)S.job * NBUCK);
-    if (sp) hist_a_flush(ha + NBUCK, P.gh_cnt + (size_t)S.sjob * NBUCK);
-  }
   const int base = i * NSLOT;
   if (KIND == 2 && ha && S.kind == K_L1) {   // l1 sets use neither slot otherwise before pass 2
     warp_acc(acc, nv, base + SLOT_W2, d_w1);
@@ -522,22 +518,41 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
   const int nch = g.N / W;
   const int per = (nch + (int)gridDim.x - 1) / (int)gridDim.x;
   const int c0 = min(nch, (int)blockIdx.x * per), c1 = min(nch, c0 + per);
-  p1_xrun<T, AD, CK, NA>(P, C, f, c0, c1, xs_wr, acc, nv, st);
-  for (int seg = 1; seg < P.nseg1; ++seg) {
-    const int i = P.seg_set[seg], bl = P.seg_blk[seg];
-    const int kd = P.set[i].kind;
-    const int K = kd == K_BOUNDS ? 0 : (kd == K_DIST ? 1 : 2);
-    switch (K * 4 + P.set[i].prim[bl]) {
+  // The CTA's range in sub-ranges of p1_sub chunks, every segment over one
+  // sub-range before the next: x (and its z / y neighbour planes), which each
+  // segment re-reads, is then still in L2 when the next segment asks for it.
+  // The round-A counts of a set accumulate in shared memory across the
+  // sub-ranges and are flushed when another set's counts need the buffer.
+  const int sub = P.p1_sub > 0 ? P.p1_sub : max(per, 1);
+  int hset = -1;                      // the set whose counts ha holds
+  auto flush = [&]() {
+    if (hset < 0) return;
+    const SetD<T>& S = P.set[hset];
+    hist_a_flush(ha, P.gh_cnt + (size_t)S.job * NBUCK);
+    if (f.check && S.s) hist_a_flush(ha + NBUCK, P.gh_cnt + (size_t)S.sjob * NBUCK);
+    hset = -1;
+  };
+  for (int s0 = c0; s0 < c1; s0 += sub) {
+    const int s1 = min(c1, s0 + sub);
+    p1_xrun<T, AD, CK, NA>(P, C, f, s0, s1, xs_wr, acc, nv, st);
+    for (int seg = 1; seg < P.nseg1; ++seg) {
+      const int i = P.seg_set[seg], bl = P.seg_blk[seg];
+      const int kd = P.set[i].kind;
+      const int K = kd == K_BOUNDS ? 0 : (kd == K_DIST ? 1 : 2);
+      unsigned* hai = (ha && K == 2 && P.set[i].job >= 0 && C.job[P.set[i].job].mode == JM_SEARCH) ? ha : nullptr;
+      if (hai && hset != i) { flush(); hset = i; }
+      switch (K * 4 + P.set[i].prim[bl]) {
 #define P1CASE(KK, PP) \
-      case KK * 4 + PP: p1_run<T, KK, PP, AD, CK, NA>(P, C, i, bl, f, par, c0, c1, xs_rd, acc, nv, st, \
-          (P.set[i].job >= 0 && C.job[P.set[i].job].mode == JM_SEARCH) ? ha : nullptr); break;
-      P1CASE(0, PRIM_I) P1CASE(0, PRIM_Z) P1CASE(0, PRIM_Y) P1CASE(0, PRIM_X)
-      P1CASE(1, PRIM_I)
-      P1CASE(2, PRIM_I) P1CASE(2, PRIM_Z) P1CASE(2, PRIM_Y) P1CASE(2, PRIM_X)
+        case KK * 4 + PP: p1_run<T, KK, PP, AD, CK, NA>(P, C, i, bl, f, par, s0, s1, xs_rd, acc, nv, st, hai); break;
+        P1CASE(0, PRIM_I) P1CASE(0, PRIM_Z) P1CASE(0, PRIM_Y) P1CASE(0, PRIM_X)
+        P1CASE(1, PRIM_I)
+        P1CASE(2, PRIM_I) P1CASE(2, PRIM_Z) P1CASE(2, PRIM_Y) P1CASE(2, PRIM_X)
 #undef P1CASE
-      default: break;   // the distance block is I; blur/mask sets take the scalar kernels
+        default: break;   // the distance block is I; blur/mask sets take the scalar kernels
+      }
     }
   }
+  if (ha) flush();
   double* stage = P.partials + (size_t)gridDim.x * nv;
   if (finish_reduction(acc, nv, P.partials, P.counter, stage, sh)) {
     if (P.nranks > 1) {

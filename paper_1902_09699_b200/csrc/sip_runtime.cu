@@ -467,6 +467,14 @@ struct Engine : EngineBase {
       CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_selB<T>, BLOCK, selb_smem()));
       g_sel = std::max(1, std::min(tiles, nsm * std::max(occ, 1)));
     }
+    {   // pass 1 sub-ranges (tiles of BLOCK chunks; 0 = the CTA's whole range).
+        // Measured: x larger than ~half of L2 (C5-L1, 268 MB) 23.6 -> 22.5 ms
+        // per step with 8-tile sub-ranges; x that stays in L2 anyway (C4,
+        // 33.5 MB) 2.65 -> 2.71 ms (more pipeline starts and count flushes)
+      const char* e = getenv("SIP_P1_SUB");
+      const bool big = (double)g.N * sizeof(T) > 64.0 * (1 << 20);
+      Pr.p1_sub = (e ? atoi(e) : (big ? 8 : 0)) * BLOCK;
+    }
     smem_p1v = pass1_smem(P, false, Pr.selv2);        // k_pass1t: slots + bulk-copy stages (+ round-A counts)
     smem_p1a = pass1_smem(P, true, Pr.selv2);
     // pass 1: segment-major over one contiguous chunk range per CTA
