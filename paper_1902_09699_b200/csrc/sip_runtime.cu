@@ -155,7 +155,7 @@ struct Engine : EngineBase {
     memset(&none, 0, sizeof(none));
     CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, l2_window ? &l2av : &none));
   }
-  int g_cgf = 1, g_cg2f = 1, g_rhsf = 1;   // lean CG / rhs grids (4 CTAs per SM)
+  int g_cg1p = 1, g_cg2p = 1, g_rhsf = 1;   // lean CG (z pairs) / rhs grids
   bool vec = false;
   size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0, smem_p1v = 0, smem_p1a = 0;
   // graph
@@ -447,8 +447,15 @@ struct Engine : EngineBase {
     }
     g_vec = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 8));
     // lean CG / rhs: one wave of resident CTAs (4 per SM)
-    g_cgf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
-    g_cg2f = g_cgf;   // 5-6 CTAs / SM measured no faster (latency per chunk, not occupancy)
+    // CG over z pairs (one thread, two chunks): one resident wave, 4 (k_cg1f)
+    // / 3 (k_cg2f, 77 registers) CTAs per SM, fewer if the registers say so
+    auto wave = [&](const void* fn, int want) {
+      int occ = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BLOCK, 0));
+      return std::max(1, std::min((g.N / W / 2 + BLOCK - 1) / BLOCK, nsm * std::max(1, std::min(occ, want))));
+    };
+    g_cg1p = wave(ndim == 3 ? (const void*)k_cg1f<T, true> : (const void*)k_cg1f<T, false>, 4);
+    g_cg2p = wave(ndim == 3 ? (const void*)k_cg2f<T, true> : (const void*)k_cg2f<T, false>, 3);
     g_rhsf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
@@ -536,7 +543,7 @@ struct Engine : EngineBase {
     Pr.poison = getenv("SIP_POISON") ? 1 : 0;
     Pr.init_zero = vec ? 0 : 1;
     Pr.fibv = (nfib_sets && nranks > 1) ? dalloc<double>(4 * MAXP) : nullptr;
-    const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cgf, g_cg2f, g_rhsf, g_fib, g_fibw, g_svd});
+    const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cg1p, g_cg2p, g_rhsf, g_fib, g_fibw, g_svd});
     Pr.partials = dalloc<double>(std::max((size_t)(gmax + 2) * (nv1 + 8), (size_t)(g_sel + 2) * MAXJOBS * 3));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -849,8 +856,8 @@ struct Engine : EngineBase {
   const bool sel_debug = getenv("SIP_SEL_DEBUG") != nullptr;
   void launch_cg1(int j) {
     if (lean_cg()) {
-      if (ndim == 3) lk(k_cg1f<T, true>, g_cgf, BLOCK, 0, Pr, j);
-      else lk(k_cg1f<T, false>, g_cgf, BLOCK, 0, Pr, j);
+      if (ndim == 3) lk(k_cg1f<T, true>, g_cg1p, BLOCK, 0, Pr, j);
+      else lk(k_cg1f<T, false>, g_cg1p, BLOCK, 0, Pr, j);
     } else {
       k_cg1<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
     }
@@ -858,8 +865,8 @@ struct Engine : EngineBase {
   }
   void launch_cg2(int j) {
     if (lean_cg()) {
-      if (ndim == 3) lk(k_cg2f<T, true>, g_cg2f, BLOCK, 0, Pr, j);
-      else lk(k_cg2f<T, false>, g_cg2f, BLOCK, 0, Pr, j);
+      if (ndim == 3) lk(k_cg2f<T, true>, g_cg2p, BLOCK, 0, Pr, j);
+      else lk(k_cg2f<T, false>, g_cg2p, BLOCK, 0, Pr, j);
     } else k_cg2<T><<<g_pts, BLOCK, 0, stream>>>(Pr, j);
     ++launches;
   }

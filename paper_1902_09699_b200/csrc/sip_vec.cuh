@@ -274,6 +274,176 @@ __device__ __forceinline__ double cg2_chunks(const Prob<T>& P, const Ctrl& C, in
   return rr;
 }
 
+// cg1e over z pairs (see cg2p_chunks): the chunks at planes 2q and 2q + 1;
+// p_j is rebuilt at planes z, z+1, z+2 (and y+1, x+1 of both), 14 loads for
+// two chunks instead of 16.  Same per-point arithmetic as cg1e_chunks.
+template <class T, bool HY>
+__device__ __forceinline__ double cg1ep_chunks(const Prob<T>& P, const Ctrl& C, int j, int q_first, int q_step) {
+  constexpr int W = VT<T>::W;
+  const Geo& g = P.g;
+  const CoefT<T> k = coefs_present(P, C);
+  const T beta = (T)C.beta;
+  const bool usep = j > 0;
+  const T* r = P.r;
+  const T* po = usep ? p_slot(P, j - 1) : P.r;
+  T* pw = p_slot(P, j);
+  const int ncr = g.nx / W;
+  FastDiv dncr;
+  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
+  const int pl = g.plane, nx = g.nx;
+  const int cpp = pl / W;
+  const int npair = ((g.nz + 1) >> 1) * cpp;
+  double pq = 0.0;
+#pragma unroll 1
+  for (int q = q_first; q < npair; q += q_step) {
+    const int zp = (int)g.dplane.div((uint32_t)(q * W));
+    const int c = q + zp * cpp;
+    const bool two = 2 * zp + 1 < g.nz;
+    const int pt0 = c * W, pt1 = pt0 + pl;
+    const CGLoc<T> L(g, k, c, ncr, dncr);
+    const bool zhi1 = 2 * zp + 1 + g.z0 < g.nz_g - 1;
+    T a0[W], a1[W], a2[W], y0[W], y1[W];
+    VT<T>::ldT(r + pt0, a0);
+    VT<T>::ldT(r + pt1, a1);
+    VT<T>::ldT(r + pt1 + pl, a2);
+    if (HY) { VT<T>::ldT(r + pt0 + nx, y0); VT<T>::ldT(r + pt1 + nx, y1); }
+    T x0 = r[pt0 + W], x1 = r[pt1 + W];
+    if (usep) {
+      T b0[W], b1[W], b2[W], c0[W], c1[W];
+      VT<T>::ldT(po + pt0, b0);
+      VT<T>::ldT(po + pt1, b1);
+      VT<T>::ldT(po + pt1 + pl, b2);
+      if (HY) { VT<T>::ldT(po + pt0 + nx, c0); VT<T>::ldT(po + pt1 + nx, c1); }
+      const T bx0 = po[pt0 + W], bx1 = po[pt1 + W];
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        a0[e] = a0[e] + beta * b0[e];
+        a1[e] = a1[e] + beta * b1[e];
+        a2[e] = a2[e] + beta * b2[e];
+        if (HY) { y0[e] = y0[e] + beta * c0[e]; y1[e] = y1[e] + beta * c1[e]; }
+      }
+      x0 = x0 + beta * bx0;
+      x1 = x1 + beta * bx1;
+    }
+    VT<T>::stT(pw + pt0, a0);
+    if (two) VT<T>::stT(pw + pt1, a1);
+    // chunk 0 (plane z): z pair with a1; chunk 1 (plane z+1): z pair with a2
+    T sI0 = 0, sz0 = 0, sy0 = 0, sx0 = 0, sI1 = 0, sz1 = 0, sy1 = 0, sx1 = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      sI0 += a0[e] * a0[e];
+      sI1 += a1[e] * a1[e];
+      const T d0 = a1[e] - a0[e], d1 = a2[e] - a1[e];
+      sz0 += d0 * d0;
+      sz1 += d1 * d1;
+      if (HY) {
+        const T e0 = y0[e] - a0[e], e1 = y1[e] - a1[e];
+        sy0 += e0 * e0;
+        sy1 += e1 * e1;
+      }
+      if (e < W - 1) {
+        const T f0 = a0[e + 1] - a0[e], f1 = a1[e + 1] - a1[e];
+        sx0 += f0 * f0;
+        sx1 += f1 * f1;
+      }
+    }
+    if (L.xhi) {
+      const T f0 = x0 - a0[W - 1], f1 = x1 - a1[W - 1];
+      sx0 += f0 * f0;
+      sx1 += f1 * f1;
+    }
+    T s0 = L.cI * sI0 + (L.zhi ? L.cz * sz0 : (T)0) + L.cx * sx0;
+    T s1 = L.cI * sI1 + (zhi1 ? L.cz * sz1 : (T)0) + L.cx * sx1;
+    if (HY && L.yhi) { s0 += L.cy * sy0; s1 += L.cy * sy1; }
+    if (P.ub) {
+      T u[W];
+      VT<T>::ldT(P.ub + pt0, u);
+#pragma unroll
+      for (int e = 0; e < W; ++e) s0 += a0[e] * u[e];
+      if (two) {
+        VT<T>::ldT(P.ub + pt1, u);
+#pragma unroll
+        for (int e = 0; e < W; ++e) s1 += a1[e] * u[e];
+      }
+    }
+    pq += (double)s0;
+    if (two) pq += (double)s1;
+  }
+  return pq;
+}
+
+// cg2 over z pairs: one thread takes the chunk at plane 2q and the one above
+// it (plane 2q + 1), so the four planes z-1 .. z+2 of p serve both stencils
+// (14 loads for two chunks instead of 16) and two chunks' loads are in flight
+// per thread.  Same per-point arithmetic as cg2_chunks.
+template <class T, bool HY>
+__device__ __forceinline__ double cg2p_chunks(const Prob<T>& P, const Ctrl& C, int j, int q_first, int q_step) {
+  constexpr int W = VT<T>::W;
+  const Geo& g = P.g;
+  const CoefT<T> k = coefs_present(P, C);
+  const T alpha = (T)C.alpha;
+  const T* p = p_slot(P, j);
+  const int ncr = g.nx / W;
+  FastDiv dncr;
+  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
+  const int pl = g.plane, nx = g.nx;
+  const int cpp = pl / W;                    // chunks per plane
+  const int npair = ((g.nz + 1) >> 1) * cpp;
+  double rr = 0.0;
+#pragma unroll 1
+  for (int q = q_first; q < npair; q += q_step) {
+    const int zp = (int)g.dplane.div((uint32_t)(q * W));   // plane pair
+    const int c = q + zp * cpp;                            // chunk at plane 2 zp
+    const bool two = 2 * zp + 1 < g.nz;
+    const int pt0 = c * W, pt1 = pt0 + pl;
+    const CGLoc<T> L(g, k, c, ncr, dncr);
+    CGLoc<T> L1 = L;
+    L1.zlo = true;
+    L1.zhi = 2 * zp + 1 + g.z0 < g.nz_g - 1;
+    T zm[W], a0[W], a1[W], z2[W], y0m[W], y0p[W], y1m[W], y1p[W], r0[W], r1[W] = {};
+    VT<T>::ldT(p + pt0 - pl, zm);
+    VT<T>::ldT(p + pt0, a0);
+    VT<T>::ldT(p + pt1, a1);
+    VT<T>::ldT(p + pt1 + pl, z2);
+    if (HY) {
+      VT<T>::ldT(p + pt0 - nx, y0m); VT<T>::ldT(p + pt0 + nx, y0p);
+      VT<T>::ldT(p + pt1 - nx, y1m); VT<T>::ldT(p + pt1 + nx, y1p);
+    }
+    const T xl0 = p[pt0 - 1], xr0 = p[pt0 + W], xl1 = p[pt1 - 1], xr1 = p[pt1 + W];
+    VT<T>::ldcs(P.r + pt0, r0);
+    if (two) VT<T>::ldcs(P.r + pt1, r1);
+    T q0[W], q1[W];
+    L.template apply<W>(a0, zm, a1, y0m, y0p, xl0, xr0, HY, q0);
+    L1.template apply<W>(a1, a0, z2, y1m, y1p, xl1, xr1, HY, q1);
+    if (P.ub) {
+      T u[W];
+      VT<T>::ldT(P.ub + pt0, u);
+#pragma unroll
+      for (int e = 0; e < W; ++e) q0[e] += u[e];
+      if (two) {
+        VT<T>::ldT(P.ub + pt1, u);
+#pragma unroll
+        for (int e = 0; e < W; ++e) q1[e] += u[e];
+      }
+    }
+    T s0 = 0, s1 = 0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      r0[e] = r0[e] - alpha * q0[e];
+      s0 += r0[e] * r0[e];
+      r1[e] = r1[e] - alpha * q1[e];
+      s1 += r1[e] * r1[e];
+    }
+    VT<T>::stT(P.r + pt0, r0);
+    rr += (double)s0;
+    if (two) {
+      VT<T>::stT(P.r + pt1, r1);
+      rr += (double)s1;
+    }
+  }
+  return rr;
+}
+
 // k_cg1f(j): p_j = r + beta p_{j-1} (p_0 = r) and <p_j, C p_j>; p_j -> slot j
 template <class T, bool HY>
 __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<T> P, int j) {
@@ -293,7 +463,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
   if (!C.cg_active) return;
   __shared__ double sh[NWARP + 1];
   __shared__ double out[1];
-  double pq = cg1e_chunks<T, HY, true>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
+  double pq = cg1ep_chunks<T, HY>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
   pq = block_sum(pq, sh);
   if (threadIdx.x == 0) P.partials[blockIdx.x] = pq;
   if (last_block(P.counter)) {
@@ -308,13 +478,13 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
 
 // k_cg2f(j): r -= alpha C p_j and <r, r> (the x update is deferred to k_cgx)
 template <class T, bool HY>
-__global__ void __launch_bounds__(BLOCK, 4) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
+__global__ void __launch_bounds__(BLOCK, 3) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
   pdl_begin();
   Ctrl& C = *P.ctrl;
   if (C.stopped || !C.cg_active) return;
   __shared__ double sh[NWARP + 1];
   __shared__ double out[1];
-  double rr = cg2_chunks<T, HY, true>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
+  double rr = cg2p_chunks<T, HY>(P, C, j, blockIdx.x * BLOCK + threadIdx.x, gridDim.x * BLOCK);
   rr = block_sum(rr, sh);
   if (threadIdx.x == 0) P.partials[blockIdx.x] = rr;
   if (last_block(P.counter)) {
