@@ -456,6 +456,8 @@ struct Engine : EngineBase {
     };
     g_cg1p = wave(ndim == 3 ? (const void*)k_cg1f<T, true> : (const void*)k_cg1f<T, false>, 4);
     g_cg2p = wave(ndim == 3 ? (const void*)k_cg2f<T, true> : (const void*)k_cg2f<T, false>, 3);
+    g_rhsp = wave(ndim == 3 ? (const void*)k_rhsp<T, true> : (const void*)k_rhsp<T, false>,
+                  getenv("SIP_RHS_PAIRS") ? std::max(1, atoi(getenv("SIP_RHS_PAIRS"))) : 3);
     g_rhsf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
@@ -838,8 +840,13 @@ struct Engine : EngineBase {
   void launch_blur(int mode, int j) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, mode, j); ++launches; }
   void launch_rhs() {
     if (vec) {
-      if (ndim == 3) lk(k_rhsf<T, true>, g_rhsf, BLOCK, 0, Pr);
-      else lk(k_rhsf<T, false>, g_rhsf, BLOCK, 0, Pr);
+      if (rhs_pairs) {
+        if (ndim == 3) lk(k_rhsp<T, true>, g_rhsp, BLOCK, 0, Pr);
+        else lk(k_rhsp<T, false>, g_rhsp, BLOCK, 0, Pr);
+      } else {
+        if (ndim == 3) lk(k_rhsf<T, true>, g_rhsf, BLOCK, 0, Pr);
+        else lk(k_rhsf<T, false>, g_rhsf, BLOCK, 0, Pr);
+      }
     } else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
@@ -854,6 +861,8 @@ struct Engine : EngineBase {
            !getenv("SIP_NO_SMALL_CG");
   }
   const bool sel_debug = getenv("SIP_SEL_DEBUG") != nullptr;
+  const bool rhs_pairs = getenv("SIP_RHS_PAIRS") != nullptr;
+  int g_rhsp = 1;
   void launch_cg1(int j) {
     if (lean_cg()) {
       if (ndim == 3) lk(k_cg1f<T, true>, g_cg1p, BLOCK, 0, Pr, j);

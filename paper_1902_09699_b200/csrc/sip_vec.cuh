@@ -626,4 +626,141 @@ __global__ void __launch_bounds__(BLOCK, 4) k_rhsf(const __grid_constant__ Prob<
   }
 }
 
+
+// k_rhsp: k_rhsf over z pairs (the chunks at planes 2q and 2q + 1, as the CG
+// kernels): a D_z block's u at plane z serves as the lower neighbour of the
+// chunk above, x's planes z-1 .. z+2 serve both stencils, and every block's
+// loads for two chunks are in flight together.  Same per-point arithmetic.
+template <class T, bool HY>
+__global__ void __launch_bounds__(BLOCK, 3) k_rhsp(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
+  constexpr int W = VT<T>::W;
+  Ctrl& C = *P.ctrl;
+  if (C.stopped) return;
+  __shared__ double sh[NWARP + 1];
+  __shared__ double out[2];
+  const Geo& g = P.g;
+  const int par = C.k & 1;
+  const CoefT<T> k = coefs_present(P, C);
+  const int ncr = g.nx / W;
+  FastDiv dncr;
+  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
+  const int pl = g.plane, nx = g.nx;
+  const int cpp = pl / W;
+  const int npair = ((g.nz + 1) >> 1) * cpp;
+  double bb = 0.0, rr = 0.0;
+  for (int q = blockIdx.x * BLOCK + threadIdx.x; q < npair; q += gridDim.x * BLOCK) {
+    const int zp = (int)g.dplane.div((uint32_t)(q * W));
+    const int c = q + zp * cpp;
+    const bool two = 2 * zp + 1 < g.nz;
+    const int pt0 = c * W, pt1 = pt0 + pl;
+    T b0[W], b1[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) { b0[e] = 0; b1[e] = 0; }
+    for (int i = 0; i < P.P; ++i) {
+      const SetD<T>& S = P.set[i];
+      const T rho = (T)C.rho[i];
+      for (int bl = 0; bl < S.nblk; ++bl) {
+        const int prim = S.prim[bl];
+        const T* y = S.y[par] + (int64_t)bl * g.ld + pt0;
+        const T* v = S.v[par] + (int64_t)bl * g.ld + pt0;
+        T y0[W], v0[W], y1[W], v1[W], u0[W], u1[W];
+        if (prim == PRIM_Z || prim == PRIM_Y) {   // read again as the z / y neighbour: keep in L2
+          VT<T>::ldT(y, y0); VT<T>::ldT(v, v0);
+          VT<T>::ldT(y + pl, y1); VT<T>::ldT(v + pl, v1);
+        } else {
+          VT<T>::ldcs(y, y0); VT<T>::ldcs(v, v0);
+          VT<T>::ldcs(y + pl, y1); VT<T>::ldcs(v + pl, v1);
+        }
+        if (prim == PRIM_Z) {                 // D_z^T u = u[z-1] - u[z]; chunk 1's u[z-1] is chunk 0's u
+          T ym[W], vm[W];
+          VT<T>::ldT(y - pl, ym);
+          VT<T>::ldT(v - pl, vm);
+          const T ih = (T)g.ihz;
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            u0[e] = rho * y0[e] + v0[e];
+            u1[e] = rho * y1[e] + v1[e];
+            b0[e] += ((rho * ym[e] + vm[e]) - u0[e]) * ih;
+            b1[e] += (u0[e] - u1[e]) * ih;
+          }
+          continue;
+        }
+#pragma unroll
+        for (int e = 0; e < W; ++e) { u0[e] = rho * y0[e] + v0[e]; u1[e] = rho * y1[e] + v1[e]; }
+        if (prim == PRIM_I) {
+#pragma unroll
+          for (int e = 0; e < W; ++e) { b0[e] += u0[e]; b1[e] += u1[e]; }
+        } else if (prim == PRIM_X) {        // D_x^T u = u[x-1] - u[x]
+          const T ul0 = rho * y[-1] + v[-1];
+          const T ul1 = rho * y[pl - 1] + v[pl - 1];
+          const T ih = (T)g.ihx;
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            b0[e] += ((e > 0 ? u0[e - 1] : ul0) - u0[e]) * ih;
+            b1[e] += ((e > 0 ? u1[e - 1] : ul1) - u1[e]) * ih;
+          }
+        } else {                            // D_y^T: u[y-1] - u[y]
+          T ym0[W], vm0[W], ym1[W], vm1[W];
+          VT<T>::ldT(y - nx, ym0); VT<T>::ldT(v - nx, vm0);
+          VT<T>::ldT(y + pl - nx, ym1); VT<T>::ldT(v + pl - nx, vm1);
+          const T ih = (T)g.ihy;
+#pragma unroll
+          for (int e = 0; e < W; ++e) {
+            b0[e] += ((rho * ym0[e] + vm0[e]) - u0[e]) * ih;
+            b1[e] += ((rho * ym1[e] + vm1[e]) - u1[e]) * ih;
+          }
+        }
+      }
+    }
+    // r = b - C x (Eq. 25's residual at the warm start x^k)
+    const CGLoc<T> L(g, k, c, ncr, dncr);
+    CGLoc<T> L1 = L;
+    L1.zlo = true;
+    L1.zhi = 2 * zp + 1 + g.z0 < g.nz_g - 1;
+    T zm[W], a0[W], a1[W], z2[W], y0m[W], y0p[W], y1m[W], y1p[W];
+    VT<T>::ldT(P.x + pt0 - pl, zm);
+    VT<T>::ldT(P.x + pt0, a0);
+    VT<T>::ldT(P.x + pt1, a1);
+    VT<T>::ldT(P.x + pt1 + pl, z2);
+    if (HY) {
+      VT<T>::ldT(P.x + pt0 - nx, y0m); VT<T>::ldT(P.x + pt0 + nx, y0p);
+      VT<T>::ldT(P.x + pt1 - nx, y1m); VT<T>::ldT(P.x + pt1 + nx, y1p);
+    }
+    const T xl0 = P.x[pt0 - 1], xr0 = P.x[pt0 + W], xl1 = P.x[pt1 - 1], xr1 = P.x[pt1 + W];
+    T q0[W], q1[W];
+    L.template apply<W>(a0, zm, a1, y0m, y0p, xl0, xr0, HY, q0);
+    L1.template apply<W>(a1, a0, z2, y1m, y1p, xl1, xr1, HY, q1);
+    T sb0 = 0, sr0 = 0, sb1 = 0, sr1 = 0, r0[W], r1[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      r0[e] = b0[e] - q0[e];
+      sb0 += b0[e] * b0[e];
+      sr0 += r0[e] * r0[e];
+      r1[e] = b1[e] - q1[e];
+      sb1 += b1[e] * b1[e];
+      sr1 += r1[e] * r1[e];
+    }
+    VT<T>::stT(P.r + pt0, r0);
+    bb += (double)sb0;
+    rr += (double)sr0;
+    if (two) {
+      VT<T>::stT(P.r + pt1, r1);
+      bb += (double)sb1;
+      rr += (double)sr1;
+    }
+  }
+  bb = block_sum(bb, sh);
+  rr = block_sum(rr, sh);
+  if (threadIdx.x == 0) { P.partials[blockIdx.x * 2] = bb; P.partials[blockIdx.x * 2 + 1] = rr; }
+  if (last_block(P.counter)) {
+    reduce_partials(P.partials, 2, out, sh);
+    if (threadIdx.x == 0) {
+      *P.counter = 0u;
+      if (P.nranks > 1) publish(P, out, 2, 0, 1);
+      else fin_rhs(C, out);
+    }
+  }
+}
+
 }  // namespace sip
