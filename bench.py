@@ -243,7 +243,7 @@ def run_reference(args, prob):
 
 # ------------------------------------------------------------------ CUDA arm
 KINDS_RL = ("rhs", "cg1", "cg2", "cgx", "pass1", "select", "pass2")
-KNAME = {"rhs": "k_rhsf", "cg1": "k_cg1f", "cg2": "k_cg2f", "cgx": "k_cgx", "pass1": "k_pass1t",
+KNAME = {"rhs": "k_rhsp", "cg1": "k_cg1f", "cg2": "k_cg2f", "cgx": "k_cgx", "pass1": "k_pass1t",
          "select": "k_selectf", "pass2": "k_pass2t"}
 
 

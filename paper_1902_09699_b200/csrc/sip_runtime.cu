@@ -155,7 +155,7 @@ struct Engine : EngineBase {
     memset(&none, 0, sizeof(none));
     CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, l2_window ? &l2av : &none));
   }
-  int g_cg1p = 1, g_cg2p = 1, g_rhsf = 1;   // lean CG (z pairs) / rhs grids
+  int g_cg1p = 1, g_cg2p = 1, g_rhsp = 1;   // lean CG / rhs grids (z pairs)
   bool vec = false;
   size_t smem_p1 = 0, smem_p2 = 0, smem_init = 0, smem_p1v = 0, smem_p1a = 0;
   // graph
@@ -456,9 +456,7 @@ struct Engine : EngineBase {
     };
     g_cg1p = wave(ndim == 3 ? (const void*)k_cg1f<T, true> : (const void*)k_cg1f<T, false>, 4);
     g_cg2p = wave(ndim == 3 ? (const void*)k_cg2f<T, true> : (const void*)k_cg2f<T, false>, 3);
-    g_rhsp = wave(ndim == 3 ? (const void*)k_rhsp<T, true> : (const void*)k_rhsp<T, false>,
-                  getenv("SIP_RHS_PAIRS") ? std::max(1, atoi(getenv("SIP_RHS_PAIRS"))) : 3);
-    g_rhsf = std::max(1, std::min((g.N / W + BLOCK - 1) / BLOCK, nsm * 4));
+    g_rhsp = wave(ndim == 3 ? (const void*)k_rhsp<T, true> : (const void*)k_rhsp<T, false>, 3);
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1
     // select v2 (sip_select2.cuh): single-rank fp32 runs with a radix job
@@ -545,7 +543,7 @@ struct Engine : EngineBase {
     Pr.poison = getenv("SIP_POISON") ? 1 : 0;
     Pr.init_zero = vec ? 0 : 1;
     Pr.fibv = (nfib_sets && nranks > 1) ? dalloc<double>(4 * MAXP) : nullptr;
-    const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cg1p, g_cg2p, g_rhsf, g_fib, g_fibw, g_svd});
+    const int gmax = std::max({g_pts, g_sel, g_p2, g_vec, g_p1, g_cg1p, g_cg2p, g_rhsp, g_fib, g_fibw, g_svd});
     Pr.partials = dalloc<double>(std::max((size_t)(gmax + 2) * (nv1 + 8), (size_t)(g_sel + 2) * MAXJOBS * 3));
     if (nranks > 1) {   // gather slots of the z-slab finalisers (sip_team.cuh)
       int xs_ = 0;
@@ -840,13 +838,8 @@ struct Engine : EngineBase {
   void launch_blur(int mode, int j) { k_blur_t<T><<<g_pts, BLOCK, 0, stream>>>(Pr, mode, j); ++launches; }
   void launch_rhs() {
     if (vec) {
-      if (rhs_pairs) {
-        if (ndim == 3) lk(k_rhsp<T, true>, g_rhsp, BLOCK, 0, Pr);
-        else lk(k_rhsp<T, false>, g_rhsp, BLOCK, 0, Pr);
-      } else {
-        if (ndim == 3) lk(k_rhsf<T, true>, g_rhsf, BLOCK, 0, Pr);
-        else lk(k_rhsf<T, false>, g_rhsf, BLOCK, 0, Pr);
-      }
+      if (ndim == 3) lk(k_rhsp<T, true>, g_rhsp, BLOCK, 0, Pr);
+      else lk(k_rhsp<T, false>, g_rhsp, BLOCK, 0, Pr);
     } else k_rhs<T><<<g_pts, BLOCK, 0, stream>>>(Pr);
     ++launches;
   }
@@ -861,8 +854,6 @@ struct Engine : EngineBase {
            !getenv("SIP_NO_SMALL_CG");
   }
   const bool sel_debug = getenv("SIP_SEL_DEBUG") != nullptr;
-  const bool rhs_pairs = getenv("SIP_RHS_PAIRS") != nullptr;
-  int g_rhsp = 1;
   void launch_cg1(int j) {
     if (lean_cg()) {
       if (ndim == 3) lk(k_cg1f<T, true>, g_cg1p, BLOCK, 0, Pr, j);

@@ -529,108 +529,16 @@ __global__ void __launch_bounds__(BLOCK) k_cgsmall(const __grid_constant__ Prob<
   }
 }
 
-// k_rhsf: the lean flat rhs (Eq. 21 line 1, Eq. 25): b = sum_i A_i^T (rho_i
-// y_i + v_i), r = b - C x, ||b||^2, ||r||^2.  Every field stores 0 at the
-// entries an operator block does not have (pads) and in the ghost planes, so
-// the transposed differences need no masks: D^T u at a point is u(point - 1
-// step) - u(point), whose absent terms read those zeros (reading L3).
-template <class T, bool HY>
-__global__ void __launch_bounds__(BLOCK, 4) k_rhsf(const __grid_constant__ Prob<T> P) {
-  pdl_begin();
-  constexpr int W = VT<T>::W;
-  Ctrl& C = *P.ctrl;
-  if (C.stopped) return;
-  __shared__ double sh[NWARP + 1];
-  __shared__ double out[2];
-  const Geo& g = P.g;
-  const int par = C.k & 1;
-  const CoefT<T> k = coefs_present(P, C);
-  const int nch = g.N / W;
-  const int ncr = g.nx / W;
-  FastDiv dncr;
-  dncr.d = P.dncr.d; dncr.m = P.dncr.m; dncr.l = P.dncr.l;
-  const int pl = g.plane, nx = g.nx;
-  double bb = 0.0, rr = 0.0;
-  for (int c = blockIdx.x * BLOCK + threadIdx.x; c < nch; c += gridDim.x * BLOCK) {
-    const int pt0 = c * W;
-    T b[W];
-#pragma unroll
-    for (int e = 0; e < W; ++e) b[e] = 0;
-    for (int i = 0; i < P.P; ++i) {
-      const SetD<T>& S = P.set[i];
-      const T rho = (T)C.rho[i];
-      for (int bl = 0; bl < S.nblk; ++bl) {
-        const int prim = S.prim[bl];
-        const T* y = S.y[par] + (int64_t)bl * g.ld + pt0;
-        const T* v = S.v[par] + (int64_t)bl * g.ld + pt0;
-        T yy[W], vv[W], u[W];
-        if (prim == PRIM_Z || prim == PRIM_Y) {   // read again as the z / y neighbour: keep in L2
-          VT<T>::ldT(y, yy);
-          VT<T>::ldT(v, vv);
-        } else {
-          VT<T>::ldcs(y, yy);
-          VT<T>::ldcs(v, vv);
-        }
-#pragma unroll
-        for (int e = 0; e < W; ++e) u[e] = rho * yy[e] + vv[e];
-        if (prim == PRIM_I) {
-#pragma unroll
-          for (int e = 0; e < W; ++e) b[e] += u[e];
-        } else if (prim == PRIM_X) {        // D_x^T u = u[x-1] - u[x]
-          const T ul = rho * y[-1] + v[-1];
-          const T ih = (T)g.ihx;
-#pragma unroll
-          for (int e = 0; e < W; ++e) b[e] += ((e > 0 ? u[e - 1] : ul) - u[e]) * ih;
-        } else {                            // D_z^T / D_y^T: u[z-1] - u[z]
-          const int d = prim == PRIM_Z ? pl : nx;
-          T ym[W], vm[W];
-          VT<T>::ldT(y - d, ym);
-          VT<T>::ldT(v - d, vm);
-          const T ih = (T)(prim == PRIM_Z ? g.ihz : g.ihy);
-#pragma unroll
-          for (int e = 0; e < W; ++e) b[e] += ((rho * ym[e] + vm[e]) - u[e]) * ih;
-        }
-      }
-    }
-    // r = b - C x (Eq. 25's residual at the warm start x^k)
-    const CGLoc<T> L(g, k, c, ncr, dncr);
-    T a0[W], a1[W], a2[W], a3[W], a4[W];
-    VT<T>::ldT(P.x + pt0, a0);
-    VT<T>::ldT(P.x + pt0 - pl, a1);
-    VT<T>::ldT(P.x + pt0 + pl, a2);
-    if (HY) { VT<T>::ldT(P.x + pt0 - nx, a3); VT<T>::ldT(P.x + pt0 + nx, a4); }
-    const T xl = P.x[pt0 - 1], xr = P.x[pt0 + W];
-    T q[W], r[W];
-    L.template apply<W>(a0, a1, a2, a3, a4, xl, xr, HY, q);
-    T sb = 0, sr = 0;
-#pragma unroll
-    for (int e = 0; e < W; ++e) {
-      r[e] = b[e] - q[e];
-      sb += b[e] * b[e];
-      sr += r[e] * r[e];
-    }
-    VT<T>::stT(P.r + pt0, r);
-    bb += (double)sb;
-    rr += (double)sr;
-  }
-  bb = block_sum(bb, sh);
-  rr = block_sum(rr, sh);
-  if (threadIdx.x == 0) { P.partials[blockIdx.x * 2] = bb; P.partials[blockIdx.x * 2 + 1] = rr; }
-  if (last_block(P.counter)) {
-    reduce_partials(P.partials, 2, out, sh);
-    if (threadIdx.x == 0) {
-      *P.counter = 0u;
-      if (P.nranks > 1) publish(P, out, 2, 0, 1);
-      else fin_rhs(C, out);
-    }
-  }
-}
-
-
-// k_rhsp: k_rhsf over z pairs (the chunks at planes 2q and 2q + 1, as the CG
+// k_rhsp: the vectorised rhs (Eq. 21 line 1, Eq. 25): b = sum_i A_i^T
+// (rho_i y_i + v_i), r = b - C x, ||b||^2, ||r||^2.  Every field stores 0 at
+// the entries an operator block does not have (pads) and in the ghost
+// planes, so the transposed differences need no masks: D^T u at a point is
+// u(point - 1 step) - u(point), whose absent terms read those zeros (reading
+// L3).  Over z pairs (the chunks at planes 2q and 2q + 1, as the CG
 // kernels): a D_z block's u at plane z serves as the lower neighbour of the
 // chunk above, x's planes z-1 .. z+2 serve both stencils, and every block's
-// loads for two chunks are in flight together.  Same per-point arithmetic.
+// loads for two chunks are in flight together (measured: C4 rhs 1.09 ->
+// 0.93 ms per step, C5-L1 9.9 -> 7.9 ms, against one chunk per thread).
 template <class T, bool HY>
 __global__ void __launch_bounds__(BLOCK, 3) k_rhsp(const __grid_constant__ Prob<T> P) {
   pdl_begin();
