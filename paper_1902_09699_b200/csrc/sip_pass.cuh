@@ -574,108 +574,137 @@ __host__ inline size_t pass1_smem(int P, bool adapt, bool selv2 = false) {
 // KIND: 0 l1 ball (soft threshold at theta), 1 cardinality (keep > tau and the
 // first keep_eq == tau in index order), 2 l2 ball / annulus (radial factor)
 template <class T, int KIND>
-__device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, int bl, int lt, int tpb,
+__device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, int bl, int lp, int tpb,
                                         const IterFlags& f, int par, double* acc, int nv, int* s_w) {
+  // tiles 2 lp and 2 lp + 1 of the block (BLOCK chunks each, k_tiecountf's
+  // tiles): one chunk of each per thread, both chunks' loads in flight
+  // together (one chunk per thread left too few bytes in flight)
   using K = KeyT<T>;
   using U = typename K::U;
   constexpr int W = VT<T>::W;
+  constexpr int H = 2;
   const Geo& g = P.g;
   const SetD<T>& S = P.set[i];
   const int nch = g.N / W;
-  const int c = lt * BLOCK + threadIdx.x;
-  const bool valid = c < nch;
-  const int pt0 = (valid ? c : nch - 1) * W;
   const int prim = S.prim[bl];
-  bool padc, lastx;   // once per chunk (no per-element operator dispatch)
-  {
-    const int iz = (int)g.dplane.div((uint32_t)pt0);
-    const int r = pt0 - iz * g.plane;
-    const int iy = (int)g.dnx.div((uint32_t)r);
-    padc = prim == PRIM_Z ? (iz + g.z0 >= g.nz_g - 1) : (prim == PRIM_Y ? iy >= g.ny - 1 : false);
-    lastx = prim == PRIM_X && (r - iy * g.nx + W >= g.nx);
-  }
-  const int64_t off = (int64_t)bl * g.ld + pt0;
-  T wv[W], y0[W], v0[W];
-  VT<T>::ldT(S.w + off, wv);
-  if (f.dots) {
-    VT<T>::ldT(S.y[par ^ 1] + off, y0);
-    VT<T>::ldT(S.v[par ^ 1] + off, v0);
-  }
-  bool pad[W];
+  bool valid[H], pad[H][W];
+  int pt0[H];
+  int64_t off[H];
+  T wv[H][W], y0[H][W], v0[H][W];
 #pragma unroll
-  for (int e = 0; e < W; ++e) pad[e] = !valid || padc || (lastx && e == W - 1);
-  T y[W];
+  for (int h = 0; h < H; ++h) {
+    const int c = (2 * lp + h) * BLOCK + threadIdx.x;
+    valid[h] = c < nch;
+    pt0[h] = (valid[h] ? c : nch - 1) * W;
+    off[h] = (int64_t)bl * g.ld + pt0[h];
+    VT<T>::ldT(S.w + off[h], wv[h]);
+    if (f.dots) {
+      VT<T>::ldT(S.y[par ^ 1] + off[h], y0[h]);
+      VT<T>::ldT(S.v[par ^ 1] + off[h], v0[h]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < H; ++h) {   // pads once per chunk (no per-element operator dispatch)
+    const int iz = (int)g.dplane.div((uint32_t)pt0[h]);
+    const int r = pt0[h] - iz * g.plane;
+    const int iy = (int)g.dnx.div((uint32_t)r);
+    const bool padc = prim == PRIM_Z ? (iz + g.z0 >= g.nz_g - 1) : (prim == PRIM_Y ? iy >= g.ny - 1 : false);
+    const bool lastx = prim == PRIM_X && (r - iy * g.nx + W >= g.nx);
+#pragma unroll
+    for (int e = 0; e < W; ++e) pad[h][e] = !valid[h] || padc || (lastx && e == W - 1);
+  }
+  T y[H][W];
   if (KIND == 0) {
     const Job& J = C.job[S.job];
     const T th = (T)J.theta;
     const bool done = J.mode == JM_DONE, keep = (J.mode == JM_INSIDE || J.mode == JM_ALL);
 #pragma unroll
-    for (int e = 0; e < W; ++e) {
-      const T w = wv[e];
-      if (done) {
-        const T a = (sizeof(T) == 8) ? (T)(fabs((double)w) - J.theta) : fabsf((float)w) - th;
-        y[e] = a > (T)0 ? (w > (T)0 ? a : -a) : (T)0;   // soft threshold
-      } else {
-        y[e] = keep ? w : (T)0;
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        const T w = wv[h][e];
+        if (done) {
+          const T a = (sizeof(T) == 8) ? (T)(fabs((double)w) - J.theta) : fabsf((float)w) - th;
+          y[h][e] = a > (T)0 ? (w > (T)0 ? a : -a) : (T)0;   // soft threshold
+        } else {
+          y[h][e] = keep ? w : (T)0;
+        }
       }
-    }
   } else if (KIND == 1) {
     const Job& J = C.job[S.job];
     const U tau = (U)J.tau;
-    bool keep[W];
-    int cnt = 0;
+    bool keep[H][W];
+    int cnt[H] = {0, 0};
 #pragma unroll
-    for (int e = 0; e < W; ++e) {
-      const U key = K::key(wv[e]);
-      keep[e] = (J.mode == JM_ALL) || (J.mode == JM_DONE && key > tau);
-      cnt += (J.mode == JM_DONE && !pad[e] && key == tau) ? 1 : 0;
-    }
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+      for (int e = 0; e < W; ++e) {
+        const U key = K::key(wv[h][e]);
+        keep[h][e] = (J.mode == JM_ALL) || (J.mode == JM_DONE && key > tau);
+        cnt[h] += (J.mode == JM_DONE && !pad[h][e] && key == tau) ? 1 : 0;
+      }
     if (J.mode == JM_DONE) {
       if (J.ties) {   // the first keep_eq entries == tau in index order (L6)
         const int* toff = P.tiecnt + (size_t)S.job * P.ntiles_max;
-        long long r = (long long)toff[bl * tpb + lt] + block_excl_count(cnt, s_w);
 #pragma unroll
-        for (int e = 0; e < W; ++e)
-          if (!pad[e] && K::key(wv[e]) == tau) { if (r < J.keep_eq) keep[e] = true; ++r; }
+        for (int h = 0; h < H; ++h) {
+          const int t = 2 * lp + h;
+          const int ex = block_excl_count(cnt[h], s_w);   // every thread (block barrier inside)
+          if (t >= tpb) continue;
+          long long r = (long long)toff[bl * tpb + t] + ex;
+#pragma unroll
+          for (int e = 0; e < W; ++e)
+            if (!pad[h][e] && K::key(wv[h][e]) == tau) { if (r < J.keep_eq) keep[h][e] = true; ++r; }
+        }
       } else {
 #pragma unroll
-        for (int e = 0; e < W; ++e) if (K::key(wv[e]) == tau) keep[e] = true;
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+          for (int e = 0; e < W; ++e) if (K::key(wv[h][e]) == tau) keep[h][e] = true;
       }
     }
-#pragma unroll
-    for (int e = 0; e < W; ++e) y[e] = keep[e] ? wv[e] : (T)0;
     unsigned long long hsum = 0;   // support fingerprint (test instrument)
-    const unsigned long long gbase = (unsigned long long)bl * ((unsigned long long)g.nz_g * g.plane) +
-                                     (unsigned long long)g.z0 * g.plane + (unsigned long long)pt0;
 #pragma unroll
-    for (int e = 0; e < W; ++e)
-      if (!pad[e] && y[e] != (T)0) hsum += supp_mix(gbase + e);
+    for (int h = 0; h < H; ++h) {
+#pragma unroll
+      for (int e = 0; e < W; ++e) y[h][e] = keep[h][e] ? wv[h][e] : (T)0;
+      const unsigned long long gbase = (unsigned long long)bl * ((unsigned long long)g.nz_g * g.plane) +
+                                       (unsigned long long)g.z0 * g.plane + (unsigned long long)pt0[h];
+#pragma unroll
+      for (int e = 0; e < W; ++e)
+        if (!pad[h][e] && y[h][e] != (T)0) hsum += supp_mix(gbase + e);
+    }
     supp_add_warp(C, i, hsum);
   } else {
     const T sc = (T)C.ann_scale[i];
     const int az = C.ann_zero[i];
 #pragma unroll
-    for (int e = 0; e < W; ++e)
-      y[e] = az ? ((bl == 0 && pt0 + e == S.first_real) ? (T)C.sig_lo[i] : (T)0) : wv[e] * sc;
+    for (int h = 0; h < H; ++h)
+#pragma unroll
+      for (int e = 0; e < W; ++e)
+        y[h][e] = az ? ((bl == 0 && pt0[h] + e == S.first_real) ? (T)C.sig_lo[i] : (T)0) : wv[h][e] * sc;
   }
   const T rho = (T)C.rho[i];
-  T yn[W], vn[W];
   T a_gv = 0, a_gg = 0, a_vv = 0;
 #pragma unroll
-  for (int e = 0; e < W; ++e) {
-    const T yt = pad[e] ? (T)0 : y[e];
-    const T vt = pad[e] ? (T)0 : rho * (yt - wv[e]);    // Eq. 21 as rho (y - w), L26
-    yn[e] = yt;
-    vn[e] = vt;
-    if (f.dots && !pad[e]) {
-      const T dg = y0[e] - yt;
-      const T dv = vt - v0[e];
-      a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+  for (int h = 0; h < H; ++h) {
+    T yn[W], vn[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) {
+      const T yt = pad[h][e] ? (T)0 : y[h][e];
+      const T vt = pad[h][e] ? (T)0 : rho * (yt - wv[h][e]);    // Eq. 21 as rho (y - w), L26
+      yn[e] = yt;
+      vn[e] = vt;
+      if (f.dots && !pad[h][e]) {
+        const T dg = y0[h][e] - yt;
+        const T dv = vt - v0[h][e];
+        a_gv += dg * dv; a_gg += dg * dg; a_vv += dv * dv;
+      }
     }
-  }
-  if (valid) {
-    VT<T>::stT(S.y[par ^ 1] + off, yn);
-    VT<T>::stT(S.v[par ^ 1] + off, vn);
+    if (valid[h]) {
+      VT<T>::stT(S.y[par ^ 1] + off[h], yn);
+      VT<T>::stT(S.v[par ^ 1] + off[h], vn);
+    }
   }
   if (f.dots) {
     warp_acc(acc, nv, i * 4 + 0, (double)a_gv);
@@ -701,7 +730,7 @@ __device__ inline void fin_pass2(const Prob<T>& P, Ctrl& C, const double* stage)
 }
 
 template <class T, int AD, int CK>
-__global__ void __launch_bounds__(BLOCK, 4) k_pass2t(const __grid_constant__ Prob<T> P) {
+__global__ void __launch_bounds__(BLOCK, AD == 0 ? 4 : 3) k_pass2t(const __grid_constant__ Prob<T> P) {
   pdl_begin();
   using K = KeyT<T>;
   using U = typename K::U;
@@ -718,17 +747,18 @@ __global__ void __launch_bounds__(BLOCK, 4) k_pass2t(const __grid_constant__ Pro
   for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
   __syncthreads();
   const int nch = g.N / W;
-  const int tpb = (nch + BLOCK - 1) / BLOCK;
-  int sg = blockIdx.x / tpb, lt = blockIdx.x - sg * tpb;
+  const int tpb = (nch + BLOCK - 1) / BLOCK;   // k_tiecountf's tiles per block
+  const int ppb = (tpb + 1) / 2;               // tile pairs per block
+  int sg = blockIdx.x / ppb, lp = blockIdx.x - sg * ppb;
   while (sg < P.nseg2) {
     const int i = P.seg2_set[sg], bl = P.seg2_blk[sg];
     switch (P.set[i].kind) {
-      case K_L1: p2_tile<T, 0>(P, C, i, bl, lt, tpb, f, par, acc, nv, s_w); break;
-      case K_CARD: p2_tile<T, 1>(P, C, i, bl, lt, tpb, f, par, acc, nv, s_w); break;
-      default: p2_tile<T, 2>(P, C, i, bl, lt, tpb, f, par, acc, nv, s_w); break;
+      case K_L1: p2_tile<T, 0>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
+      case K_CARD: p2_tile<T, 1>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
+      default: p2_tile<T, 2>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
     }
-    lt += gridDim.x;
-    while (lt >= tpb) { lt -= tpb; ++sg; }
+    lp += gridDim.x;
+    while (lp >= ppb) { lp -= ppb; ++sg; }
   }
   // Eq. 26 numerators of l1 / cardinality sets from s (check iterations)
   if (f.check) {
