@@ -58,6 +58,8 @@ struct Prob {
   unsigned* ccnt;                 // [MAXJOBS][select grid]: candidates per CTA region
   long long cand_per;             // candidate region per select CTA (entries)
   int sel_grid;                   // the grid k_selectf is sized for (regions, ccnt stride)
+  int p1_hint;                    // pass 1: L2 eviction hints on the staged copies (0 none, 1 x evict_last, 2 + others evict_first)
+  int p1_pool, p1a_pool;          // pass 1: array slots of the bulk-copy stage pool (plain, adapt iterations)
   int p1_sub;                     // pass 1: chunks per sub-range (every segment runs over one sub-range before the next)
   int selv2;                      // single-rank fp32: round A in pass 1, k_selB / k_selC (sip_select2.cuh)
   unsigned* gf_cnt;               // select v2: k_selB's candidate histogram [MAXJOBS][256]

@@ -203,6 +203,19 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
   const T ih = (T)(PRIM == PRIM_Z ? g.ihz : PRIM == PRIM_Y ? g.ihy : g.ihx);
   double d_w2 = 0, d_hv = 0, d_hh = 0, d_vh = 0, d_gv = 0, d_gg = 0, d_vv = 0, d_fn = 0, d_s2 = 0;
   double d_w1 = 0, d_s1 = 0;   // select v2: ||w||_1, ||s||_1 of an l1 radix job
+  {   // the staged arrays of this segment (the issue below copies exactly these)
+    constexpr bool nb = PRIM == PRIM_Z || PRIM == PRIM_Y;
+    unsigned m = (1u << A_X) | (1u << A_Y) | (1u << A_V);
+    if (nb) m |= 1u << A_XN;
+    if (KIND == 1 || (KIND == 0 && lop)) m |= 1u << A_M;
+    if (KIND == 0 && hip) m |= 1u << A_HI;
+    if (NA > A_VH0 && dots) {
+      m |= (1u << A_VH0) | (1u << A_XS);
+      if (nb) m |= 1u << A_XSN;
+      if (pointwise) m |= (1u << A_Y0) | (1u << A_V0);
+    }
+    st.set_layout(m);
+  }
   const int ntile = (c1 - c0 + BLOCK - 1) / BLOCK;
   auto issue = [&](int t) {
     const int cs = c0 + t * BLOCK;
@@ -229,12 +242,13 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
         src[A_V0] = (const char*)(vw + o); by[A_V0] = b;
       }
     }
-    st.issue(t & 1, NA, src, by);
+    st.issue(t % st.ns, NA, src, by, P.p1_hint,
+             (1u << A_X) | (1u << A_XN) | (NA > A_XS ? (1u << A_XS) : 0u) | (NA > A_XSN ? (1u << A_XSN) : 0u));
   };
-  if (ntile > 0) issue(0);
+  for (int q = 0; q < st.ns - 1 && q < ntile; ++q) issue(q);
   for (int t = 0; t < ntile; ++t) {
-    if (t + 1 < ntile) issue(t + 1);
-    const int s = t & 1;
+    if (t + st.ns - 1 < ntile) issue(t + st.ns - 1);
+    const int s = t % st.ns;
     st.wait(s);
     const int c = c0 + t * BLOCK + (int)threadIdx.x;
     T hw_[W] = {}, hs_[W] = {};   // round-A keys of this chunk (zeros: not counted)
@@ -358,7 +372,7 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
       hist_a<T>(ha, hw_);
       if (sp) hist_a<T>(ha + NBUCK, hs_);
     }
-    __syncthreads();   // stage s is refilled by the issue of tile t + 2
+    __syncthreads();   // stage s is refilled by the issue of tile t + ns
   }
   const int base = i * NSLOT;
   if (KIND == 2 && ha && S.kind == K_L1) {   // l1 sets use neither slot otherwise before pass 2
@@ -394,6 +408,13 @@ __device__ __forceinline__ void p1_xrun(const Prob<T>& P, const Ctrl& C, const I
   const int hcount = C.hist_count, hhead = C.hist_head;
   const int hslot = (hhead + 1) % HIST_S;
   double x2 = 0.0, d2[HIST_S] = {0, 0, 0, 0, 0};
+  {
+    unsigned m = 1u;
+    if (check)
+      for (int js = 0; js < HIST_S; ++js)
+        if ((hhead - js + HIST_S) % HIST_S < hcount) m |= 1u << (1 + js);
+    st.set_layout(m);
+  }
   const int ntile = (c1 - c0 + BLOCK - 1) / BLOCK;
   auto issue = [&](int t) {
     const int cs = c0 + t * BLOCK;
@@ -408,12 +429,12 @@ __device__ __forceinline__ void p1_xrun(const Prob<T>& P, const Ctrl& C, const I
 #pragma unroll
       for (int js = 0; js < HIST_S; ++js)
         if ((hhead - js + HIST_S) % HIST_S < hcount) { src[1 + js] = (const char*)(P.hist[js] + o); by[1 + js] = b; }
-    st.issue(t & 1, NA, src, by);
+    st.issue(t % st.ns, NA, src, by, P.p1_hint, 1u);   // x: read again by every segment
   };
-  if (ntile > 0) issue(0);
+  for (int q = 0; q < st.ns - 1 && q < ntile; ++q) issue(q);
   for (int t = 0; t < ntile; ++t) {
-    if (t + 1 < ntile) issue(t + 1);
-    const int s = t & 1;
+    if (t + st.ns - 1 < ntile) issue(t + st.ns - 1);
+    const int s = t % st.ns;
     st.wait(s);
     const int c = c0 + t * BLOCK + (int)threadIdx.x;
     if (c < c1) {
@@ -497,7 +518,7 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
   if (C.stopped) return;
   extern __shared__ __align__(16) double acc[];
   __shared__ double sh[NWARP + 1];
-  __shared__ uint64_t bars[2];
+  __shared__ uint64_t bars[SMAX];
   const Geo& g = P.g;
   const IterFlags f = iter_flags<AD, CK>(C);
   const int nv = P.P * NSLOT + NEVOL;
@@ -508,10 +529,11 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
   for (int v = threadIdx.x; v < NWARP * nv; v += BLOCK) acc[v] = 0.0;
   Stage2<NA> st;
   const size_t accb = (((size_t)NWARP * nv * sizeof(double) + 127) / 128) * 128;
-  st.init(bars, reinterpret_cast<char*>(acc) + accb, BLOCK);
-  // select v2 round A: two count histograms (w, s) after the stages
+  const int pool = AD == 0 ? P.p1_pool : P.p1a_pool;
+  st.init(bars, reinterpret_cast<char*>(acc) + accb, BLOCK, pool);
+  // select v2 round A: two count histograms (w, s) after the stage pool
   unsigned* ha = P.selv2 ? reinterpret_cast<unsigned*>(reinterpret_cast<char*>(acc) + accb +
-                                                       (size_t)2 * NA * (BLOCK + 1) * 16)
+                                                       (size_t)pool * (BLOCK + 1) * 16)
                          : nullptr;
   if (ha)
     for (int d = threadIdx.x; d < 2 * NBUCK; d += BLOCK) ha[d] = 0u;
@@ -564,9 +586,9 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
 }
 
 // dynamic shared memory of k_pass1t<T, AD, .>: per-warp slots + two stages
-__host__ inline size_t pass1_smem(int P, bool adapt, bool selv2 = false) {
+__host__ inline size_t pass1_smem(int P, int pool, bool selv2 = false) {
   const size_t accb = ((size_t)NWARP * (P * NSLOT + NEVOL) * sizeof(double) + 127) / 128 * 128;
-  return accb + (size_t)2 * (adapt ? P1_NA_ADAPT : P1_NA_PLAIN) * (BLOCK + 1) * 16 +
+  return accb + (size_t)pool * (BLOCK + 1) * 16 +
          (selv2 ? (size_t)2 * NBUCK * sizeof(unsigned) : 0);
 }
 

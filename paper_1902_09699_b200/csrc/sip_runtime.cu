@@ -481,13 +481,29 @@ struct Engine : EngineBase {
       const char* e = getenv("SIP_P1_SUB");
       const bool big = (double)g.N * sizeof(T) > 64.0 * (1 << 20);
       Pr.p1_sub = (e ? atoi(e) : (big ? 8 : 0)) * BLOCK;
+      const char* h = getenv("SIP_P1_HINT");
+      Pr.p1_hint = h ? atoi(h) : 1;   // x (and the Alg. 2 x snapshot) evict_last: re-read by every segment
     }
-    smem_p1v = pass1_smem(P, false, Pr.selv2);        // k_pass1t: slots + bulk-copy stages (+ round-A counts)
-    smem_p1a = pass1_smem(P, true, Pr.selv2);
-    // pass 1: segment-major over one contiguous chunk range per CTA
-    // (3 CTAs / SM plain, 2 on adapt iterations: registers + stage buffers)
-    g_p1 = std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * 3));
-    g_p1a = std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * 2));
+    {
+      const char* e1 = getenv("SIP_P1_POOL");
+      const char* e2 = getenv("SIP_P1A_POOL");
+      Pr.p1_pool = e1 ? std::max(2 * P1_NA_PLAIN, atoi(e1)) : 2 * P1_NA_PLAIN;
+      Pr.p1a_pool = e2 ? std::max(2 * P1_NA_ADAPT, atoi(e2)) : 2 * P1_NA_ADAPT;
+    }
+    smem_p1v = pass1_smem(P, Pr.p1_pool, Pr.selv2);   // k_pass1t: slots + bulk-copy stage pool (+ round-A counts)
+    smem_p1a = pass1_smem(P, Pr.p1a_pool, Pr.selv2);
+    // pass 1: segment-major over one contiguous chunk range per CTA, one
+    // resident wave (CTAs per SM from registers + stage buffers)
+    {
+      auto wave1 = [&](const void* fn, size_t smem, int cap) {
+        int occ = 0;
+        CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, BLOCK, smem));
+        return std::max(1, std::min(g.N / VT<T>::W / BLOCK, nsm * std::max(1, std::min(occ, cap))));
+      };
+      g_p1 = wave1((const void*)k_pass1t<T, 0, 0>, smem_p1v, 3);
+      g_p1a = wave1((const void*)k_pass1t<T, 1, 0>, smem_p1a, 2);
+    }
     if (vec && sizeof(T) == 4) {
       // per-CTA candidate regions of the select grid: a CTA visits at most
       // ceil(chunks / (grid * BLOCK * SEL_U)) iterations of BLOCK * SEL_U chunks

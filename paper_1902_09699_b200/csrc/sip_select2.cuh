@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
     Ctrl& C = *P.ctrl;
     if (C.stopped) return;
     extern __shared__ __align__(16) char sb_buf[];
-    __shared__ uint64_t bars[2];
+    __shared__ uint64_t bars[SMAX];
     __shared__ SelRange s_rng[MAXJOBS];
     __shared__ unsigned s_cn;
     __shared__ double sh[NWARP + 1];
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
     const int nch = g.N / W;
     const int nj = C.njobs;
     Stage2<1> st;
-    st.init(bars, sb_buf, SB_TILE);
+    st.init(bars, sb_buf, SB_TILE, 2);
     const int lane = threadIdx.x & 31;
     bool any = false;
     for (int jb = 0; jb < nj; ++jb) {
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
             const unsigned k = key32((float)v[e]);
             const bool ab = k >= hi;
             n_ab += ab ? 1u : 0u;
-            s_ab += ab ? kval(k) : 0.0;
+            s_ab += (double)(ab ? __uint_as_float(k) : 0.0f);   // one select + one conversion
             mine |= (unsigned)(k - lo1 < wid1) << (u * W + e);
           }
         }
