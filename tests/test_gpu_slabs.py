@@ -180,6 +180,15 @@ def test_slab_multilevel_matches_oracle(shape, levels, kinds, ranks):
 
 
 def test_slab_multilevel_fp32_c5_like():
+    """C5-like fp32 multilevel on 4 virtual z slabs against the fp64 oracle,
+    with the bars of test_multilevel_fp32_small_c5_like (non-convex sets:
+    trajectory parity, reading L24): coarse levels take the oracle's
+    iterations and CG steps; the finest level's CG counts equal the
+    oracle's up to the first stop check that differs, its stop iteration
+    within one check period; x within 1e-3 of the oracle when both stop at
+    the same check, else within eps_evol = 1e-2 (the resolution of the stop
+    test itself, Eq. 27); every constraint violated by <= 1e-3 where the
+    oracle's is, else by no more than the oracle's + 1e-3."""
     prob = G.c5(seed=4, shape=(32, 32, 16))
     o = dict(prob.options, cg_tol_floor=10 * float(np.finfo(np.float32).eps))
     x_ref, _, logs = O.parsdmm_multilevel(prob.shape, prob.sets, prob.m, 3, **o)
@@ -188,13 +197,21 @@ def test_slab_multilevel_fp32_c5_like():
     m = torch.tensor(prob.m, dtype=torch.float32, device="cuda")
     x = torch.empty_like(m)
     per, st = g.project_multilevel(m, x, 3, max_iter=200, tol=1e-3)
-    # non-convex sets: trajectory parity (L24), see test_multilevel_fp32_small_c5_like
+    for l in (2, 1):
+        assert per[l]["iterations"] == logs[l].iterations, (l, per[l]["iterations"], logs[l].iterations)
+        assert per[l]["cg_iterations"] == logs[l].cg_total, (l, per[l]["cg_iterations"], logs[l].cg_total)
+    ig, io = per[0]["iterations"], logs[0].iterations
+    assert abs(ig - io) <= 5, (ig, io)
+    lg = g.get_log(200)
+    n = min(ig, io) - 1
+    np.testing.assert_array_equal(lg["cg"][:n], logs[0].cg_per_iter[:n])
     xg = x.double().cpu().numpy().ravel()
-    assert O.relres(xg, x_ref.ravel()) < 1e-2
+    rl = O.relres(xg, x_ref.ravel())
+    assert rl < (1e-3 if ig == io else 1e-2), (rl, ig, io)
     from test_gpu_parity import absolute_set
     for sd in prob.sets:
         sda = absolute_set(sd, prob)
         fg = O.feas(sda, O.apply_A(prob.shape, sd, xg))
         fo = O.feas(sda, O.apply_A(prob.shape, sd, x_ref.ravel()))
-        assert fg <= 1.5 * fo + 1e-4, (sd.op, sd.kind, fg, fo)
+        assert fg <= max(fo, 1e-3) + (1e-3 if fo > 1e-3 else 0.0), (sd.op, sd.kind, fg, fo)
     g.close()
