@@ -367,6 +367,9 @@ def run_cuda(args, prob):
         lv_probs = [prob]
     scale = m_np.size / prob.N                                    # this rank's share of the bytes
     table = roofline_table(prob, prof, ips, args.n_cg, word, peaks["hbm_gbs"], lv_probs)
+    if "select" in table and world == 1:   # the single-rank threshold searches
+        table["select"]["kernel"] = ("k_selsmall" if 3 * prob.N <= 8192 else
+                                     "k_selB+k_selC" if word == 4 else "k_selectf")
     for v in table.values():
         v["bytes_per_step"] *= scale
         v["achieved_gbs"] *= scale
@@ -376,7 +379,7 @@ def run_cuda(args, prob):
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if dom and os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(prob.name, {}).get(KNAME[dom])
+        traffic = json.load(open(tpath)).get(prob.name, {}).get(table[dom]["kernel"])
     model = byte_model(prob, args.n_cg, word)
     it_model_gbs = model["iteration"] * scale * (args.steps * ips) / (sum(lvl_ms[:1]) / 1e3) / 1e9
 
