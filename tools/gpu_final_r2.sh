@@ -16,5 +16,11 @@ done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/r2_bench_reference.json 2>&1
 timeout 600 python tools/fig1_dykstra.py --out $O/r2_fig1_dykstra.json > $O/r2_fig1.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file $O/r2_launches_c4.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/r2_ncu_list.log 2>&1
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_cg1f|k_cg2f|k_selB|k_pass1t|k_rhsp|k_pass2t" --launch-skip 60 --launch-count 12 -f -o $O/r2_full python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/r2_ncu_full.log 2>&1
-tail -2 $O/r2_ncu_full.log
+rm -f $O/r2_full*.ncu-rep
+for k in k_cg1f k_cg2f k_pass1t k_rhsp k_selB k_selC k_pass2t k_cgx; do
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:"$k" --launch-skip 6 --launch-count 2 -f -o $O/r2_full_$k python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/r2_ncu_full_$k.log 2>&1
+  tail -1 $O/r2_ncu_full_$k.log
+done
+if [ -n "$SANITIZE" ]; then
+  timeout 600 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_case.py > $O/r2_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -5 $O/r2_memcheck.log
+fi
