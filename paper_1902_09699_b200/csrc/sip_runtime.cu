@@ -455,7 +455,7 @@ struct Engine : EngineBase {
       return std::max(1, std::min((g.N / W / 2 + BLOCK - 1) / BLOCK, nsm * std::max(1, std::min(occ, want))));
     };
     g_cg1p = wave(ndim == 3 ? (const void*)k_cg1f<T, true> : (const void*)k_cg1f<T, false>, 4);
-    g_cg2p = wave(ndim == 3 ? (const void*)k_cg2f<T, true> : (const void*)k_cg2f<T, false>, 3);
+    g_cg2p = wave(ndim == 3 ? (const void*)k_cg2f<T, true> : (const void*)k_cg2f<T, false>, CG2_MINB);
     g_rhsp = wave(ndim == 3 ? (const void*)k_rhsp<T, true> : (const void*)k_rhsp<T, false>, 3);
     const int nv1 = P * NSLOT + NEVOL;
     smem_p1 = (size_t)NWARP * nv1 * sizeof(double);   // scalar k_pass1

@@ -15,6 +15,9 @@
 #pragma once
 #include "sip_kernels.cuh"
 
+#ifndef CG2_MINB
+#define CG2_MINB 3
+#endif
 namespace sip {
 
 template <class T> struct VT;
@@ -478,7 +481,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_cg1f(const __grid_constant__ Prob<
 
 // k_cg2f(j): r -= alpha C p_j and <r, r> (the x update is deferred to k_cgx)
 template <class T, bool HY>
-__global__ void __launch_bounds__(BLOCK, 3) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
+__global__ void __launch_bounds__(BLOCK, CG2_MINB) k_cg2f(const __grid_constant__ Prob<T> P, int j) {
   pdl_begin();
   Ctrl& C = *P.ctrl;
   if (C.stopped || !C.cg_active) return;
