@@ -15,6 +15,12 @@
 #include "sip_stage.cuh"
 #include "sip_select2.cuh"
 
+#ifndef P2_H
+#define P2_H 2        // pass 2: tiles per CTA step (one chunk of each per thread)
+#endif
+#ifndef P2_MINB
+#define P2_MINB 4
+#endif
 namespace sip {
 
 struct IterFlags { bool adapt, dots, check; };
@@ -604,7 +610,7 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
   using K = KeyT<T>;
   using U = typename K::U;
   constexpr int W = VT<T>::W;
-  constexpr int H = 2;
+  constexpr int H = P2_H;
   const Geo& g = P.g;
   const SetD<T>& S = P.set[i];
   const int nch = g.N / W;
@@ -615,7 +621,7 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
   T wv[H][W], y0[H][W], v0[H][W];
 #pragma unroll
   for (int h = 0; h < H; ++h) {
-    const int c = (2 * lp + h) * BLOCK + threadIdx.x;
+    const int c = (H * lp + h) * BLOCK + threadIdx.x;
     valid[h] = c < nch;
     pt0[h] = (valid[h] ? c : nch - 1) * W;
     off[h] = (int64_t)bl * g.ld + pt0[h];
@@ -656,7 +662,7 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
     const Job& J = C.job[S.job];
     const U tau = (U)J.tau;
     bool keep[H][W];
-    int cnt[H] = {0, 0};
+    int cnt[H] = {};
 #pragma unroll
     for (int h = 0; h < H; ++h)
 #pragma unroll
@@ -670,7 +676,7 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
         const int* toff = P.tiecnt + (size_t)S.job * P.ntiles_max;
 #pragma unroll
         for (int h = 0; h < H; ++h) {
-          const int t = 2 * lp + h;
+          const int t = H * lp + h;
           const int ex = block_excl_count(cnt[h], s_w);   // every thread (block barrier inside)
           if (t >= tpb) continue;
           long long r = (long long)toff[bl * tpb + t] + ex;
@@ -752,7 +758,7 @@ __device__ inline void fin_pass2(const Prob<T>& P, Ctrl& C, const double* stage)
 }
 
 template <class T, int AD, int CK>
-__global__ void __launch_bounds__(BLOCK, AD == 0 ? 4 : 3) k_pass2t(const __grid_constant__ Prob<T> P) {
+__global__ void __launch_bounds__(BLOCK, AD == 0 ? P2_MINB : 3) k_pass2t(const __grid_constant__ Prob<T> P) {
   pdl_begin();
   using K = KeyT<T>;
   using U = typename K::U;
@@ -770,7 +776,7 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 4 : 3) k_pass2t(const __grid_
   __syncthreads();
   const int nch = g.N / W;
   const int tpb = (nch + BLOCK - 1) / BLOCK;   // k_tiecountf's tiles per block
-  const int ppb = (tpb + 1) / 2;               // tile pairs per block
+  const int ppb = (tpb + P2_H - 1) / P2_H;     // tile groups per block
   int sg = blockIdx.x / ppb, lp = blockIdx.x - sg * ppb;
   while (sg < P.nseg2) {
     const int i = P.seg2_set[sg], bl = P.seg2_blk[sg];
