@@ -48,6 +48,10 @@ struct Prob {
   unsigned* gh_cnt;               // [MAXJOBS][NBUCK]
   unsigned long long* gh_s0;      // [MAXJOBS][NBUCK]
   unsigned long long* gh_s1;
+  unsigned long long* gh_ta;      // select v2 round A: sums of key bits 19..12 per bucket [MAXJOBS][NBUCK]
+  int sel_tsum;
+  int selb_ns;                    // k_selB: stages of its bulk-copy ring
+  unsigned* sel_gen;              // k_selCF: rounds released by the resolving CTA (only ever grows)                   // select v2: pass 1 accumulates gh_ta for l1 jobs on non-check iterations
   int* tiecnt;                    // [MAXJOBS][ntiles]
   int ntiles_max;
   // flattened segments (sip_flat.cuh): pass1 = x work + every (set, block);

@@ -375,7 +375,8 @@ __device__ __forceinline__ void p1_run(const Prob<T>& P, const Ctrl& C, int i, i
       d_s2 += (double)a_s2;
     }
     if (KIND == 2 && ha) {   // every lane of the warp (warp-grouped counts)
-      hist_a<T>(ha, hw_);
+      // s counts on check iterations, else (l1) the sub-bucket sums of w
+      hist_a<T>(ha, hw_, (P.sel_tsum && !check && S.kind == K_L1) ? ha + NBUCK : nullptr);
       if (sp) hist_a<T>(ha + NBUCK, hs_);
     }
     __syncthreads();   // stage s is refilled by the issue of tile t + ns
@@ -558,6 +559,7 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? 3 : 2) k_pass1t(const __grid_
     const SetD<T>& S = P.set[hset];
     hist_a_flush(ha, P.gh_cnt + (size_t)S.job * NBUCK);
     if (f.check && S.s) hist_a_flush(ha + NBUCK, P.gh_cnt + (size_t)S.sjob * NBUCK);
+    else if (P.sel_tsum && !f.check && S.kind == K_L1) hist_a_flush(ha + NBUCK, P.gh_ta + (size_t)S.job * NBUCK);
     hset = -1;
   };
   for (int s0 = c0; s0 < c1; s0 += sub) {

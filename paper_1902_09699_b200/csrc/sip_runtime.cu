@@ -119,6 +119,7 @@ struct Engine : EngineBase {
   // of the grid by cuBLAS GEMMs along each axis (plain library GEMMs)
   bool cgv = false;              // vectorised CG kernels (vec, or vec except a separable blur set)
   bool sel_small = false;        // every radix job small: k_selsmall (one CTA per job)
+  bool selc_fused = false;       // select v2: the candidate rounds in one launch (k_selCF)
   size_t smem_bf = 0;
   int g_bf = 1;
   int ndct_sets = 0;
@@ -468,10 +469,14 @@ struct Engine : EngineBase {
       if (Pr.set[i].job >= 0 && (long long)Pr.set[i].nblk * g.N > SEL_SMALL_MAX) sel_small = false;
     if (sel_small) CU(cudaFuncSetAttribute(k_selsmall<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)selsmall_smem()));
     Pr.selv2 = (vec && sizeof(T) == 4 && nranks == 1 && njobs > 0 && !ndct_sets && !sel_small && !getenv("SIP_SEL_V1")) ? 1 : 0;
+    // round A's sub-bucket sums for l1 jobs (one l1 candidate bucket); SIP_SEL_NOTSUM=1: counts only
+    Pr.sel_tsum = (Pr.selv2 && !getenv("SIP_SEL_NOTSUM")) ? 1 : 0;
+    selc_fused = Pr.selv2 && getenv("SIP_SELC_FUSED") && atoi(getenv("SIP_SELC_FUSED")) == 1;
     if (Pr.selv2) {   // k_selB / k_selC: one resident wave (the candidate regions are per CTA)
       int occ = 0;
-      CU(cudaFuncSetAttribute(k_selB<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)selb_smem()));
-      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_selB<T>, BLOCK, selb_smem()));
+      Pr.selb_ns = getenv("SIP_SELB_NS") ? std::min(SMAX, std::max(2, atoi(getenv("SIP_SELB_NS")))) : 2;
+      CU(cudaFuncSetAttribute(k_selB<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)selb_smem(Pr.selb_ns)));
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_selB<T>, BLOCK, selb_smem(Pr.selb_ns)));
       g_sel = std::max(1, std::min(tiles, nsm * std::max(occ, 1)));
     }
     {   // pass 1 sub-ranges (tiles of BLOCK chunks; 0 = the CTA's whole range).
@@ -577,6 +582,10 @@ struct Engine : EngineBase {
     Pr.gh_cnt = dalloc<unsigned>((size_t)MAXJOBS * NBUCK);
     Pr.gh_s0 = dalloc<unsigned long long>((size_t)MAXJOBS * NBUCK);
     Pr.gh_s1 = dalloc<unsigned long long>((size_t)MAXJOBS * NBUCK);
+    Pr.gh_ta = dalloc<unsigned long long>((size_t)MAXJOBS * NBUCK);
+    Pr.sel_gen = dalloc<unsigned>(1);
+    CU(cudaMemsetAsync(Pr.sel_gen, 0, sizeof(unsigned), stream));
+    CU(cudaMemsetAsync(Pr.gh_ta, 0, sizeof(unsigned long long) * MAXJOBS * NBUCK, stream));
     CU(cudaMemsetAsync(Pr.gh_cnt, 0, sizeof(unsigned) * MAXJOBS * NBUCK, stream));
     CU(cudaMemsetAsync(Pr.gh_s0, 0, sizeof(unsigned long long) * MAXJOBS * NBUCK, stream));
     CU(cudaMemsetAsync(Pr.gh_s1, 0, sizeof(unsigned long long) * MAXJOBS * NBUCK, stream));
@@ -975,8 +984,9 @@ struct Engine : EngineBase {
       if (sel_small) {
         lk(k_selsmall<T>, hc.njobs, BLOCK, selsmall_smem(), Pr); ++launches; mark(KB_SELECT);
       } else if (Pr.selv2) {   // one streaming pass + candidate rounds (round A ran in pass 1)
-        lk(k_selB<T>, g_sel, BLOCK, selb_smem(), Pr); ++launches; mark(KB_SELECT);
-        for (int r = 2; r <= 4; ++r) { lk(k_selC<T>, g_sel, BLOCK, 0, Pr, r); ++launches; mark(KB_SELECT); }
+        lk(k_selB<T>, g_sel, BLOCK, selb_smem(Pr.selb_ns), Pr); ++launches; mark(KB_SELECT);
+        if (selc_fused) { lk(k_selCF<T>, g_sel, BLOCK, 0, Pr); ++launches; mark(KB_SELECT); }
+        else for (int r = 2; r <= 4; ++r) { lk(k_selC<T>, g_sel, BLOCK, 0, Pr, r); ++launches; mark(KB_SELECT); }
       } else {
         for (int r = 1; r <= KeyT<T>::ROUNDS; ++r) { launch_select(r); mark(KB_SELECT); }
       }

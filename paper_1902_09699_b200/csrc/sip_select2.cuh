@@ -38,22 +38,32 @@ __device__ __forceinline__ double kval(unsigned key) { return (double)__uint_as_
 // one shared atomic per non-zero entry (grouping the lanes of a warp by
 // bucket with __match_any_sync first was measured slower: pass 1 3.24 vs
 // 2.65 ms per C4 step)
+// With t (l1 jobs, non-check iterations) also the sum of every entry's key
+// bits 19..12 (its 1/256 sub-bucket): the bucket's value sum is then known to
+// within count x 2^12 ulps, which pins sum_j max(|w_j| - e, 0) at every bucket
+// edge to ~1e-4 of itself, so k_selB's l1 window is one bucket wide, as for
+// the cardinality count.
+constexpr int T_SHIFT = 12;
 template <class T>
-__device__ __forceinline__ void hist_a(unsigned* h, const T* v) {
+__device__ __forceinline__ void hist_a(unsigned* h, const T* v, unsigned* t = nullptr) {
   if constexpr (sizeof(T) == 4) {
     constexpr int W = VT<T>::W;
 #pragma unroll
     for (int e = 0; e < W; ++e) {
       const unsigned k = key32((float)v[e]);
-      if (k) atomicAdd(&h[k >> A_SHIFT], 1u);
+      if (k) {
+        atomicAdd(&h[k >> A_SHIFT], 1u);
+        if (t) atomicAdd(&t[k >> A_SHIFT], (k >> T_SHIFT) & 0xffu);
+      }
     }
   }
 }
-__device__ __forceinline__ void hist_a_flush(unsigned* h, unsigned* g) {
+template <class G>
+__device__ __forceinline__ void hist_a_flush(unsigned* h, G* g) {
   __syncthreads();
   for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
     const unsigned c = h[d];
-    if (c) { atomicAdd(g + d, c); h[d] = 0u; }
+    if (c) { atomicAdd(g + d, (G)c); h[d] = 0u; }
   }
   __syncthreads();
 }
@@ -94,7 +104,13 @@ __device__ __forceinline__ double edge_a(int d) {
   return d < 0x7f8 ? kval((unsigned)d << A_SHIFT) : 3.4028234663852886e38;
 }
 
-__device__ inline SelRange range_of_job(const Job& J, const unsigned* gcnt) {
+// 2^12 ulps of the keys of round-A bucket d (one exponent per bucket)
+__device__ __forceinline__ double tstep_a(int d) {
+  const int ex = d >> 3;                        // exponent field (11-bit digit = exponent + 3 mantissa bits)
+  return ldexp(1.0, (ex ? ex : 1) - 150 + T_SHIFT);
+}
+
+__device__ inline SelRange range_of_job(const Job& J, const unsigned* gcnt, const unsigned long long* gta) {
   __shared__ unsigned long long s_u[NWARP];
   __shared__ double s_d[NWARP];
   __shared__ int s_best[2];
@@ -104,12 +120,23 @@ __device__ inline SelRange range_of_job(const Job& J, const unsigned* gcnt) {
   unsigned c[PER];
   unsigned long long ct = 0;
   double et = 0.0, e1t = 0.0;
+  double lo_[PER], hi_[PER];   // bounds of the bucket's value sum
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    c[q] = __ldcg(gcnt + d0 + q);
+    const int d = d0 + q;
+    c[q] = __ldcg(gcnt + d);
     ct += c[q];
-    et += (double)c[q] * edge_a(d0 + q);
-    e1t += (double)c[q] * edge_a(d0 + q + 1);
+    if (gta && d < 0x7f8) {
+      const double ts = tstep_a(d);
+      const double tq = (double)__ldcg(gta + d);
+      lo_[q] = (double)c[q] * edge_a(d) + tq * ts;
+      hi_[q] = lo_[q] + (double)c[q] * ts;
+    } else {
+      lo_[q] = (double)c[q] * edge_a(d);
+      hi_[q] = (double)c[q] * edge_a(d + 1);
+    }
+    et += lo_[q];
+    e1t += hi_[q];
   }
   const unsigned long long c_after = suffix_excl<unsigned long long>(ct, s_u);
   const double e_after = suffix_excl<double>(et, s_d);
@@ -124,8 +151,8 @@ __device__ inline SelRange range_of_job(const Job& J, const unsigned* gcnt) {
     const int d = d0 + q;
     C += c[q];
     const double e = edge_a(d);
-    E += (double)c[q] * e;
-    E1 += (double)c[q] * edge_a(d + 1);
+    E += lo_[q];
+    E1 += hi_[q];
     if (J.kind == K_CARD) {
       if (C >= (unsigned long long)J.k && best_hi < d) best_hi = d;
     } else {
@@ -261,7 +288,7 @@ __device__ void resolve_window(Ctrl& C, Job& J, const unsigned* hc, const unsign
 // 0 issues the next tile before the CTA works on the current one), so the
 // loads are decoupled from the per-entry work and from register pressure.
 constexpr int SB_TILE = 2048;                 // chunks (16 B) per stage: 32 KB
-__host__ inline size_t selb_smem() { return (size_t)2 * (SB_TILE + 1) * 16; }
+__host__ inline size_t selb_smem(int ns = 2) { return (size_t)ns * (SB_TILE + 1) * 16; }
 
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> P) {
@@ -284,14 +311,16 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
     const int nch = g.N / W;
     const int nj = C.njobs;
     Stage2<1> st;
-    st.init(bars, sb_buf, SB_TILE, 2);
+    const int ns = P.selb_ns;                 // stages: ns - 1 tiles in flight while one is worked on
+    st.init(bars, sb_buf, SB_TILE, ns);
     const int lane = threadIdx.x & 31;
     bool any = false;
     for (int jb = 0; jb < nj; ++jb) {
       const Job& J = C.job[jb];
       if (!job_live(J, check)) continue;
       any = true;
-      const SelRange R = range_of_job(J, P.gh_cnt + (size_t)jb * NBUCK);
+      const bool ts = P.sel_tsum && !check && !J.on_s && J.kind == K_L1;   // pass 1's rule
+      const SelRange R = range_of_job(J, P.gh_cnt + (size_t)jb * NBUCK, ts ? P.gh_ta + (size_t)jb * NBUCK : nullptr);
       if (threadIdx.x == 0) s_rng[jb] = R;
       __syncthreads();
       double* part = P.partials + ((size_t)blockIdx.x * MAXJOBS + jb) * 3;
@@ -319,7 +348,7 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
         tile_of(i, &c0, &cnt, &src);
         const char* sp[1] = {reinterpret_cast<const char*>(src)};
         const unsigned by[1] = {(unsigned)cnt * 16u};
-        st.issue(i & 1, 1, sp, by);
+        st.issue(i % ns, 1, sp, by);
       };
       const bool sums = J.kind == K_L1;
       const int fsh = sel_shift((unsigned long long)(hi - lo), FB_BITS);
@@ -330,10 +359,10 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
       double s_ab = 0.0;
       const unsigned lo1 = lo > 1u ? lo : 1u;   // zeros are never candidates
       const unsigned wid1 = hi > lo1 ? hi - lo1 : 0u;
-      if (nmine > 0) issue(0);
+      for (int q = 0; q < ns - 1 && q < nmine; ++q) issue(q);
       for (int i = 0; i < nmine; ++i) {
-        if (i + 1 < nmine) issue(i + 1);
-        const int sidx = i & 1;
+        if (i + ns - 1 < nmine) issue(i + ns - 1);   // the stage worked on at i - 1
+        const int sidx = i % ns;
         st.wait(sidx);
         int c0, cnt;
         const T* src;
@@ -383,7 +412,7 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
             }
           }
         }
-        __syncthreads();   // the stage is refilled by the issue of tile i + 2
+        __syncthreads();   // the stage is refilled by the issue of tile i + ns
       }
       // this CTA's candidate histogram into the job's (non-zero buckets only)
       __syncthreads();
@@ -432,7 +461,10 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
         // the candidates' 256-bucket histogram narrows the window (round 1)
         if (J.mode == JM_SEARCH && J.round == 1)
           resolve_window(C, J, P.gf_cnt + (size_t)jb * FB_N, P.gf_s0 + (size_t)jb * FB_N, FB_BITS);
-        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;   // next round A
+        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {   // next round A
+          P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;
+          P.gh_ta[(size_t)jb * NBUCK + d] = 0ull;
+        }
         for (int d = threadIdx.x; d < FB_N; d += BLOCK) {
           P.gf_cnt[(size_t)jb * FB_N + d] = 0u;
           P.gf_s0[(size_t)jb * FB_N + d] = 0ull;
@@ -445,6 +477,86 @@ __global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> 
 }
 
 // ---------------------------------------------------------------- k_selC
+// One candidate round: this CTA's histogram of the window's keys into the
+// job's global histogram; the last CTA resolves the window.  Returns whether
+// any job took part (the same answer in every CTA).
+template <class T>
+__device__ bool selc_round(const Prob<T>& P, Ctrl& C, int round, bool check, unsigned* gen = nullptr) {
+  using LB = Limbs<float>;
+  __shared__ unsigned h_cnt[NBUCK];
+  __shared__ unsigned h_l[LB::N][NBUCK];
+  const int nj = C.njobs;
+  bool any = false;
+  for (int jb = 0; jb < nj; ++jb) {
+    const Job& J = C.job[jb];
+    if (J.mode != JM_SEARCH || J.round != round || (J.on_s && !check)) continue;
+    any = true;
+    const bool sums = J.kind == K_L1;
+    const unsigned lo = (unsigned)J.prefix;
+    const unsigned long long width = J.width;
+    const int sh = sel_shift(width, 11);
+    for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+      h_cnt[d] = 0u;
+#pragma unroll
+      for (int q = 0; q < LB::N; ++q) h_l[q][d] = 0u;
+    }
+    __syncthreads();
+    // this CTA's candidate region (k_selB's CTA of the same index),
+    // coalesced, eight loads in flight per thread; only the window's keys
+    // (a small part after k_selB's round) reach the shared histogram
+    const unsigned* cand = P.cand[jb] + (size_t)blockIdx.x * P.cand_per;
+    const int n = (int)__ldcg(P.ccnt + (size_t)jb * gridDim.x + blockIdx.x);
+    for (int qb = 0; qb < n; qb += BLOCK * 8) {
+      unsigned kk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = qb + u * BLOCK + (int)threadIdx.x;
+        kk[u] = q < n ? __ldcg(cand + q) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned k = kk[u];
+        if (qb + u * BLOCK + (int)threadIdx.x >= n || k < lo || (unsigned long long)(k - lo) >= width) continue;
+        const int d = (int)((k - lo) >> sh);
+        atomicAdd(&h_cnt[d], 1u);
+        if (sums) {
+          unsigned l[LB::N];
+          LB::split(k, l);
+#pragma unroll
+          for (int t = 0; t < LB::N; ++t) atomicAdd(&h_l[t][d], l[t]);
+        }
+      }
+    }
+    __syncthreads();
+    unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
+    unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
+    for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+      if (!h_cnt[d]) continue;
+      atomicAdd(gc + d, h_cnt[d]);
+      if (sums) atomicAdd(g0 + d, (unsigned long long)h_l[0][d] + ((unsigned long long)h_l[1][d] << 16));
+    }
+    __syncthreads();
+  }
+  if (!any) return false;
+  if (last_block(P.counter)) {
+    for (int jb = 0; jb < nj; ++jb) {
+      Job& J = C.job[jb];
+      if (J.mode != JM_SEARCH || J.round != round || (J.on_s && !check)) continue;
+      resolve_window(C, J, P.gh_cnt + (size_t)jb * NBUCK, P.gh_s0 + (size_t)jb * NBUCK, 11);
+      for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
+        P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;
+        P.gh_s0[(size_t)jb * NBUCK + d] = 0ull;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      *P.counter = 0u;
+      if (gen) { __threadfence(); atomicAdd(gen, 1u); }   // release the round (k_selCF)
+    }
+  }
+  return true;
+}
+
 template <class T>
 __global__ void __launch_bounds__(BLOCK) k_selC(const __grid_constant__ Prob<T> P, int round) {
   pdl_begin();
@@ -453,75 +565,44 @@ __global__ void __launch_bounds__(BLOCK) k_selC(const __grid_constant__ Prob<T> 
     if (gridDim.x != (unsigned)P.sel_grid) __trap();   // one CTA per k_selB region
     Ctrl& C = *P.ctrl;
     if (C.stopped) return;
-    using LB = Limbs<float>;
-    __shared__ unsigned h_cnt[NBUCK];
-    __shared__ unsigned h_l[LB::N][NBUCK];
+    selc_round(P, C, round, (C.k % C.opt.check_every) == 0);
+  }
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The candidate rounds 2..4 in one launch: between rounds every CTA waits
+// for the last CTA's window (a release counter that only ever grows, read by
+// each CTA before its first arrival, so no reset races).  The grid is one
+// resident wave (k_selB's), and the next kernel launches only after all of
+// this grid's CTAs run (PDL), so the spin cannot starve a CTA of a slot.
+template <class T>
+__global__ void __launch_bounds__(BLOCK) k_selCF(const __grid_constant__ Prob<T> P) {
+  pdl_begin();
+  if constexpr (sizeof(T) != 4) return;
+  else {
+    if (gridDim.x != (unsigned)P.sel_grid) __trap();
+    Ctrl& C = *P.ctrl;
+    if (C.stopped) return;
+    __shared__ unsigned s_base;
+    if (threadIdx.x == 0) s_base = ld_acquire(P.sel_gen);
+    __syncthreads();
+    const unsigned base = s_base;
     const bool check = (C.k % C.opt.check_every) == 0;
-    const int nj = C.njobs;
-    bool any = false;
-    for (int jb = 0; jb < nj; ++jb) {
-      const Job& J = C.job[jb];
-      if (J.mode != JM_SEARCH || J.round != round || (J.on_s && !check)) continue;
-      any = true;
-      const bool sums = J.kind == K_L1;
-      const unsigned lo = (unsigned)J.prefix;
-      const unsigned long long width = J.width;
-      const int sh = sel_shift(width, 11);
-      for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
-        h_cnt[d] = 0u;
-#pragma unroll
-        for (int q = 0; q < LB::N; ++q) h_l[q][d] = 0u;
+    unsigned nb = 0;
+    for (int round = 2; round <= 4; ++round) {
+      if (!selc_round(P, C, round, check, P.sel_gen)) break;   // no job left (every CTA agrees)
+      ++nb;
+      // the last CTA bumps sel_gen once its window is written; wait for it
+      if (threadIdx.x == 0) {
+        while ((int)(ld_acquire(P.sel_gen) - base) < (int)nb) __nanosleep(32);
+        __threadfence();
       }
       __syncthreads();
-      // this CTA's candidate region (k_selB's CTA of the same index),
-      // coalesced, eight loads in flight per thread; only the window's keys
-      // (a small part after k_selB's round) reach the shared histogram
-      const unsigned* cand = P.cand[jb] + (size_t)blockIdx.x * P.cand_per;
-      const int n = (int)__ldcg(P.ccnt + (size_t)jb * gridDim.x + blockIdx.x);
-      for (int qb = 0; qb < n; qb += BLOCK * 8) {
-        unsigned kk[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int q = qb + u * BLOCK + (int)threadIdx.x;
-          kk[u] = q < n ? __ldcg(cand + q) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const unsigned k = kk[u];
-          if (qb + u * BLOCK + (int)threadIdx.x >= n || k < lo || (unsigned long long)(k - lo) >= width) continue;
-          const int d = (int)((k - lo) >> sh);
-          atomicAdd(&h_cnt[d], 1u);
-          if (sums) {
-            unsigned l[LB::N];
-            LB::split(k, l);
-#pragma unroll
-            for (int t = 0; t < LB::N; ++t) atomicAdd(&h_l[t][d], l[t]);
-          }
-        }
-      }
-      __syncthreads();
-      unsigned* gc = P.gh_cnt + (size_t)jb * NBUCK;
-      unsigned long long* g0 = P.gh_s0 + (size_t)jb * NBUCK;
-      for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
-        if (!h_cnt[d]) continue;
-        atomicAdd(gc + d, h_cnt[d]);
-        if (sums) atomicAdd(g0 + d, (unsigned long long)h_l[0][d] + ((unsigned long long)h_l[1][d] << 16));
-      }
-      __syncthreads();
-    }
-    if (!any) return;
-    if (last_block(P.counter)) {
-      for (int jb = 0; jb < nj; ++jb) {
-        Job& J = C.job[jb];
-        if (J.mode != JM_SEARCH || J.round != round || (J.on_s && !check)) continue;
-        resolve_window(C, J, P.gh_cnt + (size_t)jb * NBUCK, P.gh_s0 + (size_t)jb * NBUCK, 11);
-        for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {
-          P.gh_cnt[(size_t)jb * NBUCK + d] = 0u;
-          P.gh_s0[(size_t)jb * NBUCK + d] = 0ull;
-        }
-        __syncthreads();
-      }
-      if (threadIdx.x == 0) *P.counter = 0u;
     }
   }
 }
@@ -533,9 +614,12 @@ __global__ void k_seldbg(const __grid_constant__ Prob<T> P) {
   if (threadIdx.x || blockIdx.x || C.stopped) return;
   for (int jb = 0; jb < C.njobs; ++jb) {
     const Job& J = C.job[jb];
-    printf("k=%d job=%d on_s=%d kind=%d mode=%d round=%d theta=%.17g tau=%llu cnt_above=%lld sum_above=%.17g prefix=%llu width=%llu keep_eq=%lld ties=%d\n",
+    unsigned long long ncand = 0;   // k_selB's candidates (select v2 only)
+    if (P.selv2)
+      for (int b = 0; b < P.sel_grid; ++b) ncand += P.ccnt[(size_t)jb * P.sel_grid + b];
+    printf("k=%d job=%d on_s=%d kind=%d mode=%d round=%d theta=%.17g tau=%llu cnt_above=%lld sum_above=%.17g prefix=%llu width=%llu keep_eq=%lld ties=%d ncand=%llu\n",
            C.k, jb, J.on_s, J.kind, J.mode, J.round, J.theta, J.tau, J.cnt_above, J.sum_above, J.prefix, J.width,
-           J.keep_eq, J.ties);
+           J.keep_eq, J.ties, ncand);
   }
 }
 
