@@ -21,6 +21,14 @@ for k in k_cg1f k_cg2f k_pass1t k_rhsp k_selB k_selC k_pass2t k_cgx; do
   timeout 600 ncu --set full --import-source on --clock-control none -k regex:"$k" --launch-skip 6 --launch-count 2 -f -o $O/r2_full_$k python bench.py --steps 1 --warmup 1 --no-cpu-baseline > $O/r2_ncu_full_$k.log 2>&1
   tail -1 $O/r2_ncu_full_$k.log
 done
+# summaries are made here (the reports together can exceed gpurun_out's 64 MiB limit);
+# reports are then dropped, largest first, until the directory fits
+for f in $O/r2_full_*.ncu-rep; do
+  python tools/ncu_summary.py $f > ${f%.ncu-rep}.summary.txt 2>&1
+done
+while [ $(du -sm $O | cut -f1) -ge 56 ]; do
+  big=$(ls -S $O/*.ncu-rep 2>/dev/null | head -1); [ -z "$big" ] && break; rm -f $big
+done
 if [ -n "$SANITIZE" ]; then
   timeout 600 compute-sanitizer --tool memcheck --print-limit 20 python tools/sanitize_case.py > $O/r2_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -5 $O/r2_memcheck.log
 fi

@@ -83,8 +83,14 @@ if os.path.exists(lst):
                           "and three k_selC rounds), ncu launch list of profiles/r02_final_c4.md")
     json.dump(tj, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 
+sums = sorted(f for f in os.listdir(G) if f.startswith("r2_full") and f.endswith(".summary.txt"))
 reps = sorted(f for f in os.listdir(G) if f.startswith("r2_full") and f.endswith(".ncu-rep"))
-if reps:
+if sums:   # made on the GPU box by tools/gpu_final_r2.sh (the reports themselves may not travel back)
+    out += ["## ncu --set full --import-source on, hot kernels of a C4 step (`tools/ncu_summary.py`)", "", "```"]
+    for f in sums:
+        out.append(open(os.path.join(G, f)).read().rstrip())
+    out += ["```", ""]
+elif reps:
     out += ["## ncu --set full --import-source on, hot kernels of a C4 step (`tools/ncu_summary.py`)", "", "```"]
     for f in reps:
         out.append(sh([sys.executable, "tools/ncu_summary.py", os.path.join(G, f)]).rstrip())
