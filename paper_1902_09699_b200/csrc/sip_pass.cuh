@@ -18,6 +18,9 @@
 #ifndef P2_H
 #define P2_H 2        // pass 2: tiles per CTA step (one chunk of each per thread)
 #endif
+#ifndef P2_H0
+#define P2_H0 4       // iterations without the Alg. 2 products (AD == 0): four (C5-L1 pass 2 11.45 -> 10.7 ms per step, C4 unchanged)
+#endif
 #ifndef P2_MINB
 #define P2_MINB 4
 #endif
@@ -603,7 +606,7 @@ __host__ inline size_t pass1_smem(int P, int pool, bool selv2 = false) {
 // ------------------------------------------------------------ pass 2
 // KIND: 0 l1 ball (soft threshold at theta), 1 cardinality (keep > tau and the
 // first keep_eq == tau in index order), 2 l2 ball / annulus (radial factor)
-template <class T, int KIND>
+template <class T, int KIND, int H>
 __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, int bl, int lp, int tpb,
                                         const IterFlags& f, int par, double* acc, int nv, int* s_w) {
   // tiles 2 lp and 2 lp + 1 of the block (BLOCK chunks each, k_tiecountf's
@@ -612,7 +615,6 @@ __device__ __forceinline__ void p2_tile(const Prob<T>& P, const Ctrl& C, int i, 
   using K = KeyT<T>;
   using U = typename K::U;
   constexpr int W = VT<T>::W;
-  constexpr int H = P2_H;
   const Geo& g = P.g;
   const SetD<T>& S = P.set[i];
   const int nch = g.N / W;
@@ -778,14 +780,15 @@ __global__ void __launch_bounds__(BLOCK, AD == 0 ? P2_MINB : 3) k_pass2t(const _
   __syncthreads();
   const int nch = g.N / W;
   const int tpb = (nch + BLOCK - 1) / BLOCK;   // k_tiecountf's tiles per block
-  const int ppb = (tpb + P2_H - 1) / P2_H;     // tile groups per block
+  constexpr int H = AD == 0 ? P2_H0 : P2_H;
+  const int ppb = (tpb + H - 1) / H;           // tile groups per block
   int sg = blockIdx.x / ppb, lp = blockIdx.x - sg * ppb;
   while (sg < P.nseg2) {
     const int i = P.seg2_set[sg], bl = P.seg2_blk[sg];
     switch (P.set[i].kind) {
-      case K_L1: p2_tile<T, 0>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
-      case K_CARD: p2_tile<T, 1>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
-      default: p2_tile<T, 2>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
+      case K_L1: p2_tile<T, 0, H>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
+      case K_CARD: p2_tile<T, 1, H>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
+      default: p2_tile<T, 2, H>(P, C, i, bl, lp, tpb, f, par, acc, nv, s_w); break;
     }
     lp += gridDim.x;
     while (lp >= ppb) { lp -= ppb; ++sg; }

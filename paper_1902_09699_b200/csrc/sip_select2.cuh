@@ -287,11 +287,17 @@ __device__ void resolve_window(Ctrl& C, Job& J, const unsigned* hc, const unsign
 // filled by 1D bulk async copies (cp.async.bulk, mbarrier expect_tx; thread
 // 0 issues the next tile before the CTA works on the current one), so the
 // loads are decoupled from the per-entry work and from register pressure.
-constexpr int SB_TILE = 2048;                 // chunks (16 B) per stage: 32 KB
+#ifndef SIP_SB_TILE
+#define SIP_SB_TILE 2048
+#endif
+#ifndef SIP_SELB_MINB
+#define SIP_SELB_MINB 2
+#endif
+constexpr int SB_TILE = SIP_SB_TILE;          // chunks (16 B) per stage: 32 KB
 __host__ inline size_t selb_smem(int ns = 2) { return (size_t)ns * (SB_TILE + 1) * 16; }
 
 template <class T>
-__global__ void __launch_bounds__(BLOCK) k_selB(const __grid_constant__ Prob<T> P) {
+__global__ void __launch_bounds__(BLOCK, SIP_SELB_MINB) k_selB(const __grid_constant__ Prob<T> P) {
   pdl_begin();
   if constexpr (sizeof(T) != 4) return;
   else {

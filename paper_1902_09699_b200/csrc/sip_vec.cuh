@@ -542,8 +542,11 @@ __global__ void __launch_bounds__(BLOCK) k_cgsmall(const __grid_constant__ Prob<
 // chunk above, x's planes z-1 .. z+2 serve both stencils, and every block's
 // loads for two chunks are in flight together (measured: C4 rhs 1.09 ->
 // 0.93 ms per step, C5-L1 9.9 -> 7.9 ms, against one chunk per thread).
+#ifndef RHS_MINB
+#define RHS_MINB 3
+#endif
 template <class T, bool HY>
-__global__ void __launch_bounds__(BLOCK, 3) k_rhsp(const __grid_constant__ Prob<T> P) {
+__global__ void __launch_bounds__(BLOCK, RHS_MINB) k_rhsp(const __grid_constant__ Prob<T> P) {
   pdl_begin();
   constexpr int W = VT<T>::W;
   Ctrl& C = *P.ctrl;
