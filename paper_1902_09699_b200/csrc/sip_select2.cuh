@@ -195,7 +195,11 @@ __device__ __forceinline__ int sel_shift(unsigned long long width, int dbits) {
   while ((1ull << b) < width) ++b;        // ceil(log2(width))
   return b > dbits ? b - dbits : 0;
 }
-constexpr int FB_BITS = 8;                // k_selB's histogram of the candidates: 256 buckets
+#ifndef SIP_FB_BITS
+#define SIP_FB_BITS 9
+#endif
+constexpr int FB_BITS = SIP_FB_BITS;      // k_selB's histogram of the candidates: 512 buckets, so a
+                                          // one-bucket window (2^20 keys) needs one k_selC round, not two
 constexpr int FB_N = 1 << FB_BITS;
 
 // last CTA of k_selC: the bucket d* of the window holding the answer (the
@@ -464,7 +468,7 @@ __global__ void __launch_bounds__(BLOCK, SIP_SELB_MINB) k_selB(const __grid_cons
           }
         }
         __syncthreads();
-        // the candidates' 256-bucket histogram narrows the window (round 1)
+        // the candidates' 2^FB_BITS-bucket histogram narrows the window (round 1)
         if (J.mode == JM_SEARCH && J.round == 1)
           resolve_window(C, J, P.gf_cnt + (size_t)jb * FB_N, P.gf_s0 + (size_t)jb * FB_N, FB_BITS);
         for (int d = threadIdx.x; d < NBUCK; d += BLOCK) {   // next round A
